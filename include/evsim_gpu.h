@@ -1,0 +1,206 @@
+/*
+ * evsim_gpu.h — C-ABI of the B200-native event-simulation hot path.
+ *
+ * Drop-in boundary for the reference simulator `evsim` (arXiv 2209.04634).
+ * Every entry point below replaces one reference interface; the citation
+ * names the reference file:line it stands in for (paths under
+ * /root/reference/proj/).  Plain pointers and sizes only: no C++ or torch
+ * types cross this boundary, so the reference's own C++ host (or ctypes,
+ * cgo, JNI ...) can bind it directly.  See INTEGRATION.md.
+ *
+ * Semantics follow the reference exactly in contrast_mode LINEAR (the
+ * reference's only mode): same integer thresholds, same strict
+ * inequalities, same timestamps, same event order (t, y, x, p).  The LOG
+ * mode is the BASELINE.json extension (log intensity + per-pixel reference
+ * state); its rule is specified in DESIGN.md §3.
+ *
+ * Error handling mirrors the reference's exceptions: a non-zero status is
+ * returned and evsim_gpu_last_error() holds the message text, which for
+ * EVSIM_GPU_INVALID_ARGUMENT is the reference's exact std::invalid_argument
+ * message (e.g. "push_frame: timestamps must be strictly increasing",
+ * include/evsim/types.hpp + src/simulate.cpp:306-318).  A failed push leaves
+ * the simulator state untouched (tests/test_simulate.cpp:66-74).
+ */
+#ifndef EVSIM_GPU_H_
+#define EVSIM_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+enum {
+  EVSIM_GPU_OK = 0,
+  EVSIM_GPU_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  EVSIM_GPU_RUNTIME = 2,          /* reference: std::runtime_error    */
+  EVSIM_GPU_CUDA = 3              /* device / driver failure          */
+};
+
+/* ---- enums: same numbering as the reference's enum classes ------------- */
+/* evsim::Method            include/evsim/types.hpp:82 */
+enum { EVSIM_METHOD_DIFFERENCE_ONLY = 0, EVSIM_METHOD_DENSE = 1, EVSIM_METHOD_SPARSE = 2,
+       EVSIM_METHOD_DIFFERENCE_INTERP = 3 };
+/* evsim::FlowQuality       include/evsim/types.hpp:83 */
+enum { EVSIM_FLOW_LOW_QUALITY = 0, EVSIM_FLOW_HIGH_QUALITY = 1 };
+/* evsim::EventsPerCrossing include/evsim/types.hpp:86 */
+enum { EVSIM_EVENTS_SINGLE = 0, EVSIM_EVENTS_MAGNITUDE = 1 };
+/* extension (BASELINE.json configs): how a chain link is turned into events */
+enum { EVSIM_CONTRAST_LINEAR = 0, EVSIM_CONTRAST_LOG = 1 };
+
+/*
+ * Mirrors evsim::SimulatorConfig field for field (include/evsim/types.hpp:88-131)
+ * followed by the extension fields.  Zero-initialise, then call
+ * evsim_gpu_config_defaults() for the reference's per-method defaults
+ * (SimulatorConfig::defaults, types.hpp:101-120).
+ */
+typedef struct evsim_gpu_config {
+  int32_t method;              /* EVSIM_METHOD_*                      */
+  int32_t c_pos;               /* > 0, intensity units (linear mode)  */
+  int32_t c_neg;               /* < 0                                 */
+  int32_t n_interp;            /* >= 0                                */
+  int32_t flow_preset;         /* EVSIM_FLOW_*                        */
+  int32_t selection_threshold; /* 0 => c_pos (effective_selection_threshold) */
+  int32_t events_per_crossing; /* EVSIM_EVENTS_*                      */
+  int32_t include_endpoints;   /* bool                                */
+  /* ---- extension ---- */
+  int32_t contrast_mode;       /* EVSIM_CONTRAST_*                    */
+  float c_pos_log;             /* > 0, log-intensity units (log mode) */
+  float c_neg_log;             /* < 0                                 */
+  float sel_log;               /* sparse selection in log mode, 0 => c_pos_log */
+  /* Flow preset override (FlowPreset, include/evsim/flow.hpp:45-59); all
+   * three 0 => flow_preset(flow_preset).  Used by the plug-in flow entry
+   * points and by tests; the reference exposes the same knobs. */
+  int32_t pyramid_levels;
+  int32_t iterations_per_level;
+  int32_t patch_radius;
+} evsim_gpu_config;
+
+/*
+ * One event in exactly evsim::Event's in-memory layout (types.hpp:54-61):
+ * x@0 (u16), y@2 (u16), t@8 (i64), p@16 (i8), sizeof 24.
+ */
+typedef struct evsim_event {
+  uint16_t x;
+  uint16_t y;
+  int64_t t;
+  int8_t p;
+} evsim_event;
+
+/*
+ * Device-side packed event: bits 0-15 x, bits 16-30 y, bit 31 = 1 for
+ * polarity -1.  Events of one push are stored contiguously in the
+ * reference's output order; segment s (one distinct timestamp) covers
+ * [seg_offset[s], seg_offset[s+1]).
+ */
+#define EVSIM_PACK_X(e) ((uint32_t)(e) & 0xFFFFu)
+#define EVSIM_PACK_Y(e) (((uint32_t)(e) >> 16) & 0x7FFFu)
+#define EVSIM_PACK_P(e) (((uint32_t)(e) >> 31) ? -1 : 1)
+
+/* Result of one push; owned by the simulator, valid until the next
+ * push / reset / destroy on the same handle. */
+typedef struct evsim_gpu_events {
+  int32_t width;
+  int32_t height;
+  int64_t n_events;
+  int32_t n_segments;
+  const int64_t* seg_t;      /* host, n_segments timestamps (strictly increasing) */
+  const int64_t* seg_offset; /* host, n_segments + 1 offsets                       */
+  const uint32_t* d_packed;  /* DEVICE pointer, n_events packed records            */
+} evsim_gpu_events;
+
+typedef struct evsim_gpu_sim evsim_gpu_sim;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* evsim_gpu_last_error(void);
+
+/* SimulatorConfig::defaults(Method)  include/evsim/types.hpp:101-120 */
+void evsim_gpu_config_defaults(int32_t method, evsim_gpu_config* out);
+
+/* SimulatorConfig::validate          include/evsim/types.hpp:126-130 */
+int evsim_gpu_config_validate(const evsim_gpu_config* cfg);
+
+/* Simulator(SimulatorConfig)          include/evsim/simulate.hpp:62-77
+ * device: CUDA ordinal.  Device memory is pooled per handle, so creating a
+ * fresh simulator per timed pass (src/bench.cpp:53-64) stays cheap. */
+int evsim_gpu_create(const evsim_gpu_config* cfg, int device, evsim_gpu_sim** out);
+
+/* Simulator::push_frame               src/simulate.cpp:306-347
+ * pixels: width*height u8, row-major; on the host unless pixels_on_device.
+ * Synchronous: on return `out` describes the events (device-resident). */
+int evsim_gpu_push_frame(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t width, int32_t height,
+                         int64_t t_us, int32_t pixels_on_device, evsim_gpu_events* out);
+
+/* Asynchronous variant: enqueues the push on the handle's CUDA stream and
+ * returns without waiting; evsim_gpu_sync() completes it.  Validation
+ * errors are still reported synchronously. */
+int evsim_gpu_push_frame_async(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t width,
+                               int32_t height, int64_t t_us, int32_t pixels_on_device);
+int evsim_gpu_sync(evsim_gpu_sim* sim, evsim_gpu_events* out);
+
+/* Copy the last push's events to host memory.
+ * format 0: packed u32 records (4 B each); format 1: evsim_event (24 B).
+ * capacity is in records; returns INVALID_ARGUMENT if too small. */
+int evsim_gpu_copy_events(evsim_gpu_sim* sim, void* host_dst, int64_t capacity, int32_t format);
+
+/* CUDA stream (cudaStream_t) the handle enqueues on, for event timing. */
+void* evsim_gpu_stream(evsim_gpu_sim* sim);
+
+/* Simulator::reset                    include/evsim/simulate.hpp:83-86 */
+int evsim_gpu_reset(evsim_gpu_sim* sim);
+void evsim_gpu_destroy(evsim_gpu_sim* sim);
+
+/* Number of kernels this handle launched so far (instrumentation). */
+int64_t evsim_gpu_kernel_launches(const evsim_gpu_sim* sim);
+
+/* ---- free functions / plug-in seams (stateless, synchronous) ----------- */
+
+/* estimate_dense_flow / PyramidalPatchFlow::estimate
+ *   src/flow.cpp:260-276, include/evsim/flow.hpp:64,88-97
+ * du, dv: host buffers of width*height floats. */
+int evsim_gpu_dense_flow(const uint8_t* prev, const uint8_t* curr, int32_t width, int32_t height,
+                         int32_t pyramid_levels, int32_t iterations, int32_t patch_radius,
+                         float* du, float* dv);
+
+/* estimate_sparse_flow / PyramidalLucasKanade::estimate
+ *   src/flow.cpp:278-381, include/evsim/flow.hpp:69-70,100-110
+ * pts: 2*M int32 (x, y); disp: 2*M float (du, dv); status: M bytes. */
+int evsim_gpu_sparse_flow(const uint8_t* prev, const uint8_t* curr, int32_t width, int32_t height,
+                          int32_t pyramid_levels, int32_t iterations, int32_t patch_radius,
+                          const int32_t* pts, int64_t n_points, float* disp, uint8_t* status);
+
+/* interpolate_frames                  src/simulate.cpp:91-121
+ * out: n*width*height bytes, out_t: n timestamps. */
+int evsim_gpu_interpolate_frames(const uint8_t* prev, const uint8_t* curr, int32_t width,
+                                 int32_t height, int64_t t_prev, int64_t t_curr, const float* du,
+                                 const float* dv, int32_t n, uint8_t* out, int64_t* out_t);
+
+/* dense_events_with_flow              src/simulate.cpp:123-128
+ * Caller-supplied flow: the seam a custom DenseFlowEstimator plugs into
+ * (include/evsim/flow.hpp:74-78).  Events in evsim_event layout; the call
+ * returns the count in *n_events and writes up to `capacity` records (pass
+ * capacity 0 to query the size).  Linear mode only (the free function is
+ * stateless). */
+int evsim_gpu_dense_events_with_flow(const uint8_t* prev, const uint8_t* curr, int32_t width,
+                                     int32_t height, int64_t t_prev, int64_t t_curr,
+                                     const float* du, const float* dv,
+                                     const evsim_gpu_config* cfg, evsim_event* events,
+                                     int64_t capacity, int64_t* n_events);
+
+/* simulate_sparse with caller-supplied sparse flow (a custom
+ * SparseFlowEstimator, include/evsim/flow.hpp:80-85):
+ * src/simulate.cpp:145-201 after the estimator call.  pts must be the
+ * selection of src/simulate.cpp:149-159 in scan order. */
+int evsim_gpu_sparse_events_with_flow(const uint8_t* prev, const uint8_t* curr, int32_t width,
+                                      int32_t height, int64_t t_prev, int64_t t_curr,
+                                      const int32_t* pts, int64_t n_points, const float* disp,
+                                      const uint8_t* status, const evsim_gpu_config* cfg,
+                                      evsim_event* events, int64_t capacity, int64_t* n_events);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EVSIM_GPU_H_ */
