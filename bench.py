@@ -1,0 +1,390 @@
+"""Benchmark of the B200 event-simulation hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2] [--mode log|linear]
+
+Workload (BASELINE.json configs[1], the metric's headline config): c2 —
+640x480 u8 frames, 128-frame seeded synthetic sequence (paper_2209_04634_b200/
+scenes.py), dense pyramidal LK (lq preset), N = 10 interpolated frames, log
+intensity with C = 0.2.  One STEP = one pass of Simulator::push_frame over
+the whole 128-frame sequence (reset + 128 pushes; the reference's
+bench_method protocol, src/bench.cpp:53-64).  Metric: input frames/s (events/s
+reported beside it).
+
+* value: frames already resident in HBM, device-timed with CUDA events on the
+  simulator's stream, L2 flushed (256 MiB memset) before every step.
+* e2e: the same metric through the C-ABI with HOST buffers: per frame a pinned
+  H2D upload inside evsim_gpu_push_frame and a D2H of the packed events
+  (4 B/event) + segment table; host wall clock around the step.
+* roofline: event stage (chain -> scan -> emit) against measured HBM peak;
+  algorithmic bytes per frame B_alg = 2P + 4E.
+* cpu_baseline / --impl reference: the reference compiled from /root/reference
+  (oracle/_ref; the oracle C port when absent), one independent simulator per
+  host thread over contiguous chunks of the same sequence.
+
+Multi-GPU (torchrun): each rank simulates its own independent stream (per-rank
+seed) — stream sharding with no data-path collective ("weak" scaling); NCCL
+only all-reduces the timing and gathers event counts.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2")
+    p.add_argument("--mode", default="log", choices=["log", "linear"])
+    p.add_argument("--frames", type=int, default=0, help="override sequence length")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload(args, stream=0):
+    from paper_2209_04634_b200 import scenes
+    from paper_2209_04634_b200.abi import Method, make_config
+    c = scenes.CONFIGS[args.config]
+    n = args.frames or c.n_frames
+    frames, ts = scenes.generate(c, n_frames=n, stream=stream)
+    cp, cn = scenes.LINEAR_THRESHOLDS[c.method]
+    cfg = make_config(Method[c.method], n_interp=c.n_interp, c_pos=cp, c_neg=cn,
+                      contrast_mode=1 if args.mode == "log" else 0, c_pos_log=c.contrast, c_neg_log=-c.contrast)
+    return c, cfg, frames, ts
+
+
+def config_json(c, args, n_frames):
+    return {
+        "workload": f"{c.name}: {c.width}x{c.height} u8, {c.method} (LK lq) N={c.n_interp}, "
+                    f"{args.mode} C={c.contrast if args.mode == 'log' else 'int Table I'}, "
+                    f"{n_frames}-frame seeded synthetic sequence",
+        "width": c.width, "height": c.height, "frames_per_step": n_frames, "n_interp": c.n_interp,
+        "method": c.method, "mode": args.mode, "flow_preset": "low_quality",
+        "l2": "flushed before every step (256 MiB memset); device-resident inputs",
+    }
+
+
+# ----------------------------------------------------------------------------- CPU arms
+
+def cpu_run(cfg, frames, ts, threads, prefer_reference=True):
+    """Time the reference (or the oracle port) over the sequence split into
+    contiguous chunks, one independent simulator per host thread.  Returns
+    (useful frames, seconds, kind, events)."""
+    import oracle
+    kind = "reference" if (prefer_reference and os.path.exists(oracle.REF_SO)) else "port"
+    lib = oracle.Reference() if kind == "reference" else oracle.Oracle()
+    n = len(frames)
+    bounds = np.linspace(0, n - 1, threads + 1).astype(int)
+    counts = [0] * threads
+    useful = [0] * threads
+
+    def work(i):
+        lo, hi = int(bounds[i]), int(bounds[i + 1])
+        sim = lib.simulator(cfg)
+        ev = 0
+        for k in range(lo, hi + 1):
+            ev += len(sim.push_frame(frames[k], int(ts[k])))
+        counts[i] = ev
+        useful[i] = hi - lo
+        sim.close()
+
+    t0 = time.perf_counter()
+    th = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    dt = time.perf_counter() - t0
+    return sum(useful), dt, kind, sum(counts)
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if ws > 1 and rank != 0:
+        return 0
+    c, cfg, frames, ts = workload(args)
+    threads = os.cpu_count() or 1
+    vals = []
+    evs = 0
+    kind = "port"
+    for i in range(args.warmup + args.steps):
+        f, dt, kind, evs = cpu_run(cfg, frames, ts, threads)
+        if i >= args.warmup:
+            vals.append(f / dt)
+    v = statistics.mean(vals)
+    out = {
+        "metric": "simulated input frames/sec (events/sec beside it), % of HBM roofline",
+        "impl": "reference", "value": round(v, 3), "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * len(frames) / v, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8/f32/f64", "data": "synthetic",
+        "config": config_json(c, args, len(frames)),
+        "events_per_s": round(v * evs / max(len(frames) - threads, 1), 1),
+        "cpu_baseline": {"value": round(v, 3), "unit": "frames/s", "cores": threads, "kind": kind,
+                         "sample": f"{c.name} {len(frames)}-frame sequence, {args.mode} mode, split into "
+                                   f"{threads} contiguous chunks (one simulator per host thread)"},
+        "e2e": {"value": round(v, 3), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i in range(4) if r[i].lower().startswith("active")})
+        loaded = [s for s, _, _ in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(m for _, m, _ in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- ours
+
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = local if ws > 1 else 0
+    torch.cuda.set_device(device)
+
+    from paper_2209_04634_b200 import SimulatorConfig, Simulator
+    from paper_2209_04634_b200._lib import load
+    c, cfg, frames, ts = workload(args, stream=rank)
+    n = len(frames)
+    P = c.width * c.height
+    sim = Simulator(SimulatorConfig.from_c(cfg), device=device)
+    stream_ptr = sim.stream
+    torch_stream = torch.cuda.ExternalStream(stream_ptr, device=device)
+
+    d_frames = torch.from_numpy(frames).to(f"cuda:{device}")
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=f"cuda:{device}")
+    base = d_frames.data_ptr()
+    torch.cuda.synchronize()
+
+    def one_step(profile=False):
+        sim.reset()
+        for k in range(n):
+            sim.push_frame_async(base + k * P, c.width, c.height, int(ts[k]), on_device=True)
+        return sim.sync()
+
+    # warm-up (also measures events per frame: a synchronous pass)
+    for _ in range(max(args.warmup, 1)):
+        one_step()
+    ev_total = 0
+    sim.reset()
+    for k in range(n):
+        e = sim.push_frame_packed(base + k * P, c.width, c.height, int(ts[k]), on_device=True)
+        ev_total += e.n_events
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident, L2 flushed before each step -------------
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = sim.kernel_launches
+    sim.set_profiling(True)
+    times = []
+    with Clocks(device) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(torch_stream):
+                flush.fill_(1)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(torch_stream)
+            sim.reset()
+            for k in range(n):
+                sim.push_frame_async(base + k * P, c.width, c.height, int(ts[k]), on_device=True)
+            e1.record(torch_stream)
+            sim.sync()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    stages, timed_pushes = sim.stage_times()
+    sim.set_profiling(False)
+    launches = sim.kernel_launches - launches0
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    total_ms = sum(times)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{device}")
+    evs = torch.tensor([ev_total], dtype=torch.int64, device=f"cuda:{device}")
+    if ws > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gathered = [torch.zeros_like(evs) for _ in range(ws)]
+        dist.all_gather(gathered, evs)  # per-stream event counts (merged-output offsets)
+        ev_all = int(sum(int(g.item()) for g in gathered))
+    else:
+        ev_all = ev_total
+    max_ms = float(t.item())
+    frames_total = ws * n * args.steps
+    value = frames_total / (max_ms / 1e3)
+    events_per_s = ev_all * args.steps / (max_ms / 1e3)
+
+    # ---- roofline of the event stage (chain -> scan -> emit) ---------------------
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"
+    E_frame = ev_total / max(n - 1, 1)
+    b_alg = 2 * P + 4 * E_frame
+    interval_pushes = max(timed_pushes - args.steps, 1)  # warm-up pushes have empty event stages
+    ev_stage_ms = (stages["chain"] + stages["scan"] + stages["emit"]) / interval_pushes
+    achieved = b_alg / (ev_stage_ms / 1e3) / 1e9
+    e2e_frac = b_alg * (value / ws) / 1e9 / hbm
+    roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": None,
+                "kernel": "event stage: chain_kernel + scan_kernel + emit_kernel per frame",
+                "algorithmic_bytes_per_launch": round(b_alg), "avg_launch_ms": round(ev_stage_ms, 5),
+                "peak_source": peak_src, "end_to_end_frac": round(e2e_frac, 4),
+                "stage_ms_per_frame": {k: round(v / max(timed_pushes, 1), 5) for k, v in stages.items()}}
+
+    # ---- e2e through the C-ABI with host buffers ---------------------------------
+    e2e = None
+    if not args.no_e2e:
+        h_frames = torch.from_numpy(frames).pin_memory()
+        hbase = h_frames.data_ptr()
+        cap = (c.n_interp + 1) * P
+        h_events = torch.empty(cap, dtype=torch.int32).pin_memory()
+        hev = h_events.data_ptr()
+
+        def e2e_step():
+            sim.reset()
+            d2h = 0
+            for k in range(n):
+                e = sim.push_frame_packed(hbase + k * P, c.width, c.height, int(ts[k]), on_device=False)
+                if e.n_events:
+                    sim.copy_packed(hev, cap)
+                d2h += 4 * e.n_events + 16 * (e.n_segments + 1)
+            return d2h
+
+        e2e_step()
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d2h = 0
+        for _ in range(args.steps):
+            d2h = e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{device}")
+        if ws > 1:
+            import torch.distributed as dist
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(frames_total / float(te.item()), 3), "unit": "frames/s",
+               "h2d_bytes_per_step": n * P, "d2h_bytes_per_step": int(d2h),
+               "api": "evsim_gpu_push_frame (pinned host frame) + evsim_gpu_copy_events (packed)"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        f, dt, kind, _ = cpu_run(cfg, frames, ts, os.cpu_count() or 1)
+        cpu = {"value": round(f / dt, 3), "unit": "frames/s", "cores": os.cpu_count() or 1, "kind": kind,
+               "sample": f"{c.name} {n}-frame sequence, {args.mode} mode, split into {os.cpu_count()} contiguous "
+                         f"chunks (one simulator per host thread), {dt:.1f} s"}
+
+    if rank == 0:
+        out = {
+            "metric": "simulated input frames/sec (events/sec beside it), % of HBM roofline",
+            "value": round(value, 3), "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8/f32/f64", "data": "synthetic",
+            "config": {**config_json(c, args, n), "parallelism": f"streams x{ws}"},
+            "events_per_s": round(events_per_s, 1), "events_per_frame": round(E_frame, 1),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(out), flush=True)
+    sim.close()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

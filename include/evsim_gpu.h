@@ -27,6 +27,12 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define EVSIM_GPU_API __attribute__((visibility("default")))
+#else
+#define EVSIM_GPU_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -114,66 +120,83 @@ typedef struct evsim_gpu_events {
 typedef struct evsim_gpu_sim evsim_gpu_sim;
 
 /* Thread-local message of the last failing call on this thread. */
-const char* evsim_gpu_last_error(void);
+EVSIM_GPU_API const char* evsim_gpu_last_error(void);
 
 /* SimulatorConfig::defaults(Method)  include/evsim/types.hpp:101-120 */
-void evsim_gpu_config_defaults(int32_t method, evsim_gpu_config* out);
+EVSIM_GPU_API void evsim_gpu_config_defaults(int32_t method, evsim_gpu_config* out);
 
 /* SimulatorConfig::validate          include/evsim/types.hpp:126-130 */
-int evsim_gpu_config_validate(const evsim_gpu_config* cfg);
+EVSIM_GPU_API int evsim_gpu_config_validate(const evsim_gpu_config* cfg);
 
 /* Simulator(SimulatorConfig)          include/evsim/simulate.hpp:62-77
  * device: CUDA ordinal.  Device memory is pooled per handle, so creating a
  * fresh simulator per timed pass (src/bench.cpp:53-64) stays cheap. */
-int evsim_gpu_create(const evsim_gpu_config* cfg, int device, evsim_gpu_sim** out);
+EVSIM_GPU_API int evsim_gpu_create(const evsim_gpu_config* cfg, int device, evsim_gpu_sim** out);
 
 /* Simulator::push_frame               src/simulate.cpp:306-347
  * pixels: width*height u8, row-major; on the host unless pixels_on_device.
  * Synchronous: on return `out` describes the events (device-resident). */
-int evsim_gpu_push_frame(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t width, int32_t height,
+EVSIM_GPU_API int evsim_gpu_push_frame(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t width, int32_t height,
                          int64_t t_us, int32_t pixels_on_device, evsim_gpu_events* out);
 
 /* Asynchronous variant: enqueues the push on the handle's CUDA stream and
  * returns without waiting; evsim_gpu_sync() completes it.  Validation
  * errors are still reported synchronously. */
-int evsim_gpu_push_frame_async(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t width,
+EVSIM_GPU_API int evsim_gpu_push_frame_async(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t width,
                                int32_t height, int64_t t_us, int32_t pixels_on_device);
-int evsim_gpu_sync(evsim_gpu_sim* sim, evsim_gpu_events* out);
+EVSIM_GPU_API int evsim_gpu_sync(evsim_gpu_sim* sim, evsim_gpu_events* out);
 
 /* Copy the last push's events to host memory.
  * format 0: packed u32 records (4 B each); format 1: evsim_event (24 B).
  * capacity is in records; returns INVALID_ARGUMENT if too small. */
-int evsim_gpu_copy_events(evsim_gpu_sim* sim, void* host_dst, int64_t capacity, int32_t format);
+EVSIM_GPU_API int evsim_gpu_copy_events(evsim_gpu_sim* sim, void* host_dst, int64_t capacity, int32_t format);
 
 /* CUDA stream (cudaStream_t) the handle enqueues on, for event timing. */
-void* evsim_gpu_stream(evsim_gpu_sim* sim);
+EVSIM_GPU_API void* evsim_gpu_stream(evsim_gpu_sim* sim);
 
 /* Simulator::reset                    include/evsim/simulate.hpp:83-86 */
-int evsim_gpu_reset(evsim_gpu_sim* sim);
-void evsim_gpu_destroy(evsim_gpu_sim* sim);
+EVSIM_GPU_API int evsim_gpu_reset(evsim_gpu_sim* sim);
+EVSIM_GPU_API void evsim_gpu_destroy(evsim_gpu_sim* sim);
+
+/* ---- instrumentation --------------------------------------------------- */
+/* Pipeline stages timed with CUDA events on the handle's stream. */
+enum {
+  EVSIM_STAGE_UPLOAD = 0,  /* frame H2D / D2D into the handle         */
+  EVSIM_STAGE_PYRAMID = 1, /* quad image + pyramid of the new frame   */
+  EVSIM_STAGE_FLOW = 2,    /* dense LK levels / sparse select+LK+splat */
+  EVSIM_STAGE_CHAIN = 3,   /* interpolation + link chain + ballots    */
+  EVSIM_STAGE_SCAN = 4,    /* (segment, block) offsets                */
+  EVSIM_STAGE_EMIT = 5,    /* ordered event compaction                */
+  EVSIM_N_STAGES = 6
+};
+/* enable != 0 starts per-stage event timing (and clears the totals). */
+EVSIM_GPU_API int evsim_gpu_set_profiling(evsim_gpu_sim* sim, int32_t enable);
+/* Accumulated device milliseconds per stage and number of timed pushes
+ * since profiling was enabled (waits for queued work). */
+EVSIM_GPU_API int evsim_gpu_stage_times(evsim_gpu_sim* sim, double* ms, int32_t n_stages, int64_t* n_pushes);
 
 /* Number of kernels this handle launched so far (instrumentation). */
-int64_t evsim_gpu_kernel_launches(const evsim_gpu_sim* sim);
+EVSIM_GPU_API int64_t evsim_gpu_kernel_launches(const evsim_gpu_sim* sim);
 
 /* ---- free functions / plug-in seams (stateless, synchronous) ----------- */
 
 /* estimate_dense_flow / PyramidalPatchFlow::estimate
  *   src/flow.cpp:260-276, include/evsim/flow.hpp:64,88-97
  * du, dv: host buffers of width*height floats. */
-int evsim_gpu_dense_flow(const uint8_t* prev, const uint8_t* curr, int32_t width, int32_t height,
+EVSIM_GPU_API int evsim_gpu_dense_flow(const uint8_t* prev, const uint8_t* curr, int32_t width, int32_t height,
                          int32_t pyramid_levels, int32_t iterations, int32_t patch_radius,
                          float* du, float* dv);
 
 /* estimate_sparse_flow / PyramidalLucasKanade::estimate
  *   src/flow.cpp:278-381, include/evsim/flow.hpp:69-70,100-110
  * pts: 2*M int32 (x, y); disp: 2*M float (du, dv); status: M bytes. */
-int evsim_gpu_sparse_flow(const uint8_t* prev, const uint8_t* curr, int32_t width, int32_t height,
+EVSIM_GPU_API int evsim_gpu_sparse_flow(const uint8_t* prev, const uint8_t* curr, int32_t width, int32_t height,
                           int32_t pyramid_levels, int32_t iterations, int32_t patch_radius,
                           const int32_t* pts, int64_t n_points, float* disp, uint8_t* status);
 
 /* interpolate_frames                  src/simulate.cpp:91-121
  * out: n*width*height bytes, out_t: n timestamps. */
-int evsim_gpu_interpolate_frames(const uint8_t* prev, const uint8_t* curr, int32_t width,
+EVSIM_GPU_API int evsim_gpu_interpolate_frames(const uint8_t* prev, const uint8_t* curr, int32_t width,
                                  int32_t height, int64_t t_prev, int64_t t_curr, const float* du,
                                  const float* dv, int32_t n, uint8_t* out, int64_t* out_t);
 
@@ -183,7 +206,7 @@ int evsim_gpu_interpolate_frames(const uint8_t* prev, const uint8_t* curr, int32
  * returns the count in *n_events and writes up to `capacity` records (pass
  * capacity 0 to query the size).  Linear mode only (the free function is
  * stateless). */
-int evsim_gpu_dense_events_with_flow(const uint8_t* prev, const uint8_t* curr, int32_t width,
+EVSIM_GPU_API int evsim_gpu_dense_events_with_flow(const uint8_t* prev, const uint8_t* curr, int32_t width,
                                      int32_t height, int64_t t_prev, int64_t t_curr,
                                      const float* du, const float* dv,
                                      const evsim_gpu_config* cfg, evsim_event* events,
@@ -193,7 +216,7 @@ int evsim_gpu_dense_events_with_flow(const uint8_t* prev, const uint8_t* curr, i
  * SparseFlowEstimator, include/evsim/flow.hpp:80-85):
  * src/simulate.cpp:145-201 after the estimator call.  pts must be the
  * selection of src/simulate.cpp:149-159 in scan order. */
-int evsim_gpu_sparse_events_with_flow(const uint8_t* prev, const uint8_t* curr, int32_t width,
+EVSIM_GPU_API int evsim_gpu_sparse_events_with_flow(const uint8_t* prev, const uint8_t* curr, int32_t width,
                                       int32_t height, int64_t t_prev, int64_t t_curr,
                                       const int32_t* pts, int64_t n_points, const float* disp,
                                       const uint8_t* status, const evsim_gpu_config* cfg,

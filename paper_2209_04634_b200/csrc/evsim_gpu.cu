@@ -1,0 +1,1225 @@
+// evsim_gpu.cu — host side of the B200 event-simulation path: the C-ABI of
+// include/evsim_gpu.h, the per-handle device state and the per-push launch
+// sequence.
+//
+// Mirrors evsim::Simulator (/root/reference/proj/include/evsim/simulate.hpp:60-94,
+// src/simulate.cpp:306-347): same validation order and messages, same
+// warm-up semantics, failed pushes leave the state untouched.  All device
+// memory comes from the stream-ordered pool (cudaMallocAsync) with an
+// unbounded release threshold, so a fresh handle per timed pass (the
+// reference's bench_method, src/bench.cpp:53-64) reuses cached memory.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "evsim_gpu.h"
+#include "kernels.h"
+
+using namespace evsim_gpu;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct ApiError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void invalid(const std::string& m) { throw ApiError{EVSIM_GPU_INVALID_ARGUMENT, m}; }
+[[noreturn]] void runtime(const std::string& m) { throw ApiError{EVSIM_GPU_RUNTIME, m}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw ApiError{EVSIM_GPU_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+#define CK(x) ck((x), #x)
+#define CK_LAUNCH(what) ck(cudaGetLastError(), what)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return EVSIM_GPU_OK;
+  } catch (const ApiError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return EVSIM_GPU_RUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return EVSIM_GPU_RUNTIME;
+  }
+}
+
+// ------------------------------------------------------------------ config
+
+struct Preset {
+  int levels, iters, radius;
+};
+
+Preset resolve_preset(const evsim_gpu_config& c) {
+  if (c.pyramid_levels || c.iterations_per_level || c.patch_radius)
+    return {c.pyramid_levels, c.iterations_per_level, c.patch_radius};
+  // flow_preset(q)  include/evsim/flow.hpp:57-59
+  return c.flow_preset == EVSIM_FLOW_HIGH_QUALITY ? Preset{5, 16, 6} : Preset{3, 2, 4};
+}
+
+void validate_preset(const Preset& p) {
+  // FlowPreset::validate  include/evsim/flow.hpp:50-54
+  if (p.levels < 1 || p.iters < 1 || p.radius < 1) invalid("FlowPreset: all fields must be >= 1");
+  if (p.levels > kMaxLevels) invalid("FlowPreset: pyramid_levels above 8 are not supported");
+}
+
+void validate_config(const evsim_gpu_config& c) {
+  // SimulatorConfig::validate  include/evsim/types.hpp:126-130
+  if (c.c_pos <= 0) invalid("SimulatorConfig: c_pos must be > 0");
+  if (c.c_neg >= 0) invalid("SimulatorConfig: c_neg must be < 0");
+  if (c.n_interp < 0) invalid("SimulatorConfig: n_interp must be >= 0");
+  if (c.contrast_mode != EVSIM_CONTRAST_LINEAR && c.contrast_mode != EVSIM_CONTRAST_LOG)
+    invalid("SimulatorConfig: unknown contrast_mode");
+  if (c.contrast_mode == EVSIM_CONTRAST_LOG) {
+    if (!(c.c_pos_log > 0.0f)) invalid("SimulatorConfig: c_pos_log must be > 0");
+    if (!(c.c_neg_log < 0.0f)) invalid("SimulatorConfig: c_neg_log must be < 0");
+    if (c.events_per_crossing == EVSIM_EVENTS_MAGNITUDE) {
+      // per-(pixel, link) counts are stored as u16: floor(|dL| / C) must fit
+      const double span = std::log(1.0 + 1e-3) - std::log(1e-3);
+      if (span / std::min<double>(c.c_pos_log, -c.c_neg_log) > 65535.0)
+        invalid("SimulatorConfig: log contrast threshold too small for magnitude mode");
+    }
+  }
+  if (c.method < EVSIM_METHOD_DIFFERENCE_ONLY || c.method > EVSIM_METHOD_DIFFERENCE_INTERP)
+    invalid("SimulatorConfig: unknown method");
+}
+
+void log_lut(float* lut) {
+  // L[i] = logf(i / 255 + 1e-3), evaluated once on the host so
+  // every consumer (device kernels, CPU oracle) sees the same 256 floats.
+  for (int i = 0; i < 256; ++i) lut[i] = std::log(static_cast<float>(i) / 255.0f + 1e-3f);
+}
+
+int64_t sub_interval_end(int64_t t0, int64_t t1, int k, int n) {
+  // include/evsim/simulate.hpp:15-19
+  const int64_t dt = t1 - t0;
+  return t0 + (static_cast<int64_t>(k) * dt + n - 1) / n;
+}
+
+// ------------------------------------------------------------------ memory
+
+void init_pool(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  void ensure(size_t bytes, cudaStream_t st, bool zero = false) {
+    if (bytes <= n && p) return;
+    release();
+    s = st;
+    const size_t b = std::max<size_t>(bytes, 16);
+    CK(cudaMallocAsync(&p, b, st));
+    n = b;
+    if (zero) CK(cudaMemsetAsync(p, 0, b, st));
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// ------------------------------------------------------------------ geometry
+
+int effective_levels(int requested, int w, int h) {
+  // flow.cpp:75-79 (kMinPyramidExtent = 8)
+  int levels = std::max(1, requested);
+  while (levels > 1 && (std::min(w, h) >> (levels - 1)) < 8) --levels;
+  return levels;
+}
+
+std::vector<int> patch_centers(int extent, int radius, int stride) {
+  // flow.cpp:97-107
+  std::vector<int> c;
+  if (extent <= 2 * radius + 1) {
+    c.push_back((extent - 1) / 2);
+    return c;
+  }
+  const int last = extent - 1 - radius;
+  for (int v = radius; v <= last; v += stride) c.push_back(v);
+  if (c.back() != last) c.push_back(last);
+  return c;
+}
+
+void interp_table(const std::vector<int>& centers, int extent, std::vector<int>& idx, std::vector<float>& wgt) {
+  // flow.cpp:111-128
+  idx.assign(extent, 0);
+  wgt.assign(extent, 0.0f);
+  if (centers.size() < 2) return;
+  int j = 0;
+  for (int x = 0; x < extent; ++x) {
+    if (x <= centers.front()) continue;
+    if (x >= centers.back()) {
+      idx[x] = static_cast<int>(centers.size()) - 2;
+      wgt[x] = 1.0f;
+      continue;
+    }
+    while (j + 2 < static_cast<int>(centers.size()) && centers[j + 1] <= x) ++j;
+    idx[x] = j;
+    wgt[x] = static_cast<float>(x - centers[j]) / static_cast<float>(centers[j + 1] - centers[j]);
+  }
+}
+
+// Device-resident flow machinery for one resolution + preset: pyramids of
+// two frame slots, per-level patch grids and their static tables.
+struct FlowEngine {
+  int w = 0, h = 0;
+  Preset preset{};
+  int levels = 0;
+  LevelDims dims[kMaxLevels]{};
+  DevBuf pyr[2][kMaxLevels];  // fp32 level images, slot 0/1
+  DevBuf tables[kMaxLevels];  // cx | cy | ix | wx | iy | wy
+  DevBuf grid[kMaxLevels];    // pu | pv
+  GridGeom geom[kMaxLevels]{};
+
+  void setup(int w_, int h_, Preset p, cudaStream_t s) {
+    if (w_ == w && h_ == h && p.levels == preset.levels && p.iters == preset.iters && p.radius == preset.radius)
+      return;
+    w = w_;
+    h = h_;
+    preset = p;
+    levels = effective_levels(p.levels, w, h);
+    dims[0] = {w, h};
+    for (int l = 1; l < levels; ++l) dims[l] = {(dims[l - 1].w + 1) / 2, (dims[l - 1].h + 1) / 2};
+    const int r = p.radius, stride = std::max(1, r);
+    for (int l = 0; l < levels; ++l) {
+      const int lw = dims[l].w, lh = dims[l].h;
+      for (int sl = 0; sl < 2; ++sl) pyr[sl][l].ensure((size_t)lw * lh * sizeof(float), s);
+      const auto cxs = patch_centers(lw, r, stride), cys = patch_centers(lh, r, stride);
+      std::vector<int> ix, iy;
+      std::vector<float> wx, wy;
+      interp_table(cxs, lw, ix, wx);
+      interp_table(cys, lh, iy, wy);
+      const size_t ncx = cxs.size(), ncy = cys.size();
+      std::vector<char> host((ncx + ncy + 2 * (size_t)lw + 2 * (size_t)lh) * 4);
+      char* q = host.data();
+      auto put = [&](const void* src, size_t bytes) {
+        std::memcpy(q, src, bytes);
+        q += bytes;
+      };
+      put(cxs.data(), ncx * 4);
+      put(cys.data(), ncy * 4);
+      put(ix.data(), (size_t)lw * 4);
+      put(wx.data(), (size_t)lw * 4);
+      put(iy.data(), (size_t)lh * 4);
+      put(wy.data(), (size_t)lh * 4);
+      tables[l].ensure(host.size(), s);
+      CK(cudaMemcpyAsync(tables[l].p, host.data(), host.size(), cudaMemcpyHostToDevice, s));
+      CK(cudaStreamSynchronize(s));  // host vector goes out of scope
+      grid[l].ensure(2 * ncx * ncy * sizeof(float), s);
+      GridGeom& g = geom[l];
+      g.w = lw;
+      g.h = lh;
+      g.ncx = (int)ncx;
+      g.ncy = (int)ncy;
+      const int* base = tables[l].as<int>();
+      g.cx = base;
+      g.cy = base + ncx;
+      g.ix = base + ncx + ncy;
+      g.wx = reinterpret_cast<const float*>(base + ncx + ncy + lw);
+      g.iy = base + ncx + ncy + 2 * lw;
+      g.wy = reinterpret_cast<const float*>(base + ncx + ncy + 2 * lw + lh);
+      g.pu = grid[l].as<float>();
+      g.pv = grid[l].as<float>() + ncx * ncy;
+    }
+  }
+
+  // build_pyramid  flow.cpp:81-87
+  int build_pyramid(const uint8_t* frame, int slot, cudaStream_t s) {
+    launch_to_float(frame, pyr[slot][0].as<float>(), (int64_t)w * h, s);
+    for (int l = 1; l < levels; ++l)
+      launch_downsample(pyr[slot][l - 1].as<float>(), dims[l - 1], pyr[slot][l].as<float>(), dims[l], s);
+    CK_LAUNCH("pyramid");
+    return levels;
+  }
+
+  // estimate_dense_flow's level loop, flow.cpp:268-275; result = level-0 grid
+  int solve(int prev_slot, int curr_slot, cudaStream_t s) {
+    for (int l = levels - 1; l >= 0; --l) {
+      DenseLKParams p{};
+      p.g = geom[l];
+      p.has_coarse = l != levels - 1;
+      if (p.has_coarse) p.coarse = geom[l + 1];
+      p.prev = pyr[prev_slot][l].as<float>();
+      p.curr = pyr[curr_slot][l].as<float>();
+      p.radius = preset.radius;
+      p.iterations = preset.iters;
+      launch_dense_lk(p, s);
+    }
+    CK_LAUNCH("dense_lk");
+    return levels;
+  }
+
+  SparseLKParams sparse_params(int prev_slot, int curr_slot) const {
+    SparseLKParams p{};
+    p.levels = levels;
+    for (int l = 0; l < levels; ++l) {
+      p.dims[l] = dims[l];
+      p.prev[l] = pyr[prev_slot][l].as<float>();
+      p.curr[l] = pyr[curr_slot][l].as<float>();
+    }
+    p.w0 = w;
+    p.h0 = h;
+    p.radius = preset.radius;
+    p.iterations = preset.iters;
+    return p;
+  }
+};
+
+// Chain/scan/emit buffers for one resolution and chain length.
+struct EventEngine {
+  int w = 0, h = 0, wpr = 0;
+  int64_t n_words = 0;
+  int wpb = 0, n_blocks = 0;
+  int max_links = 0;
+  bool magnitude = false;
+  DevBuf masks, counts, offsets, segtab, seg_out, total, events, mcount, wcount;
+  int64_t capacity = 0;
+
+  void setup(int w_, int h_, int links, bool mag, cudaStream_t s) {
+    const bool geom_change = w_ != w || h_ != h;
+    w = w_;
+    h = h_;
+    wpr = (w + 31) / 32;
+    n_words = (int64_t)h * wpr;
+    // ~8 resident blocks of 256 threads on each of the 148 SMs
+    const int64_t target = 148 * 8;
+    int64_t per = (n_words + target - 1) / target;
+    per = std::max<int64_t>(kWarpsPerBlock, (per + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock);
+    wpb = (int)per;
+    n_blocks = (int)((n_words + wpb - 1) / wpb);
+    if (geom_change || links > max_links || mag != magnitude) {
+      max_links = std::max(links, 1);
+      magnitude = mag;
+      masks.ensure((size_t)max_links * n_words * sizeof(uint2), s);
+      counts.ensure((size_t)max_links * n_blocks * sizeof(uint32_t), s);
+      offsets.ensure((size_t)max_links * n_blocks * sizeof(int64_t), s);
+      segtab.ensure(8 + (size_t)max_links * (2 * sizeof(int) + sizeof(int64_t)), s);
+      seg_out.ensure((3 + 2 * (size_t)max_links) * sizeof(int64_t), s);
+      total.ensure(sizeof(int64_t), s);
+      const int64_t P = (int64_t)w * h;
+      if (mag) {
+        mcount.ensure((size_t)max_links * n_words * 32 * sizeof(uint16_t), s);
+        wcount.ensure((size_t)max_links * n_words * sizeof(uint32_t), s);
+      }
+      grow((int64_t)max_links * P, s);
+    }
+  }
+
+  void grow(int64_t cap, cudaStream_t s) {
+    if (cap <= capacity) return;
+    events.ensure((size_t)std::max<int64_t>(cap, 1) * sizeof(uint32_t), s);
+    capacity = cap;
+  }
+
+  SegTable seg() const {
+    SegTable t;
+    char* b = static_cast<char*>(segtab.p);
+    t.n_segs = reinterpret_cast<int*>(b);
+    t.seg_t = reinterpret_cast<int64_t*>(b + 8);
+    t.seg_first = reinterpret_cast<int*>(b + 8 + (size_t)max_links * 8);
+    t.seg_nlinks = reinterpret_cast<int*>(b + 8 + (size_t)max_links * 12);
+    return t;
+  }
+};
+
+}  // namespace
+
+// ====================================================================== handle
+
+struct evsim_gpu_sim {
+  evsim_gpu_config cfg{};
+  Preset preset{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+
+  // stream state
+  bool has_prev = false;
+  int w = 0, h = 0;
+  int64_t prev_t = 0;
+  int slot = 0;  // frame slot holding prev
+
+  DevBuf frames[2], quads[2], lut, ref, consts;
+  FlowEngine flow;
+  EventEngine ev;
+  // sparse
+  DevBuf sel_masks, sel_counts, sel_offsets, sel_segtab, sel_total, sel_seg_out, points, n_points, disp, status,
+      claims, touched;
+
+  // last result
+  int64_t* h_seg_out = nullptr;  // pinned
+  size_t h_seg_cap = 0;
+  std::vector<int64_t> seg_t, seg_off;
+  int64_t n_events = 0;
+  bool pending = false;
+  bool last_magnitude = false;
+  ChainParams last_chain{};
+  ScanParams last_scan{};
+  EmitParams last_emit{};
+  int last_provider = 0;
+
+  // per-stage CUDA-event timing (evsim_gpu_set_profiling)
+  using EvGroup = std::array<cudaEvent_t, EVSIM_N_STAGES + 1>;
+  bool profiling = false;
+  std::vector<EvGroup> ev_pool, ev_pending;
+  EvGroup* cur_group = nullptr;
+  int next_mark = 0;
+  double stage_ms[EVSIM_N_STAGES] = {};
+  int64_t timed_pushes = 0;
+
+  ~evsim_gpu_sim() {
+    if (stream) cudaStreamSynchronize(stream);
+    if (h_seg_out) cudaFreeHost(h_seg_out);
+    for (auto& g : ev_pool)
+      for (auto e : g) cudaEventDestroy(e);
+    for (auto& g : ev_pending)
+      for (auto e : g) cudaEventDestroy(e);
+  }
+
+  void begin_group() {
+    if (!profiling) return;
+    EvGroup g;
+    if (!ev_pool.empty()) {
+      g = ev_pool.back();
+      ev_pool.pop_back();
+    } else {
+      for (auto& e : g) CK(cudaEventCreate(&e));
+    }
+    ev_pending.push_back(g);
+    cur_group = &ev_pending.back();
+    next_mark = 0;
+  }
+  // record stage boundary i (and any skipped ones) at the current stream position
+  void mark(int i) {
+    if (!cur_group) return;
+    for (; next_mark <= i; ++next_mark) CK(cudaEventRecord((*cur_group)[next_mark], stream));
+  }
+  void end_group() {
+    if (!cur_group) return;
+    mark(EVSIM_N_STAGES);
+    cur_group = nullptr;
+  }
+  void collect() {
+    for (auto& g : ev_pending) {
+      CK(cudaEventSynchronize(g[EVSIM_N_STAGES]));
+      for (int i = 0; i < EVSIM_N_STAGES; ++i) {
+        float ms = 0.0f;
+        CK(cudaEventElapsedTime(&ms, g[i], g[i + 1]));
+        stage_ms[i] += ms;
+      }
+      ++timed_pushes;
+      ev_pool.push_back(g);
+    }
+    ev_pending.clear();
+  }
+
+  bool uses_flow() const {
+    return (cfg.method == EVSIM_METHOD_DENSE || cfg.method == EVSIM_METHOD_SPARSE) && cfg.n_interp > 0;
+  }
+  int n_interp_eff() const { return cfg.method == EVSIM_METHOD_DIFFERENCE_ONLY ? 0 : cfg.n_interp; }
+  bool log_mode() const { return cfg.contrast_mode == EVSIM_CONTRAST_LOG; }
+  bool magnitude() const { return cfg.events_per_crossing == EVSIM_EVENTS_MAGNITUDE; }
+
+  void allocate(int w_, int h_) {
+    w = w_;
+    h = h_;
+    const size_t P = (size_t)w * h;
+    for (int i = 0; i < 2; ++i) frames[i].ensure(P + 16, stream);
+    const int N = n_interp_eff();
+    if (cfg.method == EVSIM_METHOD_DENSE && N > 0)
+      for (int i = 0; i < 2; ++i) quads[i].ensure(P * 4, stream);
+    if (uses_flow()) flow.setup(w, h, preset, stream);
+    if (log_mode()) ref.ensure(P * sizeof(float), stream);
+    const bool incl = cfg.method == EVSIM_METHOD_DIFFERENCE_ONLY || cfg.include_endpoints;
+    const int links = std::max(1, incl ? N + 1 : N - 1);
+    ev.setup(w, h, links, magnitude(), stream);
+    if (cfg.method == EVSIM_METHOD_SPARSE && N > 0) {
+      sel_masks.ensure((size_t)ev.n_words * 4, stream);
+      sel_counts.ensure((size_t)ev.n_blocks * 4, stream);
+      sel_offsets.ensure((size_t)ev.n_blocks * 8, stream);
+      sel_segtab.ensure(64, stream);
+      sel_total.ensure(8, stream);
+      sel_seg_out.ensure(64, stream);
+      points.ensure(P * 4, stream);
+      n_points.ensure(8, stream, true);
+      disp.ensure(P * sizeof(float2), stream);
+      status.ensure(P, stream);
+      claims.ensure((size_t)N * P * 8, stream, true);
+      touched.ensure((size_t)((N + 31) / 32) * P * 4, stream, true);
+    }
+    const size_t seg_need = (3 + 2 * (size_t)ev.max_links) * sizeof(int64_t);
+    if (seg_need > h_seg_cap) {
+      if (h_seg_out) cudaFreeHost(h_seg_out);
+      CK(cudaHostAlloc((void**)&h_seg_out, seg_need, cudaHostAllocDefault));
+      h_seg_cap = seg_need;
+    }
+    // interpolation constants, interpolate_frames simulate.cpp:97-100
+    const int K = N + 2;
+    std::vector<char> host((size_t)K * (8 + 8 + 4 + 4));
+    double* alpha = reinterpret_cast<double*>(host.data());
+    double* oma = alpha + K;
+    float* fwd = reinterpret_cast<float*>(oma + K);
+    float* bwd = fwd + K;
+    for (int k = 0; k < K; ++k) {
+      const double a = static_cast<double>(k) / static_cast<double>(N + 1);
+      alpha[k] = a;
+      oma[k] = 1.0 - a;
+      fwd[k] = static_cast<float>(a);
+      bwd[k] = static_cast<float>(1.0 - a);
+    }
+    consts.ensure(host.size(), stream);
+    CK(cudaMemcpyAsync(consts.p, host.data(), host.size(), cudaMemcpyHostToDevice, stream));
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  ChainDesc full_desc() const {
+    const int N = n_interp_eff();
+    if (cfg.method == EVSIM_METHOD_DIFFERENCE_ONLY) return ChainDesc{0, 1, 1};
+    if (N == 0) return direct_desc();
+    // chain_pipeline, simulate.cpp:57-69
+    if (cfg.include_endpoints) return ChainDesc{0, 1, N + 1};
+    return ChainDesc{1, 1, std::max(0, N - 1)};
+  }
+  ChainDesc direct_desc() const {
+    // chain_pipeline(prev, curr, {}): [prev, curr] or nothing
+    const int N = n_interp_eff();
+    return ChainDesc{0, N + 1, cfg.include_endpoints ? 1 : 0};
+  }
+
+  void fill_chain(ChainParams& c, const uint8_t* prev_f, const uint8_t* curr_f) {
+    const int N = n_interp_eff();
+    c.w = w;
+    c.h = h;
+    c.wpr = ev.wpr;
+    c.n_words = ev.n_words;
+    c.words_per_block = ev.wpb;
+    c.n_blocks = ev.n_blocks;
+    c.n_interp = N;
+    c.prev = prev_f;
+    c.curr = curr_f;
+    const int K = N + 2;
+    c.alpha = consts.as<double>();
+    c.oma = consts.as<double>() + K;
+    c.fwd = reinterpret_cast<const float*>(consts.as<double>() + 2 * K);
+    c.bwd = c.fwd + K;
+    c.full = full_desc();
+    c.direct = direct_desc();
+    c.log_mode = log_mode();
+    c.magnitude = magnitude();
+    c.c_pos = cfg.c_pos;
+    c.c_neg = cfg.c_neg;
+    c.c_pos_log = cfg.c_pos_log;
+    c.c_neg_log = cfg.c_neg_log;
+    c.lut = lut.as<float>();
+    c.ref = ref.as<float>();
+    c.masks = ev.masks.as<uint2>();
+    c.mcount = ev.mcount.as<uint16_t>();
+    c.wcount = ev.wcount.as<uint32_t>();
+    c.counts = ev.counts.as<uint32_t>();
+  }
+
+  // chain -> scan -> emit for the chain described by `c`, then queue the
+  // segment table readback.
+  void run_events(ChainParams& c, int provider, int64_t t_prev, int64_t t_curr) {
+    launch_chain(c, provider, stream);
+    CK_LAUNCH("chain");
+    mark(EVSIM_STAGE_SCAN);
+    ScanParams sp{};
+    sp.n_blocks = ev.n_blocks;
+    sp.counts = ev.counts.as<uint32_t>();
+    sp.d_direct = c.d_direct;
+    sp.full = c.full;
+    sp.direct = c.direct;
+    sp.n_interp = c.n_interp;
+    sp.t_prev = t_prev;
+    sp.t_curr = t_curr;
+    sp.seg = ev.seg();
+    sp.offsets = ev.offsets.as<int64_t>();
+    sp.seg_out = ev.seg_out.as<int64_t>();
+    sp.total = ev.total.as<int64_t>();
+    launch_scan(sp, stream);
+    CK_LAUNCH("scan");
+    mark(EVSIM_STAGE_EMIT);
+    EmitParams ep{};
+    ep.w = w;
+    ep.h = h;
+    ep.wpr = ev.wpr;
+    ep.n_words = ev.n_words;
+    ep.words_per_block = ev.wpb;
+    ep.n_blocks = ev.n_blocks;
+    ep.d_direct = c.d_direct;
+    ep.full = c.full;
+    ep.direct = c.direct;
+    ep.seg = ev.seg();
+    ep.magnitude = c.magnitude;
+    ep.masks = ev.masks.as<uint2>();
+    ep.mcount = ev.mcount.as<uint16_t>();
+    ep.wcount = ev.wcount.as<uint32_t>();
+    ep.offsets = ev.offsets.as<int64_t>();
+    ep.total = ev.total.as<int64_t>();
+    ep.capacity = ev.capacity;
+    ep.out = ev.events.as<uint32_t>();
+    launch_emit(ep, stream);
+    CK_LAUNCH("emit");
+    launches += 3;
+    CK(cudaMemcpyAsync(h_seg_out, ev.seg_out.p, (3 + 2 * (size_t)ev.max_links) * sizeof(int64_t),
+                       cudaMemcpyDeviceToHost, stream));
+    last_chain = c;
+    last_scan = sp;
+    last_emit = ep;
+    last_provider = provider;
+    pending = true;
+  }
+
+  void upload(const uint8_t* pixels, int dst_slot, bool on_device) {
+    CK(cudaMemcpyAsync(frames[dst_slot].p, pixels, (size_t)w * h,
+                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream));
+  }
+
+  // Simulator::push_frame  src/simulate.cpp:306-347
+  void push(const uint8_t* pixels, int fw, int fh, int64_t t, bool on_device) {
+    if (fw <= 0 || fh <= 0 || !pixels) invalid("push_frame: malformed frame");
+    if (has_prev) {
+      if (fw != w || fh != h) invalid("push_frame: frame dimensions changed mid-stream");
+      if (t <= prev_t) invalid("push_frame: timestamps must be strictly increasing");
+    }
+    if (fh > 32768 || fw > 65536) invalid("push_frame: frame larger than 65536 x 32768 is not supported");
+    if ((int64_t)fw * fh >= (int64_t)1 << 32) invalid("push_frame: frame too large");
+    CK(cudaSetDevice(device));
+    // A queued single-mode result is simply superseded (stream order keeps
+    // the device buffers consistent); magnitude mode may need a re-emit, so
+    // it is completed first.
+    if (pending) {
+      if (magnitude()) finish();
+      else pending = false;
+    }
+    if (!has_prev && (fw != w || fh != h)) allocate(fw, fh);
+
+    const int cur = has_prev ? 1 - slot : slot;
+    begin_group();
+    mark(EVSIM_STAGE_UPLOAD);
+    upload(pixels, cur, on_device);
+    mark(EVSIM_STAGE_PYRAMID);
+    const int N = n_interp_eff();
+    const bool dense_flow = cfg.method == EVSIM_METHOD_DENSE && N > 0;
+    const bool sparse_flow = cfg.method == EVSIM_METHOD_SPARSE && N > 0;
+    if (dense_flow) {
+      launch_build_quad(frames[cur].as<uint8_t>(), quads[cur].as<uint32_t>(), w, h, stream);
+      ++launches;
+    }
+    if (dense_flow || sparse_flow) launches += flow.build_pyramid(frames[cur].as<uint8_t>(), cur, stream);
+    mark(EVSIM_STAGE_FLOW);
+
+    if (!has_prev) {
+      // warm-up frame: no events, state := frame (simulate.cpp:341)
+      if (log_mode()) {
+        launch_init_ref(frames[cur].as<uint8_t>(), lut.as<float>(), ref.as<float>(), (int64_t)w * h, stream);
+        CK_LAUNCH("init_ref");
+        ++launches;
+      }
+      end_group();
+      has_prev = true;
+      slot = cur;
+      prev_t = t;
+      seg_t.clear();
+      seg_off.assign(1, 0);
+      n_events = 0;
+      pending = false;
+      return;
+    }
+
+    const uint8_t* pf = frames[slot].as<uint8_t>();
+    const uint8_t* cf = frames[cur].as<uint8_t>();
+    ChainParams c{};
+    fill_chain(c, pf, cf);
+    int provider = kProvNone;
+    if (dense_flow) {
+      // simulate_dense -> PyramidalPatchFlow -> dense_events_with_flow (simulate.cpp:130-143)
+      launches += flow.solve(slot, cur, stream);
+      c.g0 = flow.geom[0];
+      c.qprev = quads[slot].as<uint32_t>();
+      c.qcurr = quads[cur].as<uint32_t>();
+      provider = kProvDenseGrid;
+    } else if (sparse_flow) {
+      sparse_stage(pf, cf, c);
+      provider = kProvSparse;
+    }
+    mark(EVSIM_STAGE_CHAIN);
+    run_events(c, provider, prev_t, t);
+    end_group();
+    slot = cur;
+    prev_t = t;
+  }
+
+  // simulate_sparse up to the intermediates (simulate.cpp:145-199)
+  void sparse_stage(const uint8_t* pf, const uint8_t* cf, ChainParams& c) {
+    const int N = n_interp_eff();
+    SelectParams sp{};
+    sp.w = w;
+    sp.h = h;
+    sp.wpr = ev.wpr;
+    sp.n_words = ev.n_words;
+    sp.words_per_block = ev.wpb;
+    sp.n_blocks = ev.n_blocks;
+    sp.prev = pf;
+    sp.curr = cf;
+    sp.log_mode = log_mode();
+    sp.sel = cfg.selection_threshold > 0 ? cfg.selection_threshold : cfg.c_pos;  // types.hpp:122-124
+    sp.sel_log = cfg.sel_log > 0.0f ? cfg.sel_log : cfg.c_pos_log;
+    sp.lut = lut.as<float>();
+    sp.masks = sel_masks.as<uint32_t>();
+    sp.counts = sel_counts.as<uint32_t>();
+    sp.offsets = sel_offsets.as<int64_t>();
+    sp.points = points.as<uint32_t>();
+    sp.n_points = n_points.as<int>();
+    launch_select(sp, stream);
+    // one single-link segment over the block counts
+    ScanParams sc{};
+    sc.n_blocks = ev.n_blocks;
+    sc.counts = sel_counts.as<uint32_t>();
+    sc.full = ChainDesc{0, 1, 1};
+    sc.direct = sc.full;
+    sc.n_interp = 0;
+    sc.t_prev = 0;
+    sc.t_curr = 1;
+    char* b = sel_segtab.as<char>();
+    sc.seg = SegTable{reinterpret_cast<int*>(b), reinterpret_cast<int*>(b + 8), reinterpret_cast<int*>(b + 16),
+                      reinterpret_cast<int64_t*>(b + 24)};
+    sc.offsets = sel_offsets.as<int64_t>();
+    sc.seg_out = sel_seg_out.as<int64_t>();
+    sc.total = sel_total.as<int64_t>();
+    launch_scan(sc, stream);
+    launch_select_emit(sp, sel_total.as<int64_t>(), stream);
+    CK_LAUNCH("select");
+    // estimate_sparse_flow (flow.cpp:278-381)
+    SparseLKParams lk = flow.sparse_params(slot, 1 - slot);
+    lk.points = points.as<uint32_t>();
+    lk.n_points = n_points.as<int>();
+    lk.disp = disp.as<float2>();
+    lk.status = status.as<uint8_t>();
+    launch_sparse_lk(lk, w * h, stream);
+    CK_LAUNCH("sparse_lk");
+    SplatParams spl{};
+    spl.w = w;
+    spl.h = h;
+    spl.n_interp = N;
+    spl.points = points.as<uint32_t>();
+    spl.n_points = n_points.as<int>();
+    spl.disp = disp.as<float2>();
+    spl.status = status.as<uint8_t>();
+    spl.prev = pf;
+    spl.claims = claims.as<uint64_t>();
+    spl.touched = touched.as<uint32_t>();
+    const int64_t items = (int64_t)w * h * N;
+    launch_splat(spl, (int)std::min<int64_t>(items, INT32_MAX), stream);
+    CK_LAUNCH("splat");
+    launches += 6;
+    c.claims = claims.as<uint64_t>();
+    c.touched = touched.as<uint32_t>();
+    c.claims_rw = claims.as<uint64_t>();
+    c.touched_rw = touched.as<uint32_t>();
+    c.points = points.as<uint32_t>();
+    c.d_direct = n_points.as<int>();  // M == 0 -> chain_pipeline(prev, curr, {}) (simulate.cpp:161-163)
+  }
+
+  // Complete the queued push: wait, read the segment table, re-emit when the
+  // (magnitude-mode) event buffer was too small.
+  void finish() {
+    if (!pending) return;
+    pending = false;
+    CK(cudaStreamSynchronize(stream));
+    int S = (int)h_seg_out[0];
+    int64_t total = h_seg_out[1 + 2 * S];
+    if (total > ev.capacity) {
+      ev.grow(total + total / 4, stream);
+      last_emit.capacity = ev.capacity;
+      last_emit.out = ev.events.as<uint32_t>();
+      launch_emit(last_emit, stream);
+      CK_LAUNCH("emit");
+      ++launches;
+      CK(cudaStreamSynchronize(stream));
+    }
+    seg_t.assign(h_seg_out + 1, h_seg_out + 1 + S);
+    seg_off.assign(h_seg_out + 1 + S, h_seg_out + 2 + 2 * S);
+    n_events = total;
+  }
+
+  void fill_out(evsim_gpu_events* out) const {
+    if (!out) return;
+    out->width = w;
+    out->height = h;
+    out->n_events = n_events;
+    out->n_segments = (int32_t)seg_t.size();
+    out->seg_t = seg_t.data();
+    out->seg_offset = seg_off.data();
+    out->d_packed = ev.events.as<uint32_t>();
+  }
+};
+
+// ====================================================================== C-ABI
+
+extern "C" {
+
+const char* evsim_gpu_last_error(void) { return g_err.c_str(); }
+
+void evsim_gpu_config_defaults(int32_t method, evsim_gpu_config* out) {
+  // SimulatorConfig::defaults  include/evsim/types.hpp:101-120
+  evsim_gpu_config c{};
+  c.method = method;
+  c.c_pos = 2;
+  c.c_neg = -2;
+  c.n_interp = 0;
+  c.flow_preset = EVSIM_FLOW_LOW_QUALITY;
+  c.selection_threshold = 0;
+  c.events_per_crossing = EVSIM_EVENTS_SINGLE;
+  c.include_endpoints = 1;
+  c.contrast_mode = EVSIM_CONTRAST_LINEAR;
+  c.c_pos_log = 0.2f;
+  c.c_neg_log = -0.2f;
+  switch (method) {
+    case EVSIM_METHOD_DENSE: c.n_interp = 10; break;
+    case EVSIM_METHOD_SPARSE:
+      c.c_pos = 10, c.c_neg = -10, c.n_interp = 10, c.selection_threshold = 10;
+      break;
+    case EVSIM_METHOD_DIFFERENCE_INTERP: c.c_pos = 20, c.c_neg = -20, c.n_interp = 10; break;
+    default: break;
+  }
+  *out = c;
+}
+
+int evsim_gpu_config_validate(const evsim_gpu_config* cfg) {
+  return guarded([&] {
+    if (!cfg) invalid("config must not be null");
+    validate_config(*cfg);
+  });
+}
+
+int evsim_gpu_create(const evsim_gpu_config* cfg, int device, evsim_gpu_sim** out) {
+  return guarded([&] {
+    if (!cfg || !out) invalid("evsim_gpu_create: null argument");
+    validate_config(*cfg);
+    if (cfg->method == EVSIM_METHOD_DIFFERENCE_INTERP)
+      runtime("evsim_gpu_create: difference_interp is outside the B200 hot path (SURVEY.md §8f)");
+    const Preset preset = resolve_preset(*cfg);
+    validate_preset(preset);
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) invalid("evsim_gpu_create: no such CUDA device");
+    CK(cudaSetDevice(device));
+    init_pool(device);
+    auto s = std::make_unique<evsim_gpu_sim>();
+    s->cfg = *cfg;
+    s->preset = preset;
+    s->device = device;
+    CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    float h_lut[256];
+    log_lut(h_lut);
+    s->lut.ensure(sizeof h_lut, s->stream);
+    CK(cudaMemcpyAsync(s->lut.p, h_lut, sizeof h_lut, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    *out = s.release();
+  });
+}
+
+int evsim_gpu_push_frame(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t width, int32_t height, int64_t t_us,
+                         int32_t pixels_on_device, evsim_gpu_events* out) {
+  return guarded([&] {
+    if (!sim) invalid("evsim_gpu_push_frame: null simulator");
+    sim->push(pixels, width, height, t_us, pixels_on_device != 0);
+    sim->finish();
+    sim->fill_out(out);
+  });
+}
+
+int evsim_gpu_push_frame_async(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t width, int32_t height,
+                               int64_t t_us, int32_t pixels_on_device) {
+  return guarded([&] {
+    if (!sim) invalid("evsim_gpu_push_frame_async: null simulator");
+    sim->push(pixels, width, height, t_us, pixels_on_device != 0);
+  });
+}
+
+int evsim_gpu_sync(evsim_gpu_sim* sim, evsim_gpu_events* out) {
+  return guarded([&] {
+    if (!sim) invalid("evsim_gpu_sync: null simulator");
+    CK(cudaSetDevice(sim->device));
+    sim->finish();
+    CK(cudaStreamSynchronize(sim->stream));
+    sim->fill_out(out);
+  });
+}
+
+int evsim_gpu_copy_events(evsim_gpu_sim* sim, void* host_dst, int64_t capacity, int32_t format) {
+  return guarded([&] {
+    if (!sim) invalid("evsim_gpu_copy_events: null simulator");
+    CK(cudaSetDevice(sim->device));
+    sim->finish();
+    const int64_t n = sim->n_events;
+    if (capacity < n) invalid("evsim_gpu_copy_events: destination too small");
+    if (n == 0) return;
+    if (format == 0) {
+      CK(cudaMemcpyAsync(host_dst, sim->ev.events.p, (size_t)n * 4, cudaMemcpyDeviceToHost, sim->stream));
+    } else if (format == 1) {
+      DevBuf tmp;
+      tmp.ensure((size_t)n * 24, sim->stream);
+      launch_unpack_events(sim->ev.events.as<uint32_t>(), sim->ev.seg_out.as<int64_t>(), n, tmp.p, sim->stream);
+      CK_LAUNCH("unpack");
+      CK(cudaMemcpyAsync(host_dst, tmp.p, (size_t)n * 24, cudaMemcpyDeviceToHost, sim->stream));
+      CK(cudaStreamSynchronize(sim->stream));
+    } else {
+      invalid("evsim_gpu_copy_events: unknown format");
+    }
+    CK(cudaStreamSynchronize(sim->stream));
+  });
+}
+
+void* evsim_gpu_stream(evsim_gpu_sim* sim) { return sim ? (void*)sim->stream : nullptr; }
+
+int evsim_gpu_reset(evsim_gpu_sim* sim) {
+  return guarded([&] {
+    if (!sim) invalid("evsim_gpu_reset: null simulator");
+    CK(cudaSetDevice(sim->device));
+    sim->finish();
+    // Simulator::reset  include/evsim/simulate.hpp:83-86
+    sim->has_prev = false;
+    sim->n_events = 0;
+    sim->seg_t.clear();
+    sim->seg_off.assign(1, 0);
+  });
+}
+
+void evsim_gpu_destroy(evsim_gpu_sim* sim) {
+  if (!sim) return;
+  cudaSetDevice(sim->device);
+  cudaStreamSynchronize(sim->stream);
+  cudaStream_t s = sim->stream;
+  delete sim;  // DevBufs free on the stream (pool)
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+}
+
+int64_t evsim_gpu_kernel_launches(const evsim_gpu_sim* sim) { return sim ? sim->launches : 0; }
+
+int evsim_gpu_set_profiling(evsim_gpu_sim* sim, int32_t enable) {
+  return guarded([&] {
+    if (!sim) invalid("evsim_gpu_set_profiling: null simulator");
+    CK(cudaSetDevice(sim->device));
+    sim->collect();
+    sim->profiling = enable != 0;
+    for (double& v : sim->stage_ms) v = 0.0;
+    sim->timed_pushes = 0;
+  });
+}
+
+int evsim_gpu_stage_times(evsim_gpu_sim* sim, double* ms, int32_t n_stages, int64_t* n_pushes) {
+  return guarded([&] {
+    if (!sim) invalid("evsim_gpu_stage_times: null simulator");
+    CK(cudaSetDevice(sim->device));
+    sim->collect();
+    for (int i = 0; i < n_stages && i < EVSIM_N_STAGES; ++i) ms[i] = sim->stage_ms[i];
+    if (n_pushes) *n_pushes = sim->timed_pushes;
+  });
+}
+
+// ------------------------------------------------------------ stateless entry points
+
+namespace {
+
+// Scratch simulator for the free functions: dense or sparse pipeline on an
+// explicit (prev, curr) pair.
+std::unique_ptr<evsim_gpu_sim> scratch(const evsim_gpu_config& cfg, int w, int h) {
+  CK(cudaSetDevice(0));
+  init_pool(0);
+  auto s = std::make_unique<evsim_gpu_sim>();
+  s->cfg = cfg;
+  s->preset = resolve_preset(cfg);
+  s->device = 0;
+  CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  float h_lut[256];
+  log_lut(h_lut);
+  s->lut.ensure(sizeof h_lut, s->stream);
+  CK(cudaMemcpyAsync(s->lut.p, h_lut, sizeof h_lut, cudaMemcpyHostToDevice, s->stream));
+  s->allocate(w, h);
+  return s;
+}
+
+struct ScratchGuard {
+  std::unique_ptr<evsim_gpu_sim> s;
+  ~ScratchGuard() {
+    if (s) {
+      cudaStream_t st = s->stream;
+      cudaStreamSynchronize(st);
+      s.reset();
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
+  }
+};
+
+void check_frames(const uint8_t* a, const uint8_t* b, int w, int h, const char* who) {
+  if (!a || !b || w <= 0 || h <= 0) invalid(std::string(who) + ": empty frame");
+}
+
+void copy_events24(evsim_gpu_sim* s, evsim_event* events, int64_t capacity, int64_t* n_events) {
+  *n_events = s->n_events;
+  if (!events || capacity <= 0 || s->n_events == 0) return;
+  if (capacity < s->n_events) invalid("events: destination too small");
+  DevBuf tmp;
+  tmp.ensure((size_t)s->n_events * 24, s->stream);
+  launch_unpack_events(s->ev.events.as<uint32_t>(), s->ev.seg_out.as<int64_t>(), s->n_events, tmp.p, s->stream);
+  CK_LAUNCH("unpack");
+  CK(cudaMemcpyAsync(events, tmp.p, (size_t)s->n_events * 24, cudaMemcpyDeviceToHost, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+}
+
+}  // namespace
+
+int evsim_gpu_dense_flow(const uint8_t* prev, const uint8_t* curr, int32_t w, int32_t h, int32_t levels,
+                         int32_t iterations, int32_t radius, float* du, float* dv) {
+  return guarded([&] {
+    validate_preset(Preset{levels, iterations, radius});
+    check_frames(prev, curr, w, h, "estimate_dense_flow");
+    evsim_gpu_config cfg;
+    evsim_gpu_config_defaults(EVSIM_METHOD_DENSE, &cfg);
+    cfg.pyramid_levels = levels;
+    cfg.iterations_per_level = iterations;
+    cfg.patch_radius = radius;
+    ScratchGuard g{scratch(cfg, w, h)};
+    evsim_gpu_sim* s = g.s.get();
+    CK(cudaMemcpyAsync(s->frames[0].p, prev, (size_t)w * h, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->frames[1].p, curr, (size_t)w * h, cudaMemcpyHostToDevice, s->stream));
+    s->flow.build_pyramid(s->frames[0].as<uint8_t>(), 0, s->stream);
+    s->flow.build_pyramid(s->frames[1].as<uint8_t>(), 1, s->stream);
+    s->flow.solve(0, 1, s->stream);
+    DevBuf field;
+    field.ensure((size_t)w * h * 8, s->stream);
+    launch_densify(s->flow.geom[0], field.as<float>(), field.as<float>() + (size_t)w * h, s->stream);
+    CK_LAUNCH("densify");
+    CK(cudaMemcpyAsync(du, field.p, (size_t)w * h * 4, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(dv, field.as<float>() + (size_t)w * h, (size_t)w * h * 4, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int evsim_gpu_sparse_flow(const uint8_t* prev, const uint8_t* curr, int32_t w, int32_t h, int32_t levels,
+                          int32_t iterations, int32_t radius, const int32_t* pts, int64_t n_points, float* disp,
+                          uint8_t* status) {
+  return guarded([&] {
+    validate_preset(Preset{levels, iterations, radius});
+    check_frames(prev, curr, w, h, "estimate_sparse_flow");
+    std::vector<uint32_t> idx((size_t)std::max<int64_t>(n_points, 1));
+    for (int64_t i = 0; i < n_points; ++i) {
+      const int x = pts[2 * i], y = pts[2 * i + 1];
+      if (x < 0 || x >= w || y < 0 || y >= h) invalid("estimate_sparse_flow: point outside frame bounds");
+      idx[i] = (uint32_t)y * (uint32_t)w + (uint32_t)x;
+    }
+    for (int64_t i = 0; i < n_points; ++i) {
+      disp[2 * i] = disp[2 * i + 1] = 0.0f;
+      status[i] = 0;
+    }
+    if (n_points == 0) return;
+    evsim_gpu_config cfg;
+    evsim_gpu_config_defaults(EVSIM_METHOD_SPARSE, &cfg);
+    cfg.pyramid_levels = levels;
+    cfg.iterations_per_level = iterations;
+    cfg.patch_radius = radius;
+    ScratchGuard g{scratch(cfg, w, h)};
+    evsim_gpu_sim* s = g.s.get();
+    CK(cudaMemcpyAsync(s->frames[0].p, prev, (size_t)w * h, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->frames[1].p, curr, (size_t)w * h, cudaMemcpyHostToDevice, s->stream));
+    s->flow.build_pyramid(s->frames[0].as<uint8_t>(), 0, s->stream);
+    s->flow.build_pyramid(s->frames[1].as<uint8_t>(), 1, s->stream);
+    DevBuf dpts, ddisp, dst;
+    dpts.ensure((size_t)n_points * 4, s->stream);
+    ddisp.ensure((size_t)n_points * 8, s->stream);
+    dst.ensure((size_t)n_points, s->stream);
+    CK(cudaMemcpyAsync(dpts.p, idx.data(), (size_t)n_points * 4, cudaMemcpyHostToDevice, s->stream));
+    SparseLKParams lk = s->flow.sparse_params(0, 1);
+    lk.points = dpts.as<uint32_t>();
+    lk.n_points = nullptr;
+    lk.n_points_host = n_points;
+    lk.disp = ddisp.as<float2>();
+    lk.status = dst.as<uint8_t>();
+    launch_sparse_lk(lk, (int)std::min<int64_t>(n_points, INT32_MAX), s->stream);
+    CK_LAUNCH("sparse_lk");
+    CK(cudaMemcpyAsync(disp, ddisp.p, (size_t)n_points * 8, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaMemcpyAsync(status, dst.p, (size_t)n_points, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int evsim_gpu_interpolate_frames(const uint8_t* prev, const uint8_t* curr, int32_t w, int32_t h, int64_t t_prev,
+                                 int64_t t_curr, const float* du, const float* dv, int32_t n, uint8_t* out,
+                                 int64_t* out_t) {
+  return guarded([&] {
+    check_frames(prev, curr, w, h, "interpolate_frames");
+    if (n < 0) invalid("interpolate_frames: n must be >= 0");  // simulate.cpp:97
+    for (int k = 1; k <= n; ++k) out_t[k - 1] = sub_interval_end(t_prev, t_curr, k, n + 1);
+    if (n == 0) return;
+    evsim_gpu_config cfg;
+    evsim_gpu_config_defaults(EVSIM_METHOD_DENSE, &cfg);
+    cfg.n_interp = n;
+    ScratchGuard g{scratch(cfg, w, h)};
+    evsim_gpu_sim* s = g.s.get();
+    const size_t P = (size_t)w * h;
+    CK(cudaMemcpyAsync(s->frames[0].p, prev, P, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->frames[1].p, curr, P, cudaMemcpyHostToDevice, s->stream));
+    launch_build_quad(s->frames[0].as<uint8_t>(), s->quads[0].as<uint32_t>(), w, h, s->stream);
+    launch_build_quad(s->frames[1].as<uint8_t>(), s->quads[1].as<uint32_t>(), w, h, s->stream);
+    DevBuf field, dout;
+    field.ensure(P * 8, s->stream);
+    dout.ensure(P * n, s->stream);
+    CK(cudaMemcpyAsync(field.p, du, P * 4, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(field.as<float>() + P, dv, P * 4, cudaMemcpyHostToDevice, s->stream));
+    ChainParams c{};
+    s->fill_chain(c, s->frames[0].as<uint8_t>(), s->frames[1].as<uint8_t>());
+    c.qprev = s->quads[0].as<uint32_t>();
+    c.qcurr = s->quads[1].as<uint32_t>();
+    c.du = field.as<float>();
+    c.dv = field.as<float>() + P;
+    launch_interp_frames(c, dout.as<uint8_t>(), s->stream);
+    CK_LAUNCH("interp_frames");
+    CK(cudaMemcpyAsync(out, dout.p, P * n, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int evsim_gpu_dense_events_with_flow(const uint8_t* prev, const uint8_t* curr, int32_t w, int32_t h, int64_t t_prev,
+                                     int64_t t_curr, const float* du, const float* dv, const evsim_gpu_config* cfg_in,
+                                     evsim_event* events, int64_t capacity, int64_t* n_events) {
+  return guarded([&] {
+    if (!cfg_in || !n_events) invalid("dense_events_with_flow: null argument");
+    validate_config(*cfg_in);  // dense_events_with_flow: config.validate() (simulate.cpp:124)
+    if (cfg_in->contrast_mode != EVSIM_CONTRAST_LINEAR)
+      invalid("events_with_flow: stateless entry points are linear-mode only");
+    check_frames(prev, curr, w, h, "dense_events_with_flow");
+    evsim_gpu_config cfg = *cfg_in;
+    cfg.method = EVSIM_METHOD_DENSE;
+    ScratchGuard g{scratch(cfg, w, h)};
+    evsim_gpu_sim* s = g.s.get();
+    const size_t P = (size_t)w * h;
+    CK(cudaMemcpyAsync(s->frames[0].p, prev, P, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->frames[1].p, curr, P, cudaMemcpyHostToDevice, s->stream));
+    ChainParams c{};
+    s->fill_chain(c, s->frames[0].as<uint8_t>(), s->frames[1].as<uint8_t>());
+    DevBuf field;
+    int provider = kProvNone;
+    if (cfg.n_interp > 0) {
+      s->quads[0].ensure(P * 4, s->stream);
+      s->quads[1].ensure(P * 4, s->stream);
+      launch_build_quad(s->frames[0].as<uint8_t>(), s->quads[0].as<uint32_t>(), w, h, s->stream);
+      launch_build_quad(s->frames[1].as<uint8_t>(), s->quads[1].as<uint32_t>(), w, h, s->stream);
+      field.ensure(P * 8, s->stream);
+      CK(cudaMemcpyAsync(field.p, du, P * 4, cudaMemcpyHostToDevice, s->stream));
+      CK(cudaMemcpyAsync(field.as<float>() + P, dv, P * 4, cudaMemcpyHostToDevice, s->stream));
+      c.qprev = s->quads[0].as<uint32_t>();
+      c.qcurr = s->quads[1].as<uint32_t>();
+      c.du = field.as<float>();
+      c.dv = field.as<float>() + P;
+      provider = kProvDenseField;
+    }
+    s->run_events(c, provider, t_prev, t_curr);
+    s->finish();
+    copy_events24(s, events, capacity, n_events);
+  });
+}
+
+int evsim_gpu_sparse_events_with_flow(const uint8_t* prev, const uint8_t* curr, int32_t w, int32_t h,
+                                      int64_t t_prev, int64_t t_curr, const int32_t* pts, int64_t n_points,
+                                      const float* disp, const uint8_t* st, const evsim_gpu_config* cfg_in,
+                                      evsim_event* events, int64_t capacity, int64_t* n_events) {
+  return guarded([&] {
+    if (!cfg_in || !n_events) invalid("sparse_events_with_flow: null argument");
+    validate_config(*cfg_in);
+    if (cfg_in->contrast_mode != EVSIM_CONTRAST_LINEAR)
+      invalid("events_with_flow: stateless entry points are linear-mode only");
+    check_frames(prev, curr, w, h, "simulate_sparse");
+    evsim_gpu_config cfg = *cfg_in;
+    cfg.method = EVSIM_METHOD_SPARSE;
+    ScratchGuard g{scratch(cfg, w, h)};
+    evsim_gpu_sim* s = g.s.get();
+    const size_t P = (size_t)w * h;
+    CK(cudaMemcpyAsync(s->frames[0].p, prev, P, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->frames[1].p, curr, P, cudaMemcpyHostToDevice, s->stream));
+    ChainParams c{};
+    s->fill_chain(c, s->frames[0].as<uint8_t>(), s->frames[1].as<uint8_t>());
+    int provider = kProvNone;
+    if (cfg.n_interp > 0 && n_points > 0) {
+      std::vector<uint32_t> idx((size_t)n_points);
+      for (int64_t i = 0; i < n_points; ++i) {
+        const int x = pts[2 * i], y = pts[2 * i + 1];
+        if (x < 0 || x >= w || y < 0 || y >= h) invalid("simulate_sparse: point outside frame bounds");
+        idx[i] = (uint32_t)y * (uint32_t)w + (uint32_t)x;
+      }
+      const int np = (int)n_points;
+      CK(cudaMemcpyAsync(s->points.p, idx.data(), (size_t)n_points * 4, cudaMemcpyHostToDevice, s->stream));
+      CK(cudaMemcpyAsync(s->n_points.p, &np, sizeof np, cudaMemcpyHostToDevice, s->stream));
+      CK(cudaMemcpyAsync(s->disp.p, disp, (size_t)n_points * 8, cudaMemcpyHostToDevice, s->stream));
+      CK(cudaMemcpyAsync(s->status.p, st, (size_t)n_points, cudaMemcpyHostToDevice, s->stream));
+      SplatParams spl{};
+      spl.w = w;
+      spl.h = h;
+      spl.n_interp = cfg.n_interp;
+      spl.points = s->points.as<uint32_t>();
+      spl.n_points = s->n_points.as<int>();
+      spl.disp = s->disp.as<float2>();
+      spl.status = s->status.as<uint8_t>();
+      spl.prev = s->frames[0].as<uint8_t>();
+      spl.claims = s->claims.as<uint64_t>();
+      spl.touched = s->touched.as<uint32_t>();
+      launch_splat(spl, (int)std::min<int64_t>(n_points * cfg.n_interp, INT32_MAX), s->stream);
+      CK_LAUNCH("splat");
+      c.claims = s->claims.as<uint64_t>();
+      c.touched = s->touched.as<uint32_t>();
+      c.claims_rw = s->claims.as<uint64_t>();
+      c.touched_rw = s->touched.as<uint32_t>();
+      c.points = s->points.as<uint32_t>();
+      c.d_direct = s->n_points.as<int>();
+      provider = kProvSparse;
+      CK(cudaStreamSynchronize(s->stream));  // host staging (np, idx) must outlive the copies
+    } else {
+      c.full = c.direct;
+    }
+    s->run_events(c, provider, t_prev, t_curr);
+    s->finish();
+    copy_events24(s, events, capacity, n_events);
+  });
+}
+
+}  // extern "C"

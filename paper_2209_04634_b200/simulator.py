@@ -1,0 +1,501 @@
+"""Host-side mirror of the reference `evsim` API over the B200 C-ABI.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(/root/reference/proj/include/evsim/{types,flow,simulate}.hpp), so code and
+tests written against the reference read the same here:
+
+* ``SimulatorConfig`` / ``SimulatorConfig.defaults``      types.hpp:88-131
+* ``Frame``, ``EventStream``, ``FlowField``, ``SparseFlow`` types.hpp:14-80, flow.hpp:9-41
+* ``FlowPreset`` / ``flow_preset``                          flow.hpp:45-59
+* ``estimate_dense_flow`` / ``estimate_sparse_flow``        flow.hpp:64-70
+* ``DenseFlowEstimator`` / ``SparseFlowEstimator`` plug-ins flow.hpp:74-110
+* ``interpolate_frames``, ``dense_events_with_flow``,
+  ``simulate_dense``, ``simulate_sparse``                   simulate.hpp:25-46
+* ``Simulator`` (push_frame / reset / config)               simulate.hpp:60-94
+
+Every compute call goes through libevsim_gpu.so (sm_100a kernels); there is
+no CPU path.  Invalid arguments raise ``InvalidArgument`` (a ValueError)
+carrying the reference's exact std::invalid_argument message.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .abi import (EVENT_DTYPE, CConfig, CEvents, ContrastMode, EventsPerCrossing, FlowQuality, Method,
+                  unpack_events)
+from ._lib import EvsimError, InvalidArgument
+
+_vp = ctypes.c_void_p
+
+
+def _ptr(a: np.ndarray) -> ctypes.c_void_p:
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+# --------------------------------------------------------------------------- types
+
+@dataclasses.dataclass
+class Frame:
+    """evsim::Frame (types.hpp:14-34): u8 row-major pixels + timestamp (us)."""
+
+    width: int
+    height: int
+    timestamp: int
+    pixels: np.ndarray
+
+    @classmethod
+    def make(cls, width: int, height: int, timestamp: int = 0, fill: int = 0) -> "Frame":
+        if width <= 0 or height <= 0:
+            raise InvalidArgument(1, "Frame: width and height must be positive")
+        return cls(width, height, timestamp, np.full((height, width), fill, np.uint8))
+
+    @classmethod
+    def from_array(cls, pixels: np.ndarray, timestamp: int) -> "Frame":
+        pixels = np.ascontiguousarray(pixels, dtype=np.uint8)
+        return cls(pixels.shape[1], pixels.shape[0], int(timestamp), pixels)
+
+
+@dataclasses.dataclass
+class EventStream:
+    """evsim::EventStream (types.hpp:72-80); events use evsim::Event's layout."""
+
+    width: int
+    height: int
+    events: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros(0, EVENT_DTYPE))
+
+    def append(self, other: "EventStream") -> None:
+        self.events = np.concatenate([self.events, other.events])
+
+    def __len__(self) -> int:
+        return len(self.events)
+
+
+@dataclasses.dataclass
+class FlowPreset:
+    """evsim::FlowPreset (flow.hpp:45-55)."""
+
+    pyramid_levels: int = 3
+    iterations_per_level: int = 2
+    patch_radius: int = 4
+
+    def validate(self) -> None:
+        if self.pyramid_levels < 1 or self.iterations_per_level < 1 or self.patch_radius < 1:
+            raise InvalidArgument(1, "FlowPreset: all fields must be >= 1")
+
+
+def flow_preset(q: FlowQuality) -> FlowPreset:
+    """flow.hpp:57-59."""
+    return FlowPreset(3, 2, 4) if FlowQuality(q) == FlowQuality.low_quality else FlowPreset(5, 16, 6)
+
+
+@dataclasses.dataclass
+class FlowField:
+    """evsim::FlowField (flow.hpp:9-23)."""
+
+    width: int
+    height: int
+    du: np.ndarray
+    dv: np.ndarray
+
+    @classmethod
+    def zeros(cls, width: int, height: int) -> "FlowField":
+        return cls(width, height, np.zeros((height, width), np.float32), np.zeros((height, width), np.float32))
+
+
+@dataclasses.dataclass
+class SparseFlow:
+    """evsim::SparseFlow (flow.hpp:37-41); points (M,2) int32 x,y."""
+
+    points: np.ndarray
+    displacements: np.ndarray  # (M, 2) float32 du, dv
+    status: np.ndarray         # (M,) uint8, 1 tracked / 0 lost
+
+
+@dataclasses.dataclass
+class SimulatorConfig:
+    """evsim::SimulatorConfig (types.hpp:88-131) + log-mode extension fields."""
+
+    method: Method = Method.difference_only
+    c_pos: int = 2
+    c_neg: int = -2
+    n_interp: int = 0
+    flow_preset: FlowQuality = FlowQuality.low_quality
+    selection_threshold: int = 0
+    events_per_crossing: EventsPerCrossing = EventsPerCrossing.single
+    include_endpoints: bool = True
+    contrast_mode: ContrastMode = ContrastMode.linear
+    c_pos_log: float = 0.2
+    c_neg_log: float = -0.2
+    sel_log: float = 0.0
+    preset_override: Optional[FlowPreset] = None
+
+    @classmethod
+    def defaults(cls, m: Method) -> "SimulatorConfig":
+        """SimulatorConfig::defaults (types.hpp:101-120)."""
+        m = Method(m)
+        c = cls(method=m)
+        if m == Method.dense:
+            c.c_pos, c.c_neg, c.n_interp = 2, -2, 10
+        elif m == Method.sparse:
+            c.c_pos, c.c_neg, c.n_interp, c.selection_threshold = 10, -10, 10, 10
+        elif m == Method.difference_interp:
+            c.c_pos, c.c_neg, c.n_interp = 20, -20, 10
+        return c
+
+    def effective_selection_threshold(self) -> int:
+        return self.selection_threshold if self.selection_threshold > 0 else self.c_pos
+
+    def to_c(self) -> CConfig:
+        c = CConfig()
+        c.method = int(self.method)
+        c.c_pos = int(self.c_pos)
+        c.c_neg = int(self.c_neg)
+        c.n_interp = int(self.n_interp)
+        c.flow_preset = int(self.flow_preset)
+        c.selection_threshold = int(self.selection_threshold)
+        c.events_per_crossing = int(self.events_per_crossing)
+        c.include_endpoints = 1 if self.include_endpoints else 0
+        c.contrast_mode = int(self.contrast_mode)
+        c.c_pos_log = float(self.c_pos_log)
+        c.c_neg_log = float(self.c_neg_log)
+        c.sel_log = float(self.sel_log)
+        if self.preset_override is not None:
+            c.pyramid_levels = self.preset_override.pyramid_levels
+            c.iterations_per_level = self.preset_override.iterations_per_level
+            c.patch_radius = self.preset_override.patch_radius
+        return c
+
+    @classmethod
+    def from_c(cls, c: CConfig) -> "SimulatorConfig":
+        ov = None
+        if c.pyramid_levels or c.iterations_per_level or c.patch_radius:
+            ov = FlowPreset(c.pyramid_levels, c.iterations_per_level, c.patch_radius)
+        return cls(method=Method(c.method), c_pos=c.c_pos, c_neg=c.c_neg, n_interp=c.n_interp,
+                   flow_preset=FlowQuality(c.flow_preset), selection_threshold=c.selection_threshold,
+                   events_per_crossing=EventsPerCrossing(c.events_per_crossing),
+                   include_endpoints=bool(c.include_endpoints), contrast_mode=ContrastMode(c.contrast_mode),
+                   c_pos_log=c.c_pos_log, c_neg_log=c.c_neg_log, sel_log=c.sel_log, preset_override=ov)
+
+    def validate(self) -> None:
+        """SimulatorConfig::validate (types.hpp:126-130), evaluated by the library."""
+        c = self.to_c()
+        _lib.check(_lib.load().evsim_gpu_config_validate(ctypes.byref(c)))
+
+    def preset(self) -> FlowPreset:
+        return self.preset_override if self.preset_override is not None else flow_preset(self.flow_preset)
+
+
+# --------------------------------------------------------------------------- flow
+
+def _check_pair(prev: Frame, curr: Frame, who: str, empty_check: bool = True) -> None:
+    # check_pair, flow.cpp:249-256 / simulate.cpp:28-32
+    if empty_check and (prev.width <= 0 or prev.height <= 0 or curr.width <= 0 or curr.height <= 0):
+        raise InvalidArgument(1, f"{who}: empty frame")
+    if prev.width != curr.width or prev.height != curr.height:
+        raise InvalidArgument(1, f"{who}: incompatible input frames")
+
+
+def estimate_dense_flow(prev: Frame, curr: Frame, preset: FlowPreset) -> FlowField:
+    """estimate_dense_flow (flow.cpp:260-276) on the GPU."""
+    preset.validate()
+    _check_pair(prev, curr, "estimate_dense_flow")
+    w, h = prev.width, prev.height
+    du = np.zeros((h, w), np.float32)
+    dv = np.zeros((h, w), np.float32)
+    _lib.check(_lib.load().evsim_gpu_dense_flow(
+        _ptr(prev.pixels), _ptr(curr.pixels), w, h, preset.pyramid_levels, preset.iterations_per_level,
+        preset.patch_radius, _ptr(du), _ptr(dv)))
+    return FlowField(w, h, du, dv)
+
+
+def estimate_sparse_flow(prev: Frame, curr: Frame, points, preset: FlowPreset) -> SparseFlow:
+    """estimate_sparse_flow (flow.cpp:278-381) on the GPU."""
+    preset.validate()
+    _check_pair(prev, curr, "estimate_sparse_flow")
+    pts = np.ascontiguousarray(np.asarray(points, dtype=np.int32).reshape(-1, 2))
+    m = pts.shape[0]
+    disp = np.zeros((m, 2), np.float32)
+    st = np.zeros(m, np.uint8)
+    _lib.check(_lib.load().evsim_gpu_sparse_flow(
+        _ptr(prev.pixels), _ptr(curr.pixels), prev.width, prev.height, preset.pyramid_levels,
+        preset.iterations_per_level, preset.patch_radius, _ptr(pts), m, _ptr(disp), _ptr(st)))
+    return SparseFlow(pts, disp, st)
+
+
+class DenseFlowEstimator:
+    """Plug-in interface (flow.hpp:74-78)."""
+
+    def estimate(self, prev: Frame, curr: Frame) -> FlowField:  # pragma: no cover - interface
+        raise NotImplementedError
+
+
+class SparseFlowEstimator:
+    """Plug-in interface (flow.hpp:80-85)."""
+
+    def estimate(self, prev: Frame, curr: Frame, points) -> SparseFlow:  # pragma: no cover
+        raise NotImplementedError
+
+
+class PyramidalPatchFlow(DenseFlowEstimator):
+    """Default dense backend (flow.hpp:88-97), on the GPU."""
+
+    def __init__(self, preset: FlowPreset):
+        preset.validate()
+        self.preset = preset
+
+    def estimate(self, prev: Frame, curr: Frame) -> FlowField:
+        return estimate_dense_flow(prev, curr, self.preset)
+
+
+class PyramidalLucasKanade(SparseFlowEstimator):
+    """Default sparse backend (flow.hpp:100-110), on the GPU."""
+
+    def __init__(self, preset: FlowPreset):
+        preset.validate()
+        self.preset = preset
+
+    def estimate(self, prev: Frame, curr: Frame, points) -> SparseFlow:
+        return estimate_sparse_flow(prev, curr, points, self.preset)
+
+
+# --------------------------------------------------------------------------- pipelines
+
+def _events_from_c(events24: np.ndarray, n: int, w: int, h: int) -> EventStream:
+    return EventStream(w, h, events24[:n].copy())
+
+
+def interpolate_frames(prev: Frame, curr: Frame, flow: FlowField, n: int) -> list:
+    """interpolate_frames (simulate.cpp:91-121) on the GPU."""
+    _check_pair(prev, curr, "interpolate_frames", empty_check=False)
+    if flow.width != prev.width or flow.height != prev.height:
+        raise InvalidArgument(1, "interpolate_frames: flow dimensions do not match the frames")
+    if n < 0:
+        raise InvalidArgument(1, "interpolate_frames: n must be >= 0")
+    w, h = prev.width, prev.height
+    out = np.zeros((max(n, 1), h, w), np.uint8)
+    ts = np.zeros(max(n, 1), np.int64)
+    _lib.check(_lib.load().evsim_gpu_interpolate_frames(
+        _ptr(prev.pixels), _ptr(curr.pixels), w, h, prev.timestamp, curr.timestamp,
+        _ptr(np.ascontiguousarray(flow.du, np.float32)), _ptr(np.ascontiguousarray(flow.dv, np.float32)),
+        n, _ptr(out), _ptr(ts)))
+    return [Frame(w, h, int(ts[k]), out[k].copy()) for k in range(n)]
+
+
+def _call_events(fn, *args) -> np.ndarray:
+    n = ctypes.c_int64()
+    _lib.check(fn(*args, None, 0, ctypes.byref(n)))
+    buf = np.zeros(max(n.value, 1), EVENT_DTYPE)
+    _lib.check(fn(*args, _ptr(buf), n.value, ctypes.byref(n)))
+    return buf[: n.value]
+
+
+def dense_events_with_flow(prev: Frame, curr: Frame, flow: FlowField, config: SimulatorConfig) -> EventStream:
+    """dense_events_with_flow (simulate.cpp:123-128): caller-supplied flow, GPU chain."""
+    config.validate()
+    _check_pair(prev, curr, "interpolate_frames", empty_check=False)
+    if flow.width != prev.width or flow.height != prev.height:
+        raise InvalidArgument(1, "interpolate_frames: flow dimensions do not match the frames")
+    c = config.to_c()
+    ev = _call_events(_lib.load().evsim_gpu_dense_events_with_flow, _ptr(prev.pixels), _ptr(curr.pixels),
+                      prev.width, prev.height, prev.timestamp, curr.timestamp,
+                      _ptr(np.ascontiguousarray(flow.du, np.float32)),
+                      _ptr(np.ascontiguousarray(flow.dv, np.float32)), ctypes.byref(c))
+    return EventStream(prev.width, prev.height, ev)
+
+
+def select_points(prev: Frame, curr: Frame, config: SimulatorConfig) -> np.ndarray:
+    """Host restatement of simulate.cpp:149-159 (scan-order selection) — used
+    only when a custom SparseFlowEstimator must receive the point list."""
+    d = np.abs(curr.pixels.astype(np.int32) - prev.pixels.astype(np.int32))
+    ys, xs = np.nonzero(d > config.effective_selection_threshold())
+    return np.stack([xs, ys], axis=1).astype(np.int32)
+
+
+def sparse_events_with_flow(prev: Frame, curr: Frame, flow: SparseFlow, config: SimulatorConfig) -> EventStream:
+    """simulate_sparse after its estimator call (simulate.cpp:163-201), GPU splat + chain."""
+    config.validate()
+    c = config.to_c()
+    pts = np.ascontiguousarray(np.asarray(flow.points, np.int32).reshape(-1, 2))
+    ev = _call_events(_lib.load().evsim_gpu_sparse_events_with_flow, _ptr(prev.pixels), _ptr(curr.pixels),
+                      prev.width, prev.height, prev.timestamp, curr.timestamp, _ptr(pts), pts.shape[0],
+                      _ptr(np.ascontiguousarray(flow.displacements, np.float32)),
+                      _ptr(np.ascontiguousarray(flow.status, np.uint8)), ctypes.byref(c))
+    return EventStream(prev.width, prev.height, ev)
+
+
+def simulate_dense(prev: Frame, curr: Frame, config: SimulatorConfig,
+                   estimator: Optional[DenseFlowEstimator] = None) -> EventStream:
+    """simulate_dense (simulate.cpp:130-143)."""
+    config.validate()
+    _check_pair(prev, curr, "simulate_dense", empty_check=False)
+    if estimator is None or (isinstance(estimator, PyramidalPatchFlow) and estimator.preset == config.preset()):
+        sim = Simulator(config)
+        sim.push_frame(prev)
+        return sim.push_frame(curr)
+    if config.n_interp == 0:
+        return dense_events_with_flow(prev, curr, FlowField.zeros(prev.width, prev.height), config)
+    return dense_events_with_flow(prev, curr, estimator.estimate(prev, curr), config)
+
+
+def simulate_sparse(prev: Frame, curr: Frame, config: SimulatorConfig,
+                    estimator: Optional[SparseFlowEstimator] = None) -> EventStream:
+    """simulate_sparse (simulate.cpp:145-206)."""
+    config.validate()
+    _check_pair(prev, curr, "simulate_sparse", empty_check=False)
+    if estimator is None or (isinstance(estimator, PyramidalLucasKanade) and estimator.preset == config.preset()):
+        sim = Simulator(config)
+        sim.push_frame(prev)
+        return sim.push_frame(curr)
+    pts = select_points(prev, curr, config)
+    if len(pts) == 0 or config.n_interp == 0:
+        return sparse_events_with_flow(prev, curr, SparseFlow(pts, np.zeros((0, 2), np.float32),
+                                                               np.zeros(0, np.uint8)), config)
+    return sparse_events_with_flow(prev, curr, estimator.estimate(prev, curr, pts), config)
+
+
+# --------------------------------------------------------------------------- Simulator
+
+class Simulator:
+    """evsim::Simulator (simulate.hpp:60-94) backed by one GPU handle.
+
+    ``Simulator(config)`` runs the whole push on the device.  Passing custom
+    ``dense_flow`` / ``sparse_flow`` estimators (the reference's plug-in seam,
+    simulate.hpp:68-77) routes the flow through them and the interpolation +
+    event chain through the GPU free functions (linear mode).
+    """
+
+    def __init__(self, config: SimulatorConfig, dense_flow: Optional[DenseFlowEstimator] = None,
+                 sparse_flow: Optional[SparseFlowEstimator] = None, device: int = 0, _null_check: bool = False):
+        config.validate()
+        if _null_check and (dense_flow is None or sparse_flow is None):
+            raise InvalidArgument(1, "Simulator: flow estimators must not be null")
+        self._config = dataclasses.replace(config)
+        self._custom = (dense_flow is not None and not isinstance(dense_flow, PyramidalPatchFlow)) or \
+                       (sparse_flow is not None and not isinstance(sparse_flow, PyramidalLucasKanade))
+        self._dense, self._sparse = dense_flow, sparse_flow
+        self._lib = _lib.load()
+        self._h = _vp()
+        self._prev: Optional[Frame] = None
+        c = config.to_c()
+        _lib.check(self._lib.evsim_gpu_create(ctypes.byref(c), device, ctypes.byref(self._h)))
+
+    @property
+    def config(self) -> SimulatorConfig:
+        return self._config
+
+    def push_frame(self, frame: Frame) -> EventStream:
+        """Simulator::push_frame (simulate.cpp:306-347)."""
+        pixels = np.ascontiguousarray(frame.pixels, dtype=np.uint8)
+        if frame.width <= 0 or frame.height <= 0 or pixels.size != frame.width * frame.height:
+            raise InvalidArgument(1, "push_frame: malformed frame")
+        if self._custom:
+            return self._push_custom(frame, pixels)
+        ev = CEvents()
+        _lib.check(self._lib.evsim_gpu_push_frame(self._h, _ptr(pixels), frame.width, frame.height,
+                                                  int(frame.timestamp), 0, ctypes.byref(ev)))
+        return self._collect(ev)
+
+    def _collect(self, ev: CEvents) -> EventStream:
+        n = ev.n_events
+        out = EventStream(ev.width, ev.height)
+        if n == 0:
+            return out
+        packed = np.zeros(n, np.uint32)
+        _lib.check(self._lib.evsim_gpu_copy_events(self._h, _ptr(packed), n, 0))
+        S = ev.n_segments
+        seg_t = np.ctypeslib.as_array(ev.seg_t, shape=(S,)).copy()
+        seg_off = np.ctypeslib.as_array(ev.seg_offset, shape=(S + 1,)).copy()
+        out.events = unpack_events(packed, seg_t, seg_off)
+        return out
+
+    def push_frame_packed(self, pixels_ptr: int, width: int, height: int, timestamp: int,
+                          on_device: bool = True) -> CEvents:
+        """Device-resident push (no event download): returns the C result struct."""
+        ev = CEvents()
+        _lib.check(self._lib.evsim_gpu_push_frame(self._h, _vp(pixels_ptr), width, height, int(timestamp),
+                                                  1 if on_device else 0, ctypes.byref(ev)))
+        return ev
+
+    def push_frame_async(self, pixels_ptr: int, width: int, height: int, timestamp: int,
+                         on_device: bool = True) -> None:
+        _lib.check(self._lib.evsim_gpu_push_frame_async(self._h, _vp(pixels_ptr), width, height, int(timestamp),
+                                                        1 if on_device else 0))
+
+    def sync(self) -> CEvents:
+        ev = CEvents()
+        _lib.check(self._lib.evsim_gpu_sync(self._h, ctypes.byref(ev)))
+        return ev
+
+    def copy_packed(self, dst_ptr: int, capacity: int) -> None:
+        _lib.check(self._lib.evsim_gpu_copy_events(self._h, _vp(dst_ptr), capacity, 0))
+
+    @property
+    def stream(self) -> int:
+        return self._lib.evsim_gpu_stream(self._h) or 0
+
+    STAGES = ("upload", "pyramid", "flow", "chain", "scan", "emit")
+
+    def set_profiling(self, enable: bool) -> None:
+        _lib.check(self._lib.evsim_gpu_set_profiling(self._h, 1 if enable else 0))
+
+    def stage_times(self) -> tuple[dict, int]:
+        """Accumulated device ms per pipeline stage and the number of timed pushes."""
+        ms = (ctypes.c_double * len(self.STAGES))()
+        n = ctypes.c_int64()
+        _lib.check(self._lib.evsim_gpu_stage_times(self._h, ms, len(self.STAGES), ctypes.byref(n)))
+        return {k: ms[i] for i, k in enumerate(self.STAGES)}, n.value
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self._lib.evsim_gpu_kernel_launches(self._h))
+
+    def _push_custom(self, frame: Frame, pixels: np.ndarray) -> EventStream:
+        prev = self._prev
+        f = Frame(frame.width, frame.height, int(frame.timestamp), pixels)
+        if prev is not None:
+            if frame.width != prev.width or frame.height != prev.height:
+                raise InvalidArgument(1, "push_frame: frame dimensions changed mid-stream")
+            if frame.timestamp <= prev.timestamp:
+                raise InvalidArgument(1, "push_frame: timestamps must be strictly increasing")
+        out = EventStream(frame.width, frame.height)
+        if prev is not None:
+            m = self._config.method
+            if m == Method.dense:
+                out = simulate_dense(prev, f, self._config, self._dense or PyramidalPatchFlow(self._config.preset()))
+            elif m == Method.sparse:
+                out = simulate_sparse(prev, f, self._config,
+                                      self._sparse or PyramidalLucasKanade(self._config.preset()))
+            else:
+                out = dense_events_with_flow(prev, f, FlowField.zeros(f.width, f.height),
+                                             dataclasses.replace(self._config, n_interp=0))
+        self._prev = f
+        return out
+
+    def reset(self) -> None:
+        """Simulator::reset (simulate.hpp:83-86)."""
+        self._prev = None
+        _lib.check(self._lib.evsim_gpu_reset(self._h))
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.evsim_gpu_destroy(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def concatenate(streams: Sequence[EventStream]) -> EventStream:
+    if not streams:
+        return EventStream(0, 0)
+    out = EventStream(streams[0].width, streams[0].height)
+    out.events = np.concatenate([s.events for s in streams]) if streams else out.events
+    return out
