@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--frames", type=int, default=0, help="override sequence length")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--batch", type=int, default=0,
+                   help="frames per push_frames call (0 = the simulator's maximum; 1 = frame-by-frame)")
     return p.parse_args()
 
 
@@ -233,19 +235,26 @@ def run_ours(args):
     base = d_frames.data_ptr()
     torch.cuda.synchronize()
 
-    def one_step(profile=False):
-        sim.reset()
-        for k in range(n):
-            sim.push_frame_async(base + k * P, c.width, c.height, int(ts[k]), on_device=True)
-        return sim.sync()
+    batch = args.batch or sim.max_batch
+    batch = max(1, min(batch, sim.max_batch, n))
 
-    # warm-up (also measures events per frame: a synchronous pass)
+    def enqueue_step():
+        # reset + the whole sequence in batches of `batch` frames (one launch
+        # sequence per batch); the first frame is the warm-up frame
+        sim.reset()
+        for a in range(0, n, batch):
+            nb = min(batch, n - a)
+            sim.push_frames_device(base + a * P, nb, c.width, c.height, ts[a:a + nb], on_device=True, sync=False)
+
+    # warm-up, then an untimed synchronous pass that counts the events
     for _ in range(max(args.warmup, 1)):
-        one_step()
+        enqueue_step()
+        sim.sync()
     ev_total = 0
     sim.reset()
-    for k in range(n):
-        e = sim.push_frame_packed(base + k * P, c.width, c.height, int(ts[k]), on_device=True)
+    for a in range(0, n, batch):
+        nb = min(batch, n - a)
+        e = sim.push_frames_device(base + a * P, nb, c.width, c.height, ts[a:a + nb], on_device=True, sync=True)
         ev_total += e.n_events
     torch.cuda.synchronize()
 
@@ -264,9 +273,7 @@ def run_ours(args):
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(torch_stream)
-            sim.reset()
-            for k in range(n):
-                sim.push_frame_async(base + k * P, c.width, c.height, int(ts[k]), on_device=True)
+            enqueue_step()
             e1.record(torch_stream)
             sim.sync()
             e1.synchronize()
@@ -303,32 +310,43 @@ def run_ours(args):
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"
     E_frame = ev_total / max(n - 1, 1)
-    b_alg = 2 * P + 4 * E_frame
-    interval_pushes = max(timed_pushes - args.steps, 1)  # warm-up pushes have empty event stages
-    ev_stage_ms = (stages["chain"] + stages["scan"] + stages["emit"]) / interval_pushes
-    achieved = b_alg / (ev_stage_ms / 1e3) / 1e9
+    b_alg = 2 * P + 4 * E_frame  # read 2 u8 frames, write 4 B per event
+    # the event stage (chain_kernel -> offsets_kernel -> segbase+emit_kernel)
+    # runs once per push_frames call, over all of the call's frame pairs
+    launches_ev = max(timed_pushes, 1)
+    pairs_timed = args.steps * (n - 1)
+    ev_stage_ms = stages["chain"] + stages["scan"] + stages["emit"]
+    bytes_per_launch = b_alg * pairs_timed / launches_ev
+    ms_per_launch = ev_stage_ms / launches_ev
+    achieved = bytes_per_launch / (ms_per_launch / 1e3) / 1e9 if ms_per_launch > 0 else 0.0
     e2e_frac = b_alg * (value / ws) / 1e9 / hbm
+    frames_timed = args.steps * n
     roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": None,
-                "kernel": "event stage: chain_kernel + scan_kernel + emit_kernel per frame",
-                "algorithmic_bytes_per_launch": round(b_alg), "avg_launch_ms": round(ev_stage_ms, 5),
-                "peak_source": peak_src, "end_to_end_frac": round(e2e_frac, 4),
-                "stage_ms_per_frame": {k: round(v / max(timed_pushes, 1), 5) for k, v in stages.items()}}
+                "kernel": "event stage = chain_kernel + offsets_kernel + emit_kernel (one push_frames call)",
+                "algorithmic_bytes_per_frame": round(b_alg), "frames_per_launch": round(pairs_timed / launches_ev, 2),
+                "algorithmic_bytes_per_launch": round(bytes_per_launch), "avg_launch_ms": round(ms_per_launch, 5),
+                "peak_source": peak_src, "end_to_end_frac": round(e2e_frac, 5),
+                "stage_us_per_frame": {k: round(1e3 * v / frames_timed, 3) for k, v in stages.items()}}
 
     # ---- e2e through the C-ABI with host buffers ---------------------------------
     e2e = None
     if not args.no_e2e:
         h_frames = torch.from_numpy(frames).pin_memory()
         hbase = h_frames.data_ptr()
-        cap = (c.n_interp + 1) * P
+        cap = (c.n_interp + 1) * P * batch
         h_events = torch.empty(cap, dtype=torch.int32).pin_memory()
         hev = h_events.data_ptr()
 
         def e2e_step():
+            # evsim_gpu_push_frames on pinned host frames (H2D inside) +
+            # evsim_gpu_copy_events of the packed events (D2H), per batch
             sim.reset()
             d2h = 0
-            for k in range(n):
-                e = sim.push_frame_packed(hbase + k * P, c.width, c.height, int(ts[k]), on_device=False)
+            for a in range(0, n, batch):
+                nb = min(batch, n - a)
+                e = sim.push_frames_device(hbase + a * P, nb, c.width, c.height, ts[a:a + nb], on_device=False,
+                                           sync=True)
                 if e.n_events:
                     sim.copy_packed(hev, cap)
                 d2h += 4 * e.n_events + 16 * (e.n_segments + 1)
@@ -351,7 +369,7 @@ def run_ours(args):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": round(frames_total / float(te.item()), 3), "unit": "frames/s",
                "h2d_bytes_per_step": n * P, "d2h_bytes_per_step": int(d2h),
-               "api": "evsim_gpu_push_frame (pinned host frame) + evsim_gpu_copy_events (packed)"}
+               "api": "evsim_gpu_push_frames (pinned host frames) + evsim_gpu_copy_events (packed)"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -366,7 +384,7 @@ def run_ours(args):
             "value": round(value, 3), "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8/f32/f64", "data": "synthetic",
-            "config": {**config_json(c, args, n), "parallelism": f"streams x{ws}"},
+            "config": {**config_json(c, args, n), "parallelism": f"streams x{ws}", "frames_per_push": batch},
             "events_per_s": round(events_per_s, 1), "events_per_frame": round(E_frame, 1),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(),

@@ -139,6 +139,20 @@ EVSIM_GPU_API int evsim_gpu_create(const evsim_gpu_config* cfg, int device, evsi
 EVSIM_GPU_API int evsim_gpu_push_frame(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t width, int32_t height,
                          int64_t t_us, int32_t pixels_on_device, evsim_gpu_events* out);
 
+/* Batched Simulator::push_frame: n_frames consecutive frames (pixels:
+ * n_frames*width*height bytes, t_us: n_frames host timestamps) in one launch
+ * sequence.  Results are identical to n_frames push_frame calls with their
+ * event streams concatenated (segments of all intervals, in order).  The
+ * whole batch is validated first and rejected atomically (state untouched).
+ * At most evsim_gpu_max_batch(sim) frames per call. */
+EVSIM_GPU_API int evsim_gpu_push_frames(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t n_frames,
+                                        int32_t width, int32_t height, const int64_t* t_us,
+                                        int32_t pixels_on_device, evsim_gpu_events* out);
+EVSIM_GPU_API int evsim_gpu_push_frames_async(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t n_frames,
+                                              int32_t width, int32_t height, const int64_t* t_us,
+                                              int32_t pixels_on_device);
+EVSIM_GPU_API int evsim_gpu_max_batch(const evsim_gpu_sim* sim);
+
 /* Asynchronous variant: enqueues the push on the handle's CUDA stream and
  * returns without waiting; evsim_gpu_sync() completes it.  Validation
  * errors are still reported synchronously. */

@@ -1,13 +1,15 @@
 // evsim_gpu.cu — host side of the B200 event-simulation path: the C-ABI of
-// include/evsim_gpu.h, the per-handle device state and the per-push launch
-// sequence.
+// include/evsim_gpu.h, the per-handle device state and the launch sequence.
 //
 // Mirrors evsim::Simulator (/root/reference/proj/include/evsim/simulate.hpp:60-94,
 // src/simulate.cpp:306-347): same validation order and messages, same
-// warm-up semantics, failed pushes leave the state untouched.  All device
-// memory comes from the stream-ordered pool (cudaMallocAsync) with an
-// unbounded release threshold, so a fresh handle per timed pass (the
-// reference's bench_method, src/bench.cpp:53-64) reuses cached memory.
+// warm-up semantics, failed pushes leave the state untouched.  A push of F
+// frames (push_frames; push_frame is F = 1) runs one launch sequence over the
+// F frame pairs; frames live in a device ring, so the previous frame and its
+// pyramid stay resident.  All device memory comes from the stream-ordered
+// pool (cudaMallocAsync) with an unbounded release threshold, so a fresh
+// handle per timed pass (the reference's bench_method, src/bench.cpp:53-64)
+// reuses cached memory.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -195,21 +197,21 @@ void interp_table(const std::vector<int>& centers, int extent, std::vector<int>&
   }
 }
 
-// Device-resident flow machinery for one resolution + preset: pyramids of
-// two frame slots, per-level patch grids and their static tables.
+// Device-resident flow machinery for one resolution + preset: the pyramid
+// ring (R frame slots), per-level patch grids (per pair) and static tables.
 struct FlowEngine {
   int w = 0, h = 0;
   Preset preset{};
   int levels = 0;
+  int R = 0, pairs = 0;
   LevelDims dims[kMaxLevels]{};
-  DevBuf pyr[2][kMaxLevels];  // fp32 level images, slot 0/1
+  DevBuf pyr[kMaxLevels];     // fp32 level images, R slots
+  DevBuf qpyr[kMaxLevels];    // float4 quad images (4 bilinear taps per pixel), R slots
   DevBuf tables[kMaxLevels];  // cx | cy | ix | wx | iy | wy
-  DevBuf grid[kMaxLevels];    // pu | pv
+  DevBuf grid[kMaxLevels];    // per pair: pu | pv
   GridGeom geom[kMaxLevels]{};
 
   void setup(int w_, int h_, Preset p, cudaStream_t s) {
-    if (w_ == w && h_ == h && p.levels == preset.levels && p.iters == preset.iters && p.radius == preset.radius)
-      return;
     w = w_;
     h = h_;
     preset = p;
@@ -219,7 +221,6 @@ struct FlowEngine {
     const int r = p.radius, stride = std::max(1, r);
     for (int l = 0; l < levels; ++l) {
       const int lw = dims[l].w, lh = dims[l].h;
-      for (int sl = 0; sl < 2; ++sl) pyr[sl][l].ensure((size_t)lw * lh * sizeof(float), s);
       const auto cxs = patch_centers(lw, r, stride), cys = patch_centers(lh, r, stride);
       std::vector<int> ix, iy;
       std::vector<float> wx, wy;
@@ -241,7 +242,6 @@ struct FlowEngine {
       tables[l].ensure(host.size(), s);
       CK(cudaMemcpyAsync(tables[l].p, host.data(), host.size(), cudaMemcpyHostToDevice, s));
       CK(cudaStreamSynchronize(s));  // host vector goes out of scope
-      grid[l].ensure(2 * ncx * ncy * sizeof(float), s);
       GridGeom& g = geom[l];
       g.w = lw;
       g.h = lh;
@@ -254,65 +254,101 @@ struct FlowEngine {
       g.wx = reinterpret_cast<const float*>(base + ncx + ncy + lw);
       g.iy = base + ncx + ncy + 2 * lw;
       g.wy = reinterpret_cast<const float*>(base + ncx + ncy + 2 * lw + lh);
-      g.pu = grid[l].as<float>();
-      g.pv = grid[l].as<float>() + ncx * ncy;
+      g.pair_stride = 2 * ncx * ncy;
+    }
+    R = pairs = 0;
+  }
+
+  void ensure(int R_, int pairs_, cudaStream_t s) {
+    if (R_ > R) {
+      for (int l = 0; l < levels; ++l) {
+        const size_t pl = (size_t)dims[l].w * dims[l].h;
+        pyr[l].release();
+        qpyr[l].release();
+        pyr[l].ensure((size_t)R_ * pl * sizeof(float), s);
+        qpyr[l].ensure((size_t)R_ * pl * sizeof(float4), s);
+      }
+      R = R_;
+    }
+    if (pairs_ > pairs) {
+      for (int l = 0; l < levels; ++l) {
+        grid[l].ensure((size_t)pairs_ * geom[l].pair_stride * sizeof(float), s);
+        geom[l].pu = grid[l].as<float>();
+        geom[l].pv = grid[l].as<float>() + geom[l].pair_stride / 2;
+      }
+      pairs = pairs_;
     }
   }
 
-  // build_pyramid  flow.cpp:81-87
-  int build_pyramid(const uint8_t* frame, int slot, cudaStream_t s) {
-    launch_to_float(frame, pyr[slot][0].as<float>(), (int64_t)w * h, s);
-    for (int l = 1; l < levels; ++l)
-      launch_downsample(pyr[slot][l - 1].as<float>(), dims[l - 1], pyr[slot][l].as<float>(), dims[l], s);
-    CK_LAUNCH("pyramid");
-    return levels;
+  PyramidParams pyramid_params(const uint8_t* frames, size_t P, uint32_t* quad_u8, int slot0) const {
+    PyramidParams p{};
+    p.levels = levels;
+    for (int l = 0; l < levels; ++l) {
+      const size_t pl = (size_t)dims[l].w * dims[l].h;
+      p.dims[l] = dims[l];
+      p.pyr[l] = Ring<float>{pyr[l].as<float>(), pl};
+      p.qpyr[l] = Ring<float4>{qpyr[l].as<float4>(), pl};
+    }
+    p.frames = Ring<const uint8_t>{frames, P};
+    p.quad_u8 = Ring<uint32_t>{quad_u8, P};
+    p.R = R;
+    p.slot0 = slot0;
+    return p;
   }
 
-  // estimate_dense_flow's level loop, flow.cpp:268-275; result = level-0 grid
-  int solve(int prev_slot, int curr_slot, cudaStream_t s) {
+  // estimate_dense_flow's level loop, flow.cpp:268-275, for n_pairs pairs;
+  // result = per-pair level-0 patch grids
+  int solve(int r0, int n_pairs, cudaStream_t s) {
     for (int l = levels - 1; l >= 0; --l) {
       DenseLKParams p{};
       p.g = geom[l];
       p.has_coarse = l != levels - 1;
       if (p.has_coarse) p.coarse = geom[l + 1];
-      p.prev = pyr[prev_slot][l].as<float>();
-      p.curr = pyr[curr_slot][l].as<float>();
+      const size_t pl = (size_t)dims[l].w * dims[l].h;
+      p.prev = Ring<const float>{pyr[l].as<float>(), pl};
+      p.qcurr = Ring<const float4>{qpyr[l].as<float4>(), pl};
+      p.R = R;
+      p.r0 = r0;
       p.radius = preset.radius;
       p.iterations = preset.iters;
-      launch_dense_lk(p, s);
+      launch_dense_lk(p, n_pairs, s);
     }
     CK_LAUNCH("dense_lk");
     return levels;
   }
 
-  SparseLKParams sparse_params(int prev_slot, int curr_slot) const {
+  SparseLKParams sparse_params(int r0) const {
     SparseLKParams p{};
     p.levels = levels;
     for (int l = 0; l < levels; ++l) {
+      const size_t pl = (size_t)dims[l].w * dims[l].h;
       p.dims[l] = dims[l];
-      p.prev[l] = pyr[prev_slot][l].as<float>();
-      p.curr[l] = pyr[curr_slot][l].as<float>();
+      p.prev[l] = Ring<const float>{pyr[l].as<float>(), pl};
+      p.curr[l] = Ring<const float>{pyr[l].as<float>(), pl};
     }
+    p.R = R;
+    p.r0 = r0;
     p.w0 = w;
     p.h0 = h;
     p.radius = preset.radius;
     p.iterations = preset.iters;
+    p.pair_stride = (size_t)w * h;
     return p;
   }
 };
 
-// Chain/scan/emit buffers for one resolution and chain length.
+// Chain / offsets / emit buffers for one resolution, links per pair and
+// number of pairs.
 struct EventEngine {
   int w = 0, h = 0, wpr = 0;
   int64_t n_words = 0;
   int wpb = 0, n_blocks = 0;
-  int max_links = 0;
+  int max_links = 0;  // links of a launch (pairs * per-pair links)
   bool magnitude = false;
-  DevBuf masks, counts, offsets, segtab, seg_out, total, events, mcount, wcount;
+  DevBuf masks, counts, prefix, link_total, segtab, segbase, seg_out, events, mcount, wcount;
   int64_t capacity = 0;
 
-  void setup(int w_, int h_, int links, bool mag, cudaStream_t s) {
-    const bool geom_change = w_ != w || h_ != h;
+  void geometry(int w_, int h_) {
     w = w_;
     h = h_;
     wpr = (w + 31) / 32;
@@ -323,22 +359,28 @@ struct EventEngine {
     per = std::max<int64_t>(kWarpsPerBlock, (per + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock);
     wpb = (int)per;
     n_blocks = (int)((n_words + wpb - 1) / wpb);
-    if (geom_change || links > max_links || mag != magnitude) {
-      max_links = std::max(links, 1);
+    max_links = 0;
+    capacity = 0;
+  }
+
+  void ensure(int links, bool mag, int64_t event_cap, cudaStream_t s) {
+    links = std::max(links, 1);
+    if (links > max_links || mag != magnitude) {
+      max_links = links;
       magnitude = mag;
       masks.ensure((size_t)max_links * n_words * sizeof(uint2), s);
       counts.ensure((size_t)max_links * n_blocks * sizeof(uint32_t), s);
-      offsets.ensure((size_t)max_links * n_blocks * sizeof(int64_t), s);
-      segtab.ensure(8 + (size_t)max_links * (2 * sizeof(int) + sizeof(int64_t)), s);
+      prefix.ensure((size_t)max_links * n_blocks * sizeof(int64_t), s);
+      link_total.ensure((size_t)max_links * sizeof(int64_t), s);
+      segtab.ensure(16 + (size_t)max_links * (2 * sizeof(int) + sizeof(int64_t)), s);
+      segbase.ensure((size_t)max_links * sizeof(int64_t), s);
       seg_out.ensure((3 + 2 * (size_t)max_links) * sizeof(int64_t), s);
-      total.ensure(sizeof(int64_t), s);
-      const int64_t P = (int64_t)w * h;
       if (mag) {
         mcount.ensure((size_t)max_links * n_words * 32 * sizeof(uint16_t), s);
         wcount.ensure((size_t)max_links * n_words * sizeof(uint32_t), s);
       }
-      grow((int64_t)max_links * P, s);
     }
+    grow(event_cap, s);
   }
 
   void grow(int64_t cap, cudaStream_t s) {
@@ -351,12 +393,19 @@ struct EventEngine {
     SegTable t;
     char* b = static_cast<char*>(segtab.p);
     t.n_segs = reinterpret_cast<int*>(b);
-    t.seg_t = reinterpret_cast<int64_t*>(b + 8);
-    t.seg_first = reinterpret_cast<int*>(b + 8 + (size_t)max_links * 8);
-    t.seg_nlinks = reinterpret_cast<int*>(b + 8 + (size_t)max_links * 12);
+    t.seg_t = reinterpret_cast<int64_t*>(b + 16);
+    t.seg_first = reinterpret_cast<int*>(b + 16 + (size_t)max_links * 8);
+    t.seg_nlinks = reinterpret_cast<int*>(b + 16 + (size_t)max_links * 12);
     return t;
   }
 };
+
+// Largest batch whose link count fits the kernels' shared-memory tables
+// (chain: 4 B per link, emit: 8 B per segment, both <= 96 KB).
+int max_batch_for(int links_per_pair) {
+  const int by_links = 12000 / std::max(links_per_pair, 1);
+  return std::max(1, std::min(kMaxBatch, by_links));
+}
 
 }  // namespace
 
@@ -373,14 +422,15 @@ struct evsim_gpu_sim {
   bool has_prev = false;
   int w = 0, h = 0;
   int64_t prev_t = 0;
-  int slot = 0;  // frame slot holding prev
+  int rhead = 0;  // ring slot of the previous frame
+  int R = 0;      // ring slots allocated
+  int pair_cap = 0;
 
-  DevBuf frames[2], quads[2], lut, ref, consts;
+  DevBuf frames, quads, lut, ref, consts;
   FlowEngine flow;
   EventEngine ev;
-  // sparse
-  DevBuf sel_masks, sel_counts, sel_offsets, sel_segtab, sel_total, sel_seg_out, points, n_points, disp, status,
-      claims, touched;
+  // sparse (per pair)
+  DevBuf sel_masks, sel_counts, points, n_points, disp, status, claims, touched;
 
   // last result
   int64_t* h_seg_out = nullptr;  // pinned
@@ -388,11 +438,7 @@ struct evsim_gpu_sim {
   std::vector<int64_t> seg_t, seg_off;
   int64_t n_events = 0;
   bool pending = false;
-  bool last_magnitude = false;
-  ChainParams last_chain{};
-  ScanParams last_scan{};
   EmitParams last_emit{};
-  int last_provider = 0;
 
   // per-stage CUDA-event timing (evsim_gpu_set_profiling)
   using EvGroup = std::array<cudaEvent_t, EVSIM_N_STAGES + 1>;
@@ -412,6 +458,7 @@ struct evsim_gpu_sim {
       for (auto e : g) cudaEventDestroy(e);
   }
 
+  // ---- profiling -----------------------------------------------------------
   void begin_group() {
     if (!profiling) return;
     EvGroup g;
@@ -449,47 +496,35 @@ struct evsim_gpu_sim {
     ev_pending.clear();
   }
 
-  bool uses_flow() const {
-    return (cfg.method == EVSIM_METHOD_DENSE || cfg.method == EVSIM_METHOD_SPARSE) && cfg.n_interp > 0;
-  }
+  // ---- configuration -------------------------------------------------------
   int n_interp_eff() const { return cfg.method == EVSIM_METHOD_DIFFERENCE_ONLY ? 0 : cfg.n_interp; }
+  bool dense_flow() const { return cfg.method == EVSIM_METHOD_DENSE && n_interp_eff() > 0; }
+  bool sparse_flow() const { return cfg.method == EVSIM_METHOD_SPARSE && n_interp_eff() > 0; }
+  bool uses_flow() const { return dense_flow() || sparse_flow(); }
   bool log_mode() const { return cfg.contrast_mode == EVSIM_CONTRAST_LOG; }
   bool magnitude() const { return cfg.events_per_crossing == EVSIM_EVENTS_MAGNITUDE; }
 
+  // chain_pipeline (simulate.cpp:57-69): which chain frames the links join
+  ChainDesc desc() const {
+    const int N = n_interp_eff();
+    if (cfg.method == EVSIM_METHOD_DIFFERENCE_ONLY) return ChainDesc{0, 1, 1};
+    if (N == 0) return ChainDesc{0, 1, cfg.include_endpoints ? 1 : 0};
+    if (cfg.include_endpoints) return ChainDesc{0, 1, N + 1};
+    return ChainDesc{1, 1, std::max(0, N - 1)};
+  }
+
+  // ---- allocation ----------------------------------------------------------
   void allocate(int w_, int h_) {
     w = w_;
     h = h_;
-    const size_t P = (size_t)w * h;
-    for (int i = 0; i < 2; ++i) frames[i].ensure(P + 16, stream);
-    const int N = n_interp_eff();
-    if (cfg.method == EVSIM_METHOD_DENSE && N > 0)
-      for (int i = 0; i < 2; ++i) quads[i].ensure(P * 4, stream);
+    R = 0;
+    pair_cap = 0;
+    rhead = 0;
     if (uses_flow()) flow.setup(w, h, preset, stream);
-    if (log_mode()) ref.ensure(P * sizeof(float), stream);
-    const bool incl = cfg.method == EVSIM_METHOD_DIFFERENCE_ONLY || cfg.include_endpoints;
-    const int links = std::max(1, incl ? N + 1 : N - 1);
-    ev.setup(w, h, links, magnitude(), stream);
-    if (cfg.method == EVSIM_METHOD_SPARSE && N > 0) {
-      sel_masks.ensure((size_t)ev.n_words * 4, stream);
-      sel_counts.ensure((size_t)ev.n_blocks * 4, stream);
-      sel_offsets.ensure((size_t)ev.n_blocks * 8, stream);
-      sel_segtab.ensure(64, stream);
-      sel_total.ensure(8, stream);
-      sel_seg_out.ensure(64, stream);
-      points.ensure(P * 4, stream);
-      n_points.ensure(8, stream, true);
-      disp.ensure(P * sizeof(float2), stream);
-      status.ensure(P, stream);
-      claims.ensure((size_t)N * P * 8, stream, true);
-      touched.ensure((size_t)((N + 31) / 32) * P * 4, stream, true);
-    }
-    const size_t seg_need = (3 + 2 * (size_t)ev.max_links) * sizeof(int64_t);
-    if (seg_need > h_seg_cap) {
-      if (h_seg_out) cudaFreeHost(h_seg_out);
-      CK(cudaHostAlloc((void**)&h_seg_out, seg_need, cudaHostAllocDefault));
-      h_seg_cap = seg_need;
-    }
+    if (log_mode()) ref.ensure((size_t)w * h * sizeof(float), stream);
+    ev.geometry(w, h);
     // interpolation constants, interpolate_frames simulate.cpp:97-100
+    const int N = n_interp_eff();
     const int K = N + 2;
     std::vector<char> host((size_t)K * (8 + 8 + 4 + 4));
     double* alpha = reinterpret_cast<double*>(host.data());
@@ -508,22 +543,76 @@ struct evsim_gpu_sim {
     CK(cudaStreamSynchronize(stream));
   }
 
-  ChainDesc full_desc() const {
-    const int N = n_interp_eff();
-    if (cfg.method == EVSIM_METHOD_DIFFERENCE_ONLY) return ChainDesc{0, 1, 1};
-    if (N == 0) return direct_desc();
-    // chain_pipeline, simulate.cpp:57-69
-    if (cfg.include_endpoints) return ChainDesc{0, 1, N + 1};
-    return ChainDesc{1, 1, std::max(0, N - 1)};
-  }
-  ChainDesc direct_desc() const {
-    // chain_pipeline(prev, curr, {}): [prev, curr] or nothing
-    const int N = n_interp_eff();
-    return ChainDesc{0, N + 1, cfg.include_endpoints ? 1 : 0};
+  // room for `pairs` pairs in one launch: ring of pairs + 1 frame slots
+  void ensure_capacity(int pairs) {
+    const size_t P = (size_t)w * h;
+    const int need_R = pairs + 1;
+    if (need_R > R) {
+      // grow the ring; the previous frame (and its pyramid) moves to slot 0
+      DevBuf nf;
+      nf.ensure((size_t)need_R * P + 16, stream);
+      if (has_prev) CK(cudaMemcpyAsync(nf.p, frames.as<uint8_t>() + (size_t)rhead * P, P, cudaMemcpyDeviceToDevice, stream));
+      std::swap(frames.p, nf.p);
+      std::swap(frames.n, nf.n);
+      std::swap(frames.s, nf.s);
+      if (dense_flow()) {
+        DevBuf nq;
+        nq.ensure((size_t)need_R * P * 4, stream);
+        if (has_prev)
+          CK(cudaMemcpyAsync(nq.p, quads.as<uint32_t>() + (size_t)rhead * P, P * 4, cudaMemcpyDeviceToDevice, stream));
+        std::swap(quads.p, nq.p);
+        std::swap(quads.n, nq.n);
+        std::swap(quads.s, nq.s);
+      }
+      if (uses_flow()) {
+        // pyramid of prev: rebuilt from the frame below (cheap, exact)
+        flow.ensure(need_R, std::max(pairs, 1), stream);
+      }
+      const int old_head = rhead;
+      rhead = 0;
+      R = need_R;
+      if (uses_flow() && has_prev) {
+        PyramidParams pp = flow.pyramid_params(frames.as<uint8_t>(), P, dense_flow() ? quads.as<uint32_t>() : nullptr, 0);
+        launch_pyramid(pp, 1, stream);
+        CK_LAUNCH("pyramid");
+      }
+      (void)old_head;
+    }
+    if (pairs > pair_cap) {
+      if (uses_flow()) flow.ensure(R, pairs, stream);
+      const int L = desc().n_links;
+      const int64_t cap = magnitude() ? 0 : (int64_t)std::max(L, 1) * pairs * (int64_t)P;
+      ev.ensure(L * pairs, magnitude(), std::max<int64_t>(cap, ev.capacity), stream);
+      if (sparse_flow()) {
+        const int N = n_interp_eff();
+        sel_masks.ensure((size_t)pairs * ev.n_words * 4, stream);
+        sel_counts.ensure((size_t)pairs * ev.n_blocks * 4, stream);
+        points.ensure((size_t)pairs * P * 4, stream);
+        n_points.ensure((size_t)pairs * sizeof(int), stream, true);
+        disp.ensure((size_t)pairs * P * sizeof(float2), stream);
+        status.ensure((size_t)pairs * P, stream);
+        claims.release();
+        claims.ensure((size_t)pairs * N * P * 4, stream, true);
+        touched.release();
+        touched.ensure((size_t)pairs * ((N + 31) / 32) * P * 4, stream, true);
+      }
+      const size_t seg_need = (3 + 2 * (size_t)ev.max_links) * sizeof(int64_t);
+      if (seg_need > h_seg_cap) {
+        if (h_seg_out) cudaFreeHost(h_seg_out);
+        h_seg_out = nullptr;
+        CK(cudaHostAlloc((void**)&h_seg_out, seg_need, cudaHostAllocDefault));
+        h_seg_cap = seg_need;
+      }
+      pair_cap = pairs;
+    }
+    if (magnitude() && ev.capacity == 0) ev.grow((int64_t)std::max(desc().n_links, 1) * pairs * (int64_t)P, stream);
   }
 
-  void fill_chain(ChainParams& c, const uint8_t* prev_f, const uint8_t* curr_f) {
+  // ---- chain params --------------------------------------------------------
+  ChainParams chain_params(int r0, int n_pairs) {
+    ChainParams c{};
     const int N = n_interp_eff();
+    const size_t P = (size_t)w * h;
     c.w = w;
     c.h = h;
     c.wpr = ev.wpr;
@@ -531,15 +620,18 @@ struct evsim_gpu_sim {
     c.words_per_block = ev.wpb;
     c.n_blocks = ev.n_blocks;
     c.n_interp = N;
-    c.prev = prev_f;
-    c.curr = curr_f;
+    c.n_pairs = n_pairs;
+    c.R = R;
+    c.r0 = r0;
+    c.frames = Ring<const uint8_t>{frames.as<uint8_t>(), P};
+    c.quads = Ring<const uint32_t>{quads.as<uint32_t>(), P};
     const int K = N + 2;
     c.alpha = consts.as<double>();
     c.oma = consts.as<double>() + K;
     c.fwd = reinterpret_cast<const float*>(consts.as<double>() + 2 * K);
     c.bwd = c.fwd + K;
-    c.full = full_desc();
-    c.direct = direct_desc();
+    c.P = P;
+    c.d = desc();
     c.log_mode = log_mode();
     c.magnitude = magnitude();
     c.c_pos = cfg.c_pos;
@@ -552,29 +644,27 @@ struct evsim_gpu_sim {
     c.mcount = ev.mcount.as<uint16_t>();
     c.wcount = ev.wcount.as<uint32_t>();
     c.counts = ev.counts.as<uint32_t>();
+    return c;
   }
 
-  // chain -> scan -> emit for the chain described by `c`, then queue the
-  // segment table readback.
-  void run_events(ChainParams& c, int provider, int64_t t_prev, int64_t t_curr) {
+  // segments -> chain -> offsets -> segbase + emit, then the segment-table
+  // readback.  ts: n_pairs + 1 frame timestamps.
+  void run_events(ChainParams& c, int provider, const int64_t* ts) {
+    const int G = c.d.n_links * c.n_pairs;
+    SegParams sp{};
+    sp.d = c.d;
+    sp.n_pairs = c.n_pairs;
+    sp.n_interp = c.n_interp;
+    sp.seg = ev.seg();
+    for (int i = 0; i <= c.n_pairs; ++i) sp.ts[i] = ts[i];
+    launch_segments(sp, stream);
+    CK_LAUNCH("segments");
     launch_chain(c, provider, stream);
     CK_LAUNCH("chain");
     mark(EVSIM_STAGE_SCAN);
-    ScanParams sp{};
-    sp.n_blocks = ev.n_blocks;
-    sp.counts = ev.counts.as<uint32_t>();
-    sp.d_direct = c.d_direct;
-    sp.full = c.full;
-    sp.direct = c.direct;
-    sp.n_interp = c.n_interp;
-    sp.t_prev = t_prev;
-    sp.t_curr = t_curr;
-    sp.seg = ev.seg();
-    sp.offsets = ev.offsets.as<int64_t>();
-    sp.seg_out = ev.seg_out.as<int64_t>();
-    sp.total = ev.total.as<int64_t>();
-    launch_scan(sp, stream);
-    CK_LAUNCH("scan");
+    OffsetParams op{G, ev.n_blocks, ev.counts.as<uint32_t>(), ev.prefix.as<int64_t>(), ev.link_total.as<int64_t>()};
+    launch_offsets(op, stream);
+    CK_LAUNCH("offsets");
     mark(EVSIM_STAGE_EMIT);
     EmitParams ep{};
     ep.w = w;
@@ -583,113 +673,119 @@ struct evsim_gpu_sim {
     ep.n_words = ev.n_words;
     ep.words_per_block = ev.wpb;
     ep.n_blocks = ev.n_blocks;
-    ep.d_direct = c.d_direct;
-    ep.full = c.full;
-    ep.direct = c.direct;
+    ep.n_links = G;
     ep.seg = ev.seg();
+    ep.prefix = ev.prefix.as<int64_t>();
+    ep.link_total = ev.link_total.as<int64_t>();
+    ep.seg_out = ev.seg_out.as<int64_t>();
     ep.magnitude = c.magnitude;
     ep.masks = ev.masks.as<uint2>();
     ep.mcount = ev.mcount.as<uint16_t>();
     ep.wcount = ev.wcount.as<uint32_t>();
-    ep.offsets = ev.offsets.as<int64_t>();
-    ep.total = ev.total.as<int64_t>();
     ep.capacity = ev.capacity;
     ep.out = ev.events.as<uint32_t>();
-    launch_emit(ep, stream);
+    launch_emit(ep, ev.segbase.as<int64_t>(), stream);
     CK_LAUNCH("emit");
-    launches += 3;
-    CK(cudaMemcpyAsync(h_seg_out, ev.seg_out.p, (3 + 2 * (size_t)ev.max_links) * sizeof(int64_t),
-                       cudaMemcpyDeviceToHost, stream));
-    last_chain = c;
-    last_scan = sp;
+    launches += 6;
+    CK(cudaMemcpyAsync(h_seg_out, ev.seg_out.p, (3 + 2 * (size_t)G) * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                       stream));
     last_emit = ep;
-    last_provider = provider;
     pending = true;
   }
 
-  void upload(const uint8_t* pixels, int dst_slot, bool on_device) {
-    CK(cudaMemcpyAsync(frames[dst_slot].p, pixels, (size_t)w * h,
-                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream));
-  }
-
-  // Simulator::push_frame  src/simulate.cpp:306-347
-  void push(const uint8_t* pixels, int fw, int fh, int64_t t, bool on_device) {
-    if (fw <= 0 || fh <= 0 || !pixels) invalid("push_frame: malformed frame");
+  // ---- push ----------------------------------------------------------------
+  // Simulator::push_frame (src/simulate.cpp:306-347) applied to F frames in
+  // order; the whole batch is validated first and rejected atomically.
+  void push(const uint8_t* pixels, int F, int fw, int fh, const int64_t* ts, bool on_device) {
+    if (F < 1) invalid("push_frames: n_frames must be >= 1");
+    if (fw <= 0 || fh <= 0 || !pixels || !ts) invalid("push_frame: malformed frame");
     if (has_prev) {
       if (fw != w || fh != h) invalid("push_frame: frame dimensions changed mid-stream");
-      if (t <= prev_t) invalid("push_frame: timestamps must be strictly increasing");
+      if (ts[0] <= prev_t) invalid("push_frame: timestamps must be strictly increasing");
     }
+    for (int j = 1; j < F; ++j)
+      if (ts[j] <= ts[j - 1]) invalid("push_frame: timestamps must be strictly increasing");
     if (fh > 32768 || fw > 65536) invalid("push_frame: frame larger than 65536 x 32768 is not supported");
-    if ((int64_t)fw * fh >= (int64_t)1 << 32) invalid("push_frame: frame too large");
+    if ((int64_t)fw * fh >= (int64_t)1 << 24 && cfg.method == EVSIM_METHOD_SPARSE)
+      invalid("push_frame: frames of 2^24 pixels or more are not supported by the sparse method");
+    if ((int64_t)fw * fh >= (int64_t)1 << 31) invalid("push_frame: frame too large");
+    const int L = desc().n_links;
+    if (F > max_batch_for(L)) invalid("push_frames: batch too large (max " + std::to_string(max_batch_for(L)) + ")");
     CK(cudaSetDevice(device));
-    // A queued single-mode result is simply superseded (stream order keeps
-    // the device buffers consistent); magnitude mode may need a re-emit, so
-    // it is completed first.
+    // A queued single-mode result is superseded (stream order keeps the
+    // device buffers consistent); magnitude mode may need a re-emit.
     if (pending) {
       if (magnitude()) finish();
       else pending = false;
     }
     if (!has_prev && (fw != w || fh != h)) allocate(fw, fh);
+    const int n_pairs = has_prev ? F : F - 1;
+    ensure_capacity(std::max(n_pairs, 1));
 
-    const int cur = has_prev ? 1 - slot : slot;
+    const size_t P = (size_t)w * h;
+    const int base = has_prev ? (rhead + 1) % R : rhead;  // ring slot of frame 0 of the batch
     begin_group();
     mark(EVSIM_STAGE_UPLOAD);
-    upload(pixels, cur, on_device);
+    {
+      // upload into the ring (at most two contiguous runs)
+      const int first = std::min(F, R - base);
+      const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+      CK(cudaMemcpyAsync(frames.as<uint8_t>() + (size_t)base * P, pixels, (size_t)first * P, kind, stream));
+      if (first < F)
+        CK(cudaMemcpyAsync(frames.as<uint8_t>(), pixels + (size_t)first * P, (size_t)(F - first) * P, kind, stream));
+    }
     mark(EVSIM_STAGE_PYRAMID);
-    const int N = n_interp_eff();
-    const bool dense_flow = cfg.method == EVSIM_METHOD_DENSE && N > 0;
-    const bool sparse_flow = cfg.method == EVSIM_METHOD_SPARSE && N > 0;
-    if (dense_flow) {
-      launch_build_quad(frames[cur].as<uint8_t>(), quads[cur].as<uint32_t>(), w, h, stream);
+    if (uses_flow()) {
+      PyramidParams pp = flow.pyramid_params(frames.as<uint8_t>(), P, dense_flow() ? quads.as<uint32_t>() : nullptr, base);
+      launch_pyramid(pp, F, stream);
+      CK_LAUNCH("pyramid");
+      launches += flow.levels;
+    }
+    if (!has_prev && log_mode()) {
+      // warm-up frame: ref := L(frame0)
+      launch_init_ref(frames.as<uint8_t>() + (size_t)base * P, lut.as<float>(), ref.as<float>(), (int64_t)P, stream);
+      CK_LAUNCH("init_ref");
       ++launches;
     }
-    if (dense_flow || sparse_flow) launches += flow.build_pyramid(frames[cur].as<uint8_t>(), cur, stream);
     mark(EVSIM_STAGE_FLOW);
-
-    if (!has_prev) {
-      // warm-up frame: no events, state := frame (simulate.cpp:341)
-      if (log_mode()) {
-        launch_init_ref(frames[cur].as<uint8_t>(), lut.as<float>(), ref.as<float>(), (int64_t)w * h, stream);
-        CK_LAUNCH("init_ref");
-        ++launches;
+    const int r0 = has_prev ? rhead : base;
+    std::vector<int64_t> pts(n_pairs + 1);
+    if (has_prev) {
+      pts[0] = prev_t;
+      for (int j = 0; j < F; ++j) pts[j + 1] = ts[j];
+    } else {
+      for (int j = 0; j < F; ++j) pts[j] = ts[j];
+    }
+    if (n_pairs > 0) {
+      ChainParams c = chain_params(r0, n_pairs);
+      int provider = kProvNone;
+      if (dense_flow()) {
+        // simulate_dense -> PyramidalPatchFlow -> dense_events_with_flow (simulate.cpp:130-143)
+        launches += flow.solve(r0, n_pairs, stream);
+        c.g0 = flow.geom[0];
+        provider = kProvDenseGrid;
+      } else if (sparse_flow()) {
+        sparse_stage(r0, n_pairs, c);
+        provider = kProvSparse;
       }
-      end_group();
-      has_prev = true;
-      slot = cur;
-      prev_t = t;
+      mark(EVSIM_STAGE_CHAIN);
+      run_events(c, provider, pts.data());
+    } else {
       seg_t.clear();
       seg_off.assign(1, 0);
       n_events = 0;
       pending = false;
-      return;
     }
-
-    const uint8_t* pf = frames[slot].as<uint8_t>();
-    const uint8_t* cf = frames[cur].as<uint8_t>();
-    ChainParams c{};
-    fill_chain(c, pf, cf);
-    int provider = kProvNone;
-    if (dense_flow) {
-      // simulate_dense -> PyramidalPatchFlow -> dense_events_with_flow (simulate.cpp:130-143)
-      launches += flow.solve(slot, cur, stream);
-      c.g0 = flow.geom[0];
-      c.qprev = quads[slot].as<uint32_t>();
-      c.qcurr = quads[cur].as<uint32_t>();
-      provider = kProvDenseGrid;
-    } else if (sparse_flow) {
-      sparse_stage(pf, cf, c);
-      provider = kProvSparse;
-    }
-    mark(EVSIM_STAGE_CHAIN);
-    run_events(c, provider, prev_t, t);
     end_group();
-    slot = cur;
-    prev_t = t;
+    rhead = (base + F - 1) % R;
+    prev_t = ts[F - 1];
+    has_prev = true;
   }
 
-  // simulate_sparse up to the intermediates (simulate.cpp:145-199)
-  void sparse_stage(const uint8_t* pf, const uint8_t* cf, ChainParams& c) {
+  // simulate_sparse up to the intermediates (simulate.cpp:145-199), all pairs
+  void sparse_stage(int r0, int n_pairs, ChainParams& c) {
     const int N = n_interp_eff();
+    const size_t P = (size_t)w * h;
     SelectParams sp{};
     sp.w = w;
     sp.h = h;
@@ -697,65 +793,61 @@ struct evsim_gpu_sim {
     sp.n_words = ev.n_words;
     sp.words_per_block = ev.wpb;
     sp.n_blocks = ev.n_blocks;
-    sp.prev = pf;
-    sp.curr = cf;
+    sp.R = R;
+    sp.r0 = r0;
+    sp.frames = Ring<const uint8_t>{frames.as<uint8_t>(), P};
     sp.log_mode = log_mode();
     sp.sel = cfg.selection_threshold > 0 ? cfg.selection_threshold : cfg.c_pos;  // types.hpp:122-124
     sp.sel_log = cfg.sel_log > 0.0f ? cfg.sel_log : cfg.c_pos_log;
     sp.lut = lut.as<float>();
     sp.masks = sel_masks.as<uint32_t>();
     sp.counts = sel_counts.as<uint32_t>();
-    sp.offsets = sel_offsets.as<int64_t>();
     sp.points = points.as<uint32_t>();
     sp.n_points = n_points.as<int>();
-    launch_select(sp, stream);
-    // one single-link segment over the block counts
-    ScanParams sc{};
-    sc.n_blocks = ev.n_blocks;
-    sc.counts = sel_counts.as<uint32_t>();
-    sc.full = ChainDesc{0, 1, 1};
-    sc.direct = sc.full;
-    sc.n_interp = 0;
-    sc.t_prev = 0;
-    sc.t_curr = 1;
-    char* b = sel_segtab.as<char>();
-    sc.seg = SegTable{reinterpret_cast<int*>(b), reinterpret_cast<int*>(b + 8), reinterpret_cast<int*>(b + 16),
-                      reinterpret_cast<int64_t*>(b + 24)};
-    sc.offsets = sel_offsets.as<int64_t>();
-    sc.seg_out = sel_seg_out.as<int64_t>();
-    sc.total = sel_total.as<int64_t>();
-    launch_scan(sc, stream);
-    launch_select_emit(sp, sel_total.as<int64_t>(), stream);
+    sp.P = P;
+    launch_select(sp, n_pairs, stream);
     CK_LAUNCH("select");
     // estimate_sparse_flow (flow.cpp:278-381)
-    SparseLKParams lk = flow.sparse_params(slot, 1 - slot);
+    SparseLKParams lk = flow.sparse_params(r0);
     lk.points = points.as<uint32_t>();
     lk.n_points = n_points.as<int>();
     lk.disp = disp.as<float2>();
     lk.status = status.as<uint8_t>();
-    launch_sparse_lk(lk, w * h, stream);
+    launch_sparse_lk(lk, (int)std::min<size_t>(P, INT32_MAX), n_pairs, stream);
     CK_LAUNCH("sparse_lk");
+    splat_stage(r0, n_pairs, c);
+    launches += 3;
+    (void)N;
+  }
+
+  void splat_stage(int r0, int n_pairs, ChainParams& c) {
+    const int N = n_interp_eff();
+    const size_t P = (size_t)w * h;
     SplatParams spl{};
     spl.w = w;
     spl.h = h;
     spl.n_interp = N;
+    spl.R = R;
+    spl.r0 = r0;
+    spl.frames = Ring<const uint8_t>{frames.as<uint8_t>(), P};
     spl.points = points.as<uint32_t>();
     spl.n_points = n_points.as<int>();
     spl.disp = disp.as<float2>();
     spl.status = status.as<uint8_t>();
-    spl.prev = pf;
-    spl.claims = claims.as<uint64_t>();
+    spl.claims = claims.as<uint32_t>();
     spl.touched = touched.as<uint32_t>();
-    const int64_t items = (int64_t)w * h * N;
-    launch_splat(spl, (int)std::min<int64_t>(items, INT32_MAX), stream);
+    spl.P = P;
+    launch_splat(spl, (int)std::min<int64_t>((int64_t)P * N, INT32_MAX), n_pairs, stream);
     CK_LAUNCH("splat");
-    launches += 6;
-    c.claims = claims.as<uint64_t>();
+    c.claims = claims.as<uint32_t>();
     c.touched = touched.as<uint32_t>();
-    c.claims_rw = claims.as<uint64_t>();
-    c.touched_rw = touched.as<uint32_t>();
     c.points = points.as<uint32_t>();
-    c.d_direct = n_points.as<int>();  // M == 0 -> chain_pipeline(prev, curr, {}) (simulate.cpp:161-163)
+    c.n_points = n_points.as<int>();
+    // chain_pipeline(prev, curr, {}) when nothing was selected
+    // (simulate.cpp:161-163) equals the full chain over copies of prev,
+    // except in log mode without endpoints, where it emits nothing
+    //
+    c.skip_empty = log_mode() && !cfg.include_endpoints;
   }
 
   // Complete the queued push: wait, read the segment table, re-emit when the
@@ -770,13 +862,22 @@ struct evsim_gpu_sim {
       ev.grow(total + total / 4, stream);
       last_emit.capacity = ev.capacity;
       last_emit.out = ev.events.as<uint32_t>();
-      launch_emit(last_emit, stream);
+      launch_emit(last_emit, ev.segbase.as<int64_t>(), stream);
       CK_LAUNCH("emit");
-      ++launches;
+      launches += 2;
       CK(cudaStreamSynchronize(stream));
     }
-    seg_t.assign(h_seg_out + 1, h_seg_out + 1 + S);
-    seg_off.assign(h_seg_out + 1 + S, h_seg_out + 2 + 2 * S);
+    // report only the segments that hold events
+    seg_t.clear();
+    seg_off.clear();
+    for (int s = 0; s < S; ++s) {
+      const int64_t a = h_seg_out[1 + S + s], b = h_seg_out[2 + S + s];
+      if (b > a) {
+        seg_t.push_back(h_seg_out[1 + s]);
+        seg_off.push_back(a);
+      }
+    }
+    seg_off.push_back(total);
     n_events = total;
   }
 
@@ -793,6 +894,22 @@ struct evsim_gpu_sim {
 };
 
 // ====================================================================== C-ABI
+
+namespace {
+
+void make_sim(evsim_gpu_sim* s, const evsim_gpu_config& cfg, int device) {
+  s->cfg = cfg;
+  s->preset = resolve_preset(cfg);
+  s->device = device;
+  CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  float h_lut[256];
+  log_lut(h_lut);
+  s->lut.ensure(sizeof h_lut, s->stream);
+  CK(cudaMemcpyAsync(s->lut.p, h_lut, sizeof h_lut, cudaMemcpyHostToDevice, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -836,23 +953,14 @@ int evsim_gpu_create(const evsim_gpu_config* cfg, int device, evsim_gpu_sim** ou
     validate_config(*cfg);
     if (cfg->method == EVSIM_METHOD_DIFFERENCE_INTERP)
       runtime("evsim_gpu_create: difference_interp is outside the B200 hot path (SURVEY.md §8f)");
-    const Preset preset = resolve_preset(*cfg);
-    validate_preset(preset);
+    validate_preset(resolve_preset(*cfg));
     int n = 0;
     CK(cudaGetDeviceCount(&n));
     if (device < 0 || device >= n) invalid("evsim_gpu_create: no such CUDA device");
     CK(cudaSetDevice(device));
     init_pool(device);
     auto s = std::make_unique<evsim_gpu_sim>();
-    s->cfg = *cfg;
-    s->preset = preset;
-    s->device = device;
-    CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-    float h_lut[256];
-    log_lut(h_lut);
-    s->lut.ensure(sizeof h_lut, s->stream);
-    CK(cudaMemcpyAsync(s->lut.p, h_lut, sizeof h_lut, cudaMemcpyHostToDevice, s->stream));
-    CK(cudaStreamSynchronize(s->stream));
+    make_sim(s.get(), *cfg, device);
     *out = s.release();
   });
 }
@@ -861,7 +969,17 @@ int evsim_gpu_push_frame(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t widt
                          int32_t pixels_on_device, evsim_gpu_events* out) {
   return guarded([&] {
     if (!sim) invalid("evsim_gpu_push_frame: null simulator");
-    sim->push(pixels, width, height, t_us, pixels_on_device != 0);
+    sim->push(pixels, 1, width, height, &t_us, pixels_on_device != 0);
+    sim->finish();
+    sim->fill_out(out);
+  });
+}
+
+int evsim_gpu_push_frames(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t n_frames, int32_t width,
+                          int32_t height, const int64_t* t_us, int32_t pixels_on_device, evsim_gpu_events* out) {
+  return guarded([&] {
+    if (!sim) invalid("evsim_gpu_push_frames: null simulator");
+    sim->push(pixels, n_frames, width, height, t_us, pixels_on_device != 0);
     sim->finish();
     sim->fill_out(out);
   });
@@ -871,8 +989,21 @@ int evsim_gpu_push_frame_async(evsim_gpu_sim* sim, const uint8_t* pixels, int32_
                                int64_t t_us, int32_t pixels_on_device) {
   return guarded([&] {
     if (!sim) invalid("evsim_gpu_push_frame_async: null simulator");
-    sim->push(pixels, width, height, t_us, pixels_on_device != 0);
+    sim->push(pixels, 1, width, height, &t_us, pixels_on_device != 0);
   });
+}
+
+int evsim_gpu_push_frames_async(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t n_frames, int32_t width,
+                                int32_t height, const int64_t* t_us, int32_t pixels_on_device) {
+  return guarded([&] {
+    if (!sim) invalid("evsim_gpu_push_frames_async: null simulator");
+    sim->push(pixels, n_frames, width, height, t_us, pixels_on_device != 0);
+  });
+}
+
+int evsim_gpu_max_batch(const evsim_gpu_sim* sim) {
+  if (!sim) return 0;
+  return max_batch_for(sim->desc().n_links);
 }
 
 int evsim_gpu_sync(evsim_gpu_sim* sim, evsim_gpu_events* out) {
@@ -961,27 +1092,22 @@ int evsim_gpu_stage_times(evsim_gpu_sim* sim, double* ms, int32_t n_stages, int6
 
 namespace {
 
-// Scratch simulator for the free functions: dense or sparse pipeline on an
-// explicit (prev, curr) pair.
-std::unique_ptr<evsim_gpu_sim> scratch(const evsim_gpu_config& cfg, int w, int h) {
-  CK(cudaSetDevice(0));
-  init_pool(0);
-  auto s = std::make_unique<evsim_gpu_sim>();
-  s->cfg = cfg;
-  s->preset = resolve_preset(cfg);
-  s->device = 0;
-  CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-  float h_lut[256];
-  log_lut(h_lut);
-  s->lut.ensure(sizeof h_lut, s->stream);
-  CK(cudaMemcpyAsync(s->lut.p, h_lut, sizeof h_lut, cudaMemcpyHostToDevice, s->stream));
-  s->allocate(w, h);
-  return s;
-}
-
-struct ScratchGuard {
+// Scratch simulator for the free functions: one (prev, curr) pair in ring
+// slots 0 and 1.
+struct Scratch {
   std::unique_ptr<evsim_gpu_sim> s;
-  ~ScratchGuard() {
+  Scratch(const evsim_gpu_config& cfg, int w, int h, const uint8_t* prev, const uint8_t* curr) {
+    CK(cudaSetDevice(0));
+    init_pool(0);
+    s = std::make_unique<evsim_gpu_sim>();
+    make_sim(s.get(), cfg, 0);
+    s->allocate(w, h);
+    s->ensure_capacity(1);
+    const size_t P = (size_t)w * h;
+    CK(cudaMemcpyAsync(s->frames.p, prev, P, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaMemcpyAsync(s->frames.as<uint8_t>() + P, curr, P, cudaMemcpyHostToDevice, s->stream));
+  }
+  ~Scratch() {
     if (s) {
       cudaStream_t st = s->stream;
       cudaStreamSynchronize(st);
@@ -989,6 +1115,13 @@ struct ScratchGuard {
       cudaStreamSynchronize(st);
       cudaStreamDestroy(st);
     }
+  }
+  evsim_gpu_sim* operator->() { return s.get(); }
+  void pyramids() {
+    PyramidParams pp = s->flow.pyramid_params(s->frames.as<uint8_t>(), (size_t)s->w * s->h,
+                                              s->dense_flow() ? s->quads.as<uint32_t>() : nullptr, 0);
+    launch_pyramid(pp, 2, s->stream);
+    CK_LAUNCH("pyramid");
   }
 };
 
@@ -1020,12 +1153,8 @@ int evsim_gpu_dense_flow(const uint8_t* prev, const uint8_t* curr, int32_t w, in
     cfg.pyramid_levels = levels;
     cfg.iterations_per_level = iterations;
     cfg.patch_radius = radius;
-    ScratchGuard g{scratch(cfg, w, h)};
-    evsim_gpu_sim* s = g.s.get();
-    CK(cudaMemcpyAsync(s->frames[0].p, prev, (size_t)w * h, cudaMemcpyHostToDevice, s->stream));
-    CK(cudaMemcpyAsync(s->frames[1].p, curr, (size_t)w * h, cudaMemcpyHostToDevice, s->stream));
-    s->flow.build_pyramid(s->frames[0].as<uint8_t>(), 0, s->stream);
-    s->flow.build_pyramid(s->frames[1].as<uint8_t>(), 1, s->stream);
+    Scratch s(cfg, w, h, prev, curr);
+    s.pyramids();
     s->flow.solve(0, 1, s->stream);
     DevBuf field;
     field.ensure((size_t)w * h * 8, s->stream);
@@ -1056,27 +1185,24 @@ int evsim_gpu_sparse_flow(const uint8_t* prev, const uint8_t* curr, int32_t w, i
     if (n_points == 0) return;
     evsim_gpu_config cfg;
     evsim_gpu_config_defaults(EVSIM_METHOD_SPARSE, &cfg);
+    cfg.n_interp = 1;
     cfg.pyramid_levels = levels;
     cfg.iterations_per_level = iterations;
     cfg.patch_radius = radius;
-    ScratchGuard g{scratch(cfg, w, h)};
-    evsim_gpu_sim* s = g.s.get();
-    CK(cudaMemcpyAsync(s->frames[0].p, prev, (size_t)w * h, cudaMemcpyHostToDevice, s->stream));
-    CK(cudaMemcpyAsync(s->frames[1].p, curr, (size_t)w * h, cudaMemcpyHostToDevice, s->stream));
-    s->flow.build_pyramid(s->frames[0].as<uint8_t>(), 0, s->stream);
-    s->flow.build_pyramid(s->frames[1].as<uint8_t>(), 1, s->stream);
+    Scratch s(cfg, w, h, prev, curr);
+    s.pyramids();
     DevBuf dpts, ddisp, dst;
     dpts.ensure((size_t)n_points * 4, s->stream);
     ddisp.ensure((size_t)n_points * 8, s->stream);
     dst.ensure((size_t)n_points, s->stream);
     CK(cudaMemcpyAsync(dpts.p, idx.data(), (size_t)n_points * 4, cudaMemcpyHostToDevice, s->stream));
-    SparseLKParams lk = s->flow.sparse_params(0, 1);
+    SparseLKParams lk = s->flow.sparse_params(0);
     lk.points = dpts.as<uint32_t>();
     lk.n_points = nullptr;
     lk.n_points_host = n_points;
     lk.disp = ddisp.as<float2>();
     lk.status = dst.as<uint8_t>();
-    launch_sparse_lk(lk, (int)std::min<int64_t>(n_points, INT32_MAX), s->stream);
+    launch_sparse_lk(lk, (int)std::min<int64_t>(n_points, INT32_MAX), 1, s->stream);
     CK_LAUNCH("sparse_lk");
     CK(cudaMemcpyAsync(disp, ddisp.p, (size_t)n_points * 8, cudaMemcpyDeviceToHost, s->stream));
     CK(cudaMemcpyAsync(status, dst.p, (size_t)n_points, cudaMemcpyDeviceToHost, s->stream));
@@ -1095,22 +1221,16 @@ int evsim_gpu_interpolate_frames(const uint8_t* prev, const uint8_t* curr, int32
     evsim_gpu_config cfg;
     evsim_gpu_config_defaults(EVSIM_METHOD_DENSE, &cfg);
     cfg.n_interp = n;
-    ScratchGuard g{scratch(cfg, w, h)};
-    evsim_gpu_sim* s = g.s.get();
+    Scratch s(cfg, w, h, prev, curr);
     const size_t P = (size_t)w * h;
-    CK(cudaMemcpyAsync(s->frames[0].p, prev, P, cudaMemcpyHostToDevice, s->stream));
-    CK(cudaMemcpyAsync(s->frames[1].p, curr, P, cudaMemcpyHostToDevice, s->stream));
-    launch_build_quad(s->frames[0].as<uint8_t>(), s->quads[0].as<uint32_t>(), w, h, s->stream);
-    launch_build_quad(s->frames[1].as<uint8_t>(), s->quads[1].as<uint32_t>(), w, h, s->stream);
+    launch_build_quad(s->frames.as<uint8_t>(), s->quads.as<uint32_t>(), w, h, s->stream);
+    launch_build_quad(s->frames.as<uint8_t>() + P, s->quads.as<uint32_t>() + P, w, h, s->stream);
     DevBuf field, dout;
     field.ensure(P * 8, s->stream);
     dout.ensure(P * n, s->stream);
     CK(cudaMemcpyAsync(field.p, du, P * 4, cudaMemcpyHostToDevice, s->stream));
     CK(cudaMemcpyAsync(field.as<float>() + P, dv, P * 4, cudaMemcpyHostToDevice, s->stream));
-    ChainParams c{};
-    s->fill_chain(c, s->frames[0].as<uint8_t>(), s->frames[1].as<uint8_t>());
-    c.qprev = s->quads[0].as<uint32_t>();
-    c.qcurr = s->quads[1].as<uint32_t>();
+    ChainParams c = s->chain_params(0, 1);
     c.du = field.as<float>();
     c.dv = field.as<float>() + P;
     launch_interp_frames(c, dout.as<uint8_t>(), s->stream);
@@ -1131,32 +1251,25 @@ int evsim_gpu_dense_events_with_flow(const uint8_t* prev, const uint8_t* curr, i
     check_frames(prev, curr, w, h, "dense_events_with_flow");
     evsim_gpu_config cfg = *cfg_in;
     cfg.method = EVSIM_METHOD_DENSE;
-    ScratchGuard g{scratch(cfg, w, h)};
-    evsim_gpu_sim* s = g.s.get();
+    Scratch s(cfg, w, h, prev, curr);
     const size_t P = (size_t)w * h;
-    CK(cudaMemcpyAsync(s->frames[0].p, prev, P, cudaMemcpyHostToDevice, s->stream));
-    CK(cudaMemcpyAsync(s->frames[1].p, curr, P, cudaMemcpyHostToDevice, s->stream));
-    ChainParams c{};
-    s->fill_chain(c, s->frames[0].as<uint8_t>(), s->frames[1].as<uint8_t>());
+    ChainParams c = s->chain_params(0, 1);
     DevBuf field;
     int provider = kProvNone;
     if (cfg.n_interp > 0) {
-      s->quads[0].ensure(P * 4, s->stream);
-      s->quads[1].ensure(P * 4, s->stream);
-      launch_build_quad(s->frames[0].as<uint8_t>(), s->quads[0].as<uint32_t>(), w, h, s->stream);
-      launch_build_quad(s->frames[1].as<uint8_t>(), s->quads[1].as<uint32_t>(), w, h, s->stream);
+      launch_build_quad(s->frames.as<uint8_t>(), s->quads.as<uint32_t>(), w, h, s->stream);
+      launch_build_quad(s->frames.as<uint8_t>() + P, s->quads.as<uint32_t>() + P, w, h, s->stream);
       field.ensure(P * 8, s->stream);
       CK(cudaMemcpyAsync(field.p, du, P * 4, cudaMemcpyHostToDevice, s->stream));
       CK(cudaMemcpyAsync(field.as<float>() + P, dv, P * 4, cudaMemcpyHostToDevice, s->stream));
-      c.qprev = s->quads[0].as<uint32_t>();
-      c.qcurr = s->quads[1].as<uint32_t>();
       c.du = field.as<float>();
       c.dv = field.as<float>() + P;
       provider = kProvDenseField;
     }
-    s->run_events(c, provider, t_prev, t_curr);
+    const int64_t ts[2] = {t_prev, t_curr};
+    s->run_events(c, provider, ts);
     s->finish();
-    copy_events24(s, events, capacity, n_events);
+    copy_events24(s.s.get(), events, capacity, n_events);
   });
 }
 
@@ -1172,15 +1285,12 @@ int evsim_gpu_sparse_events_with_flow(const uint8_t* prev, const uint8_t* curr, 
     check_frames(prev, curr, w, h, "simulate_sparse");
     evsim_gpu_config cfg = *cfg_in;
     cfg.method = EVSIM_METHOD_SPARSE;
-    ScratchGuard g{scratch(cfg, w, h)};
-    evsim_gpu_sim* s = g.s.get();
-    const size_t P = (size_t)w * h;
-    CK(cudaMemcpyAsync(s->frames[0].p, prev, P, cudaMemcpyHostToDevice, s->stream));
-    CK(cudaMemcpyAsync(s->frames[1].p, curr, P, cudaMemcpyHostToDevice, s->stream));
-    ChainParams c{};
-    s->fill_chain(c, s->frames[0].as<uint8_t>(), s->frames[1].as<uint8_t>());
+    const bool with_points = cfg.n_interp > 0 && n_points > 0;
+    if (!with_points) cfg.n_interp = 0;  // chain_pipeline(prev, curr, {}) (simulate.cpp:161-163)
+    Scratch s(cfg, w, h, prev, curr);
+    ChainParams c = s->chain_params(0, 1);
     int provider = kProvNone;
-    if (cfg.n_interp > 0 && n_points > 0) {
+    if (with_points) {
       std::vector<uint32_t> idx((size_t)n_points);
       for (int64_t i = 0; i < n_points; ++i) {
         const int x = pts[2 * i], y = pts[2 * i + 1];
@@ -1192,33 +1302,14 @@ int evsim_gpu_sparse_events_with_flow(const uint8_t* prev, const uint8_t* curr, 
       CK(cudaMemcpyAsync(s->n_points.p, &np, sizeof np, cudaMemcpyHostToDevice, s->stream));
       CK(cudaMemcpyAsync(s->disp.p, disp, (size_t)n_points * 8, cudaMemcpyHostToDevice, s->stream));
       CK(cudaMemcpyAsync(s->status.p, st, (size_t)n_points, cudaMemcpyHostToDevice, s->stream));
-      SplatParams spl{};
-      spl.w = w;
-      spl.h = h;
-      spl.n_interp = cfg.n_interp;
-      spl.points = s->points.as<uint32_t>();
-      spl.n_points = s->n_points.as<int>();
-      spl.disp = s->disp.as<float2>();
-      spl.status = s->status.as<uint8_t>();
-      spl.prev = s->frames[0].as<uint8_t>();
-      spl.claims = s->claims.as<uint64_t>();
-      spl.touched = s->touched.as<uint32_t>();
-      launch_splat(spl, (int)std::min<int64_t>(n_points * cfg.n_interp, INT32_MAX), s->stream);
-      CK_LAUNCH("splat");
-      c.claims = s->claims.as<uint64_t>();
-      c.touched = s->touched.as<uint32_t>();
-      c.claims_rw = s->claims.as<uint64_t>();
-      c.touched_rw = s->touched.as<uint32_t>();
-      c.points = s->points.as<uint32_t>();
-      c.d_direct = s->n_points.as<int>();
+      s->splat_stage(0, 1, c);
       provider = kProvSparse;
       CK(cudaStreamSynchronize(s->stream));  // host staging (np, idx) must outlive the copies
-    } else {
-      c.full = c.direct;
     }
-    s->run_events(c, provider, t_prev, t_curr);
+    const int64_t ts[2] = {t_prev, t_curr};
+    s->run_events(c, provider, ts);
     s->finish();
-    copy_events24(s, events, capacity, n_events);
+    copy_events24(s.s.get(), events, capacity, n_events);
   });
 }
 

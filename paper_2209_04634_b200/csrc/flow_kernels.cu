@@ -3,8 +3,9 @@
 //
 // Replaces src/flow.cpp of the reference (/root/reference/proj).  Every
 // float/double operation keeps the reference's operation order and rounding
-// (see evsim_device.cuh); fp64 sums are accumulated in the reference's k-order
-// by one thread per patch / point, so results are bit-identical.
+// (see evsim_device.cuh); fp64 sums that are not exact are accumulated in the
+// reference's k-order by one thread per patch / point, so results are
+// bit-identical.
 #include "evsim_device.cuh"
 #include "kernels.h"
 
@@ -12,28 +13,49 @@ namespace evsim_gpu {
 
 // ---------------------------------------------------------------- pyramid
 
-// to_float  flow.cpp:23-27
-__global__ void to_float_kernel(const uint8_t* __restrict__ src, float* __restrict__ dst, int64_t n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) dst[i] = (float)src[i];
-}
-
-// downsample  flow.cpp:30-42: 0.25f * (((a + b) + c) + d), odd edges replicate
-__global__ void downsample_kernel(const float* __restrict__ src, LevelDims sd, float* __restrict__ dst,
-                                  LevelDims dd) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y * blockDim.y + threadIdx.y;
-  if (x >= dd.w || y >= dd.h) return;
+// One pyramid level of one frame: the fp32 level image (to_float /
+// downsample, flow.cpp:23-42) and its QUAD image — per pixel the four taps
+// sample() reads (flow.cpp:45-57): (x0,y0) (x1,y0) (x0,y1) (x1,y1) with the
+// replicate clamp — so a bilinear sample is one 16-byte gather.  Level 0 also
+// writes the u8 quad used by sample_u8 in the interpolation.
+__device__ __forceinline__ float level_value(const uint8_t* __restrict__ f0, const float* __restrict__ src,
+                                             LevelDims sd, int x, int y, bool level0) {
+  if (level0) return (float)f0[(size_t)y * sd.w + x];
+  // downsample  flow.cpp:30-42: 0.25f * (((a + b) + c) + d), odd edges replicate
   const int x0 = 2 * x, y0 = 2 * y;
   const int x1 = min(2 * x + 1, sd.w - 1);
   const int y1 = min(2 * y + 1, sd.h - 1);
   const float* r0 = src + (size_t)y0 * sd.w;
   const float* r1 = src + (size_t)y1 * sd.w;
-  const float s = fadd(fadd(fadd(r0[x0], r0[x1]), r1[x0]), r1[x1]);
-  dst[(size_t)y * dd.w + x] = fmul(0.25f, s);
+  return fmul(0.25f, fadd(fadd(fadd(r0[x0], r0[x1]), r1[x0]), r1[x1]));
 }
 
-// Quad image: the four bilinear taps of sample_u8 (simulate.cpp:10-26) per pixel.
+__global__ void pyramid_level_kernel(PyramidParams p, int l) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  const LevelDims dd = p.dims[l];
+  if (x >= dd.w) return;
+  const int slot = (p.slot0 + (int)blockIdx.z) % p.R;
+  const bool level0 = l == 0;
+  const uint8_t* f0 = p.frames.at(slot);
+  const float* src = level0 ? nullptr : p.pyr[l - 1].at(slot);
+  const int x1 = min(x + 1, dd.w - 1), y1 = min(y + 1, dd.h - 1);
+  // level-0 reads the u8 frame at the level's own coordinates
+  const LevelDims rd = level0 ? dd : p.dims[l - 1];
+  const float a00 = level_value(f0, src, rd, x, y, level0);
+  const float a10 = level_value(f0, src, rd, x1, y, level0);
+  const float a01 = level_value(f0, src, rd, x, y1, level0);
+  const float a11 = level_value(f0, src, rd, x1, y1, level0);
+  const size_t i = (size_t)y * dd.w + x;
+  p.pyr[l].at(slot)[i] = a00;
+  p.qpyr[l].at(slot)[i] = make_float4(a00, a10, a01, a11);
+  if (level0 && p.quad_u8.base) {
+    p.quad_u8.at(slot)[i] =
+        (uint32_t)a00 | ((uint32_t)a10 << 8) | ((uint32_t)a01 << 16) | ((uint32_t)a11 << 24);
+  }
+}
+
+// Quad image of a u8 frame only (stateless interpolation entry point).
 __global__ void build_quad_kernel(const uint8_t* __restrict__ src, uint32_t* __restrict__ dst, int w, int h) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y;
@@ -44,6 +66,20 @@ __global__ void build_quad_kernel(const uint8_t* __restrict__ src, uint32_t* __r
   const uint8_t* r1 = src + (size_t)y1 * w;
   dst[(size_t)y * w + x] = (uint32_t)r0[x] | ((uint32_t)r0[x1] << 8) | ((uint32_t)r1[x] << 16) |
                            ((uint32_t)r1[x1] << 24);
+}
+
+// sample() (flow.cpp:45-57) through a quad image: one 16-byte gather.
+__device__ __forceinline__ float sample_quadf(const float4* __restrict__ q, int w, int h, float x, float y) {
+  x = clamp_ref(x, 0.0f, (float)(w - 1));
+  y = clamp_ref(y, 0.0f, (float)(h - 1));
+  const int x0 = (int)x;
+  const int y0 = (int)y;
+  const float fx = fsub(x, (float)x0);
+  const float fy = fsub(y, (float)y0);
+  const float4 a = __ldg(q + (size_t)y0 * w + x0);
+  const float top = lerp_ref(a.x, a.y, fx);
+  const float bot = lerp_ref(a.z, a.w, fx);
+  return lerp_ref(top, bot, fy);
 }
 
 // ---------------------------------------------------------------- dense LK
@@ -69,7 +105,8 @@ __device__ __forceinline__ void densify_at(const GridGeom& g, int x, int y, floa
 }
 
 // upsample_flow evaluated at one fine pixel (flow.cpp:130-147): bilinear
-// sample of the densified coarse field, divided by the level ratio.
+// sample of the densified coarse field, divided by the level ratio.  Only
+// the values at the patch centres are ever read by solve_level (:174-175).
 __device__ __forceinline__ void upsample_at(const GridGeom& c, int fw, int fh, int x, int y, float& u,
                                             float& v) {
   const float rx = __fdiv_rn((float)c.w, (float)fw);
@@ -97,11 +134,217 @@ __device__ __forceinline__ float grad_y(const float* __restrict__ im, int w, int
   return fmul(0.5f, fsub(__ldg(im + (size_t)min(y + 1, h - 1) * w + x), __ldg(im + (size_t)max(y - 1, 0) * w + x)));
 }
 
-// solve_level's per-patch loop (flow.cpp:170-215), one thread per patch.
-// The fp64 sums run in the reference's (oy, ox) order.
-__global__ void __launch_bounds__(128) dense_lk_kernel(DenseLKParams p) {
+constexpr int kLKTileX = 8, kLKTileY = 4;  // 32 patches per block
+constexpr int kLKPatches = kLKTileX * kLKTileY;
+constexpr int kLKThreads = 128;
+
+// Shared-memory footprint of one tile (floats): the prev level over the
+// tile's template region + 1-pixel halo (replicate-clamped), the gradients
+// (gx, gy) of the template region, and the residual products of one
+// iteration (two per template pixel per patch).
+__host__ __device__ inline int lk_region_w(int r) { return (kLKTileX - 1) * r + 2 * r + 3; }
+__host__ __device__ inline int lk_region_h(int r) { return (kLKTileY - 1) * r + 2 * r + 3; }
+__host__ __device__ inline int lk_grad_offset(int r) { return (lk_region_w(r) * lk_region_h(r) + 3) & ~3; }
+__host__ __device__ inline int lk_prod_offset(int r) {
+  return lk_grad_offset(r) + 2 * (lk_region_w(r) - 2) * (lk_region_h(r) - 2);
+}
+size_t dense_lk_smem(int r) {
+  const int d = 2 * r + 1;
+  return (size_t)(lk_prod_offset(r) + 2 * kLKPatches * d * d) * sizeof(float);
+}
+
+// solve_level's per-patch loop (flow.cpp:170-215) for a tile of 8x4 patches.
+// The template (prev values + central-difference gradients) is staged in
+// shared memory once per tile.  Each LK iteration runs in two phases:
+//   A. all 128 threads compute the float products gx*residual, gy*residual
+//      of every (patch, template pixel) — the residual's bilinear sample of
+//      curr is one 16-byte quad gather — into shared memory;
+//   B. one thread per (patch, sum) accumulates them into the fp64 sum in the
+//      reference's k order (the only sequential part), then the 2x2 solve.
+// The template sums gxx/gxy/gyy are exact in fp64 for every supported level
+// and radius (all terms are multiples of 2^-(4l+2), the total stays below
+// 2^53 of those quanta), so they are split across threads.
+template <int kR>
+__global__ void __launch_bounds__(kLKThreads) dense_lk_tile_kernel(DenseLKParams p) {
+  extern __shared__ __align__(16) float smem[];
+  const int z = blockIdx.z;  // frame pair
+  GridGeom g = p.g;
+  g.pu += z * g.pair_stride;
+  g.pv += z * g.pair_stride;
+  GridGeom coarse = p.coarse;
+  coarse.pu += z * coarse.pair_stride;
+  coarse.pv += z * coarse.pair_stride;
+  const float* __restrict__ prev = p.prev.at((p.r0 + z) % p.R);
+  const float4* __restrict__ qcurr = p.qcurr.at((p.r0 + z + 1) % p.R);
+  __shared__ float s_u[kLKPatches], s_v[kLKPatches];
+  __shared__ int s_cx[kLKPatches], s_cy[kLKPatches], s_solve[kLKPatches];
+  __shared__ double s_part[3][4][kLKPatches];
+  __shared__ double s_gxx[kLKPatches], s_gxy[kLKPatches], s_gyy[kLKPatches], s_inv[kLKPatches];
+  __shared__ double s_b[2][kLKPatches];
+  const int r = kR > 0 ? kR : p.radius;
+  const int D = 2 * r + 1, P2 = D * D;
+  const int w = g.w, h = g.h;
+  const int t = threadIdx.x;
+  const int i0 = blockIdx.x * kLKTileX, j0 = blockIdx.y * kLKTileY;
+  const int i1 = min(i0 + kLKTileX, g.ncx) - 1, j1 = min(j0 + kLKTileY, g.ncy) - 1;
+  const int rx0 = __ldg(g.cx + i0) - r - 1, ry0 = __ldg(g.cy + j0) - r - 1;
+  const int rw = __ldg(g.cx + i1) - __ldg(g.cx + i0) + 2 * r + 3;
+  const int rh = __ldg(g.cy + j1) - __ldg(g.cy + j0) + 2 * r + 3;
+  const int pitch = lk_region_w(r), gpitch = pitch - 2;
+  float* sP = smem;                                                   // [rh][pitch]
+  float2* sG = reinterpret_cast<float2*>(smem + lk_grad_offset(r));   // [rh-2][gpitch]
+  float* sB1 = smem + lk_prod_offset(r);                              // [patch][P2]
+  float* sB2 = sB1 + kLKPatches * P2;
+
+  for (int e = t; e < rw * rh; e += kLKThreads) {
+    const int yy = e / rw, xx = e - yy * rw;
+    const int sy = clampi(ry0 + yy, 0, h - 1), sx = clampi(rx0 + xx, 0, w - 1);
+    sP[yy * pitch + xx] = __ldg(prev + (size_t)sy * w + sx);
+  }
+  if (t < kLKPatches) {
+    const int i = i0 + t % kLKTileX, j = j0 + t / kLKTileX;
+    const bool valid = i < g.ncx && j < g.ncy;
+    const int cx = __ldg(g.cx + (valid ? i : i0)), cy = __ldg(g.cy + (valid ? j : j0));
+    float u = 0.0f, v = 0.0f;
+    if (valid && p.has_coarse) upsample_at(coarse, w, h, cx, cy, u, v);
+    s_cx[t] = cx;
+    s_cy[t] = cy;
+    s_u[t] = u;
+    s_v[t] = v;
+    s_solve[t] = valid;
+  }
+  __syncthreads();
+  // gradients at every template position (flow.cpp:60-73: the clamped
+  // neighbours are reproduced by the replicate-staged halo)
+  for (int e = t; e < (rw - 2) * (rh - 2); e += kLKThreads) {
+    const int yy = e / (rw - 2) + 1, xx = e - (yy - 1) * (rw - 2) + 1;
+    const float* row = sP + yy * pitch;
+    sG[(yy - 1) * gpitch + (xx - 1)] =
+        make_float2(fmul(0.5f, fsub(row[xx + 1], row[xx - 1])), fmul(0.5f, fsub(row[pitch + xx], row[xx - pitch])));
+  }
+  __syncthreads();
+  // template sums (flow.cpp:177-194): 4 row-parts per patch, exact
+  {
+    const int pt = t % kLKPatches, part = t / kLKPatches;
+    const int cx = s_cx[pt], cy = s_cy[pt];
+    double gxx = 0.0, gxy = 0.0, gyy = 0.0;
+    for (int oy = -r + part; oy <= r; oy += 4) {
+      const int py = clampi(cy + oy, 0, h - 1);
+      const float2* grow = sG + (py - ry0 - 1) * gpitch - rx0 - 1;
+      for (int ox = -r; ox <= r; ++ox) {
+        const float2 gr = grow[clampi(cx + ox, 0, w - 1)];
+        gxx = dadd(gxx, (double)fmul(gr.x, gr.x));
+        gxy = dadd(gxy, (double)fmul(gr.x, gr.y));
+        gyy = dadd(gyy, (double)fmul(gr.y, gr.y));
+      }
+    }
+    s_part[0][part][pt] = gxx;
+    s_part[1][part][pt] = gxy;
+    s_part[2][part][pt] = gyy;
+  }
+  __syncthreads();
+  if (t < kLKPatches) {
+    const double gxx = dadd(dadd(dadd(s_part[0][0][t], s_part[0][1][t]), s_part[0][2][t]), s_part[0][3][t]);
+    const double gxy = dadd(dadd(dadd(s_part[1][0][t], s_part[1][1][t]), s_part[1][2][t]), s_part[1][3][t]);
+    const double gyy = dadd(dadd(dadd(s_part[2][0][t], s_part[2][1][t]), s_part[2][2][t]), s_part[2][3][t]);
+    const bool solve = s_solve[t] && min_eigenvalue(gxx, gxy, gyy) > dmul(1e-4, (double)P2);
+    s_solve[t] = solve ? 1 : (s_solve[t] ? 2 : 0);  // 1 solve, 2 valid-but-flat, 0 padding
+    s_gxx[t] = gxx;
+    s_gxy[t] = gxy;
+    s_gyy[t] = gyy;
+    if (solve) s_inv[t] = __ddiv_rn(1.0, dsub(dmul(gxx, gyy), dmul(gxy, gxy)));
+  }
+  __syncthreads();
+  const float max_step = (float)r;
+  for (int it = 0; it < p.iterations; ++it) {
+    // phase A: residual products (flow.cpp:202-205, float)
+    // (batches of kU gathers in flight per thread)
+    constexpr int kU = 6;
+    for (int e0 = t; e0 < kLKPatches * P2; e0 += kLKThreads * kU) {
+      float4 q[kU];
+      float fxs[kU], fys[kU];
+      int pxs[kU], pys[kU];
+      bool ok[kU];
+#pragma unroll
+      for (int c = 0; c < kU; ++c) {
+        const int e = e0 + c * kLKThreads;
+        const int pt = e / P2, k = e - pt * P2;
+        ok[c] = e < kLKPatches * P2 && s_solve[pt] == 1;
+        q[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        pxs[c] = pys[c] = 0;
+        fxs[c] = fys[c] = 0.f;
+        if (ok[c]) {
+          const int oy = k / D - r, ox = k - (k / D) * D - r;
+          const int px = clampi(s_cx[pt] + ox, 0, w - 1), py = clampi(s_cy[pt] + oy, 0, h - 1);
+          // sample() taps (flow.cpp:45-53) of curr at (px + u, py + v)
+          const float x = clamp_ref(fadd((float)px, s_u[pt]), 0.0f, (float)(w - 1));
+          const float y = clamp_ref(fadd((float)py, s_v[pt]), 0.0f, (float)(h - 1));
+          const int x0 = (int)x, y0 = (int)y;
+          fxs[c] = fsub(x, (float)x0);
+          fys[c] = fsub(y, (float)y0);
+          q[c] = __ldg(qcurr + (size_t)y0 * w + x0);
+          pxs[c] = px;
+          pys[c] = py;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < kU; ++c) {
+        if (!ok[c]) continue;
+        const int e = e0 + c * kLKThreads;
+        const int px = pxs[c], py = pys[c];
+        const float tval = sP[(py - ry0) * pitch + (px - rx0)];
+        const float2 gr = sG[(py - ry0 - 1) * gpitch + (px - rx0 - 1)];
+        const float s = lerp_ref(lerp_ref(q[c].x, q[c].y, fxs[c]), lerp_ref(q[c].z, q[c].w, fxs[c]), fys[c]);
+        const float residual = fsub(s, tval);
+        sB1[e] = fmul(gr.x, residual);
+        sB2[e] = fmul(gr.y, residual);
+      }
+    }
+    __syncthreads();
+    // phase B: the ordered fp64 sums b1 (warp 0) and b2 (warp 1)
+    if (t < 2 * kLKPatches) {
+      const int pt = t % kLKPatches;
+      if (s_solve[pt] == 1) {
+        const float* src = (t < kLKPatches ? sB1 : sB2) + pt * P2;
+        double acc = 0.0;
+#pragma unroll 9
+        for (int k = 0; k < P2; ++k) acc = dadd(acc, (double)src[k]);
+        s_b[t / kLKPatches][pt] = acc;
+      }
+    }
+    __syncthreads();
+    if (t < kLKPatches && s_solve[t] == 1) {
+      const double b1 = s_b[0][t], b2 = s_b[1][t];
+      const double gxx = s_gxx[t], gxy = s_gxy[t], gyy = s_gyy[t], inv_det = s_inv[t];
+      float du = __double2float_rn(dmul(-dsub(dmul(gyy, b1), dmul(gxy, b2)), inv_det));
+      float dv = __double2float_rn(dmul(-dsub(dmul(gxx, b2), dmul(gxy, b1)), inv_det));
+      du = clamp_ref(du, -max_step, max_step);
+      dv = clamp_ref(dv, -max_step, max_step);
+      s_u[t] = fadd(s_u[t], du);
+      s_v[t] = fadd(s_v[t], dv);
+    }
+    __syncthreads();
+  }
+  if (t < kLKPatches && s_solve[t] != 0) {
+    const int i = i0 + t % kLKTileX, j = j0 + t / kLKTileX;
+    g.pu[(size_t)j * g.ncx + i] = s_u[t];
+    g.pv[(size_t)j * g.ncx + i] = s_v[t];
+  }
+}
+
+// Fallback for radii whose tile does not fit in shared memory (r > 10): one
+// thread per patch, template and gradients straight from L1/L2.
+__global__ void __launch_bounds__(128) dense_lk_global_kernel(DenseLKParams p) {
   const int pid = blockIdx.x * blockDim.x + threadIdx.x;
-  const GridGeom& g = p.g;
+  const int z = blockIdx.y;  // frame pair
+  GridGeom g = p.g;
+  g.pu += z * g.pair_stride;
+  g.pv += z * g.pair_stride;
+  GridGeom coarse = p.coarse;
+  coarse.pu += z * coarse.pair_stride;
+  coarse.pv += z * coarse.pair_stride;
+  const float* __restrict__ prev = p.prev.at((p.r0 + z) % p.R);
+  const float4* __restrict__ qcurr = p.qcurr.at((p.r0 + z + 1) % p.R);
   if (pid >= g.ncx * g.ncy) return;
   const int i = pid % g.ncx;
   const int j = pid / g.ncx;
@@ -109,15 +352,14 @@ __global__ void __launch_bounds__(128) dense_lk_kernel(DenseLKParams p) {
   const int cy = __ldg(g.cy + j);
   const int w = g.w, h = g.h, r = p.radius;
   float u = 0.0f, v = 0.0f;
-  if (p.has_coarse) upsample_at(p.coarse, w, h, cx, cy, u, v);
-
+  if (p.has_coarse) upsample_at(coarse, w, h, cx, cy, u, v);
   double gxx = 0.0, gxy = 0.0, gyy = 0.0;
   for (int oy = -r; oy <= r; ++oy) {
     const int py = clampi(cy + oy, 0, h - 1);
     for (int ox = -r; ox <= r; ++ox) {
       const int px = clampi(cx + ox, 0, w - 1);
-      const float a = grad_x(p.prev, w, px, py);
-      const float b = grad_y(p.prev, w, h, px, py);
+      const float a = grad_x(prev, w, px, py);
+      const float b = grad_y(prev, w, h, px, py);
       gxx = dadd(gxx, (double)fmul(a, a));
       gxy = dadd(gxy, (double)fmul(a, b));
       gyy = dadd(gyy, (double)fmul(b, b));
@@ -134,10 +376,10 @@ __global__ void __launch_bounds__(128) dense_lk_kernel(DenseLKParams p) {
         const float syv = fadd((float)py, v);
         for (int ox = -r; ox <= r; ++ox) {
           const int px = clampi(cx + ox, 0, w - 1);
-          const float a = grad_x(p.prev, w, px, py);
-          const float b = grad_y(p.prev, w, h, px, py);
-          const float tval = __ldg(p.prev + (size_t)py * w + px);
-          const float residual = fsub(sample_f32(p.curr, w, h, fadd((float)px, u), syv), tval);
+          const float a = grad_x(prev, w, px, py);
+          const float b = grad_y(prev, w, h, px, py);
+          const float tval = __ldg(prev + (size_t)py * w + px);
+          const float residual = fsub(sample_quadf(qcurr, w, h, fadd((float)px, u), syv), tval);
           b1 = dadd(b1, (double)fmul(a, residual));
           b2 = dadd(b2, (double)fmul(b, residual));
         }
@@ -185,7 +427,12 @@ __device__ __forceinline__ void sample_grads(const float* __restrict__ im, int w
 
 // estimate_sparse_flow's per-point loop (flow.cpp:309-380), one thread per point.
 __global__ void __launch_bounds__(128) sparse_lk_kernel(SparseLKParams p) {
-  const int64_t M = p.n_points ? (int64_t)*p.n_points : p.n_points_host;
+  const int z = blockIdx.y;  // frame pair
+  const int64_t M = p.n_points ? (int64_t)p.n_points[z] : p.n_points_host;
+  const uint32_t* points = p.points + z * p.pair_stride;
+  float2* disp = p.disp + z * p.pair_stride;
+  uint8_t* status = p.status + z * p.pair_stride;
+  const int sp = (p.r0 + z) % p.R, sc = (p.r0 + z + 1) % p.R;
   const int r = p.radius;
   const int patch_pixels = (2 * r + 1) * (2 * r + 1);
   const float max_step = (float)r;
@@ -193,15 +440,15 @@ __global__ void __launch_bounds__(128) sparse_lk_kernel(SparseLKParams p) {
   const float w0 = (float)p.w0, h0 = (float)p.h0;
   for (int64_t pi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pi < M;
        pi += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t idx = p.points[pi];
+    const uint32_t idx = points[pi];
     const int ptx = (int)(idx % (uint32_t)p.w0);
     const int pty = (int)(idx / (uint32_t)p.w0);
     float u = 0.0f, v = 0.0f;
     bool lost = false, solved_any = false;
     for (int l = p.levels - 1; l >= 0 && !lost; --l) {
       const int w = p.dims[l].w, h = p.dims[l].h;
-      const float* P = p.prev[l];
-      const float* C = p.curr[l];
+      const float* P = p.prev[l].at(sp);
+      const float* C = p.curr[l].at(sc);
       const float px = fsub(fmul(fadd((float)ptx, 0.5f), __fdiv_rn((float)w, w0)), 0.5f);
       const float py = fsub(fmul(fadd((float)pty, 0.5f), __fdiv_rn((float)h, h0)), 0.5f);
       if (l != p.levels - 1) {
@@ -252,20 +499,19 @@ __global__ void __launch_bounds__(128) sparse_lk_kernel(SparseLKParams p) {
     const float fx = fadd((float)ptx, u);
     const float fy = fadd((float)pty, v);
     if (!solved_any || fx < 0.0f || fx > fsub(w0, 1.0f) || fy < 0.0f || fy > fsub(h0, 1.0f)) lost = true;
-    p.disp[pi] = make_float2(u, v);
-    p.status[pi] = lost ? 0 : 1;
+    disp[pi] = make_float2(u, v);
+    status[pi] = lost ? 0 : 1;
   }
 }
 
 // ---------------------------------------------------------------- launches
 
-void launch_to_float(const uint8_t* src, float* dst, int64_t n, cudaStream_t s) {
-  to_float_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, dst, n);
-}
-
-void launch_downsample(const float* src, LevelDims sd, float* dst, LevelDims dd, cudaStream_t s) {
-  dim3 b(32, 8), g((dd.w + 31) / 32, (dd.h + 7) / 8);
-  downsample_kernel<<<g, b, 0, s>>>(src, sd, dst, dd);
+void launch_pyramid(const PyramidParams& p, int n_frames, cudaStream_t s) {
+  if (n_frames <= 0) return;
+  for (int l = 0; l < p.levels; ++l) {
+    dim3 g((p.dims[l].w + 127) / 128, p.dims[l].h, n_frames);
+    pyramid_level_kernel<<<g, 128, 0, s>>>(p, l);
+  }
 }
 
 void launch_build_quad(const uint8_t* src, uint32_t* dst, int w, int h, cudaStream_t s) {
@@ -273,9 +519,22 @@ void launch_build_quad(const uint8_t* src, uint32_t* dst, int w, int h, cudaStre
   build_quad_kernel<<<g, 128, 0, s>>>(src, dst, w, h);
 }
 
-void launch_dense_lk(const DenseLKParams& p, cudaStream_t s) {
-  const int n = p.g.ncx * p.g.ncy;
-  dense_lk_kernel<<<(n + 127) / 128, 128, 0, s>>>(p);
+void launch_dense_lk(const DenseLKParams& p, int n_pairs, cudaStream_t s) {
+  if (n_pairs <= 0) return;
+  dim3 grid((p.g.ncx + kLKTileX - 1) / kLKTileX, (p.g.ncy + kLKTileY - 1) / kLKTileY, n_pairs);
+  const int r = p.radius;
+  const size_t sm = dense_lk_smem(r);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(dense_lk_tile_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(dense_lk_tile_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(dense_lk_tile_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  if (r == 4) dense_lk_tile_kernel<4><<<grid, kLKThreads, sm, s>>>(p);
+  else if (r == 6) dense_lk_tile_kernel<6><<<grid, kLKThreads, sm, s>>>(p);
+  else if (sm <= 200 * 1024) dense_lk_tile_kernel<0><<<grid, kLKThreads, sm, s>>>(p);
+  else dense_lk_global_kernel<<<dim3((p.g.ncx * p.g.ncy + 127) / 128, n_pairs), 128, 0, s>>>(p);
 }
 
 void launch_densify(const GridGeom& g, float* du, float* dv, cudaStream_t s) {
@@ -283,11 +542,13 @@ void launch_densify(const GridGeom& g, float* du, float* dv, cudaStream_t s) {
   densify_kernel<<<grid, 128, 0, s>>>(g, du, dv);
 }
 
-void launch_sparse_lk(const SparseLKParams& p, int max_points, cudaStream_t s) {
+void launch_sparse_lk(const SparseLKParams& p, int max_points, int n_pairs, cudaStream_t s) {
+  if (n_pairs <= 0) return;
   int blocks = (max_points + 127) / 128;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  const int cap = (148 * 16 + n_pairs - 1) / n_pairs;
+  if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  sparse_lk_kernel<<<blocks, 128, 0, s>>>(p);
+  sparse_lk_kernel<<<dim3(blocks, n_pairs), 128, 0, s>>>(p);
 }
 
 }  // namespace evsim_gpu

@@ -2,6 +2,11 @@
 //
 // Parameter structs are passed by value (kernel parameter space); all
 // pointers are device pointers.  See DESIGN.md §4 for the data layout.
+//
+// Batching: one launch sequence processes F consecutive frame PAIRS of one
+// stream.  Frames live in a device ring of R slots; pair i (0..F-1) reads
+// prev = slot (r0 + i) % R and curr = slot (r0 + i + 1) % R.  Everything a
+// pair owns (patch grids, sparse points/claims, chain masks) is indexed by i.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -12,13 +17,33 @@ namespace evsim_gpu {
 
 constexpr int kWarpsPerBlock = 8;  // chain / emit kernels: 256 threads
 constexpr int kMaxLevels = 8;
+constexpr int kMaxBatch = 1024;    // frames per push_frames call
 
-// ---------------------------------------------------------------- pyramid
 struct LevelDims {
   int w, h;
 };
 
+// A per-slot device array: element (slot, i) at base[slot * stride + i].
+template <class T>
+struct Ring {
+  T* base;
+  size_t stride;
+  __host__ __device__ T* at(int slot) const { return base + (size_t)slot * stride; }
+};
+
+// ---------------------------------------------------------------- pyramid
+struct PyramidParams {
+  int levels;
+  LevelDims dims[kMaxLevels];
+  Ring<const uint8_t> frames;
+  Ring<float> pyr[kMaxLevels];
+  Ring<float4> qpyr[kMaxLevels];
+  Ring<uint32_t> quad_u8;   // base may be null (no interpolation)
+  int R, slot0;             // frame j of this launch is slot (slot0 + j) % R
+};
+
 // Patch-grid geometry of one pyramid level (flow.cpp:152-171, 220-235).
+// pu/pv: per-pair patch grids, pair i at pu + i * pair_stride.
 struct GridGeom {
   int w, h;        // level extent
   int ncx, ncy;    // patch centres per axis
@@ -28,16 +53,18 @@ struct GridGeom {
   const float* wx; // w   interp_table weight
   const int* iy;   // h
   const float* wy; // h
-  float* pu;       // ncx*ncy patch-grid flow (u)
-  float* pv;       // ncx*ncy patch-grid flow (v)
+  float* pu;
+  float* pv;
+  size_t pair_stride;
 };
 
 struct DenseLKParams {
   GridGeom g;             // this level
   GridGeom coarse;        // level + 1 (seed source) when has_coarse
   int has_coarse;
-  const float* prev;      // level image of prev (w*h fp32)
-  const float* curr;      // level image of curr
+  Ring<const float> prev; // level images
+  Ring<const float4> qcurr;
+  int R, r0;              // pair z: prev slot (r0+z)%R, curr slot (r0+z+1)%R
   int radius;
   int iterations;
 };
@@ -45,35 +72,45 @@ struct DenseLKParams {
 struct SparseLKParams {
   int levels;
   LevelDims dims[kMaxLevels];
-  const float* prev[kMaxLevels];
-  const float* curr[kMaxLevels];
+  Ring<const float> prev[kMaxLevels];
+  Ring<const float> curr[kMaxLevels];
+  int R, r0;
   int w0, h0;
   int radius, iterations;
-  const uint32_t* points;   // pixel index y*w0+x, scan order
-  const int* n_points;      // device count
-  int64_t n_points_host;    // used when n_points == nullptr
-  float2* disp;
-  uint8_t* status;
+  const uint32_t* points;   // pair i at points + i * P (pixel index y*w0+x, scan order)
+  const int* n_points;      // [pairs] device counts, or null
+  int64_t n_points_host;    // used when n_points == nullptr (single pair)
+  float2* disp;             // pair i at + i * P
+  uint8_t* status;          // pair i at + i * P
+  size_t pair_stride;       // P
 };
 
 // ---------------------------------------------------------------- chain
 enum ProviderKind { kProvNone = 0, kProvDenseGrid = 1, kProvDenseField = 2, kProvSparse = 3 };
 
-// One description of the link chain: chain frame c (c = 0..n_links) is
-// frame index start + c*step (0 = prev, 1..N interpolated, N+1 = curr).
+// Chain frame c (c = 0..n_links) of every pair is frame index start + c*step
+// (0 = prev, 1..N interpolated, N+1 = curr).
 struct ChainDesc {
   int start;
   int step;
-  int n_links;  // >= 0
+  int n_links;  // >= 0, per pair
 };
 
-// Segments = runs of links with equal timestamps (written by scan_kernel,
-// read by emit/unpack).  Usually one link per segment.
+// Segments = runs of (pair, link) with equal timestamps, over all links of
+// the launch (link g = pair * n_links + l).  Built by segments_kernel.
 struct SegTable {
   int* n_segs;       // device scalar
-  int* seg_first;    // [max links]
-  int* seg_nlinks;   // [max links]
-  int64_t* seg_t;    // [max links]
+  int* seg_first;    // [links]
+  int* seg_nlinks;   // [links]
+  int64_t* seg_t;    // [links]
+};
+
+struct SegParams {
+  ChainDesc d;
+  int n_pairs;
+  int n_interp;
+  SegTable seg;
+  int64_t ts[kMaxBatch + 1];  // frame timestamps: pair i = (ts[i], ts[i+1]]
 };
 
 struct ChainParams {
@@ -83,13 +120,13 @@ struct ChainParams {
   int words_per_block;
   int n_blocks;
   int n_interp;            // N
-  const uint8_t* prev;     // u8 frames
-  const uint8_t* curr;
-  const uint32_t* qprev;   // quad images (dense provider)
-  const uint32_t* qcurr;
-  // dense provider, grid form (level-0 patch grid + tables)
+  int n_pairs;
+  int R, r0;
+  Ring<const uint8_t> frames;
+  Ring<const uint32_t> quads;  // u8 quad images (dense provider)
+  // dense provider, grid form (level-0 patch grid + tables; per-pair pu/pv)
   GridGeom g0;
-  // dense provider, field form (caller-supplied flow)
+  // dense provider, field form (caller-supplied flow, single pair)
   const float* du;
   const float* dv;
   // interpolation constants per chain frame k (0..N+1)
@@ -97,16 +134,14 @@ struct ChainParams {
   const double* oma;       // 1.0 - alpha
   const float* fwd;        // (float)alpha
   const float* bwd;        // (float)(1.0 - alpha)
-  // sparse provider
-  const uint64_t* claims;  // N planes of P keys
-  const uint32_t* touched; // ceil(N/32) planes of P bits
-  uint64_t* claims_rw;
-  uint32_t* touched_rw;
-  const uint32_t* points;  // selected pixel indices
-  const int* d_direct;     // when non-null: *d_direct == 0 selects `direct` chain
-  // chain descriptions
-  ChainDesc full;
-  ChainDesc direct;
+  // sparse provider (per pair strides)
+  uint32_t* claims;        // [pair][N][P] keys (change << 24 | ~j)
+  uint32_t* touched;       // [pair][ceil(N/32)][P] bits
+  const uint32_t* points;  // [pair][P]
+  const int* n_points;     // [pair]
+  size_t P;
+  int skip_empty;          // log mode without endpoints: M == 0 pairs emit nothing
+  ChainDesc d;
   // event rule
   int log_mode;
   int magnitude;
@@ -114,26 +149,19 @@ struct ChainParams {
   float c_pos_log, c_neg_log;
   const float* lut;        // 256 log LUT (log mode)
   float* ref;              // P log reference state (log mode)
-  // outputs
-  uint2* masks;            // [link][n_words] (pos, neg)
-  uint16_t* mcount;        // magnitude: [link][n_words*32]
-  uint32_t* wcount;        // magnitude: [link][n_words]
-  uint32_t* counts;        // [link][n_blocks]
+  // outputs (link g = pair * d.n_links + l)
+  uint2* masks;            // [g][n_words] (pos, neg)
+  uint16_t* mcount;        // magnitude: [g][n_words*32]
+  uint32_t* wcount;        // magnitude: [g][n_words]
+  uint32_t* counts;        // [g][n_blocks] events per block
 };
 
-struct ScanParams {
+struct OffsetParams {
+  int n_rows;              // links
   int n_blocks;
-  const uint32_t* counts;  // [link][n_blocks]
-  const int* d_direct;
-  ChainDesc full;
-  ChainDesc direct;
-  int n_interp;            // timestamps: sub_interval_end over (t_prev, t_curr]
-  int64_t t_prev, t_curr;
-  SegTable seg;
-  int64_t* offsets;        // [seg][n_blocks] exclusive, segment-major
-  int64_t* seg_out;        // [0] = n_segs, [1..n_segs] seg_t, then n_segs+1 offsets
-  int64_t* total;          // device total
-  int64_t* host_total;     // host-mapped mirror (may be null)
+  const uint32_t* counts;  // [g][n_blocks]
+  int64_t* prefix;         // [g][n_blocks] exclusive
+  int64_t* link_total;     // [g]
 };
 
 struct EmitParams {
@@ -141,16 +169,15 @@ struct EmitParams {
   int64_t n_words;
   int words_per_block;
   int n_blocks;
-  const int* d_direct;
-  ChainDesc full;
-  ChainDesc direct;
+  int n_links;             // links of the launch (pairs * per-pair links)
   SegTable seg;
+  const int64_t* prefix;
+  const int64_t* link_total;
+  int64_t* seg_out;        // [0] = S, [1..S] seg_t, [1+S..1+2S] offsets (S+1); block 0
   int magnitude;
   const uint2* masks;
   const uint16_t* mcount;
   const uint32_t* wcount;
-  const int64_t* offsets;
-  const int64_t* total;
   int64_t capacity;
   uint32_t* out;
 };
@@ -161,46 +188,47 @@ struct SelectParams {
   int64_t n_words;
   int words_per_block;
   int n_blocks;
-  const uint8_t* prev;
-  const uint8_t* curr;
+  int R, r0;
+  Ring<const uint8_t> frames;
   int log_mode;
   int sel;
   float sel_log;
   const float* lut;
-  uint32_t* masks;        // [n_words]
-  uint32_t* counts;       // [n_blocks]
-  int64_t* offsets;       // [n_blocks] scratch
-  uint32_t* points;       // out: pixel indices
-  int* n_points;          // out: M
+  uint32_t* masks;        // [pair][n_words]
+  uint32_t* counts;       // [pair][n_blocks]
+  uint32_t* points;       // [pair][P]
+  int* n_points;          // [pair]
+  size_t P;
 };
 
 struct SplatParams {
   int w, h;
   int n_interp;
-  const uint32_t* points;
-  const int* n_points;
-  const float2* disp;
-  const uint8_t* status;
-  const uint8_t* prev;
-  uint64_t* claims;
-  uint32_t* touched;
+  int R, r0;
+  Ring<const uint8_t> frames;
+  const uint32_t* points;  // [pair][P]
+  const int* n_points;     // [pair]
+  const float2* disp;      // [pair][P]
+  const uint8_t* status;   // [pair][P]
+  uint32_t* claims;        // [pair][N][P]
+  uint32_t* touched;       // [pair][ceil(N/32)][P]
+  size_t P;
 };
 
 // ---------------------------------------------------------------- launches
-void launch_to_float(const uint8_t* src, float* dst, int64_t n, cudaStream_t s);
-void launch_downsample(const float* src, LevelDims sd, float* dst, LevelDims dd, cudaStream_t s);
+void launch_pyramid(const PyramidParams& p, int n_frames, cudaStream_t s);
 void launch_build_quad(const uint8_t* src, uint32_t* dst, int w, int h, cudaStream_t s);
-void launch_dense_lk(const DenseLKParams& p, cudaStream_t s);
+void launch_dense_lk(const DenseLKParams& p, int n_pairs, cudaStream_t s);
 void launch_densify(const GridGeom& g, float* du, float* dv, cudaStream_t s);
 void launch_interp_frames(const ChainParams& p, uint8_t* out, cudaStream_t s);
+void launch_segments(const SegParams& p, cudaStream_t s);
 void launch_chain(const ChainParams& p, int provider, cudaStream_t s);
-void launch_scan(const ScanParams& p, cudaStream_t s);
-void launch_emit(const EmitParams& p, cudaStream_t s);
-void launch_select(const SelectParams& p, cudaStream_t s);
-void launch_select_emit(const SelectParams& p, const int64_t* total, cudaStream_t s);
+void launch_offsets(const OffsetParams& p, cudaStream_t s);
+void launch_emit(const EmitParams& p, int64_t* segbase, cudaStream_t s);
+void launch_select(const SelectParams& p, int n_pairs, cudaStream_t s);
 void launch_init_ref(const uint8_t* frame, const float* lut, float* ref, int64_t n, cudaStream_t s);
-void launch_sparse_lk(const SparseLKParams& p, int max_points, cudaStream_t s);
-void launch_splat(const SplatParams& p, int max_points, cudaStream_t s);
+void launch_sparse_lk(const SparseLKParams& p, int max_points, int n_pairs, cudaStream_t s);
+void launch_splat(const SplatParams& p, int max_items, int n_pairs, cudaStream_t s);
 void launch_unpack_events(const uint32_t* packed, const int64_t* seg_out, int64_t n, void* out24,
                           cudaStream_t s);
 

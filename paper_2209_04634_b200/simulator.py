@@ -413,6 +413,44 @@ class Simulator:
         out.events = unpack_events(packed, seg_t, seg_off)
         return out
 
+    @property
+    def max_batch(self) -> int:
+        return int(self._lib.evsim_gpu_max_batch(self._h))
+
+    def push_frames(self, frames: np.ndarray, timestamps) -> EventStream:
+        """Batched push: identical to push_frame over each frame, events
+        concatenated.  frames: (F, H, W) uint8; timestamps: F ints.  Batches
+        larger than max_batch are split."""
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        ts = np.ascontiguousarray(np.asarray(timestamps, dtype=np.int64))
+        F, h, w = frames.shape
+        if self._custom:
+            return concatenate([self.push_frame(Frame(w, h, int(ts[k]), frames[k])) for k in range(F)])
+        parts = []
+        step = self.max_batch
+        for a in range(0, F, step):
+            b = min(F, a + step)
+            ev = CEvents()
+            _lib.check(self._lib.evsim_gpu_push_frames(self._h, _ptr(frames[a:b]), b - a, w, h, _ptr(ts[a:b]), 0,
+                                                       ctypes.byref(ev)))
+            parts.append(self._collect(ev))
+        out = concatenate(parts)
+        out.width, out.height = w, h
+        return out
+
+    def push_frames_device(self, pixels_ptr: int, n_frames: int, width: int, height: int, timestamps,
+                           on_device: bool = True, sync: bool = True) -> Optional[CEvents]:
+        """Device-resident batched push (no event download)."""
+        ts = np.ascontiguousarray(np.asarray(timestamps, dtype=np.int64))
+        if sync:
+            ev = CEvents()
+            _lib.check(self._lib.evsim_gpu_push_frames(self._h, _vp(pixels_ptr), n_frames, width, height, _ptr(ts),
+                                                       1 if on_device else 0, ctypes.byref(ev)))
+            return ev
+        _lib.check(self._lib.evsim_gpu_push_frames_async(self._h, _vp(pixels_ptr), n_frames, width, height,
+                                                         _ptr(ts), 1 if on_device else 0))
+        return None
+
     def push_frame_packed(self, pixels_ptr: int, width: int, height: int, timestamp: int,
                           on_device: bool = True) -> CEvents:
         """Device-resident push (no event download): returns the C result struct."""
