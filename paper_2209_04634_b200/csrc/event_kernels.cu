@@ -105,10 +105,21 @@ struct DenseProvider {
   __device__ __forceinline__ int interp(const ChainParams& p, const PairCtx& pc, const PixelCtx& c, int k) const {
     const float fwd = __ldg(p.fwd + k);
     const float bwd = __ldg(p.bwd + k);
-    const float fp = sample_quad(pc.qprev, p.w, p.h, fsub(c.xf, fmul(fwd, u)), fsub(c.yf, fmul(fwd, v)));
-    const float fc = sample_quad(pc.qcurr, p.w, p.h, fadd(c.xf, fmul(bwd, u)), fadd(c.yf, fmul(bwd, v)));
-    const double blend = dadd(dmul(__ldg(p.oma + k), (double)fp), dmul(__ldg(p.alpha + k), (double)fc));
-    return lround_pos(blend);
+    const float xp = fsub(c.xf, fmul(fwd, u)), yp = fsub(c.yf, fmul(fwd, v));
+    const float xc = fadd(c.xf, fmul(bwd, u)), yc = fadd(c.yf, fmul(bwd, v));
+    if constexpr (kField) {
+      // caller-supplied flow may hold NaN: the reference's exact clamp path
+      const float fp = sample_quad(pc.qprev, p.w, p.h, xp, yp);
+      const float fc = sample_quad(pc.qcurr, p.w, p.h, xc, yc);
+      const double blend = dadd(dmul(__ldg(p.oma + k), (double)fp), dmul(__ldg(p.alpha + k), (double)fc));
+      return lround_pos(blend);
+    } else {
+      // our densified flow is finite: conversion-free sampling and rounding
+      const float fp = sample_quad_fast(pc.qprev, p.w, p.h, xp, yp);
+      const float fc = sample_quad_fast(pc.qcurr, p.w, p.h, xc, yc);
+      const double blend = dadd(dmul(__ldg(p.oma + k), (double)fp), dmul(__ldg(p.alpha + k), (double)fc));
+      return lround_pos_fast(blend);
+    }
   }
   __device__ __forceinline__ void finish(const ChainParams&, const PairCtx&, const PixelCtx&) const {}
 };
@@ -253,10 +264,10 @@ __global__ void __launch_bounds__(1024) segments_kernel(SegParams p) {
 // before they are chained, so their gathers overlap.  Per-(link, block)
 // event counts go to counts[g][block].
 template <class Prov, bool kLog, bool kMag>
-__global__ void __launch_bounds__(256) chain_kernel(ChainParams p) {
+__global__ void __launch_bounds__(256, 3) chain_kernel(ChainParams p) {
   extern __shared__ uint32_t s_cnt[];  // [n_pairs * L] event counts of this block
   __shared__ float s_lut[256];
-  constexpr int kW = 2, kB = 8;
+  constexpr int kW = 2, kB = 4;
   const int L = p.d.n_links;
   const int G = L * p.n_pairs;
   for (int i = threadIdx.x; i < G; i += blockDim.x) s_cnt[i] = 0;
@@ -434,11 +445,13 @@ __global__ void __launch_bounds__(1024) segbase_kernel(EmitParams p, int64_t* se
 // finalize's stable_sort at simulate.cpp:36-40) and magnitude mode take the
 // per-lane count path: per pixel all negative events precede the positive.
 __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* __restrict__ segbase) {
-  extern __shared__ int64_t s_flat0[];  // [S] flattened offset of each segment's first item
+  extern __shared__ int64_t s_off0[];  // [S] output offset of segment s in this block minus its flat offset
   __shared__ int s_warp[kWarpsPerBlock];
   __shared__ uint32_t s_all[256], s_pos[256];
   __shared__ int s_cnt[256];
   __shared__ int64_t s_flat[256];
+  __shared__ int s_nwork;
+  constexpr int kThreadItem = 8;  // words with at most this many events: one thread writes them
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int S = *p.seg.n_segs;
@@ -446,6 +459,15 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
   const int64_t wbeg = (int64_t)b * p.words_per_block;
   const int nw = (int)(min(wbeg + p.words_per_block, p.n_words) - wbeg);
   const int n_items = S * nw;
+  // segment s of this block starts at segbase[s] + sum over its links of the
+  // events in earlier blocks
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    const int k0 = p.seg.seg_first[s], nk = p.seg.seg_nlinks[s];
+    int64_t o = segbase[s];
+    for (int k = k0; k < k0 + nk; ++k) o += p.prefix[(size_t)k * p.n_blocks + b];
+    s_off0[s] = o;
+  }
+  __syncthreads();
   int64_t carry = 0;
   for (int c0 = 0; c0 < n_items; c0 += blockDim.x) {
     const int it = c0 + threadIdx.x;
@@ -475,32 +497,52 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
     }
     int chunk_total;
     const int excl = block_exclusive_scan(cnt, s_warp, chunk_total);
-    s_all[threadIdx.x] = all;
-    s_pos[threadIdx.x] = pos;
-    s_cnt[threadIdx.x] = cnt;
-    s_flat[threadIdx.x] = carry + excl;
-    if (valid && j == 0) s_flat0[s] = carry + excl;
+    if (chunk_total == 0) {  // uniform: nothing to write in this chunk
+      carry += chunk_total;
+      continue;
+    }
+    if (valid && j == 0) s_off0[s] -= carry + excl;
+    if (threadIdx.x == 0) s_nwork = 0;
     __syncthreads();
-    if (chunk_total > 0) {
-      const int nvalid = min(n_items - c0, (int)blockDim.x);
-      for (int jj = warp; jj < nvalid; jj += kWarpsPerBlock) {
-        const int cj = s_cnt[jj];
-        if (cj == 0) continue;
-        const int item = c0 + jj;
+    // segment start in this block + this block's earlier words of the segment
+    // (flattened offset relative to the segment's first item)
+    const int64_t dst_item = valid ? s_off0[s] + carry + excl : 0;
+    const bool fast = valid && !p.magnitude && p.seg.seg_nlinks[s] == 1;
+    if (fast && cnt > 0 && cnt <= kThreadItem) {
+      // sparse word: this thread writes its few events, ascending x
+      const uint32_t wi = (uint32_t)(wbeg + j);
+      const int row = (int)(wi / (uint32_t)p.wpr);
+      const int x0 = (int)(wi - (uint32_t)row * (uint32_t)p.wpr) * 32;
+      int64_t dst = dst_item;
+      uint32_t m = all;
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        p.out[dst++] = pack_event(x0 + bit, row, !((pos >> bit) & 1u));
+      }
+    } else if (cnt > 0) {
+      const int slot = atomicAdd(&s_nwork, 1);
+      s_all[slot] = all;
+      s_pos[slot] = pos;
+      s_cnt[slot] = c0 + (int)threadIdx.x;  // item id
+      s_flat[slot] = dst_item;
+    }
+    __syncthreads();
+    {
+      const int nwork = s_nwork;
+      for (int jj = warp; jj < nwork; jj += kWarpsPerBlock) {
+        const int item = s_cnt[jj];
         const int sj = item / nw;
         const uint32_t wij = (uint32_t)(wbeg + (item - sj * nw));
         const int row = (int)(wij / (uint32_t)p.wpr);
         const int x = (int)(wij - (uint32_t)row * (uint32_t)p.wpr) * 32 + lane;
-        // segment base + this segment's events in earlier blocks + in this
-        // block's earlier words (flattened offset relative to its first item)
-        const int k0 = p.seg.seg_first[sj], nk = p.seg.seg_nlinks[sj];
-        int64_t dst0 = __ldg(segbase + sj) + (s_flat[jj] - s_flat0[sj]);
-        for (int k = k0; k < k0 + nk; ++k) dst0 += __ldg(p.prefix + (size_t)k * p.n_blocks + b);
-        if (!p.magnitude && nk == 1) {
+        const int64_t dst0 = s_flat[jj];
+        if (!p.magnitude && p.seg.seg_nlinks[sj] == 1) {
           const uint32_t aj = s_all[jj];
           if ((aj >> lane) & 1u)
             p.out[dst0 + __popc(aj & lanemask_lt())] = pack_event(x, row, !((s_pos[jj] >> lane) & 1u));
         } else {
+          const int k0 = p.seg.seg_first[sj], nk = p.seg.seg_nlinks[sj];
           int nneg = 0, npos = 0;
           for (int k = k0; k < k0 + nk; ++k) {
             const uint2 m = p.masks[(size_t)k * p.n_words + wij];

@@ -82,6 +82,46 @@ __device__ __forceinline__ float sample_quad(const uint32_t* __restrict__ q, int
   return lerp_ref(top, bot, fy);
 }
 
+// ---- conversion-pipe-free variants (F2I/I2F/F2F run at 1/4 rate on sm_100) ----
+// Valid for FINITE inputs only (the clamp uses FMNMX, which drops NaN); used
+// where the coordinates come from our own (always finite) flow.
+
+// trunc(x) for x in [0, 2^23): the RZ add leaves 2^23 + trunc(x) exactly.
+__device__ __forceinline__ float trunc_magic(float x, int& xi) {
+  const float t = __fadd_rz(x, 8388608.0f);
+  xi = __float_as_int(t) - 0x4B000000;
+  return __fsub_rn(t, 8388608.0f);
+}
+
+// byte k of v as an exact float: PRMT builds 0x4B0000bb, FADD removes 2^23.
+template <int kByte>
+__device__ __forceinline__ float byte_f(uint32_t v) {
+  return __fsub_rn(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7540 + kByte)), 8388608.0f);
+}
+
+// sample_u8 through a quad image, finite coordinates (simulate.cpp:10-26).
+__device__ __forceinline__ float sample_quad_fast(const uint32_t* __restrict__ q, int w, int h, float x, float y) {
+  x = fminf(fmaxf(x, 0.0f), (float)(w - 1));
+  y = fminf(fmaxf(y, 0.0f), (float)(h - 1));
+  int x0, y0;
+  const float x0f = trunc_magic(x, x0);
+  const float y0f = trunc_magic(y, y0);
+  const float fx = fsub(x, x0f);
+  const float fy = fsub(y, y0f);
+  const uint32_t v = __ldg(q + (size_t)y0 * w + x0);
+  const float top = lerp_ref(byte_f<0>(v), byte_f<1>(v), fx);
+  const float bot = lerp_ref(byte_f<2>(v), byte_f<3>(v), fx);
+  return lerp_ref(top, bot, fy);
+}
+
+// lround() of v in [0, 2^31) without conversions: t = 2^52 + trunc(v) (RZ),
+// its low word is trunc(v); v - trunc(v) is exact.
+__device__ __forceinline__ int lround_pos_fast(double v) {
+  const double t = __dadd_rz(v, 4503599627370496.0);
+  const double f = __dsub_rn(t, 4503599627370496.0);
+  return __double2loint(t) + ((__dsub_rn(v, f) >= 0.5) ? 1 : 0);
+}
+
 // lround() for a non-negative double (simulate.cpp:114): half away from zero.
 // v - floor(v) is exact, so the comparison with 0.5 is exact.
 __device__ __forceinline__ int lround_pos(double v) {

@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_tile_kernel(DenseLKParams
   float* sB1 = smem + lk_prod_offset(r);                              // [patch][P2]
   float* sB2 = sB1 + kLKPatches * P2;
 
+#pragma unroll 4
   for (int e = t; e < rw * rh; e += kLKThreads) {
     const int yy = e / rw, xx = e - yy * rw;
     const int sy = clampi(ry0 + yy, 0, h - 1), sx = clampi(rx0 + xx, 0, w - 1);
@@ -276,12 +277,14 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_tile_kernel(DenseLKParams
         if (ok[c]) {
           const int oy = k / D - r, ox = k - (k / D) * D - r;
           const int px = clampi(s_cx[pt] + ox, 0, w - 1), py = clampi(s_cy[pt] + oy, 0, h - 1);
-          // sample() taps (flow.cpp:45-53) of curr at (px + u, py + v)
-          const float x = clamp_ref(fadd((float)px, s_u[pt]), 0.0f, (float)(w - 1));
-          const float y = clamp_ref(fadd((float)py, s_v[pt]), 0.0f, (float)(h - 1));
-          const int x0 = (int)x, y0 = (int)y;
-          fxs[c] = fsub(x, (float)x0);
-          fys[c] = fsub(y, (float)y0);
+          // sample() taps (flow.cpp:45-53) of curr at (px + u, py + v); u, v
+          // are finite, so FMNMX clamps and the RZ-add truncation are exact
+          const float x = fminf(fmaxf(fadd((float)px, s_u[pt]), 0.0f), (float)(w - 1));
+          const float y = fminf(fmaxf(fadd((float)py, s_v[pt]), 0.0f), (float)(h - 1));
+          int x0, y0;
+          const float x0f = trunc_magic(x, x0), y0f = trunc_magic(y, y0);
+          fxs[c] = fsub(x, x0f);
+          fys[c] = fsub(y, y0f);
           q[c] = __ldg(qcurr + (size_t)y0 * w + x0);
           pxs[c] = px;
           pys[c] = py;
