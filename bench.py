@@ -235,8 +235,9 @@ def run_ours(args):
     base = d_frames.data_ptr()
     torch.cuda.synchronize()
 
-    batch = args.batch or sim.max_batch
-    batch = max(1, min(batch, sim.max_batch, n))
+    mb = sim.max_batch(c.width, c.height)
+    batch = args.batch or mb
+    batch = max(1, min(batch, mb, n))
 
     def enqueue_step():
         # reset + the whole sequence in batches of `batch` frames (one launch

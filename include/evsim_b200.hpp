@@ -363,7 +363,7 @@ class Simulator {
     }
     const int w = frames[0].width, hgt = frames[0].height;
     const std::size_t P = frames[0].pixel_count();
-    const int cap = evsim_gpu_max_batch(h_.get());
+    const int cap = evsim_gpu_max_batch(h_.get(), w, hgt);
     for (std::size_t a = 0; a < frames.size(); a += cap) {
       const std::size_t nb = std::min<std::size_t>(cap, frames.size() - a);
       std::vector<std::uint8_t> px(nb * P);

@@ -144,14 +144,15 @@ EVSIM_GPU_API int evsim_gpu_push_frame(evsim_gpu_sim* sim, const uint8_t* pixels
  * sequence.  Results are identical to n_frames push_frame calls with their
  * event streams concatenated (segments of all intervals, in order).  The
  * whole batch is validated first and rejected atomically (state untouched).
- * At most evsim_gpu_max_batch(sim) frames per call. */
+ * At most evsim_gpu_max_batch(sim, width, height) frames per call (bounded
+ * by kernel shared-memory tables and a ~6 GB per-launch buffer budget). */
 EVSIM_GPU_API int evsim_gpu_push_frames(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t n_frames,
                                         int32_t width, int32_t height, const int64_t* t_us,
                                         int32_t pixels_on_device, evsim_gpu_events* out);
 EVSIM_GPU_API int evsim_gpu_push_frames_async(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t n_frames,
                                               int32_t width, int32_t height, const int64_t* t_us,
                                               int32_t pixels_on_device);
-EVSIM_GPU_API int evsim_gpu_max_batch(const evsim_gpu_sim* sim);
+EVSIM_GPU_API int evsim_gpu_max_batch(const evsim_gpu_sim* sim, int32_t width, int32_t height);
 
 /* Asynchronous variant: enqueues the push on the handle's CUDA stream and
  * returns without waiting; evsim_gpu_sync() completes it.  Validation

@@ -402,9 +402,13 @@ struct EventEngine {
 
 // Largest batch whose link count fits the kernels' shared-memory tables
 // (chain: 4 B per link, emit: 8 B per segment, both <= 96 KB).
-int max_batch_for(int links_per_pair) {
-  const int by_links = 12000 / std::max(links_per_pair, 1);
-  return std::max(1, std::min(kMaxBatch, by_links));
+// Also keeps the per-launch event buffer + masks (12 B per link-pixel in
+// single mode) within ~6 GB of the 180 GB HBM.
+int max_batch_for(int links_per_pair, int64_t pixels) {
+  const int L = std::max(links_per_pair, 1);
+  const int by_links = 12000 / L;
+  const int64_t by_mem = (int64_t)6e9 / std::max<int64_t>(1, (int64_t)L * std::max<int64_t>(pixels, 1) * 12);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(std::min(kMaxBatch, by_links), by_mem));
 }
 
 }  // namespace
@@ -710,7 +714,8 @@ struct evsim_gpu_sim {
       invalid("push_frame: frames of 2^24 pixels or more are not supported by the sparse method");
     if ((int64_t)fw * fh >= (int64_t)1 << 31) invalid("push_frame: frame too large");
     const int L = desc().n_links;
-    if (F > max_batch_for(L)) invalid("push_frames: batch too large (max " + std::to_string(max_batch_for(L)) + ")");
+    const int fmax = max_batch_for(L, (int64_t)fw * fh);
+    if (F > fmax) invalid("push_frames: batch too large (max " + std::to_string(fmax) + ")");
     CK(cudaSetDevice(device));
     // A queued single-mode result is superseded (stream order keeps the
     // device buffers consistent); magnitude mode may need a re-emit.
@@ -1001,9 +1006,9 @@ int evsim_gpu_push_frames_async(evsim_gpu_sim* sim, const uint8_t* pixels, int32
   });
 }
 
-int evsim_gpu_max_batch(const evsim_gpu_sim* sim) {
+int evsim_gpu_max_batch(const evsim_gpu_sim* sim, int32_t width, int32_t height) {
   if (!sim) return 0;
-  return max_batch_for(sim->desc().n_links);
+  return max_batch_for(sim->desc().n_links, (int64_t)width * height);
 }
 
 int evsim_gpu_sync(evsim_gpu_sim* sim, evsim_gpu_events* out) {

@@ -413,9 +413,9 @@ class Simulator:
         out.events = unpack_events(packed, seg_t, seg_off)
         return out
 
-    @property
-    def max_batch(self) -> int:
-        return int(self._lib.evsim_gpu_max_batch(self._h))
+    def max_batch(self, width: int, height: int) -> int:
+        """Largest push_frames batch for this config at width x height."""
+        return int(self._lib.evsim_gpu_max_batch(self._h, width, height))
 
     def push_frames(self, frames: np.ndarray, timestamps) -> EventStream:
         """Batched push: identical to push_frame over each frame, events
@@ -427,7 +427,7 @@ class Simulator:
         if self._custom:
             return concatenate([self.push_frame(Frame(w, h, int(ts[k]), frames[k])) for k in range(F)])
         parts = []
-        step = self.max_batch
+        step = self.max_batch(w, h)
         for a in range(0, F, step):
             b = min(F, a + step)
             ev = CEvents()
