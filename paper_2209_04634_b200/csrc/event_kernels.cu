@@ -114,9 +114,22 @@ struct DenseProvider {
       const double blend = dadd(dmul(__ldg(p.oma + k), (double)fp), dmul(__ldg(p.alpha + k), (double)fc));
       return lround_pos(blend);
     } else {
-      // our densified flow is finite: conversion-free sampling and rounding
-      const float fp = sample_quad_fast(pc.qprev, p.w, p.h, xp, yp);
-      const float fc = sample_quad_fast(pc.qcurr, p.w, p.h, xc, yc);
+      // our densified flow is finite: both samples as fp32x2 pairs,
+      // conversion-free; (xf - fwd*u, xf + bwd*u) = xf + (-fwd, bwd)*u exactly
+      (void)xp, (void)yp, (void)xc, (void)yc;
+      const float2 nb = __ldg(p.nfb + k);
+      const f32x2 NB = pk2(nb.x, nb.y);
+      const f32x2 S = sample_quad_pair(pc.qprev, pc.qcurr, p.w, p.h, affine2(c.xf, NB, u), affine2(c.yf, NB, v));
+      const float fp = lo2(S), fc = hi2(S);
+      // The reference rounds s = RN64(RN64(oma*fp) + RN64(alpha*fc))
+      // (simulate.cpp:114).  An fp32 estimate e of it satisfies
+      // |e - s| <= 2^-24*255 + 2^-23*255 + 2^-24*256 + 3*2^-53*256 < 6.2e-5,
+      // so lround(s) = trunc(e) + (frac(e) > 0.5) whenever |frac(e) - 0.5| >
+      // 1e-4; only inside that window is the double expression evaluated.
+      const float e = __fmaf_rn(__ldg(p.oma_f + k), fp, __fmul_rn(__ldg(p.alpha_f + k), fc));
+      int n;
+      const float fr = fsub(e, trunc_magic(e, n));
+      if (fabsf(fsub(fr, 0.5f)) > 1e-4f) return n + (fr > 0.5f ? 1 : 0);
       const double blend = dadd(dmul(__ldg(p.oma + k), (double)fp), dmul(__ldg(p.alpha + k), (double)fc));
       return lround_pos_fast(blend);
     }
@@ -447,11 +460,9 @@ __global__ void __launch_bounds__(1024) segbase_kernel(EmitParams p, int64_t* se
 __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* __restrict__ segbase) {
   extern __shared__ int64_t s_off0[];  // [S] output offset of segment s in this block minus its flat offset
   __shared__ int s_warp[kWarpsPerBlock];
-  __shared__ uint32_t s_all[256], s_pos[256];
-  __shared__ int s_cnt[256];
-  __shared__ int64_t s_flat[256];
+  __shared__ int s_item[256];
+  __shared__ int64_t s_dst[256];
   __shared__ int s_nwork;
-  constexpr int kThreadItem = 8;  // words with at most this many events: one thread writes them
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int S = *p.seg.n_segs;
@@ -476,10 +487,12 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
     const int j = valid ? it - s * nw : 0;
     uint32_t pos = 0, all = 0;
     int cnt = 0;
+    bool fast = false;
     if (valid) {
       const int k0 = p.seg.seg_first[s], nk = p.seg.seg_nlinks[s];
       const int64_t wi = wbeg + j;
-      if (!p.magnitude && nk == 1) {
+      fast = !p.magnitude && nk == 1;
+      if (fast) {
         const uint2 m = p.masks[(size_t)k0 * p.n_words + wi];
         pos = m.x;
         all = m.x | m.y;
@@ -497,70 +510,85 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
     }
     int chunk_total;
     const int excl = block_exclusive_scan(cnt, s_warp, chunk_total);
-    if (chunk_total == 0) {  // uniform: nothing to write in this chunk
-      carry += chunk_total;
-      continue;
-    }
+    if (chunk_total == 0) continue;  // uniform
     if (valid && j == 0) s_off0[s] -= carry + excl;
     if (threadIdx.x == 0) s_nwork = 0;
     __syncthreads();
     // segment start in this block + this block's earlier words of the segment
     // (flattened offset relative to the segment's first item)
-    const int64_t dst_item = valid ? s_off0[s] + carry + excl : 0;
-    const bool fast = valid && !p.magnitude && p.seg.seg_nlinks[s] == 1;
-    if (fast && cnt > 0 && cnt <= kThreadItem) {
-      // sparse word: this thread writes its few events, ascending x
+    const int64_t dst = valid ? s_off0[s] + carry + excl : 0;
+    // ---- single-link words: warp-level load-balanced expansion.  The warp's
+    // 32 words hold T events; output slot q (q = lane, lane+32, ...) belongs to
+    // the word whose scan interval contains q (binary search over the warp's
+    // inclusive scan) and to that word's (q - start)-th set bit (__fns).
+    // Consecutive slots of one segment are consecutive addresses, so each
+    // store instruction writes up to 32 adjacent events.
+    {
+      const int c = fast ? cnt : 0;
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int T = __shfl_sync(kFull, incl, 31);
       const uint32_t wi = (uint32_t)(wbeg + j);
       const int row = (int)(wi / (uint32_t)p.wpr);
       const int x0 = (int)(wi - (uint32_t)row * (uint32_t)p.wpr) * 32;
-      int64_t dst = dst_item;
-      uint32_t m = all;
-      while (m) {
-        const int bit = __ffs(m) - 1;
-        m &= m - 1;
-        p.out[dst++] = pack_event(x0 + bit, row, !((pos >> bit) & 1u));
-      }
-    } else if (cnt > 0) {
-      const int slot = atomicAdd(&s_nwork, 1);
-      s_all[slot] = all;
-      s_pos[slot] = pos;
-      s_cnt[slot] = c0 + (int)threadIdx.x;  // item id
-      s_flat[slot] = dst_item;
-    }
-    __syncthreads();
-    {
-      const int nwork = s_nwork;
-      for (int jj = warp; jj < nwork; jj += kWarpsPerBlock) {
-        const int item = s_cnt[jj];
-        const int sj = item / nw;
-        const uint32_t wij = (uint32_t)(wbeg + (item - sj * nw));
-        const int row = (int)(wij / (uint32_t)p.wpr);
-        const int x = (int)(wij - (uint32_t)row * (uint32_t)p.wpr) * 32 + lane;
-        const int64_t dst0 = s_flat[jj];
-        if (!p.magnitude && p.seg.seg_nlinks[sj] == 1) {
-          const uint32_t aj = s_all[jj];
-          if ((aj >> lane) & 1u)
-            p.out[dst0 + __popc(aj & lanemask_lt())] = pack_event(x, row, !((s_pos[jj] >> lane) & 1u));
-        } else {
-          const int k0 = p.seg.seg_first[sj], nk = p.seg.seg_nlinks[sj];
-          int nneg = 0, npos = 0;
-          for (int k = k0; k < k0 + nk; ++k) {
-            const uint2 m = p.masks[(size_t)k * p.n_words + wij];
-            const int mult = p.magnitude ? (int)p.mcount[(size_t)k * p.n_words * 32 + (size_t)wij * 32 + lane] : 1;
-            if ((m.x >> lane) & 1u) npos += mult;
-            if ((m.y >> lane) & 1u) nneg += mult;
-          }
-          int incl = nneg + npos;
+      for (int q = lane; q - lane < T; q += 32) {
+        // first lane l with incl[l] > q
+        int lo = 0;
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += y;
-          }
-          int64_t dst = dst0 + incl - (nneg + npos);
-          for (int q = 0; q < nneg; ++q) p.out[dst++] = pack_event(x, row, true);
-          for (int q = 0; q < npos; ++q) p.out[dst++] = pack_event(x, row, false);
+        for (int step = 16; step > 0; step >>= 1) {
+          const int probe = __shfl_sync(kFull, incl, lo + step - 1);
+          if (probe <= q) lo += step;
+        }
+        const int src = lo < 31 ? lo : 31;
+        const int src_incl = __shfl_sync(kFull, incl, src);
+        const int src_cnt = __shfl_sync(kFull, c, src);
+        const uint32_t m = __shfl_sync(kFull, all, src);
+        const uint32_t pm = __shfl_sync(kFull, pos, src);
+        const long long d = __shfl_sync(kFull, (long long)dst, src);
+        const int sx0 = __shfl_sync(kFull, x0, src);
+        const int srow = __shfl_sync(kFull, row, src);
+        if (q < T) {
+          const int r = q - (src_incl - src_cnt);
+          const int bit = __fns(m, 0, r + 1);
+          p.out[d + r] = pack_event(sx0 + bit, srow, !((pm >> bit) & 1u));
         }
       }
+    }
+    // ---- multi-link (equal timestamps) and magnitude words: per-lane counts
+    if (valid && !fast && cnt > 0) {
+      const int slot = atomicAdd(&s_nwork, 1);
+      s_item[slot] = it;
+      s_dst[slot] = dst;
+    }
+    __syncthreads();
+    const int nwork = s_nwork;
+    for (int jj = warp; jj < nwork; jj += kWarpsPerBlock) {
+      const int item = s_item[jj];
+      const int sj = item / nw;
+      const uint32_t wij = (uint32_t)(wbeg + (item - sj * nw));
+      const int row = (int)(wij / (uint32_t)p.wpr);
+      const int x = (int)(wij - (uint32_t)row * (uint32_t)p.wpr) * 32 + lane;
+      const int k0 = p.seg.seg_first[sj], nk = p.seg.seg_nlinks[sj];
+      int nneg = 0, npos = 0;
+      for (int k = k0; k < k0 + nk; ++k) {
+        const uint2 m = p.masks[(size_t)k * p.n_words + wij];
+        const int mult = p.magnitude ? (int)p.mcount[(size_t)k * p.n_words * 32 + (size_t)wij * 32 + lane] : 1;
+        if ((m.x >> lane) & 1u) npos += mult;
+        if ((m.y >> lane) & 1u) nneg += mult;
+      }
+      int incl = nneg + npos;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int64_t d = s_dst[jj] + incl - (nneg + npos);
+      for (int q = 0; q < nneg; ++q) p.out[d++] = pack_event(x, row, true);
+      for (int q = 0; q < npos; ++q) p.out[d++] = pack_event(x, row, false);
     }
     __syncthreads();
     carry += chunk_total;

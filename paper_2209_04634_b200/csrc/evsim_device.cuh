@@ -114,6 +114,85 @@ __device__ __forceinline__ float sample_quad_fast(const uint32_t* __restrict__ q
   return lerp_ref(top, bot, fy);
 }
 
+// ---- packed fp32x2 (sm_100 FADD2 / FMUL2): two independent IEEE fp32 ops per
+// instruction, each lane rounded exactly like its scalar counterpart ----
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float lo2(f32x2 v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return lo;
+}
+__device__ __forceinline__ float hi2(f32x2 v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return hi;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 add2_rz(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("add.rz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// a + f * (b - a) on both lanes (the reference's lerp, flow.cpp:54-56).
+// CAUTION: ptxas (CUDA 12.9) contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2
+// even with --fmad=false, which would drop the reference's intermediate
+// rounding.  The final adds are therefore scalar __fadd_rn (never fused).
+__device__ __forceinline__ f32x2 lerp2(f32x2 a, f32x2 b, f32x2 f) {
+  const f32x2 m = mul2(f, sub2(b, a));
+  return pk2(__fadd_rn(lo2(a), lo2(m)), __fadd_rn(hi2(a), hi2(m)));
+}
+// (c + s*u, c + t*u) for s, t = lanes of st, as the reference's separate mul + add
+__device__ __forceinline__ f32x2 affine2(float c, f32x2 st, float u) {
+  const f32x2 m = mul2(st, pk2(u, u));
+  return pk2(__fadd_rn(c, lo2(m)), __fadd_rn(c, hi2(m)));
+}
+
+// Two sample_u8 (simulate.cpp:10-26) through quad images at once: lane 0 =
+// (x.lo, y.lo) in qa, lane 1 = (x.hi, y.hi) in qb.  Finite coordinates only.
+__device__ __forceinline__ f32x2 sample_quad_pair(const uint32_t* __restrict__ qa, const uint32_t* __restrict__ qb,
+                                                  int w, int h, f32x2 x, f32x2 y) {
+  const float wm = (float)(w - 1), hm = (float)(h - 1);
+  const f32x2 X = pk2(fminf(fmaxf(lo2(x), 0.0f), wm), fminf(fmaxf(hi2(x), 0.0f), wm));
+  const f32x2 Y = pk2(fminf(fmaxf(lo2(y), 0.0f), hm), fminf(fmaxf(hi2(y), 0.0f), hm));
+  const f32x2 C23 = pk2(8388608.0f, 8388608.0f);
+  const f32x2 TX = add2_rz(X, C23), TY = add2_rz(Y, C23);  // 2^23 + trunc
+  const int xa = __float_as_int(lo2(TX)) - 0x4B000000, xb = __float_as_int(hi2(TX)) - 0x4B000000;
+  const int ya = __float_as_int(lo2(TY)) - 0x4B000000, yb = __float_as_int(hi2(TY)) - 0x4B000000;
+  const f32x2 FX = sub2(X, sub2(TX, C23));
+  const f32x2 FY = sub2(Y, sub2(TY, C23));
+  const uint32_t va = __ldg(qa + (size_t)ya * w + xa);
+  const uint32_t vb = __ldg(qb + (size_t)yb * w + xb);
+  // bytes -> 2^23 + b (PRMT), minus 2^23 (exact)
+  const f32x2 A00 = sub2(pk2(__uint_as_float(__byte_perm(va, 0x4B000000u, 0x7540)),
+                             __uint_as_float(__byte_perm(vb, 0x4B000000u, 0x7540))), C23);
+  const f32x2 A10 = sub2(pk2(__uint_as_float(__byte_perm(va, 0x4B000000u, 0x7541)),
+                             __uint_as_float(__byte_perm(vb, 0x4B000000u, 0x7541))), C23);
+  const f32x2 A01 = sub2(pk2(__uint_as_float(__byte_perm(va, 0x4B000000u, 0x7542)),
+                             __uint_as_float(__byte_perm(vb, 0x4B000000u, 0x7542))), C23);
+  const f32x2 A11 = sub2(pk2(__uint_as_float(__byte_perm(va, 0x4B000000u, 0x7543)),
+                             __uint_as_float(__byte_perm(vb, 0x4B000000u, 0x7543))), C23);
+  return lerp2(lerp2(A00, A10, FX), lerp2(A01, A11, FX), FY);
+}
+
 // lround() of v in [0, 2^31) without conversions: t = 2^52 + trunc(v) (RZ),
 // its low word is trunc(v); v - trunc(v) is exact.
 __device__ __forceinline__ int lround_pos_fast(double v) {

@@ -530,17 +530,24 @@ struct evsim_gpu_sim {
     // interpolation constants, interpolate_frames simulate.cpp:97-100
     const int N = n_interp_eff();
     const int K = N + 2;
-    std::vector<char> host((size_t)K * (8 + 8 + 4 + 4));
+    std::vector<char> host((size_t)K * (8 + 8 + 4 + 4 + 4 + 4 + 8));
     double* alpha = reinterpret_cast<double*>(host.data());
     double* oma = alpha + K;
     float* fwd = reinterpret_cast<float*>(oma + K);
     float* bwd = fwd + K;
+    float* alpha_f = bwd + K;
+    float* oma_f = alpha_f + K;
+    float* nfb = oma_f + K;  // K float2, 8-byte aligned (K*8*2 + K*4*4 bytes before it)
     for (int k = 0; k < K; ++k) {
       const double a = static_cast<double>(k) / static_cast<double>(N + 1);
       alpha[k] = a;
       oma[k] = 1.0 - a;
       fwd[k] = static_cast<float>(a);
       bwd[k] = static_cast<float>(1.0 - a);
+      alpha_f[k] = static_cast<float>(a);
+      oma_f[k] = static_cast<float>(1.0 - a);
+      nfb[2 * k] = -fwd[k];
+      nfb[2 * k + 1] = bwd[k];
     }
     consts.ensure(host.size(), stream);
     CK(cudaMemcpyAsync(consts.p, host.data(), host.size(), cudaMemcpyHostToDevice, stream));
@@ -634,6 +641,9 @@ struct evsim_gpu_sim {
     c.oma = consts.as<double>() + K;
     c.fwd = reinterpret_cast<const float*>(consts.as<double>() + 2 * K);
     c.bwd = c.fwd + K;
+    c.alpha_f = c.bwd + K;
+    c.oma_f = c.alpha_f + K;
+    c.nfb = reinterpret_cast<const float2*>(c.oma_f + K);
     c.P = P;
     c.d = desc();
     c.log_mode = log_mode();

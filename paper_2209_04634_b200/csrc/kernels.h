@@ -134,6 +134,9 @@ struct ChainParams {
   const double* oma;       // 1.0 - alpha
   const float* fwd;        // (float)alpha
   const float* bwd;        // (float)(1.0 - alpha)
+  const float* alpha_f;    // (float)alpha   (fp32 blend estimate)
+  const float* oma_f;      // (float)oma
+  const float2* nfb;       // (-(float)alpha, (float)(1.0 - alpha))
   // sparse provider (per pair strides)
   uint32_t* claims;        // [pair][N][P] keys (change << 24 | ~j)
   uint32_t* touched;       // [pair][ceil(N/32)][P] bits
