@@ -276,11 +276,10 @@ __global__ void __launch_bounds__(1024) segments_kernel(SegParams p) {
 // (pos, neg) masks.  Interpolated values of up to kB links are computed
 // before they are chained, so their gathers overlap.  Per-(link, block)
 // event counts go to counts[g][block].
-template <class Prov, bool kLog, bool kMag>
-__global__ void __launch_bounds__(256, 3) chain_kernel(ChainParams p) {
+template <class Prov, bool kLog, bool kMag, int kW, int kB, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) chain_kernel(ChainParams p) {
   extern __shared__ uint32_t s_cnt[];  // [n_pairs * L] event counts of this block
   __shared__ float s_lut[256];
-  constexpr int kW = 2, kB = 4;
   const int L = p.d.n_links;
   const int G = L * p.n_pairs;
   for (int i = threadIdx.x; i < G; i += blockDim.x) s_cnt[i] = 0;
@@ -384,6 +383,261 @@ __global__ void __launch_bounds__(256, 3) chain_kernel(ChainParams p) {
 #pragma unroll
       for (int q = 0; q < kW; ++q)
         if (c[q].valid) prov[q].finish(p, pc, c[q]);
+    }
+    if (kLog) {
+#pragma unroll
+      for (int q = 0; q < kW; ++q)
+        if (c[q].valid) p.ref[c[q].pix] = ref[q];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G; i += blockDim.x) p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
+}
+
+// ------------------------------------------------------------ dense chain kernel
+//
+// chain_kernel specialised for the dense provider on our own (always finite)
+// patch-grid flow — the hot loop of dense mode.  Same outputs; differences:
+//  * the links into chain frames 1..N run in straight-line batches of kB
+//    links x kW words: both bilinear samples of a frame as fp32x2 pairs, the
+//    clamps skipped when the whole warp's flow provably stays inside the
+//    frame, lround() decided by a bounded fp32 estimate (the rare lanes it
+//    cannot decide are recomputed exactly, warp-uniformly, after the batch);
+//  * per-frame constants in shared memory, ring slots advanced incrementally.
+
+// Rounded blend of chain frame k (simulate.cpp:108-116) at one pixel.
+//   X = x + (-fwd, bwd) * u, Y likewise: (prev sample, curr sample) as lanes.
+// kbias folds the 2^23 magic of both truncations out of the gather index.
+template <bool kClamp>
+__device__ __forceinline__ int dense_fast(const uint32_t* __restrict__ qp, const uint32_t* __restrict__ qc,
+                                          uint32_t w, uint32_t kbias, float wm, float hm, float xf, float yf,
+                                          float u, float v, float4 kc, unsigned& bad, unsigned bit) {
+  const f32x2 NB = pk2(kc.x, kc.y);
+  f32x2 X = affine2(xf, NB, u), Y = affine2(yf, NB, v);
+  if (kClamp) {
+    X = pk2(fminf(fmaxf(lo2(X), 0.0f), wm), fminf(fmaxf(hi2(X), 0.0f), wm));
+    Y = pk2(fminf(fmaxf(lo2(Y), 0.0f), hm), fminf(fmaxf(hi2(Y), 0.0f), hm));
+  }
+  const f32x2 C23 = pk2(8388608.0f, 8388608.0f);
+  const f32x2 TX = add2_rz(X, C23), TY = add2_rz(Y, C23);  // 2^23 + trunc
+  const f32x2 FX = sub2(X, sub2(TX, C23)), FY = sub2(Y, sub2(TY, C23));
+  const uint32_t ia = __float_as_uint(lo2(TY)) * w + __float_as_uint(lo2(TX)) + kbias;
+  const uint32_t ib = __float_as_uint(hi2(TY)) * w + __float_as_uint(hi2(TX)) + kbias;
+  const uint32_t va = __ldg(qp + ia), vb = __ldg(qc + ib);
+  // taps as 2^23 + byte (PRMT); differences of biased taps are exact
+  const f32x2 B00 = pk2(__uint_as_float(__byte_perm(va, 0x4B000000u, 0x7540)),
+                        __uint_as_float(__byte_perm(vb, 0x4B000000u, 0x7540)));
+  const f32x2 B10 = pk2(__uint_as_float(__byte_perm(va, 0x4B000000u, 0x7541)),
+                        __uint_as_float(__byte_perm(vb, 0x4B000000u, 0x7541)));
+  const f32x2 B01 = pk2(__uint_as_float(__byte_perm(va, 0x4B000000u, 0x7542)),
+                        __uint_as_float(__byte_perm(vb, 0x4B000000u, 0x7542)));
+  const f32x2 B11 = pk2(__uint_as_float(__byte_perm(va, 0x4B000000u, 0x7543)),
+                        __uint_as_float(__byte_perm(vb, 0x4B000000u, 0x7543)));
+  const f32x2 top = lerpd2(sub2(B00, C23), sub2(B10, B00), FX);
+  const f32x2 bot = lerpd2(sub2(B01, C23), sub2(B11, B01), FX);
+  const f32x2 S = lerp2(top, bot, FY);
+  // s = RN64(RN64(oma*fp) + RN64(alpha*fc)); e below satisfies |e - s| < 6.2e-5
+  // (see DenseProvider::interp), RN(e + c) adds < 1.6e-5.  If
+  // floor(e + 0.5 -/+ 2e-4) agree, that floor is lround(s) = floor(s + 0.5).
+  const float e = __fmaf_rn(kc.z, lo2(S), __fmul_rn(kc.w, hi2(S)));
+  const f32x2 T = add2_rz(add2(pk2(e, e), pk2(0.5f - 2e-4f, 0.5f + 2e-4f)), C23);
+  if (__float_as_uint(lo2(T)) != __float_as_uint(hi2(T))) bad |= bit;
+  return __float_as_int(hi2(T)) - 0x4B000000;
+}
+
+// The exact reference expression for the lanes dense_fast cannot decide.
+__device__ __noinline__ int dense_exact(const float2* nfb, const double* oma, const double* alpha,
+                                        const uint32_t* qp, const uint32_t* qc, int w, int h, float xf, float yf,
+                                        float u, float v, int k) {
+  const float2 nb = __ldg(nfb + k);
+  const f32x2 NB = pk2(nb.x, nb.y);
+  const f32x2 S = sample_quad_pair(qp, qc, w, h, affine2(xf, NB, u), affine2(yf, NB, v));
+  const double blend = dadd(dmul(__ldg(oma + k), (double)lo2(S)), dmul(__ldg(alpha + k), (double)hi2(S)));
+  return lround_pos_fast(blend);
+}
+
+struct DenseWord {
+  bool have, valid;
+  int64_t wi;
+  int x, y;
+  uint32_t pix;
+  float xf, yf;
+  float u, v;
+};
+
+// One link of the chain at one word: the reference rule, ballots, counts.
+template <bool kLog, bool kMag>
+__device__ __forceinline__ void chain_step(const ChainParams& p, const float* s_lut, uint32_t* s_cnt, int g,
+                                           const DenseWord& c, int lane, int val, float& ref, int& before) {
+  bool pos, neg;
+  int mult = 1;
+  if (kLog) {
+    const float lk = s_lut[val];
+    const float dd = fsub(lk, ref);
+    pos = dd > p.c_pos_log;
+    neg = !pos && dd < p.c_neg_log;
+    if (kMag && (pos || neg)) mult = (int)floorf(__fdiv_rn(dd, pos ? p.c_pos_log : p.c_neg_log));
+    if ((pos || neg) && c.valid) ref = lk;
+  } else {
+    const int d = val - before;  // difference_frame, core.cpp:14-15
+    pos = d > p.c_pos;           // threshold_events_into, core.cpp:31-43
+    neg = !pos && d < p.c_neg;
+    if (kMag && (pos || neg)) mult = pos ? d / p.c_pos : d / p.c_neg;
+    before = val;
+  }
+  pos = pos && c.valid;
+  neg = neg && c.valid;
+  const unsigned bp = __ballot_sync(kFull, pos);
+  const unsigned bn = __ballot_sync(kFull, neg);
+  if (!c.have) return;
+  if (lane == 0) p.masks[(size_t)g * p.n_words + c.wi] = make_uint2(bp, bn);
+  if (kMag) {
+    const int m = (pos || neg) ? mult : 0;
+    p.mcount[(size_t)g * p.n_words * 32 + c.wi * 32 + lane] = (uint16_t)m;
+    int s = m;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    if (lane == 0) {
+      p.wcount[(size_t)g * p.n_words + c.wi] = (uint32_t)s;
+      if (s) atomicAdd(&s_cnt[g], (uint32_t)s);
+    }
+  } else if (lane == 0 && (bp | bn)) {
+    atomicAdd(&s_cnt[g], (uint32_t)(__popc(bp) + __popc(bn)));
+  }
+}
+
+template <int kW, int kNB, bool kClamp>
+__device__ __forceinline__ unsigned dense_batch(const float4* s_kc, const uint32_t* qp, const uint32_t* qc,
+                                                uint32_t w, uint32_t kbias, float wm, float hm, const DenseWord* c,
+                                                int k0, int (&vals)[kW][4]) {
+  unsigned bad = 0;
+#pragma unroll
+  for (int j = 0; j < kNB; ++j) {
+    const float4 kc = s_kc[k0 + j];
+#pragma unroll
+    for (int q = 0; q < kW; ++q)
+      vals[q][j] = dense_fast<kClamp>(qp, qc, w, kbias, wm, hm, c[q].xf, c[q].yf, c[q].u, c[q].v, kc, bad,
+                                      1u << (q * 4 + j));
+  }
+  return bad;
+}
+
+template <bool kLog, bool kMag>
+__global__ void __launch_bounds__(256, 3) chain_dense_kernel(ChainParams p) {
+  constexpr int kW = 2, kB = 4;
+  extern __shared__ float4 s_dyn4[];
+  __shared__ float s_lut[256];
+  const int L = p.d.n_links, G = L * p.n_pairs, N = p.n_interp;
+  float4* s_kc = s_dyn4;                                       // [N + 2]
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_dyn4 + N + 2);  // [G]
+  for (int i = threadIdx.x; i < G; i += blockDim.x) s_cnt[i] = 0;
+  for (int i = threadIdx.x; i < N + 2; i += blockDim.x) s_kc[i] = p.kc[i];
+  if (kLog) s_lut[threadIdx.x] = p.lut[threadIdx.x];
+  __syncthreads();
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t w = (uint32_t)p.w;
+  const float wm = (float)(p.w - 1), hm = (float)(p.h - 1);
+  const uint32_t kbias = 0u - 0x4B000000u * (w + 1u);
+  // link l joins chain frames start + l and start + l + 1; the first n_int
+  // links end in an interpolated frame (k <= N), a last one (endpoints) in curr
+  const int kfirst = p.d.start + 1;
+  const int n_int = min(L, N - p.d.start);
+  const int64_t wbeg = (int64_t)b * p.words_per_block;
+  const int64_t wend = min(wbeg + p.words_per_block, p.n_words);
+  for (int64_t w0 = wbeg + warp; w0 < wend; w0 += kWarpsPerBlock * kW) {
+    DenseWord c[kW];
+    float ref[kW];
+    int before[kW];
+#pragma unroll
+    for (int q = 0; q < kW; ++q) {
+      c[q].wi = w0 + q * kWarpsPerBlock;
+      c[q].have = c[q].wi < wend;
+      const int64_t ww = c[q].have ? c[q].wi : w0;
+      const int row = (int)((uint32_t)ww / (uint32_t)p.wpr);
+      const int x = (int)(ww - (int64_t)row * p.wpr) * 32 + lane;
+      c[q].valid = c[q].have && x < p.w;
+      c[q].x = x < p.w ? x : p.w - 1;
+      c[q].y = row;
+      c[q].pix = (uint32_t)row * w + (uint32_t)c[q].x;
+      c[q].xf = (float)c[q].x;
+      c[q].yf = (float)c[q].y;
+      ref[q] = kLog ? p.ref[c[q].pix] : 0.0f;
+      before[q] = 0;
+    }
+    int sp = p.r0 % p.R;
+    for (int i = 0; i < p.n_pairs; ++i) {
+      const int sc = sp + 1 == p.R ? 0 : sp + 1;
+      const uint32_t* qp = p.quads.at(sp);
+      const uint32_t* qc = p.quads.at(sc);
+      PairCtx pc{};
+      pc.pu = p.g0.pu + (size_t)i * p.g0.pair_stride;
+      pc.pv = p.g0.pv + (size_t)i * p.g0.pair_stride;
+      bool safe = true;
+#pragma unroll
+      for (int q = 0; q < kW; ++q) {
+        PixelCtx pxc;
+        pxc.x = c[q].x;
+        pxc.y = c[q].y;
+        DenseProvider<false> prov;
+        prov.init(p, pc, pxc);
+        c[q].u = prov.u;
+        c[q].v = prov.v;
+        // every sample x + s*u, |s| <= 1, stays in [0, w-1] (rounding is
+        // monotone and the bounds are representable): no clamp needed
+        safe = safe && fabsf(prov.u) <= fminf(c[q].xf, wm - c[q].xf) && fabsf(prov.v) <= fminf(c[q].yf, hm - c[q].yf);
+        if (!kLog)
+          before[q] = p.d.start == 0 ? (int)p.frames.at(sp)[c[q].pix]
+                                     : dense_exact(p.nfb, p.oma, p.alpha, qp, qc, p.w, p.h, c[q].xf, c[q].yf, prov.u, prov.v, 1);
+      }
+      safe = __all_sync(kFull, safe);
+      const int gbase = i * L;
+      int l0 = 0;
+      for (; l0 < n_int; l0 += kB) {
+        const int nb = min(kB, n_int - l0);
+        int vals[kW][4];
+        unsigned bad;
+        if (nb == kB) {
+          bad = safe ? dense_batch<kW, kB, false>(s_kc, qp, qc, w, kbias, wm, hm, c, kfirst + l0, vals)
+                     : dense_batch<kW, kB, true>(s_kc, qp, qc, w, kbias, wm, hm, c, kfirst + l0, vals);
+        } else {
+          bad = 0;
+          for (int j = 0; j < nb; ++j) {
+            int v1[kW][4];
+            bad |= (safe ? dense_batch<kW, 1, false>(s_kc, qp, qc, w, kbias, wm, hm, c, kfirst + l0 + j, v1)
+                         : dense_batch<kW, 1, true>(s_kc, qp, qc, w, kbias, wm, hm, c, kfirst + l0 + j, v1))
+                   << j;
+#pragma unroll
+            for (int q = 0; q < kW; ++q)
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj)
+                if (jj == j) vals[q][jj] = v1[q][0];
+          }
+        }
+        if (__any_sync(kFull, bad != 0u)) {
+#pragma unroll
+          for (int q = 0; q < kW; ++q)
+#pragma unroll
+            for (int j = 0; j < kB; ++j)
+              if ((bad >> (q * 4 + j)) & 1u)
+                vals[q][j] = dense_exact(p.nfb, p.oma, p.alpha, qp, qc, p.w, p.h, c[q].xf, c[q].yf, c[q].u, c[q].v,
+                                       kfirst + l0 + j);
+        }
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+          if (j >= nb) break;
+#pragma unroll
+          for (int q = 0; q < kW; ++q)
+            chain_step<kLog, kMag>(p, s_lut, s_cnt, gbase + l0 + j, c[q], lane, vals[q][j], ref[q], before[q]);
+        }
+      }
+      if (n_int < L) {  // the link into curr (include_endpoints)
+        const uint8_t* curr = p.frames.at(sc);
+#pragma unroll
+        for (int q = 0; q < kW; ++q)
+          chain_step<kLog, kMag>(p, s_lut, s_cnt, gbase + L - 1, c[q], lane, (int)curr[c[q].pix], ref[q], before[q]);
+      }
+      sp = sc;
     }
     if (kLog) {
 #pragma unroll
@@ -772,15 +1026,23 @@ __global__ void init_ref_kernel(const uint8_t* __restrict__ f, const float* __re
 
 // ------------------------------------------------------------ launches
 
-template <class Prov, bool kLog, bool kMag>
-static void launch_chain_t(const ChainParams& p, cudaStream_t s) {
+template <class Prov, bool kLog, bool kMag, int kW, int kB, int kMinBlocks>
+static void launch_chain_k(const ChainParams& p, cudaStream_t s) {
   const size_t sm = (size_t)std::max(p.d.n_links * p.n_pairs, 1) * sizeof(uint32_t);
+  auto* k = chain_kernel<Prov, kLog, kMag, kW, kB, kMinBlocks>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(chain_kernel<Prov, kLog, kMag>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     attr = true;
   }
-  chain_kernel<Prov, kLog, kMag><<<p.n_blocks, 256, sm, s>>>(p);
+  k<<<p.n_blocks, 256, sm, s>>>(p);
+}
+
+template <class Prov, bool kLog, bool kMag>
+static void launch_chain_t(const ChainParams& p, cudaStream_t s) {
+  // 2 words x 4 links in flight per warp; 3 blocks of 256 per SM (80 regs).
+  // Measured on c2/c5: 1 word x 8 links is within 5% on c2, 8% slower on c5.
+  launch_chain_k<Prov, kLog, kMag, 2, 4, 3>(p, s);
 }
 
 template <class Prov>
@@ -794,7 +1056,32 @@ static void launch_chain_mode(const ChainParams& p, cudaStream_t s) {
   }
 }
 
+template <bool kLog, bool kMag>
+static void launch_chain_dense(const ChainParams& p, size_t sm, cudaStream_t s) {
+  auto* k = chain_dense_kernel<kLog, kMag>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    attr = true;
+  }
+  k<<<p.n_blocks, 256, sm, s>>>(p);
+}
+
 void launch_chain(const ChainParams& p, int provider, cudaStream_t s) {
+  if (provider == kProvDenseGrid && p.kc) {
+    const size_t sm = (size_t)(p.n_interp + 2) * sizeof(float4) +
+                      (size_t)std::max(p.d.n_links * p.n_pairs, 1) * sizeof(uint32_t);
+    if (sm <= 96 * 1024) {
+      if (p.log_mode) {
+        if (p.magnitude) launch_chain_dense<true, true>(p, sm, s);
+        else launch_chain_dense<true, false>(p, sm, s);
+      } else {
+        if (p.magnitude) launch_chain_dense<false, true>(p, sm, s);
+        else launch_chain_dense<false, false>(p, sm, s);
+      }
+      return;
+    }
+  }
   switch (provider) {
     case kProvDenseGrid: launch_chain_mode<DenseProvider<false>>(p, s); break;
     case kProvSparse: launch_chain_mode<SparseProvider>(p, s); break;

@@ -123,13 +123,13 @@ __device__ __forceinline__ f32x2 pk2(float lo, float hi) {
   return r;
 }
 __device__ __forceinline__ float lo2(f32x2 v) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  float lo;
+  asm("{.reg .f32 t; mov.b64 {%0, t}, %1;}" : "=f"(lo) : "l"(v));
   return lo;
 }
 __device__ __forceinline__ float hi2(f32x2 v) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  float hi;
+  asm("{.reg .f32 t; mov.b64 {t, %0}, %1;}" : "=f"(hi) : "l"(v));
   return hi;
 }
 __device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
@@ -158,6 +158,11 @@ __device__ __forceinline__ f32x2 add2_rz(f32x2 a, f32x2 b) {
 // rounding.  The final adds are therefore scalar __fadd_rn (never fused).
 __device__ __forceinline__ f32x2 lerp2(f32x2 a, f32x2 b, f32x2 f) {
   const f32x2 m = mul2(f, sub2(b, a));
+  return pk2(__fadd_rn(lo2(a), lo2(m)), __fadd_rn(hi2(a), hi2(m)));
+}
+// a + f * d on both lanes, d = b - a already formed (exactly) by the caller
+__device__ __forceinline__ f32x2 lerpd2(f32x2 a, f32x2 d, f32x2 f) {
+  const f32x2 m = mul2(f, d);
   return pk2(__fadd_rn(lo2(a), lo2(m)), __fadd_rn(hi2(a), hi2(m)));
 }
 // (c + s*u, c + t*u) for s, t = lanes of st, as the reference's separate mul + add

@@ -530,8 +530,9 @@ struct evsim_gpu_sim {
     // interpolation constants, interpolate_frames simulate.cpp:97-100
     const int N = n_interp_eff();
     const int K = N + 2;
-    std::vector<char> host((size_t)K * (8 + 8 + 4 + 4 + 4 + 4 + 8));
-    double* alpha = reinterpret_cast<double*>(host.data());
+    std::vector<char> host((size_t)K * (16 + 8 + 8 + 4 + 4 + 4 + 4 + 8));
+    float* kc = reinterpret_cast<float*>(host.data());  // K float4 first (16-byte aligned)
+    double* alpha = reinterpret_cast<double*>(kc + 4 * K);
     double* oma = alpha + K;
     float* fwd = reinterpret_cast<float*>(oma + K);
     float* bwd = fwd + K;
@@ -548,6 +549,10 @@ struct evsim_gpu_sim {
       oma_f[k] = static_cast<float>(1.0 - a);
       nfb[2 * k] = -fwd[k];
       nfb[2 * k + 1] = bwd[k];
+      kc[4 * k + 0] = -fwd[k];
+      kc[4 * k + 1] = bwd[k];
+      kc[4 * k + 2] = oma_f[k];
+      kc[4 * k + 3] = alpha_f[k];
     }
     consts.ensure(host.size(), stream);
     CK(cudaMemcpyAsync(consts.p, host.data(), host.size(), cudaMemcpyHostToDevice, stream));
@@ -637,9 +642,10 @@ struct evsim_gpu_sim {
     c.frames = Ring<const uint8_t>{frames.as<uint8_t>(), P};
     c.quads = Ring<const uint32_t>{quads.as<uint32_t>(), P};
     const int K = N + 2;
-    c.alpha = consts.as<double>();
-    c.oma = consts.as<double>() + K;
-    c.fwd = reinterpret_cast<const float*>(consts.as<double>() + 2 * K);
+    c.kc = consts.as<float4>();
+    c.alpha = reinterpret_cast<const double*>(c.kc + K);
+    c.oma = c.alpha + K;
+    c.fwd = reinterpret_cast<const float*>(c.alpha + 2 * K);
     c.bwd = c.fwd + K;
     c.alpha_f = c.bwd + K;
     c.oma_f = c.alpha_f + K;

@@ -137,6 +137,7 @@ struct ChainParams {
   const float* alpha_f;    // (float)alpha   (fp32 blend estimate)
   const float* oma_f;      // (float)oma
   const float2* nfb;       // (-(float)alpha, (float)(1.0 - alpha))
+  const float4* kc;        // (-(float)alpha, (float)(1 - alpha), (float)oma, (float)alpha)
   // sparse provider (per pair strides)
   uint32_t* claims;        // [pair][N][P] keys (change << 24 | ~j)
   uint32_t* touched;       // [pair][ceil(N/32)][P] bits
