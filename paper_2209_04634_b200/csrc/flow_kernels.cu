@@ -335,6 +335,206 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_tile_kernel(DenseLKParams
   }
 }
 
+// ---------------------------------------------------------------- dense LK, warp form
+// The tile of 8x4 patches for the preset radii (4, 6) when no template
+// coordinate needs clamping (extent > 2r+1: patch_centers, flow.cpp:97-107,
+// keeps every patch inside the level).  After staging the template region,
+// each warp owns one tile row (8 patches) and runs their whole solve alone —
+// only __syncwarp, no block barriers:
+//  * template sums (exact in fp64) split over 4 row-parts
+//    per patch and combined with xor-shuffles;
+//  * per iteration, the bilinear split of every template column / row —
+//    sample(curr, px + u, py + v) (flow.cpp:203) pairs a column's x-split
+//    with a row's y-split — is tabulated; lanes = (row within a group of RPG
+//    rows, column) of one patch compute the products gx*res, gy*res;
+//  * 16 lanes (patch, b1|b2) then run the ordered fp64 sums in the
+//    reference's k order (flow.cpp:204-205) and every lane applies its
+//    patch's 2x2 solve (flow.cpp:207-213).
+__host__ __device__ constexpr int lk_pick_pitch(int rw, int d, int rpg) {
+  // smallest pitch >= rw whose RPG rows of D columns fall in distinct banks
+  for (int p = rw; p < rw + 32; ++p) {
+    bool ok = true;
+    for (int a = 1; a < rpg; ++a) {
+      const int m = (a * p) % 32;
+      if (m < d || m > 32 - d) ok = false;
+    }
+    if (ok) return p;
+  }
+  return rw;
+}
+
+template <int kR>
+struct LKWarp {
+  static constexpr int D = 2 * kR + 1, P2 = D * D;
+  static constexpr int RPG = 32 / D;                // template rows per lane group
+  static constexpr int NG = (D + RPG - 1) / RPG;    // lane groups per patch
+  static constexpr int PB = NG <= 4 ? 2 : 1;        // patches per gather batch
+  static constexpr int kPW = kLKTileX;              // patches per warp (one tile row)
+  static constexpr int rw = (kLKTileX - 1) * kR + 2 * kR + 3;
+  static constexpr int rows = (kLKTileY - 1) * kR + 2 * kR + 3;
+  static constexpr int pitch = lk_pick_pitch(rw, D, RPG);
+  static constexpr int plane = (pitch * rows + 3) & ~3;                   // floats
+  static constexpr int b_off = 3 * plane;                                 // float2 [warp][kPW][P2]
+  static constexpr int t_off = b_off + 2 * kLKTileY * kPW * P2;           // float2 [warp][2][kPW][D]
+  static constexpr int floats = t_off + 2 * kLKTileY * 2 * kPW * D;
+};
+static_assert(kLKThreads == 32 * kLKTileY, "one warp per tile row");
+
+template <int kR>
+__global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams p) {
+  using G = LKWarp<kR>;
+  constexpr int D = G::D, P2 = G::P2, RPG = G::RPG, NG = G::NG, PB = G::PB, kPW = G::kPW, pitch = G::pitch;
+  extern __shared__ __align__(16) float smem[];
+  const int z = blockIdx.z;  // frame pair
+  GridGeom g = p.g;
+  g.pu += z * g.pair_stride;
+  g.pv += z * g.pair_stride;
+  GridGeom coarse = p.coarse;
+  coarse.pu += z * coarse.pair_stride;
+  coarse.pv += z * coarse.pair_stride;
+  const float* __restrict__ prev = p.prev.at((p.r0 + z) % p.R);
+  const float4* __restrict__ qcurr = p.qcurr.at((p.r0 + z + 1) % p.R);
+  const int w = g.w, h = g.h;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int i0 = blockIdx.x * kLKTileX, j0 = blockIdx.y * kLKTileY;
+  const int i1 = min(i0 + kLKTileX, g.ncx) - 1, j1 = min(j0 + kLKTileY, g.ncy) - 1;
+  const int rx0 = __ldg(g.cx + i0) - kR - 1, ry0 = __ldg(g.cy + j0) - kR - 1;
+  const int rw = __ldg(g.cx + i1) - __ldg(g.cx + i0) + 2 * kR + 3;
+  const int rh = __ldg(g.cy + j1) - __ldg(g.cy + j0) + 2 * kR + 3;
+  float* sP = smem;               // [rows][pitch] prev, replicate-staged
+  float* sGx = smem + G::plane;   // [rows][pitch] central differences
+  float* sGy = smem + 2 * G::plane;
+  float2* sB = reinterpret_cast<float2*>(smem + G::b_off) + warp * (kPW * P2);     // [kPW][P2]
+  float2* sX = reinterpret_cast<float2*>(smem + G::t_off) + warp * (2 * kPW * D);  // [kPW][D] (x0, fx)
+  float2* sY = sX + kPW * D;                                                        // [kPW][D] (y0*w, fy)
+
+  for (int yy = warp; yy < rh; yy += kLKTileY) {
+    const float* src = prev + (size_t)clampi(ry0 + yy, 0, h - 1) * w;
+    for (int xx = lane; xx < rw; xx += 32) sP[yy * pitch + xx] = __ldg(src + clampi(rx0 + xx, 0, w - 1));
+  }
+  // this lane's patch: pl = lane & 7 of tile row `warp` (all four 8-lane parts agree)
+  const int pl = lane & 7, part = lane >> 3;
+  const int pi = i0 + pl, pj = j0 + warp;
+  const bool valid = pi < g.ncx && pj < g.ncy;
+  const int cx = __ldg(g.cx + (valid ? pi : i0)), cy = __ldg(g.cy + (valid ? pj : j0));
+  float u = 0.0f, v = 0.0f;
+  if (valid && p.has_coarse && part == 0) upsample_at(coarse, w, h, cx, cy, u, v);
+  u = __shfl_sync(kFull, u, pl);
+  v = __shfl_sync(kFull, v, pl);
+  __syncthreads();
+  for (int yy = 1 + warp; yy < rh - 1; yy += kLKTileY) {
+    const float* row = sP + yy * pitch;
+    for (int xx = 1 + lane; xx < rw - 1; xx += 32) {
+      sGx[yy * pitch + xx] = fmul(0.5f, fsub(row[xx + 1], row[xx - 1]));
+      sGy[yy * pitch + xx] = fmul(0.5f, fsub(row[pitch + xx], row[xx - pitch]));
+    }
+  }
+  __syncthreads();
+  // template sums (flow.cpp:177-194), rows part, part+4, ... of patch pl
+  const int tb = (cy - ry0) * pitch + (cx - rx0);  // region offset of the patch centre
+  double gxx = 0.0, gxy = 0.0, gyy = 0.0;
+  for (int oy = -kR + part; oy <= kR; oy += 4) {
+#pragma unroll
+    for (int ox = -kR; ox <= kR; ++ox) {
+      const int o = tb + oy * pitch + ox;
+      const float a = sGx[o], b = sGy[o];
+      gxx = dadd(gxx, (double)fmul(a, a));
+      gxy = dadd(gxy, (double)fmul(a, b));
+      gyy = dadd(gyy, (double)fmul(b, b));
+    }
+  }
+#pragma unroll
+  for (int m = 8; m <= 16; m <<= 1) {  // exact, so any combination order
+    gxx = dadd(gxx, __shfl_xor_sync(kFull, gxx, m));
+    gxy = dadd(gxy, __shfl_xor_sync(kFull, gxy, m));
+    gyy = dadd(gyy, __shfl_xor_sync(kFull, gyy, m));
+  }
+  const bool solve = valid && min_eigenvalue(gxx, gxy, gyy) > dmul(1e-4, (double)P2);
+  const double inv_det = solve ? __ddiv_rn(1.0, dsub(dmul(gxx, gyy), dmul(gxy, gxy))) : 0.0;
+  const unsigned solved = __ballot_sync(kFull, solve) & 0xFFu;  // bit j: patch j of this warp
+  const float max_step = (float)kR;
+  const float wm = (float)(w - 1), hm = (float)(h - 1);
+  // the lane's place in a patch: template row ry of each group, column ox
+  const int ry = lane / D, ox = lane - (lane / D) * D;
+  const bool lane_on = lane < RPG * D;
+  const int oxs = lane_on ? ox : 0;
+  for (int it = 0; it < p.iterations && solved; ++it) {
+    // split tables for the warp's 8 patches (flow.cpp:45-53 on px + u, py + v; u, v finite)
+#pragma unroll
+    for (int e0 = 0; e0 < kPW * D; e0 += 32) {
+      const int e = e0 + lane;
+      const int ptx = e < kPW * D ? e / D : 0, i = e - ptx * D;
+      const float uj = __shfl_sync(kFull, u, ptx), vj = __shfl_sync(kFull, v, ptx);
+      const int cxj = __shfl_sync(kFull, cx, ptx), cyj = __shfl_sync(kFull, cy, ptx);
+      if (e < kPW * D) {
+        const float x = fminf(fmaxf(fadd((float)(cxj + i - kR), uj), 0.0f), wm);
+        const float y = fminf(fmaxf(fadd((float)(cyj + i - kR), vj), 0.0f), hm);
+        int x0, y0;
+        const float x0f = trunc_magic(x, x0), y0f = trunc_magic(y, y0);
+        sX[e] = make_float2(__int_as_float(x0), fsub(x, x0f));
+        sY[e] = make_float2(__int_as_float(y0 * w), fsub(y, y0f));
+      }
+    }
+    __syncwarp();
+    // residual products gx*res, gy*res of every template pixel (flow.cpp:202-205)
+#pragma unroll 1
+    for (int pb = 0; pb < kPW; pb += PB) {
+      if (!((solved >> pb) & ((1u << PB) - 1u))) continue;  // warp-uniform
+      float4 q[PB][NG];
+      float fx[PB], fy[PB][NG];
+      int off[PB];
+#pragma unroll
+      for (int j = 0; j < PB; ++j) {
+        const float2 X = sX[(pb + j) * D + oxs];
+        fx[j] = X.y;
+        off[j] = __shfl_sync(kFull, tb, pb + j) + (ry - kR) * pitch + (ox - kR);
+#pragma unroll
+        for (int gg = 0; gg < NG; ++gg) {
+          const int oy = gg * RPG + ry;
+          const float2 Y = sY[(pb + j) * D + (oy < D ? oy : 0)];
+          fy[j][gg] = Y.y;
+          q[j][gg] = __ldg(qcurr + (__float_as_int(Y.x) + __float_as_int(X.x)));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < PB; ++j) {
+#pragma unroll
+        for (int gg = 0; gg < NG; ++gg) {
+          const int oy = gg * RPG + ry;
+          if (!lane_on || oy >= D) continue;
+          const float4 a = q[j][gg];
+          const float smp = lerp_ref(lerp_ref(a.x, a.y, fx[j]), lerp_ref(a.z, a.w, fx[j]), fy[j][gg]);
+          const int o = off[j] + gg * RPG * pitch;
+          const float res = fsub(smp, sP[o]);
+          sB[(pb + j) * P2 + oy * D + ox] = make_float2(fmul(sGx[o], res), fmul(sGy[o], res));
+        }
+      }
+    }
+    __syncwarp();
+    // ordered fp64 sums: lane = (patch, b1|b2), k order
+    double acc = 0.0;
+    if (lane < 2 * kPW && ((solved >> pl) & 1u)) {
+      const float* src = reinterpret_cast<const float*>(sB + pl * P2) + (lane >> 3);
+#pragma unroll 9
+      for (int k = 0; k < P2; ++k) acc = dadd(acc, (double)src[2 * k]);
+    }
+    const double b1 = __shfl_sync(kFull, acc, pl), b2 = __shfl_sync(kFull, acc, pl + 8);
+    __syncwarp();
+    if (solve) {
+      float du = __double2float_rn(dmul(-dsub(dmul(gyy, b1), dmul(gxy, b2)), inv_det));
+      float dv = __double2float_rn(dmul(-dsub(dmul(gxx, b2), dmul(gxy, b1)), inv_det));
+      du = clamp_ref(du, -max_step, max_step);
+      dv = clamp_ref(dv, -max_step, max_step);
+      u = fadd(u, du);
+      v = fadd(v, dv);
+    }
+  }
+  if (lane < kPW && valid) {
+    g.pu[(size_t)pj * g.ncx + pi] = u;
+    g.pv[(size_t)pj * g.ncx + pi] = v;
+  }
+}
+
 // Fallback for radii whose tile does not fit in shared memory (r > 10): one
 // thread per patch, template and gradients straight from L1/L2.
 __global__ void __launch_bounds__(128) dense_lk_global_kernel(DenseLKParams p) {
@@ -529,12 +729,17 @@ void launch_dense_lk(const DenseLKParams& p, int n_pairs, cudaStream_t s) {
   const size_t sm = dense_lk_smem(r);
   static bool attr_set = false;
   if (!attr_set) {
+    cudaFuncSetAttribute(dense_lk_warp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(dense_lk_warp_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(dense_lk_tile_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(dense_lk_tile_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(dense_lk_tile_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(dense_lk_tile_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
-  if (r == 4) dense_lk_tile_kernel<4><<<grid, kLKThreads, sm, s>>>(p);
+  const bool inside = p.g.w > 2 * r + 1 && p.g.h > 2 * r + 1;  // no template clamping
+  if (r == 4 && inside) dense_lk_warp_kernel<4><<<grid, kLKThreads, LKWarp<4>::floats * sizeof(float), s>>>(p);
+  else if (r == 6 && inside) dense_lk_warp_kernel<6><<<grid, kLKThreads, LKWarp<6>::floats * sizeof(float), s>>>(p);
+  else if (r == 4) dense_lk_tile_kernel<4><<<grid, kLKThreads, sm, s>>>(p);
   else if (r == 6) dense_lk_tile_kernel<6><<<grid, kLKThreads, sm, s>>>(p);
   else if (sm <= 200 * 1024) dense_lk_tile_kernel<0><<<grid, kLKThreads, sm, s>>>(p);
   else dense_lk_global_kernel<<<dim3((p.g.ncx * p.g.ncy + 127) / 128, n_pairs), 128, 0, s>>>(p);
