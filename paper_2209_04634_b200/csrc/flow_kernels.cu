@@ -368,14 +368,13 @@ struct LKWarp {
   static constexpr int D = 2 * kR + 1, P2 = D * D;
   static constexpr int RPG = 32 / D;                // template rows per lane group
   static constexpr int NG = (D + RPG - 1) / RPG;    // lane groups per patch
-  static constexpr int PB = NG <= 4 ? 2 : 1;        // patches per gather batch
   static constexpr int kPW = kLKTileX;              // patches per warp (one tile row)
   static constexpr int rw = (kLKTileX - 1) * kR + 2 * kR + 3;
   static constexpr int rows = (kLKTileY - 1) * kR + 2 * kR + 3;
   static constexpr int pitch = lk_pick_pitch(rw, D, RPG);
   static constexpr int plane = (pitch * rows + 3) & ~3;                   // floats
-  static constexpr int b_off = 3 * plane;                                 // float2 [warp][kPW][P2]
-  static constexpr int t_off = b_off + 2 * kLKTileY * kPW * P2;           // float2 [warp][2][kPW][D]
+  static constexpr int b_off = 3 * plane;                                 // float2 [warp][kPW][RPG*D]
+  static constexpr int t_off = b_off + 2 * kLKTileY * kPW * RPG * D;      // float2 [warp][2][kPW][D]
   static constexpr int floats = t_off + 2 * kLKTileY * 2 * kPW * D;
 };
 static_assert(kLKThreads == 32 * kLKTileY, "one warp per tile row");
@@ -383,7 +382,7 @@ static_assert(kLKThreads == 32 * kLKTileY, "one warp per tile row");
 template <int kR>
 __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams p) {
   using G = LKWarp<kR>;
-  constexpr int D = G::D, P2 = G::P2, RPG = G::RPG, NG = G::NG, PB = G::PB, kPW = G::kPW, pitch = G::pitch;
+  constexpr int D = G::D, P2 = G::P2, RPG = G::RPG, NG = G::NG, kPW = G::kPW, pitch = G::pitch;
   extern __shared__ __align__(16) float smem[];
   const int z = blockIdx.z;  // frame pair
   GridGeom g = p.g;
@@ -404,7 +403,7 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
   float* sP = smem;               // [rows][pitch] prev, replicate-staged
   float* sGx = smem + G::plane;   // [rows][pitch] central differences
   float* sGy = smem + 2 * G::plane;
-  float2* sB = reinterpret_cast<float2*>(smem + G::b_off) + warp * (kPW * P2);     // [kPW][P2]
+  float2* sB = reinterpret_cast<float2*>(smem + G::b_off) + warp * (kPW * RPG * D);  // [kPW][RPG*D]
   float2* sX = reinterpret_cast<float2*>(smem + G::t_off) + warp * (2 * kPW * D);  // [kPW][D] (x0, fx)
   float2* sY = sX + kPW * D;                                                        // [kPW][D] (y0*w, fy)
 
@@ -476,50 +475,51 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
       }
     }
     __syncwarp();
-    // residual products gx*res, gy*res of every template pixel (flow.cpp:202-205)
-#pragma unroll 1
-    for (int pb = 0; pb < kPW; pb += PB) {
-      if (!((solved >> pb) & ((1u << PB) - 1u))) continue;  // warp-uniform
-      float4 q[PB][NG];
-      float fx[PB], fy[PB][NG];
-      int off[PB];
-#pragma unroll
-      for (int j = 0; j < PB; ++j) {
-        const float2 X = sX[(pb + j) * D + oxs];
-        fx[j] = X.y;
-        off[j] = __shfl_sync(kFull, tb, pb + j) + (ry - kR) * pitch + (ox - kR);
-#pragma unroll
-        for (int gg = 0; gg < NG; ++gg) {
-          const int oy = gg * RPG + ry;
-          const float2 Y = sY[(pb + j) * D + (oy < D ? oy : 0)];
-          fy[j][gg] = Y.y;
-          q[j][gg] = __ldg(qcurr + (__float_as_int(Y.x) + __float_as_int(X.x)));
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < PB; ++j) {
-#pragma unroll
-        for (int gg = 0; gg < NG; ++gg) {
-          const int oy = gg * RPG + ry;
-          if (!lane_on || oy >= D) continue;
-          const float4 a = q[j][gg];
-          const float smp = lerp_ref(lerp_ref(a.x, a.y, fx[j]), lerp_ref(a.z, a.w, fx[j]), fy[j][gg]);
-          const int o = off[j] + gg * RPG * pitch;
-          const float res = fsub(smp, sP[o]);
-          sB[(pb + j) * P2 + oy * D + ox] = make_float2(fmul(sGx[o], res), fmul(sGy[o], res));
-        }
-      }
-    }
-    __syncwarp();
-    // ordered fp64 sums: lane = (patch, b1|b2), k order
+    // lane group by lane group (template rows gg*RPG .. gg*RPG+RPG-1, i.e. k
+    // = gg*RPG*D + lane): residual products gx*res, gy*res of the warp's 8
+    // patches (flow.cpp:202-205), then 16 lanes = (patch, b1|b2) extend the
+    // ordered fp64 sums by those k (flow.cpp:204-205, k order kept)
     double acc = 0.0;
-    if (lane < 2 * kPW && ((solved >> pl) & 1u)) {
-      const float* src = reinterpret_cast<const float*>(sB + pl * P2) + (lane >> 3);
+#pragma unroll 1
+    for (int gg = 0; gg < NG; ++gg) {
+      const int oy = gg * RPG + ry;
+      const bool on = lane_on && oy < D;
+      constexpr int kJB = 4;  // patches per gather batch
+#pragma unroll 1
+      for (int jb = 0; jb < kPW; jb += kJB) {
+        if (!((solved >> jb) & ((1u << kJB) - 1u))) continue;  // warp-uniform
+        float4 q[kJB];
+        float fx[kJB], fy[kJB];
+#pragma unroll
+        for (int jj = 0; jj < kJB; ++jj) {
+          const int j = jb + jj;
+          const float2 X = sX[j * D + oxs];
+          const float2 Y = sY[j * D + (oy < D ? oy : 0)];
+          fx[jj] = X.y;
+          fy[jj] = Y.y;
+          q[jj] = __ldg(qcurr + (__float_as_int(Y.x) + __float_as_int(X.x)));
+        }
+#pragma unroll
+        for (int jj = 0; jj < kJB; ++jj) {
+          const int j = jb + jj;
+          const int o = __shfl_sync(kFull, tb, j) + (oy - kR) * pitch + (ox - kR);
+          if (!on || !((solved >> j) & 1u)) continue;
+          const float4 a = q[jj];
+          const float smp = lerp_ref(lerp_ref(a.x, a.y, fx[jj]), lerp_ref(a.z, a.w, fx[jj]), fy[jj]);
+          const float res = fsub(smp, sP[o]);
+          sB[j * (RPG * D) + lane] = make_float2(fmul(sGx[o], res), fmul(sGy[o], res));
+        }
+      }
+      __syncwarp();
+      if (lane < 2 * kPW && ((solved >> pl) & 1u)) {
+        const int nk = min(RPG, D - gg * RPG) * D;
+        const float* src = reinterpret_cast<const float*>(sB + pl * (RPG * D)) + (lane >> 3);
 #pragma unroll 9
-      for (int k = 0; k < P2; ++k) acc = dadd(acc, (double)src[2 * k]);
+        for (int k = 0; k < nk; ++k) acc = dadd(acc, (double)src[2 * k]);
+      }
+      __syncwarp();
     }
     const double b1 = __shfl_sync(kFull, acc, pl), b2 = __shfl_sync(kFull, acc, pl + 8);
-    __syncwarp();
     if (solve) {
       float du = __double2float_rn(dmul(-dsub(dmul(gyy, b1), dmul(gxy, b2)), inv_det));
       float dv = __double2float_rn(dmul(-dsub(dmul(gxx, b2), dmul(gxy, b1)), inv_det));
