@@ -465,10 +465,11 @@ struct DenseWord {
   float u, v;
 };
 
-// One link of the chain at one word: the reference rule, ballots, counts.
+// One link of the chain at one word: the reference rule and its ballots.
+// ev = the word's events of this link (crossings, or magnitudes).
 template <bool kLog, bool kMag>
-__device__ __forceinline__ void chain_step(const ChainParams& p, const float* s_lut, uint32_t* s_cnt, int g,
-                                           const DenseWord& c, int lane, int val, float& ref, int& before) {
+__device__ __forceinline__ uint2 link_rule(const ChainParams& p, const float* s_lut, int g, const DenseWord& c,
+                                           int lane, int val, float& ref, int& before, uint32_t& ev) {
   bool pos, neg;
   int mult = 1;
   if (kLog) {
@@ -489,21 +490,17 @@ __device__ __forceinline__ void chain_step(const ChainParams& p, const float* s_
   neg = neg && c.valid;
   const unsigned bp = __ballot_sync(kFull, pos);
   const unsigned bn = __ballot_sync(kFull, neg);
-  if (!c.have) return;
-  if (lane == 0) p.masks[(size_t)g * p.n_words + c.wi] = make_uint2(bp, bn);
   if (kMag) {
     const int m = (pos || neg) ? mult : 0;
-    p.mcount[(size_t)g * p.n_words * 32 + c.wi * 32 + lane] = (uint16_t)m;
-    int s = m;
+    if (c.have) p.mcount[(size_t)g * p.n_words * 32 + c.wi * 32 + lane] = (uint16_t)m;
+    int sm = m;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-    if (lane == 0) {
-      p.wcount[(size_t)g * p.n_words + c.wi] = (uint32_t)s;
-      if (s) atomicAdd(&s_cnt[g], (uint32_t)s);
-    }
-  } else if (lane == 0 && (bp | bn)) {
-    atomicAdd(&s_cnt[g], (uint32_t)(__popc(bp) + __popc(bn)));
+    for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(kFull, sm, o);
+    ev = (uint32_t)sm;
+  } else {
+    ev = (uint32_t)__popc(bp | bn);  // a pixel crosses one way or not at all
   }
+  return make_uint2(bp, bn);
 }
 
 template <int kW, int kNB, bool kClamp>
@@ -592,6 +589,35 @@ __global__ void __launch_bounds__(256, 3) chain_dense_kernel(ChainParams p) {
       }
       safe = __all_sync(kFull, safe);
       const int gbase = i * L;
+      // lane j collects link (l & 31) == j: its masks per word and its event
+      // count; every 32 links (and at the end) the lanes store / add them at once
+      uint2 lm[kW];
+      uint32_t lwc[kW], lcnt = 0;
+#pragma unroll
+      for (int q = 0; q < kW; ++q) lm[q] = make_uint2(0u, 0u), lwc[q] = 0u;
+      auto step = [&](int l, int q, int val) {
+        uint32_t ev;
+        const uint2 m = link_rule<kLog, kMag>(p, s_lut, gbase + l, c[q], lane, val, ref[q], before[q], ev);
+        if (lane == (l & 31)) {
+          lm[q] = m;
+          if (kMag) lwc[q] = ev;
+          lcnt += ev;
+        }
+      };
+      auto flush = [&](int l) {
+        if ((l & 31) != 31 && l != L - 1) return;
+        if (lane <= (l & 31)) {
+          const int g = gbase + (l & ~31) + lane;
+#pragma unroll
+          for (int q = 0; q < kW; ++q) {
+            if (!c[q].have) continue;
+            p.masks[(size_t)g * p.n_words + c[q].wi] = lm[q];
+            if (kMag) p.wcount[(size_t)g * p.n_words + c[q].wi] = lwc[q];
+          }
+          if (lcnt) atomicAdd(&s_cnt[g], lcnt);
+        }
+        lcnt = 0;
+      };
       int l0 = 0;
       for (; l0 < n_int; l0 += kB) {
         const int nb = min(kB, n_int - l0);
@@ -627,15 +653,15 @@ __global__ void __launch_bounds__(256, 3) chain_dense_kernel(ChainParams p) {
         for (int j = 0; j < kB; ++j) {
           if (j >= nb) break;
 #pragma unroll
-          for (int q = 0; q < kW; ++q)
-            chain_step<kLog, kMag>(p, s_lut, s_cnt, gbase + l0 + j, c[q], lane, vals[q][j], ref[q], before[q]);
+          for (int q = 0; q < kW; ++q) step(l0 + j, q, vals[q][j]);
+          flush(l0 + j);
         }
       }
       if (n_int < L) {  // the link into curr (include_endpoints)
         const uint8_t* curr = p.frames.at(sc);
 #pragma unroll
-        for (int q = 0; q < kW; ++q)
-          chain_step<kLog, kMag>(p, s_lut, s_cnt, gbase + L - 1, c[q], lane, (int)curr[c[q].pix], ref[q], before[q]);
+        for (int q = 0; q < kW; ++q) step(L - 1, q, (int)curr[c[q].pix]);
+        flush(L - 1);
       }
       sp = sc;
     }
