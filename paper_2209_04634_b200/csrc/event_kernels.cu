@@ -458,7 +458,7 @@ __device__ __noinline__ int dense_exact(const float2* nfb, const double* oma, co
 
 struct DenseWord {
   bool have, valid;
-  int64_t wi;
+  uint32_t wi;  // word index (n_words < 2^32)
   int x, y;
   uint32_t pix;
   float xf, yf;
@@ -548,9 +548,10 @@ __global__ void __launch_bounds__(256, 3) chain_dense_kernel(ChainParams p) {
     int before[kW];
 #pragma unroll
     for (int q = 0; q < kW; ++q) {
-      c[q].wi = w0 + q * kWarpsPerBlock;
-      c[q].have = c[q].wi < wend;
-      const int64_t ww = c[q].have ? c[q].wi : w0;
+      const int64_t wq = w0 + q * kWarpsPerBlock;
+      c[q].have = wq < wend;
+      c[q].wi = (uint32_t)wq;
+      const int64_t ww = c[q].have ? wq : w0;
       const int row = (int)((uint32_t)ww / (uint32_t)p.wpr);
       const int x = (int)(ww - (int64_t)row * p.wpr) * 32 + lane;
       c[q].valid = c[q].have && x < p.w;

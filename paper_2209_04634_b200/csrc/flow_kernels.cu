@@ -373,8 +373,13 @@ struct LKWarp {
   static constexpr int rows = (kLKTileY - 1) * kR + 2 * kR + 3;
   static constexpr int pitch = lk_pick_pitch(rw, D, RPG);
   static constexpr int plane = (pitch * rows + 3) & ~3;                   // floats
-  static constexpr int b_off = 3 * plane;                                 // float2 [warp][kPW][RPG*D]
-  static constexpr int t_off = b_off + 2 * kLKTileY * kPW * RPG * D;      // float2 [warp][2][kPW][D]
+  // products of one lane group: two planes (gx*res, gy*res) of [kPW][S]
+  // floats per warp; S even and S, the plane offset PO chosen so that the 16
+  // phase-B lanes' 8-byte reads hit distinct bank pairs where possible
+  static constexpr int S = ((RPG * D + 1) & ~1) + (((((RPG * D + 1) & ~1) / 2) % 2) ? 0 : 2);
+  static constexpr int PO = kPW * S + ((kPW * S) % 32 == 16 ? 0 : (48 - (kPW * S) % 32) % 32);
+  static constexpr int b_off = 3 * plane;                                 // float [warp][2][PO]
+  static constexpr int t_off = b_off + kLKTileY * 2 * PO;                 // float2 [warp][2][kPW][D]
   static constexpr int floats = t_off + 2 * kLKTileY * 2 * kPW * D;
 };
 static_assert(kLKThreads == 32 * kLKTileY, "one warp per tile row");
@@ -403,7 +408,7 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
   float* sP = smem;               // [rows][pitch] prev, replicate-staged
   float* sGx = smem + G::plane;   // [rows][pitch] central differences
   float* sGy = smem + 2 * G::plane;
-  float2* sB = reinterpret_cast<float2*>(smem + G::b_off) + warp * (kPW * RPG * D);  // [kPW][RPG*D]
+  float* sB = smem + G::b_off + warp * (2 * G::PO);  // [2][PO]: plane b1 at 0, plane b2 at PO
   float2* sX = reinterpret_cast<float2*>(smem + G::t_off) + warp * (2 * kPW * D);  // [kPW][D] (x0, fx)
   float2* sY = sX + kPW * D;                                                        // [kPW][D] (y0*w, fy)
 
@@ -507,15 +512,22 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
           const float4 a = q[jj];
           const float smp = lerp_ref(lerp_ref(a.x, a.y, fx[jj]), lerp_ref(a.z, a.w, fx[jj]), fy[jj]);
           const float res = fsub(smp, sP[o]);
-          sB[j * (RPG * D) + lane] = make_float2(fmul(sGx[o], res), fmul(sGy[o], res));
+          sB[j * G::S + lane] = fmul(sGx[o], res);
+          sB[G::PO + j * G::S + lane] = fmul(sGy[o], res);
         }
       }
       __syncwarp();
       if (lane < 2 * kPW && ((solved >> pl) & 1u)) {
         const int nk = min(RPG, D - gg * RPG) * D;
-        const float* src = reinterpret_cast<const float*>(sB + pl * (RPG * D)) + (lane >> 3);
-#pragma unroll 9
-        for (int k = 0; k < nk; ++k) acc = dadd(acc, (double)src[2 * k]);
+        const float* src = sB + (lane >> 3) * G::PO + pl * G::S;
+        const float2* src2 = reinterpret_cast<const float2*>(src);
+#pragma unroll 7
+        for (int m = 0; m < nk / 2; ++m) {
+          const float2 f = src2[m];
+          acc = dadd(acc, (double)f.x);
+          acc = dadd(acc, (double)f.y);
+        }
+        if (nk & 1) acc = dadd(acc, (double)src[nk - 1]);
       }
       __syncwarp();
     }
