@@ -57,6 +57,7 @@ def parse():
     p.add_argument("--frames", type=int, default=0, help="override sequence length")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--chunk", type=int, default=0, help="e2e: frames per streamed chunk (0 = 32)")
     p.add_argument("--batch", type=int, default=0,
                    help="frames per push_frames call (0 = the simulator's maximum; 1 = frame-by-frame)")
     return p.parse_args()
@@ -340,16 +341,15 @@ def run_ours(args):
         hev = h_events.data_ptr()
 
         def e2e_step():
-            # evsim_gpu_push_frames on pinned host frames (H2D inside) +
-            # evsim_gpu_copy_events of the packed events (D2H), per batch
+            # evsim_gpu_push_frames_streamed: pinned host frames in, packed
+            # host events out; chunk j+1's H2D and chunk j-1's D2H overlap
+            # chunk j's compute
             sim.reset()
             d2h = 0
             for a in range(0, n, batch):
                 nb = min(batch, n - a)
-                e = sim.push_frames_device(hbase + a * P, nb, c.width, c.height, ts[a:a + nb], on_device=False,
-                                           sync=True)
-                if e.n_events:
-                    sim.copy_packed(hev, cap)
+                e = sim.push_frames_streamed_ptr(hbase + a * P, nb, c.width, c.height, ts[a:a + nb], hev, cap,
+                                                 chunk=args.chunk)
                 d2h += 4 * e.n_events + 16 * (e.n_segments + 1)
             return d2h
 
@@ -370,7 +370,8 @@ def run_ours(args):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": round(frames_total / float(te.item()), 3), "unit": "frames/s",
                "h2d_bytes_per_step": n * P, "d2h_bytes_per_step": int(d2h),
-               "api": "evsim_gpu_push_frames (pinned host frames) + evsim_gpu_copy_events (packed)"}
+               "api": f"evsim_gpu_push_frames_streamed (pinned host frames in, packed host events out, "
+                      f"chunks of {args.chunk or 32} frames: H2D / compute / D2H overlapped)"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -154,6 +154,19 @@ EVSIM_GPU_API int evsim_gpu_push_frames_async(evsim_gpu_sim* sim, const uint8_t*
                                               int32_t pixels_on_device);
 EVSIM_GPU_API int evsim_gpu_max_batch(const evsim_gpu_sim* sim, int32_t width, int32_t height);
 
+/* Host frames in, host events out, overlapped: the frames are pushed in
+ * chunks of `chunk` (0 = 32); chunk j+1's upload and chunk j-1's event
+ * download run on two copy streams while chunk j computes.  host_events
+ * receives the packed records (format 0 of evsim_gpu_copy_events) of all
+ * n_frames, in order; `out` gets the call's segment table, exactly as
+ * evsim_gpu_push_frames would report it.  If capacity is too small the
+ * simulation still completes, the call returns INVALID_ARGUMENT and the events
+ * stay readable with evsim_gpu_copy_events.  Single-event mode only.
+ * Same validation and errors as evsim_gpu_push_frames. */
+EVSIM_GPU_API int evsim_gpu_push_frames_streamed(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t n_frames,
+                                                 int32_t width, int32_t height, const int64_t* t_us, int32_t chunk,
+                                                 uint32_t* host_events, int64_t capacity, evsim_gpu_events* out);
+
 /* Asynchronous variant: enqueues the push on the handle's CUDA stream and
  * returns without waiting; evsim_gpu_sync() completes it.  Validation
  * errors are still reported synchronously. */

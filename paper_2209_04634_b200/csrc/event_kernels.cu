@@ -706,7 +706,9 @@ __global__ void __launch_bounds__(256) offsets_kernel(OffsetParams p) {
 __global__ void __launch_bounds__(1024) segbase_kernel(EmitParams p, int64_t* segbase) {
   __shared__ int64_t s_warp[32];
   const int S = *p.seg.n_segs;
-  int64_t carry = 0;
+  const int64_t b0 = *p.base;  // events of earlier launches of the same call
+  __syncthreads();
+  int64_t carry = b0;
   for (int s0 = 0; s0 < S; s0 += blockDim.x) {
     const int s = s0 + threadIdx.x;
     int64_t tot = 0;
@@ -726,6 +728,7 @@ __global__ void __launch_bounds__(1024) segbase_kernel(EmitParams p, int64_t* se
   if (threadIdx.x == 0) {
     p.seg_out[0] = S;
     p.seg_out[1 + 2 * S] = carry;
+    *p.base = carry;
   }
 }
 

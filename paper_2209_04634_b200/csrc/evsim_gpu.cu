@@ -345,7 +345,7 @@ struct EventEngine {
   int wpb = 0, n_blocks = 0;
   int max_links = 0;  // links of a launch (pairs * per-pair links)
   bool magnitude = false;
-  DevBuf masks, counts, prefix, link_total, segtab, segbase, seg_out, events, mcount, wcount;
+  DevBuf masks, counts, prefix, link_total, segtab, segbase, seg_out, events, mcount, wcount, base;
   int64_t capacity = 0;
 
   void geometry(int w_, int h_) {
@@ -375,6 +375,7 @@ struct EventEngine {
       segtab.ensure(16 + (size_t)max_links * (2 * sizeof(int) + sizeof(int64_t)), s);
       segbase.ensure((size_t)max_links * sizeof(int64_t), s);
       seg_out.ensure((3 + 2 * (size_t)max_links) * sizeof(int64_t), s);
+      base.ensure(sizeof(int64_t), s);
       if (mag) {
         mcount.ensure((size_t)max_links * n_words * 32 * sizeof(uint16_t), s);
         wcount.ensure((size_t)max_links * n_words * sizeof(uint32_t), s);
@@ -456,6 +457,10 @@ struct evsim_gpu_sim {
   ~evsim_gpu_sim() {
     if (stream) cudaStreamSynchronize(stream);
     if (h_seg_out) cudaFreeHost(h_seg_out);
+    for (auto& b : h_seg2)
+      if (b) cudaFreeHost(b);
+    if (s_in) cudaStreamSynchronize(s_in), cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamSynchronize(s_out), cudaStreamDestroy(s_out);
     for (auto& g : ev_pool)
       for (auto e : g) cudaEventDestroy(e);
     for (auto& g : ev_pending)
@@ -669,8 +674,11 @@ struct evsim_gpu_sim {
 
   // segments -> chain -> offsets -> segbase + emit, then the segment-table
   // readback.  ts: n_pairs + 1 frame timestamps.
-  void run_events(ChainParams& c, int provider, const int64_t* ts) {
+  // continue_call: this launch's events follow those of the previous launch of
+  // the same call (streamed chunks); otherwise they start at offset 0.
+  void run_events(ChainParams& c, int provider, const int64_t* ts, int64_t* h_seg, bool continue_call = false) {
     const int G = c.d.n_links * c.n_pairs;
+    if (!continue_call) CK(cudaMemsetAsync(ev.base.p, 0, sizeof(int64_t), stream));
     SegParams sp{};
     sp.d = c.d;
     sp.n_pairs = c.n_pairs;
@@ -698,6 +706,7 @@ struct evsim_gpu_sim {
     ep.prefix = ev.prefix.as<int64_t>();
     ep.link_total = ev.link_total.as<int64_t>();
     ep.seg_out = ev.seg_out.as<int64_t>();
+    ep.base = ev.base.as<int64_t>();
     ep.magnitude = c.magnitude;
     ep.masks = ev.masks.as<uint2>();
     ep.mcount = ev.mcount.as<uint16_t>();
@@ -707,8 +716,7 @@ struct evsim_gpu_sim {
     launch_emit(ep, ev.segbase.as<int64_t>(), stream);
     CK_LAUNCH("emit");
     launches += 6;
-    CK(cudaMemcpyAsync(h_seg_out, ev.seg_out.p, (3 + 2 * (size_t)G) * sizeof(int64_t), cudaMemcpyDeviceToHost,
-                       stream));
+    CK(cudaMemcpyAsync(h_seg, ev.seg_out.p, (3 + 2 * (size_t)G) * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
     last_emit = ep;
     pending = true;
   }
@@ -716,7 +724,7 @@ struct evsim_gpu_sim {
   // ---- push ----------------------------------------------------------------
   // Simulator::push_frame (src/simulate.cpp:306-347) applied to F frames in
   // order; the whole batch is validated first and rejected atomically.
-  void push(const uint8_t* pixels, int F, int fw, int fh, const int64_t* ts, bool on_device) {
+  void validate_batch(const uint8_t* pixels, int F, int fw, int fh, const int64_t* ts) const {
     if (F < 1) invalid("push_frames: n_frames must be >= 1");
     if (fw <= 0 || fh <= 0 || !pixels || !ts) invalid("push_frame: malformed frame");
     if (has_prev) {
@@ -732,6 +740,10 @@ struct evsim_gpu_sim {
     const int L = desc().n_links;
     const int fmax = max_batch_for(L, (int64_t)fw * fh);
     if (F > fmax) invalid("push_frames: batch too large (max " + std::to_string(fmax) + ")");
+  }
+
+  // device state for F more frames of one call
+  void prepare(int F, int fw, int fh) {
     CK(cudaSetDevice(device));
     // A queued single-mode result is superseded (stream order keeps the
     // device buffers consistent); magnitude mode may need a re-emit.
@@ -742,19 +754,38 @@ struct evsim_gpu_sim {
     if (!has_prev && (fw != w || fh != h)) allocate(fw, fh);
     const int n_pairs = has_prev ? F : F - 1;
     ensure_capacity(std::max(n_pairs, 1));
+  }
 
+  // ring slot of the first frame of the next push
+  int next_slot() const { return has_prev ? (rhead + 1) % R : rhead; }
+
+  // Upload F frames into the ring from slot `base` (at most two contiguous runs).
+  void upload(const uint8_t* pixels, int F, int base, bool on_device, cudaStream_t s) {
     const size_t P = (size_t)w * h;
-    const int base = has_prev ? (rhead + 1) % R : rhead;  // ring slot of frame 0 of the batch
+    const int first = std::min(F, R - base);
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CK(cudaMemcpyAsync(frames.as<uint8_t>() + (size_t)base * P, pixels, (size_t)first * P, kind, s));
+    if (first < F)
+      CK(cudaMemcpyAsync(frames.as<uint8_t>(), pixels + (size_t)first * P, (size_t)(F - first) * P, kind, s));
+  }
+
+  void push(const uint8_t* pixels, int F, int fw, int fh, const int64_t* ts, bool on_device) {
+    validate_batch(pixels, F, fw, fh, ts);
+    prepare(F, fw, fh);
+    enqueue(pixels, F, ts, on_device, nullptr, h_seg_out, false);
+  }
+
+  // Everything of one push after validation: upload (unless `uploaded` says
+  // the frames are already in the ring), pyramid, flow, chain, emit.
+  void enqueue(const uint8_t* pixels, int F, const int64_t* ts, bool on_device, cudaEvent_t uploaded, int64_t* h_seg,
+               bool continue_call) {
+    const size_t P = (size_t)w * h;
+    const int base = next_slot();  // ring slot of frame 0 of the batch
+    const int n_pairs = has_prev ? F : F - 1;
     begin_group();
     mark(EVSIM_STAGE_UPLOAD);
-    {
-      // upload into the ring (at most two contiguous runs)
-      const int first = std::min(F, R - base);
-      const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-      CK(cudaMemcpyAsync(frames.as<uint8_t>() + (size_t)base * P, pixels, (size_t)first * P, kind, stream));
-      if (first < F)
-        CK(cudaMemcpyAsync(frames.as<uint8_t>(), pixels + (size_t)first * P, (size_t)(F - first) * P, kind, stream));
-    }
+    if (uploaded) CK(cudaStreamWaitEvent(stream, uploaded, 0));
+    else upload(pixels, F, base, on_device, stream);
     mark(EVSIM_STAGE_PYRAMID);
     if (uses_flow()) {
       PyramidParams pp = flow.pyramid_params(frames.as<uint8_t>(), P, dense_flow() ? quads.as<uint32_t>() : nullptr, base);
@@ -790,17 +821,142 @@ struct evsim_gpu_sim {
         provider = kProvSparse;
       }
       mark(EVSIM_STAGE_CHAIN);
-      run_events(c, provider, pts.data());
+      run_events(c, provider, pts.data(), h_seg, continue_call);
     } else {
-      seg_t.clear();
-      seg_off.assign(1, 0);
-      n_events = 0;
+      if (!continue_call) {
+        seg_t.clear();
+        seg_off.assign(1, 0);
+        n_events = 0;
+      }
       pending = false;
     }
     end_group();
     rhead = (base + F - 1) % R;
     prev_t = ts[F - 1];
     has_prev = true;
+  }
+
+  // ---- streamed push: host frames in, host events out ---------------------
+  // F frames in chunks of `chunk`: the upload of chunk j+1 (copy-in stream)
+  // and the download of chunk j-1's events (copy-out stream) overlap the
+  // compute of chunk j.  Events land contiguously, exactly as one push of
+  // all F frames would leave them (segbase continues the call's offset).
+  // Single-event mode only (the output bound L*pairs*P is exact there).
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  int64_t* h_seg2[2] = {nullptr, nullptr};
+  size_t h_seg2_cap = 0;
+  bool host_short = false;
+
+  void push_streamed(const uint8_t* pixels, int F, int fw, int fh, const int64_t* ts, int chunk, uint32_t* host_dst,
+                     int64_t capacity) {
+    if (magnitude()) invalid("push_frames_streamed: magnitude mode is not supported (use push_frames)");
+    if (!host_dst && capacity > 0) invalid("push_frames_streamed: null destination");
+    validate_batch(pixels, F, fw, fh, ts);
+    prepare(F, fw, fh);
+    if (!s_in) {
+      CK(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+    }
+    const size_t seg_need = (3 + 2 * (size_t)ev.max_links) * sizeof(int64_t);
+    if (seg_need > h_seg2_cap) {
+      for (auto& b : h_seg2) {
+        if (b) cudaFreeHost(b);
+        b = nullptr;
+        CK(cudaHostAlloc((void**)&b, seg_need, cudaHostAllocDefault));
+      }
+      h_seg2_cap = seg_need;
+    }
+    const size_t P = (size_t)w * h;
+    if (chunk <= 0) chunk = std::max(1, std::min(F, 32));
+    const int n_chunks = (F + chunk - 1) / chunk;
+    std::vector<cudaEvent_t> up(n_chunks), done(n_chunks);
+    for (int j = 0; j < n_chunks; ++j) {
+      CK(cudaEventCreateWithFlags(&up[j], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&done[j], cudaEventDisableTiming));
+    }
+    // the copy-in stream must not overwrite slots still read by earlier work
+    cudaEvent_t start;
+    CK(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    CK(cudaEventRecord(start, stream));
+    CK(cudaStreamWaitEvent(s_in, start, 0));
+    CK(cudaStreamWaitEvent(s_out, start, 0));
+    // ring slots of every chunk, as the pushes will assign them
+    std::vector<int> slot(n_chunks);
+    {
+      int sl = next_slot();
+      for (int j = 0; j < n_chunks; ++j) {
+        slot[j] = sl;
+        sl = (sl + std::min(chunk, F - j * chunk)) % R;
+      }
+    }
+    auto enqueue_upload = [&](int j) {
+      const int a = j * chunk, nf = std::min(chunk, F - a);
+      upload(pixels + (size_t)a * P, nf, slot[j], false, s_in);
+      CK(cudaEventRecord(up[j], s_in));
+    };
+    seg_t.clear();
+    seg_off.clear();
+    n_events = 0;
+    host_short = false;
+    int64_t copied = 0;
+    auto drain = [&](int j) {  // chunk j's segment table and events to the host
+      CK(cudaEventSynchronize(done[j]));
+      const int64_t* hs = h_seg2[j & 1];
+      const int S = (int)hs[0];
+      const int64_t lo = copied, hi = hs[1 + 2 * S];
+      for (int q = 0; q < S; ++q) {
+        const int64_t a = hs[1 + S + q], b = hs[2 + S + q];
+        if (b > a) {
+          seg_t.push_back(hs[1 + q]);
+          seg_off.push_back(a);
+        }
+      }
+      if (hi > lo) {
+        if (hi <= capacity && !host_short) {
+          CK(cudaStreamWaitEvent(s_out, done[j], 0));
+          CK(cudaMemcpyAsync(host_dst + lo, ev.events.as<uint32_t>() + lo, (size_t)(hi - lo) * 4,
+                             cudaMemcpyDeviceToHost, s_out));
+        } else {
+          host_short = true;
+        }
+      }
+      copied = hi;
+    };
+    CK(cudaMemsetAsync(ev.base.p, 0, sizeof(int64_t), stream));
+    enqueue_upload(0);
+    for (int j = 0; j < n_chunks; ++j) {
+      if (j + 1 < n_chunks) enqueue_upload(j + 1);
+      const int a = j * chunk, nf = std::min(chunk, F - a);
+      const bool had_prev = has_prev;
+      if (!had_prev && nf == 1) {  // a warm-up chunk of one frame: no pairs, no segment table
+        h_seg2[j & 1][0] = 0;
+        h_seg2[j & 1][1] = 0;
+      }
+      enqueue(nullptr, nf, ts + a, false, up[j], h_seg2[j & 1], true);
+      CK(cudaEventRecord(done[j], stream));
+      pending = false;
+      if (j > 0) drain(j - 1);
+    }
+    drain(n_chunks - 1);
+    seg_off.push_back(copied);
+    n_events = copied;
+    CK(cudaStreamSynchronize(s_out));
+    CK(cudaStreamSynchronize(stream));
+    // the call's merged segment table on the device (for a later unpack)
+    {
+      std::vector<int64_t> t(3 + 2 * seg_t.size());
+      const int S = (int)seg_t.size();
+      t[0] = S;
+      for (int q = 0; q < S; ++q) t[1 + q] = seg_t[q], t[1 + S + q] = seg_off[q];
+      t[1 + 2 * S] = copied;
+      CK(cudaMemcpy(ev.seg_out.p, t.data(), (2 + 2 * (size_t)S) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    }
+    for (int j = 0; j < n_chunks; ++j) {
+      cudaEventDestroy(up[j]);
+      cudaEventDestroy(done[j]);
+    }
+    cudaEventDestroy(start);
+    if (host_short) invalid("push_frames_streamed: destination too small (events stay on the device; see copy_events)");
   }
 
   // simulate_sparse up to the intermediates (simulate.cpp:145-199), all pairs
@@ -883,6 +1039,7 @@ struct evsim_gpu_sim {
       ev.grow(total + total / 4, stream);
       last_emit.capacity = ev.capacity;
       last_emit.out = ev.events.as<uint32_t>();
+      CK(cudaMemsetAsync(ev.base.p, 0, sizeof(int64_t), stream));
       launch_emit(last_emit, ev.segbase.as<int64_t>(), stream);
       CK_LAUNCH("emit");
       launches += 2;
@@ -1019,6 +1176,21 @@ int evsim_gpu_push_frames_async(evsim_gpu_sim* sim, const uint8_t* pixels, int32
   return guarded([&] {
     if (!sim) invalid("evsim_gpu_push_frames_async: null simulator");
     sim->push(pixels, n_frames, width, height, t_us, pixels_on_device != 0);
+  });
+}
+
+int evsim_gpu_push_frames_streamed(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t n_frames, int32_t width,
+                                   int32_t height, const int64_t* t_us, int32_t chunk, uint32_t* host_events,
+                                   int64_t capacity, evsim_gpu_events* out) {
+  return guarded([&] {
+    if (!sim) invalid("evsim_gpu_push_frames_streamed: null simulator");
+    try {
+      sim->push_streamed(pixels, n_frames, width, height, t_us, chunk, host_events, capacity);
+    } catch (...) {
+      sim->fill_out(out);
+      throw;
+    }
+    sim->fill_out(out);
   });
 }
 
@@ -1288,7 +1460,7 @@ int evsim_gpu_dense_events_with_flow(const uint8_t* prev, const uint8_t* curr, i
       provider = kProvDenseField;
     }
     const int64_t ts[2] = {t_prev, t_curr};
-    s->run_events(c, provider, ts);
+    s->run_events(c, provider, ts, s->h_seg_out);
     s->finish();
     copy_events24(s.s.get(), events, capacity, n_events);
   });
@@ -1328,7 +1500,7 @@ int evsim_gpu_sparse_events_with_flow(const uint8_t* prev, const uint8_t* curr, 
       CK(cudaStreamSynchronize(s->stream));  // host staging (np, idx) must outlive the copies
     }
     const int64_t ts[2] = {t_prev, t_curr};
-    s->run_events(c, provider, ts);
+    s->run_events(c, provider, ts, s->h_seg_out);
     s->finish();
     copy_events24(s.s.get(), events, capacity, n_events);
   });

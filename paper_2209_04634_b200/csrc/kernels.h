@@ -178,6 +178,8 @@ struct EmitParams {
   const int64_t* prefix;
   const int64_t* link_total;
   int64_t* seg_out;        // [0] = S, [1..S] seg_t, [1+S..1+2S] offsets (S+1); block 0
+  int64_t* base;           // device scalar: output offset of this launch's first event;
+                           // segbase_kernel advances it by the launch's total
   int magnitude;
   const uint2* masks;
   const uint16_t* mcount;

@@ -438,6 +438,38 @@ class Simulator:
         out.width, out.height = w, h
         return out
 
+    def push_frames_streamed(self, frames: np.ndarray, timestamps, chunk: int = 0,
+                             out: Optional[np.ndarray] = None) -> tuple:
+        """Host frames in, host events out, upload / compute / download
+        overlapped (evsim_gpu_push_frames_streamed).  Returns (packed u32
+        records, seg_t, seg_offset); the same events push_frames returns, in
+        packed form (abi.unpack_events expands them).  `out` may be a
+        pre-allocated (ideally pinned) u32 buffer."""
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        ts = np.ascontiguousarray(np.asarray(timestamps, dtype=np.int64))
+        F, h, w = frames.shape
+        if out is None:
+            links = max(1, self.config.n_interp + 1)
+            out = np.empty(F * h * w * links, dtype=np.uint32)
+        ev = CEvents()
+        _lib.check(self._lib.evsim_gpu_push_frames_streamed(self._h, _ptr(frames), F, w, h, _ptr(ts), int(chunk),
+                                                            _ptr(out), out.size, ctypes.byref(ev)))
+        n = int(ev.n_events)
+        S = int(ev.n_segments)
+        seg_t = np.ctypeslib.as_array(ev.seg_t, shape=(S,)).copy() if S else np.zeros(0, np.int64)
+        seg_off = np.ctypeslib.as_array(ev.seg_offset, shape=(S + 1,)).copy() if S else np.zeros(1, np.int64)
+        return out[:n], seg_t, seg_off
+
+    def push_frames_streamed_ptr(self, pixels_ptr: int, n_frames: int, width: int, height: int, timestamps,
+                                 events_ptr: int, capacity: int, chunk: int = 0) -> CEvents:
+        """Raw-pointer form of push_frames_streamed (pinned host buffers)."""
+        ts = np.ascontiguousarray(np.asarray(timestamps, dtype=np.int64))
+        ev = CEvents()
+        _lib.check(self._lib.evsim_gpu_push_frames_streamed(self._h, _vp(pixels_ptr), n_frames, width, height,
+                                                            _ptr(ts), int(chunk), _vp(events_ptr), int(capacity),
+                                                            ctypes.byref(ev)))
+        return ev
+
     def push_frames_device(self, pixels_ptr: int, n_frames: int, width: int, height: int, timestamps,
                            on_device: bool = True, sync: bool = True) -> Optional[CEvents]:
         """Device-resident batched push (no event download)."""
