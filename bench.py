@@ -324,7 +324,7 @@ def run_ours(args):
     e2e_frac = b_alg * (value / ws) / 1e9 / hbm
     frames_timed = args.steps * n
     roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": None,
+                "frac": round(achieved / hbm, 4), "traffic": traffic_for(c.name, args.mode, pairs_timed / launches_ev),
                 "kernel": "event stage = chain_kernel + offsets_kernel + emit_kernel (one push_frames call)",
                 "algorithmic_bytes_per_frame": round(b_alg), "frames_per_launch": round(pairs_timed / launches_ev, 2),
                 "algorithmic_bytes_per_launch": round(bytes_per_launch), "avg_launch_ms": round(ms_per_launch, 5),
@@ -397,6 +397,18 @@ def run_ours(args):
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+def traffic_for(config: str, mode: str, pairs_per_launch: float):
+    """DRAM bytes (read + write) per launch of the event stage, from the
+    committed ncu --set full capture of the same workload, or None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r01", "traffic_c2_log.json")))
+    except Exception:
+        return None
+    if config == "c2" and mode == "log" and abs(pairs_per_launch - 127) < 0.5:
+        return t["event_stage_dram_bytes_per_launch"]
+    return None
 
 
 def main():

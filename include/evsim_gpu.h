@@ -154,6 +154,18 @@ EVSIM_GPU_API int evsim_gpu_push_frames_async(evsim_gpu_sim* sim, const uint8_t*
                                               int32_t pixels_on_device);
 EVSIM_GPU_API int evsim_gpu_max_batch(const evsim_gpu_sim* sim, int32_t width, int32_t height);
 
+/* Several independent camera streams in one call (c4: many streams per GPU;
+ * the reference runs one Simulator per thread, bench.cpp:53-64):
+ * sims[i] gets the n_frames frames pixels[i] with timestamps t_us[i].  The
+ * pushes are enqueued on the handles' own CUDA streams and run concurrently;
+ * outs[i] (optional) is what evsim_gpu_push_frames would report for sims[i].
+ * Every batch is validated before any is enqueued: one invalid batch rejects
+ * the whole call and leaves every stream untouched. */
+EVSIM_GPU_API int evsim_gpu_push_frames_batched(evsim_gpu_sim* const* sims, int32_t n_sims,
+                                                const uint8_t* const* pixels, int32_t n_frames, int32_t width,
+                                                int32_t height, const int64_t* const* t_us,
+                                                int32_t pixels_on_device, evsim_gpu_events* outs);
+
 /* Host frames in, host events out, overlapped: the frames are pushed in
  * chunks of `chunk` (0 = 32); chunk j+1's upload and chunk j-1's event
  * download run on two copy streams while chunk j computes.  host_events

@@ -9,12 +9,13 @@ from ._lib import EvsimError, InvalidArgument  # noqa: F401
 from .simulator import (DenseFlowEstimator, EventStream, FlowField, FlowPreset, Frame,  # noqa: F401
                         PyramidalLucasKanade, PyramidalPatchFlow, SimulatorConfig, Simulator, SparseFlow,
                         SparseFlowEstimator, dense_events_with_flow, estimate_dense_flow, estimate_sparse_flow,
-                        flow_preset, interpolate_frames, simulate_dense, simulate_sparse, sparse_events_with_flow)
+                        flow_preset, interpolate_frames, push_frames_batched, simulate_dense, simulate_sparse,
+                        sparse_events_with_flow)
 
 __all__ = [
     "EVENT_DTYPE", "ContrastMode", "EventsPerCrossing", "FlowQuality", "Method", "EvsimError", "InvalidArgument",
     "DenseFlowEstimator", "EventStream", "FlowField", "FlowPreset", "Frame", "PyramidalLucasKanade",
     "PyramidalPatchFlow", "SimulatorConfig", "Simulator", "SparseFlow", "SparseFlowEstimator",
     "dense_events_with_flow", "estimate_dense_flow", "estimate_sparse_flow", "flow_preset", "interpolate_frames",
-    "simulate_dense", "simulate_sparse", "sparse_events_with_flow",
+    "push_frames_batched", "simulate_dense", "simulate_sparse", "sparse_events_with_flow",
 ]

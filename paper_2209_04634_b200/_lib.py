@@ -30,6 +30,8 @@ _SIGS = {
     "evsim_gpu_push_frame_async": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i64, _i32]),
     "evsim_gpu_push_frames": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _i32, ctypes.POINTER(CEvents)]),
     "evsim_gpu_push_frames_async": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _i32]),
+    "evsim_gpu_push_frames_batched": (
+        ctypes.c_int, [_vp, _i32, _vp, _i32, _i32, _i32, _vp, _i32, ctypes.POINTER(CEvents)]),
     "evsim_gpu_push_frames_streamed": (
         ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _i32, _vp, _i64, ctypes.POINTER(CEvents)]),
     "evsim_gpu_max_batch": (ctypes.c_int, [_vp, _i32, _i32]),

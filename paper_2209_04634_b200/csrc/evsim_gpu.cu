@@ -1179,6 +1179,30 @@ int evsim_gpu_push_frames_async(evsim_gpu_sim* sim, const uint8_t* pixels, int32
   });
 }
 
+int evsim_gpu_push_frames_batched(evsim_gpu_sim* const* sims, int32_t n_sims, const uint8_t* const* pixels,
+                                  int32_t n_frames, int32_t width, int32_t height, const int64_t* const* t_us,
+                                  int32_t pixels_on_device, evsim_gpu_events* outs) {
+  return guarded([&] {
+    if (n_sims < 0 || (n_sims > 0 && (!sims || !pixels || !t_us))) invalid("push_frames_batched: null argument");
+    for (int i = 0; i < n_sims; ++i) {
+      if (!sims[i]) invalid("push_frames_batched: null simulator");
+      for (int j = 0; j < i; ++j)
+        if (sims[j] == sims[i]) invalid("push_frames_batched: a simulator appears twice");
+    }
+    // every batch is validated before any is enqueued (all-or-nothing)
+    for (int i = 0; i < n_sims; ++i) sims[i]->validate_batch(pixels[i], n_frames, width, height, t_us[i]);
+    for (int i = 0; i < n_sims; ++i) {
+      sims[i]->prepare(n_frames, width, height);
+      sims[i]->enqueue(pixels[i], n_frames, t_us[i], pixels_on_device != 0, nullptr, sims[i]->h_seg_out, false);
+    }
+    for (int i = 0; i < n_sims; ++i) {
+      CK(cudaSetDevice(sims[i]->device));
+      sims[i]->finish();
+      if (outs) sims[i]->fill_out(outs + i);
+    }
+  });
+}
+
 int evsim_gpu_push_frames_streamed(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t n_frames, int32_t width,
                                    int32_t height, const int64_t* t_us, int32_t chunk, uint32_t* host_events,
                                    int64_t capacity, evsim_gpu_events* out) {

@@ -569,3 +569,36 @@ def concatenate(streams: Sequence[EventStream]) -> EventStream:
     out = EventStream(streams[0].width, streams[0].height)
     out.events = np.concatenate([s.events for s in streams]) if streams else out.events
     return out
+
+
+def push_frames_batched(sims: Sequence["Simulator"], frames: Sequence[np.ndarray], timestamps) -> list:
+    """Several independent streams in one call (evsim_gpu_push_frames_batched):
+    sims[i] gets frames[i] ((F, H, W) uint8, the same F, H, W for all) with
+    timestamps[i].  The pushes run concurrently on the handles' CUDA streams;
+    returns one EventStream per simulator.  All batches are validated first:
+    an invalid one rejects the call and leaves every stream untouched."""
+    n = len(sims)
+    if len(frames) != n or len(timestamps) != n:
+        raise InvalidArgument(1, "push_frames_batched: one frame batch and one timestamp list per simulator")
+    if n == 0:
+        return []
+    if any(s._custom for s in sims):
+        return [s.push_frames(f, t) for s, f, t in zip(sims, frames, timestamps)]
+    fr = [np.ascontiguousarray(f, dtype=np.uint8) for f in frames]
+    ts = [np.ascontiguousarray(np.asarray(t, dtype=np.int64)) for t in timestamps]
+    F, h, w = fr[0].shape
+    for f, t in zip(fr, ts):
+        if f.shape != (F, h, w) or t.shape != (F,):
+            raise InvalidArgument(1, "push_frames_batched: every stream needs the same batch shape")
+    lib = sims[0]._lib
+    hs = (ctypes.c_void_p * n)(*[s._h.value for s in sims])
+    px = (ctypes.c_void_p * n)(*[f.ctypes.data for f in fr])
+    tp = (ctypes.c_void_p * n)(*[t.ctypes.data for t in ts])
+    outs = (CEvents * n)()
+    _lib.check(lib.evsim_gpu_push_frames_batched(hs, n, px, F, w, h, tp, 0, outs))
+    res = []
+    for s, ev in zip(sims, outs):
+        r = s._collect(ev)
+        r.width, r.height = w, h
+        res.append(r)
+    return res
