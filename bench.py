@@ -325,7 +325,7 @@ def run_ours(args):
     frames_timed = args.steps * n
     roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic_for(c.name, args.mode, pairs_timed / launches_ev),
-                "kernel": "event stage = chain_kernel + offsets_kernel + emit_kernel (one push_frames call)",
+                "kernel": "event stage = chain_dense_kernel + offsets_kernel + segbase_kernel + emit_kernel (one push_frames call)",
                 "algorithmic_bytes_per_frame": round(b_alg), "frames_per_launch": round(pairs_timed / launches_ev, 2),
                 "algorithmic_bytes_per_launch": round(bytes_per_launch), "avg_launch_ms": round(ms_per_launch, 5),
                 "peak_source": peak_src, "end_to_end_frac": round(e2e_frac, 5),
