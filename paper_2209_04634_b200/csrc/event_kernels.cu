@@ -676,6 +676,197 @@ __global__ void __launch_bounds__(256, 3) chain_dense_kernel(ChainParams p) {
   for (int i = threadIdx.x; i < G; i += blockDim.x) p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
 }
 
+// ------------------------------------------------------------ sparse chain kernel
+//
+// chain_kernel specialised for the sparse method (simulate.cpp:167-201): the
+// intermediate frame k is prev except where a splat claimed the pixel.  A
+// link whose value is prev (v0) for every lane of the word, right after a
+// link that also ended in v0 for every lane, cannot emit (linear: the
+// difference is 0; log: |L(v0) - ref| <= C was just established or ref =
+// L(v0)) and leaves the state unchanged — such links only record empty masks.
+// The first link of a pair qualifies in linear mode when it starts from v0,
+// and in log mode when the pair's chain starts at prev (endpoints included:
+// the previous link ended in this pair's prev, or ref = L(frame0)).
+template <bool kLog, bool kMag>
+__global__ void __launch_bounds__(256, 3) chain_sparse_kernel(ChainParams p) {
+  constexpr int kW = 2;
+  extern __shared__ uint32_t s_cnt[];  // [G]
+  __shared__ float s_lut[256];
+  const int L = p.d.n_links, G = L * p.n_pairs, N = p.n_interp;
+  for (int i = threadIdx.x; i < G; i += blockDim.x) s_cnt[i] = 0;
+  if (kLog) s_lut[threadIdx.x] = p.lut[threadIdx.x];
+  __syncthreads();
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t P = p.P;
+  const int kfirst = p.d.start + 1;
+  const int64_t wbeg = (int64_t)b * p.words_per_block;
+  const int64_t wend = min(wbeg + p.words_per_block, p.n_words);
+  for (int64_t w0 = wbeg + warp; w0 < wend; w0 += kWarpsPerBlock * kW) {
+    DenseWord c[kW];
+    float ref[kW];
+    int before[kW];
+#pragma unroll
+    for (int q = 0; q < kW; ++q) {
+      const int64_t wq = w0 + q * kWarpsPerBlock;
+      c[q].have = wq < wend;
+      c[q].wi = (uint32_t)wq;
+      const int64_t ww = c[q].have ? wq : w0;
+      const int row = (int)((uint32_t)ww / (uint32_t)p.wpr);
+      const int x = (int)(ww - (int64_t)row * p.wpr) * 32 + lane;
+      c[q].valid = c[q].have && x < p.w;
+      c[q].x = x < p.w ? x : p.w - 1;
+      c[q].y = row;
+      c[q].pix = (uint32_t)row * (uint32_t)p.w + (uint32_t)c[q].x;
+      ref[q] = kLog ? p.ref[c[q].pix] : 0.0f;
+      before[q] = 0;
+    }
+    for (int i = 0; i < p.n_pairs; ++i) {
+      const PairCtx pc = pair_ctx(p, i);
+      const int gbase = i * L;
+      uint2 lm[kW];
+      uint32_t lwc[kW], lcnt = 0;
+#pragma unroll
+      for (int q = 0; q < kW; ++q) lm[q] = make_uint2(0u, 0u), lwc[q] = 0u;
+      auto flush = [&](int l) {
+        if ((l & 31) != 31 && l != L - 1) return;
+        if (lane <= (l & 31)) {
+          const int g = gbase + (l & ~31) + lane;
+#pragma unroll
+          for (int q = 0; q < kW; ++q) {
+            if (!c[q].have) continue;
+            p.masks[(size_t)g * p.n_words + c[q].wi] = lm[q];
+            if (kMag) p.wcount[(size_t)g * p.n_words + c[q].wi] = lwc[q];
+          }
+          if (lcnt) atomicAdd(&s_cnt[g], lcnt);
+        }
+        lcnt = 0;
+      };
+      if (pc.skip) {  // log mode, no endpoints, nothing selected: no events
+#pragma unroll
+        for (int q = 0; q < kW; ++q) lm[q] = make_uint2(0u, 0u);
+        for (int l = 0; l < L; ++l) flush(l);
+        continue;
+      }
+      int v0[kW], vc[kW];
+      uint32_t tw0[kW], tw1[kW], at0[kW], at1[kW];
+      bool same[kW];
+#pragma unroll
+      for (int q = 0; q < kW; ++q) {
+        v0[q] = pc.prev[c[q].pix];
+        vc[q] = pc.curr[c[q].pix];
+        tw0[q] = (c[q].valid && N > 0) ? pc.touched[c[q].pix] : 0u;
+        tw1[q] = (c[q].valid && N > 32) ? pc.touched[P + c[q].pix] : 0u;
+        at0[q] = __reduce_or_sync(kFull, tw0[q]);
+        at1[q] = __reduce_or_sync(kFull, tw1[q]);
+      }
+      // value of interior chain frame k (1..N) at this lane; consumes the claim
+      auto value = [&](int q, int k) -> int {
+        const int bit = k - 1;
+        bool t;
+        if (bit < 32) t = (tw0[q] >> bit) & 1u;
+        else if (bit < 64) t = (tw1[q] >> (bit - 32)) & 1u;
+        else t = c[q].valid && ((pc.touched[(size_t)(bit >> 5) * P + c[q].pix] >> (bit & 31)) & 1u);
+        if (!t) return v0[q];
+        const size_t slot = (size_t)bit * P + c[q].pix;
+        const uint32_t key = pc.claims[slot];
+        pc.claims[slot] = 0u;
+        return pc.prev[__ldg(pc.points + (0xFFFFFFu - (key & 0xFFFFFFu)))];
+      };
+      auto any_touched = [&](int q, int k) -> bool {
+        const int bit = k - 1;
+        if (bit < 32) return (at0[q] >> bit) & 1u;
+        if (bit < 64) return (at1[q] >> (bit - 32)) & 1u;
+        return true;
+      };
+      // links that must be evaluated, as a bit set over l (bit l of ev64):
+      // an interior link ending in k (bit k-1 of the any-touched set A) is
+      // skipped when neither k nor the frame before it has a touched lane;
+      // the first link also needs a v0 start (see above); curr always counts
+      uint64_t ev64[kW];
+      const int nint = min(L, N - p.d.start);  // links ending in an interior frame
+#pragma unroll
+      for (int q = 0; q < kW; ++q) {
+        bool same0;
+        if (p.d.start == 0) {
+          before[q] = v0[q];
+          same0 = true;
+        } else {
+          // chain starts at frame 1: its value is `before` (linear) and its
+          // claim must be consumed in both modes
+          before[q] = value(q, 1);
+          same0 = !kLog && !any_touched(q, 1);
+        }
+        if (L > 64 || N > 64) {
+          ev64[q] = ~0ull;
+        } else {
+          const uint64_t A = ((uint64_t)at1[q] << 32) | at0[q];  // bit k-1: frame k touched somewhere
+          const uint64_t Al = A >> p.d.start;                     // bit l: link l's end frame touched
+          uint64_t e = Al | (Al << 1) | (same0 ? 0ull : 1ull);
+          e &= nint >= 64 ? ~0ull : ((1ull << nint) - 1ull);
+          if (nint < L) e |= 1ull << (L - 1);  // the link into curr
+          ev64[q] = e;
+        }
+      }
+      for (int lb = 0; lb < L; lb += 32) {
+        const int nl = min(32, L - lb);
+        uint32_t e32[kW];
+#pragma unroll
+        for (int q = 0; q < kW; ++q) e32[q] = (uint32_t)(lb < 64 ? ev64[q] >> lb : ~0ull);
+        if (nl < 32) {
+#pragma unroll
+          for (int q = 0; q < kW; ++q) e32[q] &= (1u << nl) - 1u;
+        }
+        uint32_t todo = e32[0];
+#pragma unroll
+        for (int q = 1; q < kW; ++q) todo |= e32[q];
+        while (todo) {
+          const int j = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const int l = lb + j, k = kfirst + l;
+#pragma unroll
+          for (int q = 0; q < kW; ++q) {
+            if (!((e32[q] >> j) & 1u)) continue;
+            const int val = k <= N ? value(q, k) : vc[q];
+            uint32_t ev;
+            const uint2 m = link_rule<kLog, kMag>(p, s_lut, gbase + l, c[q], lane, val, ref[q], before[q], ev);
+            if (lane == j) {
+              lm[q] = m;
+              if (kMag) lwc[q] = ev;
+              lcnt += ev;
+            }
+          }
+        }
+        // skipped links: empty masks (no events, state unchanged)
+#pragma unroll
+        for (int q = 0; q < kW; ++q) {
+          if (!((e32[q] >> lane) & 1u)) {
+            lm[q] = make_uint2(0u, 0u);
+            lwc[q] = 0u;
+          }
+        }
+        flush(lb + nl - 1);
+      }
+      // touched planes back to zero for the next launch
+#pragma unroll
+      for (int q = 0; q < kW; ++q) {
+        if (!c[q].valid) continue;
+        if (tw0[q]) pc.touched[c[q].pix] = 0u;
+        if (tw1[q]) pc.touched[P + c[q].pix] = 0u;
+        for (int wdx = 2; wdx < ((N + 31) >> 5); ++wdx)
+          if (pc.touched[(size_t)wdx * P + c[q].pix]) pc.touched[(size_t)wdx * P + c[q].pix] = 0u;
+      }
+    }
+    if (kLog) {
+#pragma unroll
+      for (int q = 0; q < kW; ++q)
+        if (c[q].valid) p.ref[c[q].pix] = ref[q];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G; i += blockDim.x) p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
+}
+
 // ------------------------------------------------------------ offsets
 // One warp per link row: exclusive prefix of the row's per-block counts and
 // the row total.  Chunks of 32 blocks with a running carry.
@@ -1097,7 +1288,29 @@ static void launch_chain_dense(const ChainParams& p, size_t sm, cudaStream_t s) 
   k<<<p.n_blocks, 256, sm, s>>>(p);
 }
 
+template <bool kLog, bool kMag>
+static void launch_chain_sparse(const ChainParams& p, size_t sm, cudaStream_t s) {
+  auto* k = chain_sparse_kernel<kLog, kMag>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    attr = true;
+  }
+  k<<<p.n_blocks, 256, sm, s>>>(p);
+}
+
 void launch_chain(const ChainParams& p, int provider, cudaStream_t s) {
+  if (provider == kProvSparse) {
+    const size_t sm = (size_t)std::max(p.d.n_links * p.n_pairs, 1) * sizeof(uint32_t);
+    if (p.log_mode) {
+      if (p.magnitude) launch_chain_sparse<true, true>(p, sm, s);
+      else launch_chain_sparse<true, false>(p, sm, s);
+    } else {
+      if (p.magnitude) launch_chain_sparse<false, true>(p, sm, s);
+      else launch_chain_sparse<false, false>(p, sm, s);
+    }
+    return;
+  }
   if (provider == kProvDenseGrid && p.kc) {
     const size_t sm = (size_t)(p.n_interp + 2) * sizeof(float4) +
                       (size_t)std::max(p.d.n_links * p.n_pairs, 1) * sizeof(uint32_t);

@@ -348,7 +348,9 @@ struct EventEngine {
   DevBuf masks, counts, prefix, link_total, segtab, segbase, seg_out, events, mcount, wcount, base;
   int64_t capacity = 0;
 
-  void geometry(int w_, int h_) {
+  // fixed_wpb > 0: words per block (sparse: 16, one 2-word task per warp, so
+  // blocks over busy regions do not hold idle warps for long)
+  void geometry(int w_, int h_, int fixed_wpb = 0) {
     w = w_;
     h = h_;
     wpr = (w + 31) / 32;
@@ -357,6 +359,7 @@ struct EventEngine {
     const int64_t target = 148 * 8;
     int64_t per = (n_words + target - 1) / target;
     per = std::max<int64_t>(kWarpsPerBlock, (per + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock);
+    if (fixed_wpb > 0) per = fixed_wpb;
     wpb = (int)per;
     n_blocks = (int)((n_words + wpb - 1) / wpb);
     max_links = 0;
