@@ -750,7 +750,6 @@ __global__ void __launch_bounds__(256, 3) chain_sparse_kernel(ChainParams p) {
       }
       int v0[kW], vc[kW];
       uint32_t tw0[kW], tw1[kW], at0[kW], at1[kW];
-      bool same[kW];
 #pragma unroll
       for (int q = 0; q < kW; ++q) {
         v0[q] = pc.prev[c[q].pix];

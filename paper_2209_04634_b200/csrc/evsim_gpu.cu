@@ -207,14 +207,17 @@ struct FlowEngine {
   LevelDims dims[kMaxLevels]{};
   DevBuf pyr[kMaxLevels];     // fp32 level images, R slots
   DevBuf qpyr[kMaxLevels];    // float4 quad images (4 bilinear taps per pixel), R slots
+  DevBuf tex[kMaxLevels];     // sparse: float4 (value, gx, gy, 0) per pixel, R slots
+  bool texels = false;
   DevBuf tables[kMaxLevels];  // cx | cy | ix | wx | iy | wy
   DevBuf grid[kMaxLevels];    // per pair: pu | pv
   GridGeom geom[kMaxLevels]{};
 
-  void setup(int w_, int h_, Preset p, cudaStream_t s) {
+  void setup(int w_, int h_, Preset p, bool want_texels, cudaStream_t s) {
     w = w_;
     h = h_;
     preset = p;
+    texels = want_texels;
     levels = effective_levels(p.levels, w, h);
     dims[0] = {w, h};
     for (int l = 1; l < levels; ++l) dims[l] = {(dims[l - 1].w + 1) / 2, (dims[l - 1].h + 1) / 2};
@@ -267,6 +270,10 @@ struct FlowEngine {
         qpyr[l].release();
         pyr[l].ensure((size_t)R_ * pl * sizeof(float), s);
         qpyr[l].ensure((size_t)R_ * pl * sizeof(float4), s);
+        if (texels) {
+          tex[l].release();
+          tex[l].ensure((size_t)R_ * pl * sizeof(float4), s);
+        }
       }
       R = R_;
     }
@@ -288,6 +295,7 @@ struct FlowEngine {
       p.dims[l] = dims[l];
       p.pyr[l] = Ring<float>{pyr[l].as<float>(), pl};
       p.qpyr[l] = Ring<float4>{qpyr[l].as<float4>(), pl};
+      p.tex[l] = Ring<float4>{texels ? tex[l].as<float4>() : nullptr, pl};
     }
     p.frames = Ring<const uint8_t>{frames, P};
     p.quad_u8 = Ring<uint32_t>{quad_u8, P};
@@ -323,8 +331,8 @@ struct FlowEngine {
     for (int l = 0; l < levels; ++l) {
       const size_t pl = (size_t)dims[l].w * dims[l].h;
       p.dims[l] = dims[l];
-      p.prev[l] = Ring<const float>{pyr[l].as<float>(), pl};
-      p.curr[l] = Ring<const float>{pyr[l].as<float>(), pl};
+      p.tex[l] = Ring<const float4>{tex[l].as<float4>(), pl};
+      p.qcurr[l] = Ring<const float4>{qpyr[l].as<float4>(), pl};
     }
     p.R = R;
     p.r0 = r0;
@@ -532,7 +540,7 @@ struct evsim_gpu_sim {
     R = 0;
     pair_cap = 0;
     rhead = 0;
-    if (uses_flow()) flow.setup(w, h, preset, stream);
+    if (uses_flow()) flow.setup(w, h, preset, sparse_flow(), stream);
     if (log_mode()) ref.ensure((size_t)w * h * sizeof(float), stream);
     ev.geometry(w, h);
     // interpolation constants, interpolate_frames simulate.cpp:97-100

@@ -68,6 +68,22 @@ __global__ void build_quad_kernel(const uint8_t* __restrict__ src, uint32_t* __r
                            ((uint32_t)r1[x1] << 24);
 }
 
+// Template texels of one level for the sparse solver: (value, gx, gy, 0) per
+// pixel, gx / gy the reference's central differences with replicate borders
+// (gradients, flow.cpp:60-73), so a bilinear sample of all three is 4 loads.
+__global__ void texel_kernel(PyramidParams p, int l) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  const LevelDims d = p.dims[l];
+  if (x >= d.w) return;
+  const int slot = (p.slot0 + (int)blockIdx.z) % p.R;
+  const float* im = p.pyr[l].at(slot);
+  const float* r = im + (size_t)y * d.w;
+  const float gx = fmul(0.5f, fsub(r[min(x + 1, d.w - 1)], r[max(x - 1, 0)]));
+  const float gy = fmul(0.5f, fsub(im[(size_t)min(y + 1, d.h - 1) * d.w + x], im[(size_t)max(y - 1, 0) * d.w + x]));
+  p.tex[l].at(slot)[(size_t)y * d.w + x] = make_float4(r[x], gx, gy, 0.0f);
+}
+
 // sample() (flow.cpp:45-57) through a quad image: one 16-byte gather.
 __device__ __forceinline__ float sample_quadf(const float4* __restrict__ q, int w, int h, float x, float y) {
   x = clamp_ref(x, 0.0f, (float)(w - 1));
@@ -623,21 +639,26 @@ __global__ void densify_kernel(GridGeom g, float* __restrict__ du, float* __rest
 
 // ---------------------------------------------------------------- sparse LK
 
-// sample() of the materialised gradient images (flow.cpp:328-334): gradients
-// evaluated at the four taps on the fly.
-__device__ __forceinline__ void sample_grads(const float* __restrict__ im, int w, int h, float sx, float sy,
+// sample() of the materialised gradient images and of P (flow.cpp:328-334)
+// through the template texels: the four taps carry (value, gx, gy), so one
+// bilinear sample of all three is four 16-byte loads (one when the position
+// is integral: lerp(a, b, 0) = a exactly).
+__device__ __forceinline__ void sample_texel(const float4* __restrict__ tex, int w, int h, float sx, float sy,
                                              float& a, float& b, float& val) {
   const Tap t = make_tap(sx, sy, w, h);
-  const float gx00 = grad_x(im, w, t.x0, t.y0), gx10 = grad_x(im, w, t.x1, t.y0);
-  const float gx01 = grad_x(im, w, t.x0, t.y1), gx11 = grad_x(im, w, t.x1, t.y1);
-  const float gy00 = grad_y(im, w, h, t.x0, t.y0), gy10 = grad_y(im, w, h, t.x1, t.y0);
-  const float gy01 = grad_y(im, w, h, t.x0, t.y1), gy11 = grad_y(im, w, h, t.x1, t.y1);
-  const float* r0 = im + (size_t)t.y0 * w;
-  const float* r1 = im + (size_t)t.y1 * w;
-  a = lerp_ref(lerp_ref(gx00, gx10, t.fx), lerp_ref(gx01, gx11, t.fx), t.fy);
-  b = lerp_ref(lerp_ref(gy00, gy10, t.fx), lerp_ref(gy01, gy11, t.fx), t.fy);
-  val = lerp_ref(lerp_ref(__ldg(r0 + t.x0), __ldg(r0 + t.x1), t.fx),
-                 lerp_ref(__ldg(r1 + t.x0), __ldg(r1 + t.x1), t.fx), t.fy);
+  const float4* r0 = tex + (size_t)t.y0 * w;
+  const float4 q00 = __ldg(r0 + t.x0);
+  if (t.fx == 0.0f && t.fy == 0.0f) {
+    val = q00.x;
+    a = q00.y;
+    b = q00.z;
+    return;
+  }
+  const float4* r1 = tex + (size_t)t.y1 * w;
+  const float4 q10 = __ldg(r0 + t.x1), q01 = __ldg(r1 + t.x0), q11 = __ldg(r1 + t.x1);
+  a = lerp_ref(lerp_ref(q00.y, q10.y, t.fx), lerp_ref(q01.y, q11.y, t.fx), t.fy);
+  b = lerp_ref(lerp_ref(q00.z, q10.z, t.fx), lerp_ref(q01.z, q11.z, t.fx), t.fy);
+  val = lerp_ref(lerp_ref(q00.x, q10.x, t.fx), lerp_ref(q01.x, q11.x, t.fx), t.fy);
 }
 
 // estimate_sparse_flow's per-point loop (flow.cpp:309-380), one thread per point.
@@ -662,8 +683,8 @@ __global__ void __launch_bounds__(128) sparse_lk_kernel(SparseLKParams p) {
     bool lost = false, solved_any = false;
     for (int l = p.levels - 1; l >= 0 && !lost; --l) {
       const int w = p.dims[l].w, h = p.dims[l].h;
-      const float* P = p.prev[l].at(sp);
-      const float* C = p.curr[l].at(sc);
+      const float4* T = p.tex[l].at(sp);
+      const float4* C = p.qcurr[l].at(sc);
       const float px = fsub(fmul(fadd((float)ptx, 0.5f), __fdiv_rn((float)w, w0)), 0.5f);
       const float py = fsub(fmul(fadd((float)pty, 0.5f), __fdiv_rn((float)h, h0)), 0.5f);
       if (l != p.levels - 1) {
@@ -675,7 +696,7 @@ __global__ void __launch_bounds__(128) sparse_lk_kernel(SparseLKParams p) {
         const float sy = fadd(py, (float)oy);
         for (int ox = -r; ox <= r; ++ox) {
           float a, b, tv;
-          sample_grads(P, w, h, fadd(px, (float)ox), sy, a, b, tv);
+          sample_texel(T, w, h, fadd(px, (float)ox), sy, a, b, tv);
           gxx = dadd(gxx, (double)fmul(a, a));
           gxy = dadd(gxy, (double)fmul(a, b));
           gyy = dadd(gyy, (double)fmul(b, b));
@@ -692,8 +713,8 @@ __global__ void __launch_bounds__(128) sparse_lk_kernel(SparseLKParams p) {
           for (int ox = -r; ox <= r; ++ox) {
             const float sx = fadd(px, (float)ox);
             float a, b, tv;
-            sample_grads(P, w, h, sx, sy, a, b, tv);
-            const float residual = fsub(sample_f32(C, w, h, fadd(sx, u), syv), tv);
+            sample_texel(T, w, h, sx, sy, a, b, tv);
+            const float residual = fsub(sample_quadf(C, w, h, fadd(sx, u), syv), tv);
             b1 = dadd(b1, (double)fmul(a, residual));
             b2 = dadd(b2, (double)fmul(b, residual));
           }
@@ -726,6 +747,7 @@ void launch_pyramid(const PyramidParams& p, int n_frames, cudaStream_t s) {
   for (int l = 0; l < p.levels; ++l) {
     dim3 g((p.dims[l].w + 127) / 128, p.dims[l].h, n_frames);
     pyramid_level_kernel<<<g, 128, 0, s>>>(p, l);
+    if (p.tex[l].base) texel_kernel<<<g, 128, 0, s>>>(p, l);
   }
 }
 

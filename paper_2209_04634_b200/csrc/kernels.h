@@ -39,6 +39,7 @@ struct PyramidParams {
   Ring<float> pyr[kMaxLevels];
   Ring<float4> qpyr[kMaxLevels];
   Ring<uint32_t> quad_u8;   // base may be null (no interpolation)
+  Ring<float4> tex[kMaxLevels];  // sparse: per pixel (value, gx, gy, 0); base may be null
   int R, slot0;             // frame j of this launch is slot (slot0 + j) % R
 };
 
@@ -72,8 +73,8 @@ struct DenseLKParams {
 struct SparseLKParams {
   int levels;
   LevelDims dims[kMaxLevels];
-  Ring<const float> prev[kMaxLevels];
-  Ring<const float> curr[kMaxLevels];
+  Ring<const float4> tex[kMaxLevels];    // prev: (value, gx, gy, 0) per pixel
+  Ring<const float4> qcurr[kMaxLevels];  // curr: quad images
   int R, r0;
   int w0, h0;
   int radius, iterations;
