@@ -933,6 +933,7 @@ __global__ void __launch_bounds__(1024) segbase_kernel(EmitParams p, int64_t* se
 // per-lane count path: per pixel all negative events precede the positive.
 __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* __restrict__ segbase) {
   extern __shared__ int64_t s_off0[];  // [S] output offset of segment s in this block minus its flat offset
+  int* s_list = reinterpret_cast<int*>(s_off0 + p.n_links);  // segments with events in this block
   __shared__ int s_warp[kWarpsPerBlock];
   __shared__ int s_item[256];
   __shared__ int64_t s_dst[256];
@@ -943,22 +944,38 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
   if (p.seg_out[1 + 2 * S] > p.capacity) return;  // host grows the buffer and re-emits
   const int64_t wbeg = (int64_t)b * p.words_per_block;
   const int nw = (int)(min(wbeg + p.words_per_block, p.n_words) - wbeg);
-  const int n_items = S * nw;
   // segment s of this block starts at segbase[s] + sum over its links of the
-  // events in earlier blocks
-  for (int s = threadIdx.x; s < S; s += blockDim.x) {
-    const int k0 = p.seg.seg_first[s], nk = p.seg.seg_nlinks[s];
-    int64_t o = segbase[s];
-    for (int k = k0; k < k0 + nk; ++k) o += p.prefix[(size_t)k * p.n_blocks + b];
-    s_off0[s] = o;
+  // events in earlier blocks; segments without events in this block are
+  // dropped from the item list (their masks are never read)
+  int n_nz = 0;
+  for (int s0 = 0; s0 < S; s0 += blockDim.x) {
+    const int s = s0 + threadIdx.x;
+    int nz = 0;
+    if (s < S) {
+      const int k0 = p.seg.seg_first[s], nk = p.seg.seg_nlinks[s];
+      int64_t o = segbase[s];
+      uint32_t cnt = 0;
+      for (int k = k0; k < k0 + nk; ++k) {
+        o += p.prefix[(size_t)k * p.n_blocks + b];
+        cnt += p.counts[(size_t)k * p.n_blocks + b];
+      }
+      s_off0[s] = o;
+      nz = cnt != 0u;
+    }
+    int tot;
+    const int pos = block_exclusive_scan(nz, s_warp, tot);
+    if (nz) s_list[n_nz + pos] = s;
+    n_nz += tot;
   }
   __syncthreads();
+  const int n_items = n_nz * nw;
   int64_t carry = 0;
   for (int c0 = 0; c0 < n_items; c0 += blockDim.x) {
     const int it = c0 + threadIdx.x;
     const bool valid = it < n_items;
-    const int s = valid ? it / nw : 0;
-    const int j = valid ? it - s * nw : 0;
+    const int si = valid ? it / nw : 0;
+    const int s = valid ? s_list[si] : 0;
+    const int j = valid ? it - si * nw : 0;
     uint32_t pos = 0, all = 0;
     int cnt = 0;
     bool fast = false;
@@ -1042,8 +1059,9 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
     const int nwork = s_nwork;
     for (int jj = warp; jj < nwork; jj += kWarpsPerBlock) {
       const int item = s_item[jj];
-      const int sj = item / nw;
-      const uint32_t wij = (uint32_t)(wbeg + (item - sj * nw));
+      const int sij = item / nw;
+      const int sj = s_list[sij];
+      const uint32_t wij = (uint32_t)(wbeg + (item - sij * nw));
       const int row = (int)(wij / (uint32_t)p.wpr);
       const int x = (int)(wij - (uint32_t)row * (uint32_t)p.wpr) * 32 + lane;
       const int k0 = p.seg.seg_first[sj], nk = p.seg.seg_nlinks[sj];
@@ -1342,10 +1360,10 @@ void launch_offsets(const OffsetParams& p, cudaStream_t s) {
 // segbase_kernel then emit_kernel; segbase: [links] int64 scratch
 void launch_emit(const EmitParams& p, int64_t* segbase, cudaStream_t s) {
   segbase_kernel<<<1, 1024, 0, s>>>(p, segbase);
-  const size_t sm = (size_t)std::max(p.n_links, 1) * sizeof(int64_t);
+  const size_t sm = (size_t)std::max(p.n_links, 1) * (sizeof(int64_t) + sizeof(int));
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 144 * 1024);
     attr = true;
   }
   emit_kernel<<<p.n_blocks, 256, sm, s>>>(p, segbase);

@@ -715,6 +715,7 @@ struct evsim_gpu_sim {
     ep.n_links = G;
     ep.seg = ev.seg();
     ep.prefix = ev.prefix.as<int64_t>();
+    ep.counts = ev.counts.as<uint32_t>();
     ep.link_total = ev.link_total.as<int64_t>();
     ep.seg_out = ev.seg_out.as<int64_t>();
     ep.base = ev.base.as<int64_t>();

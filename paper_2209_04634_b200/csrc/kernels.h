@@ -177,6 +177,7 @@ struct EmitParams {
   int n_links;             // links of the launch (pairs * per-pair links)
   SegTable seg;
   const int64_t* prefix;
+  const uint32_t* counts;  // [g][n_blocks] events per (link, block)
   const int64_t* link_total;
   int64_t* seg_out;        // [0] = S, [1..S] seg_t, [1+S..1+2S] offsets (S+1); block 0
   int64_t* base;           // device scalar: output offset of this launch's first event;
