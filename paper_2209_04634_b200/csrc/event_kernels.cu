@@ -161,41 +161,6 @@ __device__ __forceinline__ void DenseProvider<true>::init(const ChainParams& p, 
   v = __ldg(p.dv + c.pix);
 }
 
-// Sparse: intermediate frame k is prev with the winning splat, if any
-// (simulate.cpp:167-199).  Consumed claim slots are cleared so the planes are
-// all-zero again for the next launch.
-struct SparseProvider {
-  uint32_t tw0, tw1;  // touched bits of frames 1..64
-  __device__ __forceinline__ void init(const ChainParams& p, const PairCtx& pc, const PixelCtx& c) {
-    // padding / duplicate lanes must not read claim slots another lane clears
-    tw0 = (c.valid && p.n_interp > 0) ? pc.touched[c.pix] : 0u;
-    tw1 = (c.valid && p.n_interp > 32) ? pc.touched[p.P + c.pix] : 0u;
-  }
-  __device__ __forceinline__ bool touched_bit(const ChainParams& p, const PairCtx& pc, const PixelCtx& c,
-                                              int k) const {
-    const int b = k - 1;
-    if (b < 32) return (tw0 >> b) & 1u;
-    if (b < 64) return (tw1 >> (b - 32)) & 1u;
-    if (!c.valid) return false;
-    return (pc.touched[(size_t)(b >> 5) * p.P + c.pix] >> (b & 31)) & 1u;
-  }
-  __device__ __forceinline__ int interp(const ChainParams& p, const PairCtx& pc, const PixelCtx& c, int k) const {
-    if (!touched_bit(p, pc, c, k)) return pc.prev[c.pix];
-    const size_t slot = (size_t)(k - 1) * p.P + c.pix;
-    const uint32_t key = pc.claims[slot];
-    pc.claims[slot] = 0u;
-    const uint32_t j = 0xFFFFFFu - (key & 0xFFFFFFu);
-    return pc.prev[__ldg(pc.points + j)];
-  }
-  __device__ __forceinline__ void finish(const ChainParams& p, const PairCtx& pc, const PixelCtx& c) const {
-    const int nw = (p.n_interp + 31) >> 5;
-    for (int i = 0; i < nw; ++i) {
-      const uint32_t t = i == 0 ? tw0 : (i == 1 ? tw1 : pc.touched[(size_t)i * p.P + c.pix]);
-      if (t) pc.touched[(size_t)i * p.P + c.pix] = 0u;
-    }
-  }
-};
-
 // No intermediate frames: chains over prev/curr only (difference_only, N = 0).
 struct NoneProvider {
   __device__ __forceinline__ void init(const ChainParams&, const PairCtx&, const PixelCtx&) {}
@@ -721,8 +686,16 @@ __global__ void __launch_bounds__(256, 3) chain_sparse_kernel(ChainParams p) {
       ref[q] = kLog ? p.ref[c[q].pix] : 0.0f;
       before[q] = 0;
     }
+    int sp = p.r0 % p.R;
     for (int i = 0; i < p.n_pairs; ++i) {
-      const PairCtx pc = pair_ctx(p, i);
+      const int sc = sp + 1 == p.R ? 0 : sp + 1;
+      PairCtx pc;
+      pc.prev = p.frames.at(sp);
+      pc.curr = p.frames.at(sc);
+      pc.touched = p.touched + (size_t)i * ((N + 31) >> 5) * P;
+      pc.skip = p.skip_empty && p.n_points[i] == 0;
+      const uint8_t* svals = p.svals + (size_t)i * N * P;
+      sp = sc;
       const int gbase = i * L;
       uint2 lm[kW];
       uint32_t lwc[kW], lcnt = 0;
@@ -766,11 +739,7 @@ __global__ void __launch_bounds__(256, 3) chain_sparse_kernel(ChainParams p) {
         if (bit < 32) t = (tw0[q] >> bit) & 1u;
         else if (bit < 64) t = (tw1[q] >> (bit - 32)) & 1u;
         else t = c[q].valid && ((pc.touched[(size_t)(bit >> 5) * P + c[q].pix] >> (bit & 31)) & 1u);
-        if (!t) return v0[q];
-        const size_t slot = (size_t)bit * P + c[q].pix;
-        const uint32_t key = pc.claims[slot];
-        pc.claims[slot] = 0u;
-        return pc.prev[__ldg(pc.points + (0xFFFFFFu - (key & 0xFFFFFFu)))];
+        return t ? (int)svals[(size_t)bit * P + c[q].pix] : v0[q];
       };
       auto any_touched = [&](int q, int k) -> bool {
         const int bit = k - 1;
@@ -1222,6 +1191,27 @@ __global__ void __launch_bounds__(256) select_emit_kernel(SelectParams p) {
 // claim, replaced only by a strictly larger change) selects, per target pixel,
 // the point with the largest change and, among equals, the smallest scan
 // index j: an atomicMax on (change << 24) | (2^24 - 1 - j)  (M < 2^24).
+// Target slot, value and claim key of splat item (j, k); false when the
+// point is lost or the target falls outside the frame.
+__device__ __forceinline__ bool splat_item(const SplatParams& p, const uint8_t* prev, const uint32_t* points,
+                                           const float2* disp, const uint8_t* status, int64_t j, int k,
+                                           size_t& slot, int& value, uint32_t& key) {
+  if (!status[j]) return false;
+  const uint32_t src = points[j];
+  const int px = (int)(src % (uint32_t)p.w), py = (int)(src / (uint32_t)p.w);
+  const float alpha = __fdiv_rn((float)k, (float)(p.n_interp + 1));
+  const float2 d = disp[j];
+  const int tx = lroundf_ref(fadd((float)px, fmul(alpha, d.x)));
+  const int ty = lroundf_ref(fadd((float)py, fmul(alpha, d.y)));
+  if (tx < 0 || tx >= p.w || ty < 0 || ty >= p.h) return false;
+  const size_t idx = (size_t)ty * p.w + tx;
+  value = prev[src];
+  const int change = abs(value - (int)prev[idx]);
+  key = ((uint32_t)change << 24) | (0xFFFFFFu - (uint32_t)j);
+  slot = (size_t)(k - 1) * p.P + idx;
+  return true;
+}
+
 __global__ void splat_kernel(SplatParams p) {
   const int z = blockIdx.y;
   const int64_t M = p.n_points[z];
@@ -1234,25 +1224,49 @@ __global__ void splat_kernel(SplatParams p) {
   const uint8_t* status = p.status + (size_t)z * P;
   uint32_t* claims = p.claims + (size_t)z * N * P;
   uint32_t* touched = p.touched + (size_t)z * ((N + 31) / 32) * P;
-  const float denom = (float)(N + 1);
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = e / N;
     const int k = (int)(e - j * N) + 1;
-    if (!status[j]) continue;
-    const uint32_t src = points[j];
-    const int px = (int)(src % (uint32_t)p.w), py = (int)(src / (uint32_t)p.w);
-    const float alpha = __fdiv_rn((float)k, denom);
-    const float2 d = disp[j];
-    const int tx = lroundf_ref(fadd((float)px, fmul(alpha, d.x)));
-    const int ty = lroundf_ref(fadd((float)py, fmul(alpha, d.y)));
-    if (tx < 0 || tx >= p.w || ty < 0 || ty >= p.h) continue;
-    const size_t idx = (size_t)ty * p.w + tx;
-    const int value = prev[src];
-    const int change = abs(value - (int)prev[idx]);
-    const uint32_t key = ((uint32_t)change << 24) | (0xFFFFFFu - (uint32_t)j);
-    atomicMax(&claims[(size_t)(k - 1) * P + idx], key);
+    size_t slot;
+    int value;
+    uint32_t key;
+    if (!splat_item(p, prev, points, disp, status, j, k, slot, value, key)) continue;
+    atomicMax(&claims[slot], key);
+    const size_t idx = slot - (size_t)(k - 1) * P;
     atomicOr(&touched[(size_t)((k - 1) >> 5) * P + idx], 1u << ((k - 1) & 31));
+  }
+}
+
+// After the claims settle: the winner of every claimed slot stores its value
+// (the intermediate frame's pixel, simulate.cpp:195-197) in the u8 value plane
+// and zeroes the claim, so the chain reads one byte per touched pixel and the
+// claim planes are clean for the next launch.  Keys are unique per point, so
+// only the winner matches.
+__global__ void resolve_kernel(SplatParams p) {
+  const int z = blockIdx.y;
+  const int64_t M = p.n_points[z];
+  const int N = p.n_interp;
+  const int64_t total = M * N;
+  const size_t P = p.P;
+  const uint8_t* prev = p.frames.at((p.r0 + z) % p.R);
+  const uint32_t* points = p.points + (size_t)z * P;
+  const float2* disp = p.disp + (size_t)z * P;
+  const uint8_t* status = p.status + (size_t)z * P;
+  uint32_t* claims = p.claims + (size_t)z * N * P;
+  uint8_t* svals = p.svals + (size_t)z * N * P;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / N;
+    const int k = (int)(e - j * N) + 1;
+    size_t slot;
+    int value;
+    uint32_t key;
+    if (!splat_item(p, prev, points, disp, status, j, k, slot, value, key)) continue;
+    if (claims[slot] == key) {
+      svals[slot] = (uint8_t)value;
+      claims[slot] = 0u;
+    }
   }
 }
 
@@ -1344,7 +1358,6 @@ void launch_chain(const ChainParams& p, int provider, cudaStream_t s) {
   }
   switch (provider) {
     case kProvDenseGrid: launch_chain_mode<DenseProvider<false>>(p, s); break;
-    case kProvSparse: launch_chain_mode<SparseProvider>(p, s); break;
     case kProvDenseField: launch_chain_mode<DenseProvider<true>>(p, s); break;
     default: launch_chain_mode<NoneProvider>(p, s); break;
   }
@@ -1397,6 +1410,7 @@ void launch_splat(const SplatParams& p, int max_items, int n_pairs, cudaStream_t
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   splat_kernel<<<dim3(blocks, n_pairs), 256, 0, s>>>(p);
+  resolve_kernel<<<dim3(blocks, n_pairs), 256, 0, s>>>(p);
 }
 
 }  // namespace evsim_gpu

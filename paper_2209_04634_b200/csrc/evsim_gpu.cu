@@ -446,7 +446,7 @@ struct evsim_gpu_sim {
   FlowEngine flow;
   EventEngine ev;
   // sparse (per pair)
-  DevBuf sel_masks, sel_counts, points, n_points, disp, status, claims, touched;
+  DevBuf sel_masks, sel_counts, points, n_points, disp, status, claims, touched, svals;
 
   // last result
   int64_t* h_seg_out = nullptr;  // pinned
@@ -625,6 +625,8 @@ struct evsim_gpu_sim {
         status.ensure((size_t)pairs * P, stream);
         claims.release();
         claims.ensure((size_t)pairs * N * P * 4, stream, true);
+        svals.release();
+        svals.ensure((size_t)pairs * N * P, stream);
         touched.release();
         touched.ensure((size_t)pairs * ((N + 31) / 32) * P * 4, stream, true);
       }
@@ -1005,7 +1007,7 @@ struct evsim_gpu_sim {
     launch_sparse_lk(lk, (int)std::min<size_t>(P, INT32_MAX), n_pairs, stream);
     CK_LAUNCH("sparse_lk");
     splat_stage(r0, n_pairs, c);
-    launches += 3;
+    launches += 5;  // select mask + emit, sparse LK, splat, resolve
     (void)N;
   }
 
@@ -1026,8 +1028,10 @@ struct evsim_gpu_sim {
     spl.claims = claims.as<uint32_t>();
     spl.touched = touched.as<uint32_t>();
     spl.P = P;
+    spl.svals = svals.as<uint8_t>();
     launch_splat(spl, (int)std::min<int64_t>((int64_t)P * N, INT32_MAX), n_pairs, stream);
     CK_LAUNCH("splat");
+    c.svals = svals.as<uint8_t>();
     c.claims = claims.as<uint32_t>();
     c.touched = touched.as<uint32_t>();
     c.points = points.as<uint32_t>();

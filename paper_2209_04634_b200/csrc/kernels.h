@@ -142,6 +142,7 @@ struct ChainParams {
   // sparse provider (per pair strides)
   uint32_t* claims;        // [pair][N][P] keys (change << 24 | ~j)
   uint32_t* touched;       // [pair][ceil(N/32)][P] bits
+  const uint8_t* svals;    // [pair][N][P] winning splat values (valid where touched)
   const uint32_t* points;  // [pair][P]
   const int* n_points;     // [pair]
   size_t P;
@@ -220,6 +221,7 @@ struct SplatParams {
   const uint8_t* status;   // [pair][P]
   uint32_t* claims;        // [pair][N][P]
   uint32_t* touched;       // [pair][ceil(N/32)][P]
+  uint8_t* svals;          // [pair][N][P]
   size_t P;
 };
 
