@@ -789,19 +789,39 @@ __global__ void __launch_bounds__(256, 3) chain_sparse_kernel(ChainParams p) {
 #pragma unroll
         for (int q = 1; q < kW; ++q) todo |= e32[q];
         while (todo) {
-          const int j = __ffs(todo) - 1;
-          todo &= todo - 1;
-          const int l = lb + j, k = kfirst + l;
+          // up to 4 evaluated links at once: their value loads overlap
+          int js[4];
+          int vals[kW][4];
 #pragma unroll
-          for (int q = 0; q < kW; ++q) {
-            if (!((e32[q] >> j) & 1u)) continue;
-            const int val = k <= N ? value(q, k) : vc[q];
-            uint32_t ev;
-            const uint2 m = link_rule<kLog, kMag>(p, s_lut, gbase + l, c[q], lane, val, ref[q], before[q], ev);
-            if (lane == j) {
-              lm[q] = m;
-              if (kMag) lwc[q] = ev;
-              lcnt += ev;
+          for (int m = 0; m < 4; ++m) {
+            js[m] = todo ? __ffs(todo) - 1 : -1;
+            todo &= todo ? todo - 1 : 0u;
+          }
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+#pragma unroll
+            for (int q = 0; q < kW; ++q) {
+              const int j = js[m];
+              const int k = kfirst + lb + j;
+              vals[q][m] = (j >= 0 && ((e32[q] >> j) & 1u)) ? (k <= N ? value(q, k) : vc[q]) : 0;
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const int j = js[m];
+            if (j < 0) break;
+            const int l = lb + j;
+#pragma unroll
+            for (int q = 0; q < kW; ++q) {
+              if (!((e32[q] >> j) & 1u)) continue;
+              uint32_t ev;
+              const uint2 mk =
+                  link_rule<kLog, kMag>(p, s_lut, gbase + l, c[q], lane, vals[q][m], ref[q], before[q], ev);
+              if (lane == j) {
+                lm[q] = mk;
+                if (kMag) lwc[q] = ev;
+                lcnt += ev;
+              }
             }
           }
         }
