@@ -154,6 +154,15 @@ EVSIM_GPU_API int evsim_gpu_push_frames_async(evsim_gpu_sim* sim, const uint8_t*
                                               int32_t pixels_on_device);
 EVSIM_GPU_API int evsim_gpu_max_batch(const evsim_gpu_sim* sim, int32_t width, int32_t height);
 
+/* Row band (multi-GPU): this handle emits only the events of
+ * frame rows [y0, y1) and solves only the flow patch rows they depend on,
+ * from the full frames (every rank holds the whole frame).  Per timestamp the
+ * reference orders events by (y, x), so the global stream is, per segment,
+ * band 0's events, then band 1's, ...  (0, 0) = the whole frame (default).
+ * Only at the start of a stream (before the first push or after reset);
+ * dense and difference_only methods. */
+EVSIM_GPU_API int evsim_gpu_set_row_band(evsim_gpu_sim* sim, int32_t y0, int32_t y1);
+
 /* Several independent camera streams in one call (c4: many streams per GPU;
  * the reference runs one Simulator per thread, bench.cpp:53-64):
  * sims[i] gets the n_frames frames pixels[i] with timestamps t_us[i].  The

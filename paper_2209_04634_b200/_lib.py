@@ -35,6 +35,7 @@ _SIGS = {
     "evsim_gpu_push_frames_streamed": (
         ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _i32, _vp, _i64, ctypes.POINTER(CEvents)]),
     "evsim_gpu_max_batch": (ctypes.c_int, [_vp, _i32, _i32]),
+    "evsim_gpu_set_row_band": (ctypes.c_int, [_vp, _i32, _i32]),
     "evsim_gpu_sync": (ctypes.c_int, [_vp, ctypes.POINTER(CEvents)]),
     "evsim_gpu_copy_events": (ctypes.c_int, [_vp, _vp, _i64, _i32]),
     "evsim_gpu_stream": (_vp, [_vp]),

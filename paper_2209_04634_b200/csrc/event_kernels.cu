@@ -268,8 +268,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) chain_kernel(ChainParams p) {
       const int x = (int)(ww - (int64_t)row * p.wpr) * 32 + lane;
       c[q].valid = have[q] && x < p.w;
       c[q].x = x < p.w ? x : p.w - 1;
-      c[q].y = row;
-      c[q].pix = (size_t)row * p.w + c[q].x;
+      c[q].y = p.row0 + row;
+      c[q].pix = (size_t)c[q].y * p.w + c[q].x;
       c[q].xf = (float)c[q].x;
       c[q].yf = (float)c[q].y;
       if (kLog) ref[q] = p.ref[c[q].pix];
@@ -521,8 +521,8 @@ __global__ void __launch_bounds__(256, 3) chain_dense_kernel(ChainParams p) {
       const int x = (int)(ww - (int64_t)row * p.wpr) * 32 + lane;
       c[q].valid = c[q].have && x < p.w;
       c[q].x = x < p.w ? x : p.w - 1;
-      c[q].y = row;
-      c[q].pix = (uint32_t)row * w + (uint32_t)c[q].x;
+      c[q].y = p.row0 + row;
+      c[q].pix = (uint32_t)c[q].y * w + (uint32_t)c[q].x;
       c[q].xf = (float)c[q].x;
       c[q].yf = (float)c[q].y;
       ref[q] = kLog ? p.ref[c[q].pix] : 0.0f;
@@ -681,8 +681,8 @@ __global__ void __launch_bounds__(256, 3) chain_sparse_kernel(ChainParams p) {
       const int x = (int)(ww - (int64_t)row * p.wpr) * 32 + lane;
       c[q].valid = c[q].have && x < p.w;
       c[q].x = x < p.w ? x : p.w - 1;
-      c[q].y = row;
-      c[q].pix = (uint32_t)row * (uint32_t)p.w + (uint32_t)c[q].x;
+      c[q].y = p.row0 + row;
+      c[q].pix = (uint32_t)c[q].y * (uint32_t)p.w + (uint32_t)c[q].x;
       ref[q] = kLog ? p.ref[c[q].pix] : 0.0f;
       before[q] = 0;
     }
@@ -1013,8 +1013,9 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
       }
       const int T = __shfl_sync(kFull, incl, 31);
       const uint32_t wi = (uint32_t)(wbeg + j);
-      const int row = (int)(wi / (uint32_t)p.wpr);
-      const int x0 = (int)(wi - (uint32_t)row * (uint32_t)p.wpr) * 32;
+      const int lrow = (int)(wi / (uint32_t)p.wpr);
+      const int x0 = (int)(wi - (uint32_t)lrow * (uint32_t)p.wpr) * 32;
+      const int row = p.row0 + lrow;
       for (int q = lane; q - lane < T; q += 32) {
         // first lane l with incl[l] > q
         int lo = 0;
@@ -1051,8 +1052,9 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
       const int sij = item / nw;
       const int sj = s_list[sij];
       const uint32_t wij = (uint32_t)(wbeg + (item - sij * nw));
-      const int row = (int)(wij / (uint32_t)p.wpr);
-      const int x = (int)(wij - (uint32_t)row * (uint32_t)p.wpr) * 32 + lane;
+      const int lrow = (int)(wij / (uint32_t)p.wpr);
+      const int x = (int)(wij - (uint32_t)lrow * (uint32_t)p.wpr) * 32 + lane;
+      const int row = p.row0 + lrow;
       const int k0 = p.seg.seg_first[sj], nk = p.seg.seg_nlinks[sj];
       int nneg = 0, npos = 0;
       for (int k = k0; k < k0 + nk; ++k) {

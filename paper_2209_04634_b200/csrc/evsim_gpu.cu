@@ -212,6 +212,7 @@ struct FlowEngine {
   DevBuf tables[kMaxLevels];  // cx | cy | ix | wx | iy | wy
   DevBuf grid[kMaxLevels];    // per pair: pu | pv
   GridGeom geom[kMaxLevels]{};
+  int jrange[kMaxLevels][2]{};  // patch rows solved per level (row bands; else the full grid)
 
   void setup(int w_, int h_, Preset p, bool want_texels, cudaStream_t s) {
     w = w_;
@@ -258,8 +259,57 @@ struct FlowEngine {
       g.iy = base + ncx + ncy + 2 * lw;
       g.wy = reinterpret_cast<const float*>(base + ncx + ncy + 2 * lw + lh);
       g.pair_stride = 2 * ncx * ncy;
+      jrange[l][0] = 0;
+      jrange[l][1] = (int)ncy;
     }
     R = pairs = 0;
+  }
+
+  // Row band: the patch rows each level must solve so that the level-0 flow
+  // of event rows [y0, y1) is identical to the full-frame solve.  Level 0:
+  // densification reads grid rows iy[y], iy[y]+1 (flow.cpp:224-245); level
+  // l+1: each needed level-l centre cy seeds from the densified coarse field
+  // at sy = (cy + 0.5) * ry - 0.5 (flow.cpp:130-147), rows trunc(clamp(sy))
+  // and +1, i.e. grid rows iy'[row], +1.  Solving a patch reads only the
+  // (full) level images, so this is the whole dependency set.  Mirrors
+  // parallel.band_plan.
+  void plan_band(int y0, int y1) {
+    const int r = preset.radius, stride = std::max(1, r);
+    std::vector<std::vector<int>> cys(levels), iys(levels);
+    for (int l = 0; l < levels; ++l) {
+      cys[l] = patch_centers(dims[l].h, r, stride);
+      std::vector<float> wy;
+      interp_table(cys[l], dims[l].h, iys[l], wy);
+    }
+    std::vector<int> lo(levels, INT32_MAX), hi(levels, -1);
+    auto add = [&](int l, int j) {
+      j = std::min(j, (int)cys[l].size() - 1);
+      lo[l] = std::min(lo[l], j);
+      hi[l] = std::max(hi[l], j);
+    };
+    for (int y = y0; y < y1; ++y) {
+      add(0, iys[0][y]);
+      add(0, iys[0][y] + 1);
+    }
+    for (int l = 0; l + 1 < levels; ++l) {
+      const int hf = dims[l].h, hc = dims[l + 1].h;
+      const volatile float ry = (float)hc / (float)hf;
+      for (int j = lo[l]; j <= hi[l]; ++j) {
+        const volatile float t0 = (float)cys[l][j] + 0.5f;
+        const volatile float t1 = t0 * ry;
+        float sy = t1 - 0.5f;
+        sy = std::min(std::max(sy, 0.0f), (float)(hc - 1));
+        const int rr0 = (int)sy, rr1 = std::min(rr0 + 1, hc - 1);
+        for (int rr : {rr0, rr1}) {
+          add(l + 1, iys[l + 1][rr]);
+          add(l + 1, iys[l + 1][rr] + 1);
+        }
+      }
+    }
+    for (int l = 0; l < levels; ++l) {
+      jrange[l][0] = hi[l] >= 0 ? lo[l] : 0;
+      jrange[l][1] = hi[l] >= 0 ? hi[l] + 1 : 0;
+    }
   }
 
   void ensure(int R_, int pairs_, cudaStream_t s) {
@@ -279,7 +329,9 @@ struct FlowEngine {
     }
     if (pairs_ > pairs) {
       for (int l = 0; l < levels; ++l) {
-        grid[l].ensure((size_t)pairs_ * geom[l].pair_stride * sizeof(float), s);
+        // zeroed: with row bands, tiles past the planned rows read seeds
+        // from rows never solved (their results are never used)
+        grid[l].ensure((size_t)pairs_ * geom[l].pair_stride * sizeof(float), s, true);
         geom[l].pu = grid[l].as<float>();
         geom[l].pv = grid[l].as<float>() + geom[l].pair_stride / 2;
       }
@@ -319,7 +371,9 @@ struct FlowEngine {
       p.r0 = r0;
       p.radius = preset.radius;
       p.iterations = preset.iters;
-      launch_dense_lk(p, n_pairs, s);
+      p.jt0 = jrange[l][0];
+      p.jt1 = jrange[l][1];
+      if (p.jt1 > p.jt0) launch_dense_lk(p, n_pairs, s);
     }
     CK_LAUNCH("dense_lk");
     return levels;
@@ -441,6 +495,7 @@ struct evsim_gpu_sim {
   int rhead = 0;  // ring slot of the previous frame
   int R = 0;      // ring slots allocated
   int pair_cap = 0;
+  int band_y0 = 0, band_y1 = 0;  // row band of the events (0, 0 = the whole frame)
 
   DevBuf frames, quads, lut, ref, consts;
   FlowEngine flow;
@@ -535,14 +590,19 @@ struct evsim_gpu_sim {
 
   // ---- allocation ----------------------------------------------------------
   void allocate(int w_, int h_) {
+    if (band_y1 > h_) invalid("set_row_band: the band lies outside the frame");
     w = w_;
     h = h_;
     R = 0;
     pair_cap = 0;
     rhead = 0;
-    if (uses_flow()) flow.setup(w, h, preset, sparse_flow(), stream);
+    const bool band = band_y1 > 0;
+    if (uses_flow()) {
+      flow.setup(w, h, preset, sparse_flow(), stream);
+      if (band && dense_flow()) flow.plan_band(band_y0, band_y1);
+    }
     if (log_mode()) ref.ensure((size_t)w * h * sizeof(float), stream);
-    ev.geometry(w, h);
+    ev.geometry(w, band ? band_y1 - band_y0 : h);
     // interpolation constants, interpolate_frames simulate.cpp:97-100
     const int N = n_interp_eff();
     const int K = N + 2;
@@ -649,6 +709,7 @@ struct evsim_gpu_sim {
     const size_t P = (size_t)w * h;
     c.w = w;
     c.h = h;
+    c.row0 = band_y1 > 0 ? band_y0 : 0;
     c.wpr = ev.wpr;
     c.n_words = ev.n_words;
     c.words_per_block = ev.wpb;
@@ -710,6 +771,7 @@ struct evsim_gpu_sim {
     EmitParams ep{};
     ep.w = w;
     ep.h = h;
+    ep.row0 = c.row0;
     ep.wpr = ev.wpr;
     ep.n_words = ev.n_words;
     ep.words_per_block = ev.wpb;
@@ -1231,6 +1293,21 @@ int evsim_gpu_push_frames_streamed(evsim_gpu_sim* sim, const uint8_t* pixels, in
       throw;
     }
     sim->fill_out(out);
+  });
+}
+
+int evsim_gpu_set_row_band(evsim_gpu_sim* sim, int32_t y0, int32_t y1) {
+  return guarded([&] {
+    if (!sim) invalid("evsim_gpu_set_row_band: null simulator");
+    if (sim->has_prev) invalid("set_row_band: only at the start of a stream (before the first push or after reset)");
+    if (sim->cfg.method == EVSIM_METHOD_SPARSE || sim->cfg.method == EVSIM_METHOD_DIFFERENCE_INTERP)
+      invalid("set_row_band: only the dense and difference_only methods (sparse splats cross band borders)");
+    if (!(y0 == 0 && y1 == 0) && (y0 < 0 || y1 <= y0)) invalid("set_row_band: need 0 <= y0 < y1");
+    CK(cudaSetDevice(sim->device));
+    sim->finish();
+    sim->band_y0 = y0;
+    sim->band_y1 = y1;
+    sim->w = sim->h = 0;  // geometry is rebuilt at the next push
   });
 }
 

@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_tile_kernel(DenseLKParams
   const int D = 2 * r + 1, P2 = D * D;
   const int w = g.w, h = g.h;
   const int t = threadIdx.x;
-  const int i0 = blockIdx.x * kLKTileX, j0 = blockIdx.y * kLKTileY;
+  const int i0 = blockIdx.x * kLKTileX, j0 = p.jt0 + blockIdx.y * kLKTileY;
   const int i1 = min(i0 + kLKTileX, g.ncx) - 1, j1 = min(j0 + kLKTileY, g.ncy) - 1;
   const int rx0 = __ldg(g.cx + i0) - r - 1, ry0 = __ldg(g.cy + j0) - r - 1;
   const int rw = __ldg(g.cx + i1) - __ldg(g.cx + i0) + 2 * r + 3;
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
   const float4* __restrict__ qcurr = p.qcurr.at((p.r0 + z + 1) % p.R);
   const int w = g.w, h = g.h;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int i0 = blockIdx.x * kLKTileX, j0 = blockIdx.y * kLKTileY;
+  const int i0 = blockIdx.x * kLKTileX, j0 = p.jt0 + blockIdx.y * kLKTileY;
   const int i1 = min(i0 + kLKTileX, g.ncx) - 1, j1 = min(j0 + kLKTileY, g.ncy) - 1;
   const int rx0 = __ldg(g.cx + i0) - kR - 1, ry0 = __ldg(g.cy + j0) - kR - 1;
   const int rw = __ldg(g.cx + i1) - __ldg(g.cx + i0) + 2 * kR + 3;
@@ -576,9 +576,9 @@ __global__ void __launch_bounds__(128) dense_lk_global_kernel(DenseLKParams p) {
   coarse.pv += z * coarse.pair_stride;
   const float* __restrict__ prev = p.prev.at((p.r0 + z) % p.R);
   const float4* __restrict__ qcurr = p.qcurr.at((p.r0 + z + 1) % p.R);
-  if (pid >= g.ncx * g.ncy) return;
+  if (pid >= g.ncx * (p.jt1 - p.jt0)) return;
   const int i = pid % g.ncx;
-  const int j = pid / g.ncx;
+  const int j = p.jt0 + pid / g.ncx;
   const int cx = __ldg(g.cx + i);
   const int cy = __ldg(g.cy + j);
   const int w = g.w, h = g.h, r = p.radius;
@@ -623,8 +623,8 @@ __global__ void __launch_bounds__(128) dense_lk_global_kernel(DenseLKParams p) {
       v = fadd(v, dv);
     }
   }
-  g.pu[pid] = u;
-  g.pv[pid] = v;
+  g.pu[(size_t)j * g.ncx + i] = u;
+  g.pv[(size_t)j * g.ncx + i] = v;
 }
 
 __global__ void densify_kernel(GridGeom g, float* __restrict__ du, float* __restrict__ dv) {
@@ -758,7 +758,8 @@ void launch_build_quad(const uint8_t* src, uint32_t* dst, int w, int h, cudaStre
 
 void launch_dense_lk(const DenseLKParams& p, int n_pairs, cudaStream_t s) {
   if (n_pairs <= 0) return;
-  dim3 grid((p.g.ncx + kLKTileX - 1) / kLKTileX, (p.g.ncy + kLKTileY - 1) / kLKTileY, n_pairs);
+  // patch rows [jt0, jt1): jt0 a multiple of the tile height
+  dim3 grid((p.g.ncx + kLKTileX - 1) / kLKTileX, (p.jt1 - p.jt0 + kLKTileY - 1) / kLKTileY, n_pairs);
   const int r = p.radius;
   const size_t sm = dense_lk_smem(r);
   static bool attr_set = false;
@@ -776,7 +777,7 @@ void launch_dense_lk(const DenseLKParams& p, int n_pairs, cudaStream_t s) {
   else if (r == 4) dense_lk_tile_kernel<4><<<grid, kLKThreads, sm, s>>>(p);
   else if (r == 6) dense_lk_tile_kernel<6><<<grid, kLKThreads, sm, s>>>(p);
   else if (sm <= 200 * 1024) dense_lk_tile_kernel<0><<<grid, kLKThreads, sm, s>>>(p);
-  else dense_lk_global_kernel<<<dim3((p.g.ncx * p.g.ncy + 127) / 128, n_pairs), 128, 0, s>>>(p);
+  else dense_lk_global_kernel<<<dim3((p.g.ncx * (p.jt1 - p.jt0) + 127) / 128, n_pairs), 128, 0, s>>>(p);
 }
 
 void launch_densify(const GridGeom& g, float* du, float* dv, cudaStream_t s) {

@@ -60,6 +60,7 @@ struct GridGeom {
 };
 
 struct DenseLKParams {
+  int jt0, jt1;           // patch rows [jt0, jt1) to solve (row bands; full grid otherwise)
   GridGeom g;             // this level
   GridGeom coarse;        // level + 1 (seed source) when has_coarse
   int has_coarse;
@@ -116,6 +117,7 @@ struct SegParams {
 
 struct ChainParams {
   int w, h;
+  int row0;                // first frame row of the word grid (row bands; 0 = full frame)
   int wpr;                 // 32-pixel words per row = ceil(w/32)
   int64_t n_words;         // h * wpr
   int words_per_block;
@@ -172,6 +174,7 @@ struct OffsetParams {
 
 struct EmitParams {
   int w, h, wpr;
+  int row0;                // first frame row of the word grid
   int64_t n_words;
   int words_per_block;
   int n_blocks;

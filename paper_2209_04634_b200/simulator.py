@@ -413,6 +413,11 @@ class Simulator:
         out.events = unpack_events(packed, seg_t, seg_off)
         return out
 
+    def set_row_band(self, y0: int, y1: int) -> None:
+        """Emit only the events of rows [y0, y1) (evsim_gpu_set_row_band);
+        (0, 0) = whole frame.  Stream start only; dense / difference_only."""
+        _lib.check(self._lib.evsim_gpu_set_row_band(self._h, int(y0), int(y1)))
+
     def max_batch(self, width: int, height: int) -> int:
         """Largest push_frames batch for this config at width x height."""
         return int(self._lib.evsim_gpu_max_batch(self._h, width, height))
