@@ -58,6 +58,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--chunk", type=int, default=0, help="e2e: frames per streamed chunk (0 = 32)")
+    p.add_argument("--split", default="streams", choices=["streams", "bands"],
+                   help="N>1: one camera stream per rank (weak scaling) or row bands of one stream (strong, c5)")
     p.add_argument("--batch", type=int, default=0,
                    help="frames per push_frames call (0 = the simulator's maximum; 1 = frame-by-frame)")
     return p.parse_args()
@@ -224,10 +226,15 @@ def run_ours(args):
 
     from paper_2209_04634_b200 import SimulatorConfig, Simulator
     from paper_2209_04634_b200._lib import load
-    c, cfg, frames, ts = workload(args, stream=rank)
+    bands = args.split == "bands" and ws > 1
+    c, cfg, frames, ts = workload(args, stream=0 if bands else rank)
     n = len(frames)
     P = c.width * c.height
     sim = Simulator(SimulatorConfig.from_c(cfg), device=device)
+    if bands:
+        # every rank holds the whole frames and emits its own rows
+        from paper_2209_04634_b200.parallel import band_rows
+        sim.set_row_band(*band_rows(c.height, ws, rank))
     stream_ptr = sim.stream
     torch_stream = torch.cuda.ExternalStream(stream_ptr, device=device)
 
@@ -299,7 +306,7 @@ def run_ours(args):
     else:
         ev_all = ev_total
     max_ms = float(t.item())
-    frames_total = ws * n * args.steps
+    frames_total = (1 if bands else ws) * n * args.steps
     value = frames_total / (max_ms / 1e3)
     events_per_s = ev_all * args.steps / (max_ms / 1e3)
 
@@ -385,8 +392,10 @@ def run_ours(args):
             "metric": "simulated input frames/sec (events/sec beside it), % of HBM roofline",
             "value": round(value, 3), "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8/f32/f64", "data": "synthetic",
-            "config": {**config_json(c, args, n), "parallelism": f"streams x{ws}", "frames_per_push": batch},
+            "scaling": "strong" if bands else "weak", "vs_baseline": None, "dtype": "u8/f32/f64",
+            "data": "synthetic",
+            "config": {**config_json(c, args, n), "parallelism": f"row bands x{ws}" if bands else f"streams x{ws}",
+                       "frames_per_push": batch},
             "events_per_s": round(events_per_s, 1), "events_per_frame": round(E_frame, 1),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(),
