@@ -672,6 +672,104 @@ static void sparse_with_flow(const chain_ctx* cx, const uint8_t* prev, const uin
   free(inter); free(inter_t); free(claim_mark); free(claim_change);
 }
 
+/* difference_interp_events  simulate.cpp:212-285: d1 = the previous
+ * interval's difference frame, d2 the newly completed one (t0, t1]. */
+static int cmp_size(const void* a, const void* b) {
+  const size_t x = *(const size_t*)a, y = *(const size_t*)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+static void threshold_diff(const evsim_gpu_config* c, const int16_t* d, int w, int h, int64_t t, evvec* out) {
+  /* threshold_events_into  core.cpp:21-46 */
+  const int magnitude = c->events_per_crossing == EVSIM_EVENTS_MAGNITUDE;
+  for (int y = 0; y < h; ++y) {
+    for (int x = 0; x < w; ++x) {
+      const int v = d[(size_t)y * w + x];
+      if (v > c->c_pos) {
+        const int count = magnitude ? v / c->c_pos : 1;
+        for (int k = 0; k < count; ++k) ev_push(out, (uint16_t)x, (uint16_t)y, t, 1);
+      } else if (v < c->c_neg) {
+        const int count = magnitude ? v / c->c_neg : 1;
+        for (int k = 0; k < count; ++k) ev_push(out, (uint16_t)x, (uint16_t)y, t, -1);
+      }
+    }
+  }
+}
+
+static void diff_interp_events(const evsim_gpu_config* c, int levels, int iters, int radius,
+                               const int16_t* d1, const int16_t* d2, int w, int h, int64_t t0,
+                               int64_t t1, evvec* out) {
+  const size_t P = (size_t)w * h;
+  const int N = c->n_interp;
+  const int magnitude = c->events_per_crossing == EVSIM_EVENTS_MAGNITUDE;
+  /* active_points  simulate.cpp:78-87: scan order */
+  int64_t M = 0;
+  for (size_t i = 0; i < P; ++i) M += (d1[i] > c->c_pos || d1[i] < c->c_neg);
+  if (M > 0 && N > 0) {
+    int32_t* pts = (int32_t*)malloc((size_t)M * 2 * sizeof(int32_t));
+    int16_t* val = (int16_t*)malloc((size_t)M * sizeof(int16_t));
+    int64_t j = 0;
+    for (int y = 0; y < h; ++y)
+      for (int x = 0; x < w; ++x) {
+        const int v = d1[(size_t)y * w + x];
+        if (v > c->c_pos || v < c->c_neg) {
+          pts[2 * j] = x;
+          pts[2 * j + 1] = y;
+          val[j++] = (int16_t)v;
+        }
+      }
+    /* flow on magnitude images min(255, |d|) (simulate.cpp:223-233) */
+    uint8_t* m1 = (uint8_t*)malloc(P);
+    uint8_t* m2 = (uint8_t*)malloc(P);
+    for (size_t i = 0; i < P; ++i) {
+      m1[i] = (uint8_t)imin(255, abs((int)d1[i]));
+      m2[i] = (uint8_t)imin(255, abs((int)d2[i]));
+    }
+    float* disp = (float*)malloc((size_t)M * 2 * sizeof(float));
+    uint8_t* st = (uint8_t*)malloc((size_t)M);
+    evsim_oracle_sparse_flow(m1, m2, w, h, levels, iters, radius, pts, M, disp, st);
+    int* mark = (int*)malloc(P * sizeof(int));
+    int16_t* inter = (int16_t*)malloc(P * sizeof(int16_t));
+    size_t* touched = (size_t*)malloc((size_t)M * sizeof(size_t));
+    for (size_t i = 0; i < P; ++i) mark[i] = -1;
+    for (int k = 1; k <= N; ++k) {
+      const float alpha = (float)k / (float)(N + 1);
+      const int64_t t = sub_interval_end(t0, t1, k, N + 1);
+      int64_t nt = 0;
+      for (int64_t q = 0; q < M; ++q) {
+        if (!st[q]) continue;
+        const int tx = (int)lroundf((float)pts[2 * q] + alpha * disp[2 * q]);
+        const int ty = (int)lroundf((float)pts[2 * q + 1] + alpha * disp[2 * q + 1]);
+        if (tx < 0 || tx >= w || ty < 0 || ty >= h) continue;
+        const size_t idx = (size_t)ty * w + tx;
+        if (mark[idx] != k) {
+          mark[idx] = k;
+          inter[idx] = val[q];
+          touched[nt++] = idx;
+        } else if (abs((int)val[q]) > abs((int)inter[idx])) {
+          inter[idx] = val[q];
+        }
+      }
+      qsort(touched, (size_t)nt, sizeof(size_t), cmp_size);
+      for (int64_t q = 0; q < nt; ++q) {
+        const size_t idx = touched[q];
+        const int v = inter[idx];
+        const uint16_t ex = (uint16_t)(idx % (size_t)w), ey = (uint16_t)(idx / (size_t)w);
+        if (v > c->c_pos) {
+          int count = magnitude ? v / c->c_pos : 1;
+          while (count-- > 0) ev_push(out, ex, ey, t, 1);
+        } else if (v < c->c_neg) {
+          int count = magnitude ? v / c->c_neg : 1;
+          while (count-- > 0) ev_push(out, ex, ey, t, -1);
+        }
+      }
+    }
+    free(pts); free(val); free(m1); free(m2); free(disp); free(st); free(mark); free(inter); free(touched);
+  }
+  if (c->include_endpoints) threshold_diff(c, d2, w, h, t1, out); /* simulate.cpp:278-281 */
+  finalize(out);
+}
+
 /* ------------------------------------------------------------------------ */
 /* Simulator  include/evsim/simulate.hpp:60-94, src/simulate.cpp:306-347     */
 
@@ -683,6 +781,8 @@ struct evsim_oracle_sim {
   int64_t prev_t;
   uint8_t* prev;
   float* ref;
+  int16_t* pdiff; /* difference_interp: the previous interval's difference frame */
+  int has_pdiff;
   float lut[256];
   evvec ev;
 };
@@ -704,6 +804,8 @@ static int validate_cfg(const evsim_gpu_config* c) {
   if (c->c_pos <= 0) return fail(EVSIM_GPU_INVALID_ARGUMENT, "SimulatorConfig: c_pos must be > 0");
   if (c->c_neg >= 0) return fail(EVSIM_GPU_INVALID_ARGUMENT, "SimulatorConfig: c_neg must be < 0");
   if (c->n_interp < 0) return fail(EVSIM_GPU_INVALID_ARGUMENT, "SimulatorConfig: n_interp must be >= 0");
+  if (c->contrast_mode == EVSIM_CONTRAST_LOG && c->method == EVSIM_METHOD_DIFFERENCE_INTERP)
+    return fail(EVSIM_GPU_INVALID_ARGUMENT, "SimulatorConfig: difference_interp has no log contrast mode");
   if (c->contrast_mode == EVSIM_CONTRAST_LOG) {
     if (!(c->c_pos_log > 0.0f)) return fail(EVSIM_GPU_INVALID_ARGUMENT, "SimulatorConfig: c_pos_log must be > 0");
     if (!(c->c_neg_log < 0.0f)) return fail(EVSIM_GPU_INVALID_ARGUMENT, "SimulatorConfig: c_neg_log must be < 0");
@@ -726,11 +828,12 @@ int evsim_oracle_create(const evsim_gpu_config* cfg, evsim_oracle_sim** out) {
 
 void evsim_oracle_destroy(evsim_oracle_sim* s) {
   if (!s) return;
-  free(s->prev); free(s->ref); free(s->ev.v); free(s);
+  free(s->prev); free(s->ref); free(s->pdiff); free(s->ev.v); free(s);
 }
 
 int evsim_oracle_reset(evsim_oracle_sim* s) {
   s->has_prev = 0;
+  s->has_pdiff = 0;
   return 0;
 }
 
@@ -773,8 +876,6 @@ int evsim_oracle_push_frame(evsim_oracle_sim* s, const uint8_t* pixels, int32_t 
     if (t <= s->prev_t)
       return fail(EVSIM_GPU_INVALID_ARGUMENT, "push_frame: timestamps must be strictly increasing");
   }
-  if (s->cfg.method == EVSIM_METHOD_DIFFERENCE_INTERP)
-    return fail(EVSIM_GPU_RUNTIME, "push_frame: difference_interp is outside the B200 hot path");
   const size_t P = (size_t)w * h;
   s->ev.n = 0;
   chain_ctx cx = {&s->cfg, s->lut, s->ref};
@@ -810,6 +911,17 @@ int evsim_oracle_push_frame(evsim_oracle_sim* s, const uint8_t* pixels, int32_t 
           free(disp); free(st);
         }
         free(pts);
+        break;
+      }
+      case EVSIM_METHOD_DIFFERENCE_INTERP: {
+        /* simulate.cpp:334-341: events need the previous difference frame */
+        int16_t* d = (int16_t*)malloc(P * sizeof(int16_t));
+        for (size_t i = 0; i < P; ++i) d[i] = (int16_t)((int)pixels[i] - (int)prev[i]);
+        if (s->has_pdiff)
+          diff_interp_events(&s->cfg, s->levels, s->iters, s->radius, s->pdiff, d, w, h, s->prev_t, t, &s->ev);
+        free(s->pdiff);
+        s->pdiff = d;
+        s->has_pdiff = 1;
         break;
       }
     }

@@ -161,6 +161,8 @@ int evsim_ref_create(const evsim_gpu_config* cfg, evsim_ref_sim** out) {
                                                   std::make_shared<evsim::PyramidalPatchFlow>(p),
                                                   std::make_shared<evsim::PyramidalLucasKanade>(p));
     } else {
+      if (cfg->method == EVSIM_METHOD_DIFFERENCE_INTERP)
+        throw std::invalid_argument("SimulatorConfig: difference_interp has no log contrast mode");
       to_ref(cfg).validate();
       for (int i = 0; i < 256; ++i) s->lut[i] = std::log(static_cast<float>(i) / 255.0f + 1e-3f);
     }

@@ -9,7 +9,8 @@ from ._lib import EvsimError, InvalidArgument  # noqa: F401
 from .simulator import (DenseFlowEstimator, EventStream, FlowField, FlowPreset, Frame,  # noqa: F401
                         PyramidalLucasKanade, PyramidalPatchFlow, SimulatorConfig, Simulator, SparseFlow,
                         SparseFlowEstimator, dense_events_with_flow, estimate_dense_flow, estimate_sparse_flow,
-                        flow_preset, interpolate_frames, push_frames_batched, simulate_dense, simulate_sparse,
+                        flow_preset, interpolate_frames, push_frames_batched, simulate_dense, simulate_difference,
+                        simulate_sparse,
                         sparse_events_with_flow)
 
 __all__ = [
@@ -17,5 +18,5 @@ __all__ = [
     "DenseFlowEstimator", "EventStream", "FlowField", "FlowPreset", "Frame", "PyramidalLucasKanade",
     "PyramidalPatchFlow", "SimulatorConfig", "Simulator", "SparseFlow", "SparseFlowEstimator",
     "dense_events_with_flow", "estimate_dense_flow", "estimate_sparse_flow", "flow_preset", "interpolate_frames",
-    "push_frames_batched", "simulate_dense", "simulate_sparse", "sparse_events_with_flow",
+    "push_frames_batched", "simulate_dense", "simulate_difference", "simulate_sparse", "sparse_events_with_flow",
 ]

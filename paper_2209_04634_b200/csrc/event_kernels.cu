@@ -855,6 +855,161 @@ __global__ void __launch_bounds__(256, 3) chain_sparse_kernel(ChainParams p) {
   for (int i = threadIdx.x; i < G; i += blockDim.x) p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
 }
 
+// ------------------------------------------------------------ difference_interp kernel
+//
+// difference_interp_events (simulate.cpp:212-285) as links: link k = 1..N is
+// the warped difference frame k — the pixels a splat claimed, each carrying
+// the winning signed d1, thresholded directly (no differencing, no state);
+// the optional last link thresholds d2 = curr - prev at the interval end.
+// Links with no claimed pixel in the word are skipped (empty masks).  Pair 0
+// of a launch emits nothing when the stream has no previous difference frame
+// (simulate.cpp:334-341).
+template <bool kMag>
+__global__ void __launch_bounds__(256, 3) chain_diffinterp_kernel(ChainParams p) {
+  constexpr int kW = 2;
+  extern __shared__ uint32_t s_cnt[];  // [G]
+  const int L = p.d.n_links, G = L * p.n_pairs, N = p.n_interp;
+  for (int i = threadIdx.x; i < G; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t P = p.P;
+  const int nint = min(L, N);  // links into warped difference frames
+  const int64_t wbeg = (int64_t)b * p.words_per_block;
+  const int64_t wend = min(wbeg + p.words_per_block, p.n_words);
+  for (int64_t w0 = wbeg + warp; w0 < wend; w0 += kWarpsPerBlock * kW) {
+    DenseWord c[kW];
+#pragma unroll
+    for (int q = 0; q < kW; ++q) {
+      const int64_t wq = w0 + q * kWarpsPerBlock;
+      c[q].have = wq < wend;
+      c[q].wi = (uint32_t)wq;
+      const int64_t ww = c[q].have ? wq : w0;
+      const int row = (int)((uint32_t)ww / (uint32_t)p.wpr);
+      const int x = (int)(ww - (int64_t)row * p.wpr) * 32 + lane;
+      c[q].valid = c[q].have && x < p.w;
+      c[q].x = x < p.w ? x : p.w - 1;
+      c[q].y = p.row0 + row;
+      c[q].pix = (uint32_t)c[q].y * (uint32_t)p.w + (uint32_t)c[q].x;
+    }
+    int sp = p.r0 % p.R;
+    for (int i = 0; i < p.n_pairs; ++i) {
+      const int sc = sp + 1 == p.R ? 0 : sp + 1;
+      const uint8_t* prev = p.frames.at(sp);
+      const uint8_t* curr = p.frames.at(sc);
+      const uint32_t* touched = p.touched + (size_t)i * ((N + 31) >> 5) * P;
+      const int16_t* dvals = p.dvals + (size_t)i * N * P;
+      sp = sc;
+      const int gbase = i * L;
+      const bool skip = p.skip_first && i == 0;
+      uint2 lm[kW];
+      uint32_t lwc[kW], lcnt = 0;
+#pragma unroll
+      for (int q = 0; q < kW; ++q) lm[q] = make_uint2(0u, 0u), lwc[q] = 0u;
+      auto flush = [&](int l) {
+        if ((l & 31) != 31 && l != L - 1) return;
+        if (lane <= (l & 31)) {
+          const int g = gbase + (l & ~31) + lane;
+#pragma unroll
+          for (int q = 0; q < kW; ++q) {
+            if (!c[q].have) continue;
+            p.masks[(size_t)g * p.n_words + c[q].wi] = lm[q];
+            if (kMag) p.wcount[(size_t)g * p.n_words + c[q].wi] = lwc[q];
+          }
+          if (lcnt) atomicAdd(&s_cnt[g], lcnt);
+        }
+        lcnt = 0;
+      };
+      uint32_t tw0[kW], tw1[kW];
+      uint64_t ev64[kW];
+#pragma unroll
+      for (int q = 0; q < kW; ++q) {
+        tw0[q] = (c[q].valid && N > 0 && !skip) ? touched[c[q].pix] : 0u;
+        tw1[q] = (c[q].valid && N > 32 && !skip) ? touched[P + c[q].pix] : 0u;
+        const uint64_t A = ((uint64_t)__reduce_or_sync(kFull, tw1[q]) << 32) | __reduce_or_sync(kFull, tw0[q]);
+        uint64_t e = (N > 64 || L > 64) ? ~0ull : A & (nint >= 64 ? ~0ull : ((1ull << nint) - 1ull));
+        if (nint < L && L <= 64) e |= 1ull << (L - 1);  // the d2 link
+        ev64[q] = skip ? 0ull : e;
+      }
+      auto value = [&](int q, int k) -> int {  // signed value of link k at this lane
+        if (k > N) return (int)curr[c[q].pix] - (int)prev[c[q].pix];
+        const int bit = k - 1;
+        bool t;
+        if (bit < 32) t = (tw0[q] >> bit) & 1u;
+        else if (bit < 64) t = (tw1[q] >> (bit - 32)) & 1u;
+        else t = c[q].valid && ((touched[(size_t)(bit >> 5) * P + c[q].pix] >> (bit & 31)) & 1u);
+        return t ? (int)dvals[(size_t)bit * P + c[q].pix] : 0;
+      };
+      for (int lb = 0; lb < L; lb += 32) {
+        const int nl = min(32, L - lb);
+        uint32_t e32[kW];
+#pragma unroll
+        for (int q = 0; q < kW; ++q) {
+          e32[q] = (uint32_t)(lb < 64 ? ev64[q] >> lb : (skip ? 0ull : ~0ull));
+          if (nl < 32) e32[q] &= (1u << nl) - 1u;
+        }
+        uint32_t todo = e32[0];
+#pragma unroll
+        for (int q = 1; q < kW; ++q) todo |= e32[q];
+        while (todo) {
+          int js[4];
+          int vals[kW][4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            js[m] = todo ? __ffs(todo) - 1 : -1;
+            todo &= todo ? todo - 1 : 0u;
+          }
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int q = 0; q < kW; ++q)
+              vals[q][m] = (js[m] >= 0 && ((e32[q] >> js[m]) & 1u)) ? value(q, lb + js[m] + 1) : 0;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const int j = js[m];
+            if (j < 0) break;
+            const int l = lb + j;
+#pragma unroll
+            for (int q = 0; q < kW; ++q) {
+              if (!((e32[q] >> j) & 1u)) continue;
+              uint32_t ev;
+              float unused_ref = 0.0f;
+              int zero = 0;  // the value is the difference itself (threshold_events_into)
+              const uint2 mk = link_rule<false, kMag>(p, nullptr, gbase + l, c[q], lane, vals[q][m], unused_ref,
+                                                      zero, ev);
+              if (lane == j) {
+                lm[q] = mk;
+                if (kMag) lwc[q] = ev;
+                lcnt += ev;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kW; ++q) {
+          if (!((e32[q] >> lane) & 1u)) {
+            lm[q] = make_uint2(0u, 0u);
+            lwc[q] = 0u;
+          }
+        }
+        flush(lb + nl - 1);
+      }
+      // touched planes back to zero for the next launch
+#pragma unroll
+      for (int q = 0; q < kW; ++q) {
+        if (!c[q].valid || skip) continue;
+        uint32_t* tp = const_cast<uint32_t*>(touched);
+        if (tw0[q]) tp[c[q].pix] = 0u;
+        if (tw1[q]) tp[P + c[q].pix] = 0u;
+        for (int wdx = 2; wdx < ((N + 31) >> 5); ++wdx)
+          if (tp[(size_t)wdx * P + c[q].pix]) tp[(size_t)wdx * P + c[q].pix] = 0u;
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G; i += blockDim.x) p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
+}
+
 // ------------------------------------------------------------ offsets
 // One warp per link row: exclusive prefix of the row's per-block counts and
 // the row total.  Chunks of 32 blocks with a running carry.
@@ -1129,8 +1284,11 @@ __global__ void __launch_bounds__(256) select_mask_kernel(SelectParams p) {
   if (p.log_mode) s_lut[threadIdx.x] = p.lut[threadIdx.x];
   __syncthreads();
   const int z = blockIdx.y;
-  const uint8_t* prev = p.frames.at((p.r0 + z) % p.R);
-  const uint8_t* curr = p.frames.at((p.r0 + z + 1) % p.R);
+  // sparse: (prev, curr) of the pair; difference_interp: (f[r0+z-1], f[r0+z]) = d1
+  const int zoff = p.diff_mode ? -1 : 0;
+  const uint8_t* prev = p.frames.at((p.r0 + z + zoff + p.R) % p.R);
+  const uint8_t* curr = p.frames.at((p.r0 + z + 1 + zoff) % p.R);
+  const bool none = p.diff_mode && p.skip_first && z == 0;
   uint32_t* masks = p.masks + (size_t)z * p.n_words;
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1140,11 +1298,17 @@ __global__ void __launch_bounds__(256) select_mask_kernel(SelectParams p) {
     const int row = (int)((uint32_t)wi / (uint32_t)p.wpr);
     const int x = (int)(wi - (int64_t)row * p.wpr) * 32 + lane;
     bool take = false;
-    if (x < p.w) {
+    if (x < p.w && !none) {
       const size_t i = (size_t)row * p.w + x;
       const int a = prev[i], c = curr[i];
-      if (p.log_mode) take = fabsf(fsub(s_lut[c], s_lut[a])) > p.sel_log;
-      else take = abs(c - a) > p.sel;
+      if (p.diff_mode) {
+        const int d = c - a;
+        take = d > p.c_pos || d < p.c_neg;
+      } else if (p.log_mode) {
+        take = fabsf(fsub(s_lut[c], s_lut[a])) > p.sel_log;
+      } else {
+        take = abs(c - a) > p.sel;
+      }
     }
     const unsigned m = __ballot_sync(kFull, take);
     if (lane == 0) {
@@ -1215,9 +1379,12 @@ __global__ void __launch_bounds__(256) select_emit_kernel(SelectParams p) {
 // index j: an atomicMax on (change << 24) | (2^24 - 1 - j)  (M < 2^24).
 // Target slot, value and claim key of splat item (j, k); false when the
 // point is lost or the target falls outside the frame.
-__device__ __forceinline__ bool splat_item(const SplatParams& p, const uint8_t* prev, const uint32_t* points,
-                                           const float2* disp, const uint8_t* status, int64_t j, int k,
-                                           size_t& slot, int& value, uint32_t& key) {
+// difference_interp (diff_mode): the value is the point's signed d1 =
+// prev[src] - pprev[src] and the claim goes to the largest |d1|
+// (simulate.cpp:248-255), ties to the smallest j as in the sparse rule.
+__device__ __forceinline__ bool splat_item(const SplatParams& p, const uint8_t* prev, const uint8_t* pprev,
+                                           const uint32_t* points, const float2* disp, const uint8_t* status,
+                                           int64_t j, int k, size_t& slot, int& value, uint32_t& key) {
   if (!status[j]) return false;
   const uint32_t src = points[j];
   const int px = (int)(src % (uint32_t)p.w), py = (int)(src / (uint32_t)p.w);
@@ -1227,8 +1394,14 @@ __device__ __forceinline__ bool splat_item(const SplatParams& p, const uint8_t* 
   const int ty = lroundf_ref(fadd((float)py, fmul(alpha, d.y)));
   if (tx < 0 || tx >= p.w || ty < 0 || ty >= p.h) return false;
   const size_t idx = (size_t)ty * p.w + tx;
-  value = prev[src];
-  const int change = abs(value - (int)prev[idx]);
+  int change;
+  if (p.diff_mode) {
+    value = (int)prev[src] - (int)pprev[src];
+    change = abs(value);
+  } else {
+    value = prev[src];
+    change = abs(value - (int)prev[idx]);
+  }
   key = ((uint32_t)change << 24) | (0xFFFFFFu - (uint32_t)j);
   slot = (size_t)(k - 1) * p.P + idx;
   return true;
@@ -1241,6 +1414,7 @@ __global__ void splat_kernel(SplatParams p) {
   const int64_t total = M * N;
   const size_t P = p.P;
   const uint8_t* prev = p.frames.at((p.r0 + z) % p.R);
+  const uint8_t* pprev = p.frames.at((p.r0 + z - 1 + p.R) % p.R);
   const uint32_t* points = p.points + (size_t)z * P;
   const float2* disp = p.disp + (size_t)z * P;
   const uint8_t* status = p.status + (size_t)z * P;
@@ -1253,7 +1427,7 @@ __global__ void splat_kernel(SplatParams p) {
     size_t slot;
     int value;
     uint32_t key;
-    if (!splat_item(p, prev, points, disp, status, j, k, slot, value, key)) continue;
+    if (!splat_item(p, prev, pprev, points, disp, status, j, k, slot, value, key)) continue;
     atomicMax(&claims[slot], key);
     const size_t idx = slot - (size_t)(k - 1) * P;
     atomicOr(&touched[(size_t)((k - 1) >> 5) * P + idx], 1u << ((k - 1) & 31));
@@ -1272,11 +1446,11 @@ __global__ void resolve_kernel(SplatParams p) {
   const int64_t total = M * N;
   const size_t P = p.P;
   const uint8_t* prev = p.frames.at((p.r0 + z) % p.R);
+  const uint8_t* pprev = p.frames.at((p.r0 + z - 1 + p.R) % p.R);
   const uint32_t* points = p.points + (size_t)z * P;
   const float2* disp = p.disp + (size_t)z * P;
   const uint8_t* status = p.status + (size_t)z * P;
   uint32_t* claims = p.claims + (size_t)z * N * P;
-  uint8_t* svals = p.svals + (size_t)z * N * P;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = e / N;
@@ -1284,12 +1458,22 @@ __global__ void resolve_kernel(SplatParams p) {
     size_t slot;
     int value;
     uint32_t key;
-    if (!splat_item(p, prev, points, disp, status, j, k, slot, value, key)) continue;
+    if (!splat_item(p, prev, pprev, points, disp, status, j, k, slot, value, key)) continue;
     if (claims[slot] == key) {
-      svals[slot] = (uint8_t)value;
+      if (p.diff_mode) p.dvals[(size_t)z * N * P + slot] = (int16_t)value;
+      else p.svals[(size_t)z * N * P + slot] = (uint8_t)value;
       claims[slot] = 0u;
     }
   }
+}
+
+// difference_interp's flow images: min(255, |f_j - f_(j-1)|) (simulate.cpp:226-229)
+__global__ void mags_kernel(Ring<const uint8_t> frames, Ring<uint8_t> mags, int R, int slot0, size_t P) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const int slot = (slot0 + (int)blockIdx.y) % R;
+  const int d = (int)frames.at(slot)[i] - (int)frames.at((slot - 1 + R) % R)[i];
+  mags.at(slot)[i] = (uint8_t)min(255, abs(d));
 }
 
 __global__ void init_ref_kernel(const uint8_t* __restrict__ f, const float* __restrict__ lut, float* __restrict__ ref,
@@ -1352,7 +1536,24 @@ static void launch_chain_sparse(const ChainParams& p, size_t sm, cudaStream_t s)
   k<<<p.n_blocks, 256, sm, s>>>(p);
 }
 
+template <bool kMag>
+static void launch_chain_diffinterp(const ChainParams& p, size_t sm, cudaStream_t s) {
+  auto* k = chain_diffinterp_kernel<kMag>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    attr = true;
+  }
+  k<<<p.n_blocks, 256, sm, s>>>(p);
+}
+
 void launch_chain(const ChainParams& p, int provider, cudaStream_t s) {
+  if (provider == kProvDiffInterp) {
+    const size_t sm = (size_t)std::max(p.d.n_links * p.n_pairs, 1) * sizeof(uint32_t);
+    if (p.magnitude) launch_chain_diffinterp<true>(p, sm, s);
+    else launch_chain_diffinterp<false>(p, sm, s);
+    return;
+  }
   if (provider == kProvSparse) {
     const size_t sm = (size_t)std::max(p.d.n_links * p.n_pairs, 1) * sizeof(uint32_t);
     if (p.log_mode) {
@@ -1423,6 +1624,11 @@ void launch_select(const SelectParams& p, int n_pairs, cudaStream_t s) {
 
 void launch_init_ref(const uint8_t* frame, const float* lut, float* ref, int64_t n, cudaStream_t s) {
   init_ref_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(frame, lut, ref, n);
+}
+
+void launch_mags(Ring<const uint8_t> frames, Ring<uint8_t> mags, int R, int slot0, int n, size_t P, cudaStream_t s) {
+  if (n <= 0) return;
+  mags_kernel<<<dim3((unsigned)((P + 255) / 256), n), 256, 0, s>>>(frames, mags, R, slot0, P);
 }
 
 void launch_splat(const SplatParams& p, int max_items, int n_pairs, cudaStream_t s) {

@@ -38,7 +38,7 @@ struct ApiError {
 };
 
 [[noreturn]] void invalid(const std::string& m) { throw ApiError{EVSIM_GPU_INVALID_ARGUMENT, m}; }
-[[noreturn]] void runtime(const std::string& m) { throw ApiError{EVSIM_GPU_RUNTIME, m}; }
+[[noreturn, maybe_unused]] void runtime(const std::string& m) { throw ApiError{EVSIM_GPU_RUNTIME, m}; }
 
 void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw ApiError{EVSIM_GPU_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
@@ -101,6 +101,8 @@ void validate_config(const evsim_gpu_config& c) {
   }
   if (c.method < EVSIM_METHOD_DIFFERENCE_ONLY || c.method > EVSIM_METHOD_DIFFERENCE_INTERP)
     invalid("SimulatorConfig: unknown method");
+  if (c.method == EVSIM_METHOD_DIFFERENCE_INTERP && c.contrast_mode == EVSIM_CONTRAST_LOG)
+    invalid("SimulatorConfig: difference_interp has no log contrast mode");
 }
 
 void log_lut(float* lut) {
@@ -490,6 +492,7 @@ struct evsim_gpu_sim {
 
   // stream state
   bool has_prev = false;
+  int n_seen = 0;  // frames pushed since the stream start (difference_interp needs 2 before it emits)
   int w = 0, h = 0;
   int64_t prev_t = 0;
   int rhead = 0;  // ring slot of the previous frame
@@ -497,11 +500,11 @@ struct evsim_gpu_sim {
   int pair_cap = 0;
   int band_y0 = 0, band_y1 = 0;  // row band of the events (0, 0 = the whole frame)
 
-  DevBuf frames, quads, lut, ref, consts;
+  DevBuf frames, quads, mags, lut, ref, consts;
   FlowEngine flow;
   EventEngine ev;
   // sparse (per pair)
-  DevBuf sel_masks, sel_counts, points, n_points, disp, status, claims, touched, svals;
+  DevBuf sel_masks, sel_counts, points, n_points, disp, status, claims, touched, svals, dvals;
 
   // last result
   int64_t* h_seg_out = nullptr;  // pinned
@@ -575,7 +578,13 @@ struct evsim_gpu_sim {
   int n_interp_eff() const { return cfg.method == EVSIM_METHOD_DIFFERENCE_ONLY ? 0 : cfg.n_interp; }
   bool dense_flow() const { return cfg.method == EVSIM_METHOD_DENSE && n_interp_eff() > 0; }
   bool sparse_flow() const { return cfg.method == EVSIM_METHOD_SPARSE && n_interp_eff() > 0; }
-  bool uses_flow() const { return dense_flow() || sparse_flow(); }
+  bool diff_interp() const { return cfg.method == EVSIM_METHOD_DIFFERENCE_INTERP; }
+  bool di_flow() const { return diff_interp() && n_interp_eff() > 0; }
+  bool splats() const { return sparse_flow() || di_flow(); }  // point selection + sparse LK + splat
+  bool uses_flow() const { return dense_flow() || splats(); }
+  // frames a push keeps besides its own: prev, and for difference_interp the
+  // frame before it (the previous difference frame, simulate.cpp:334-341)
+  int kept_frames() const { return diff_interp() ? 2 : 1; }
   bool log_mode() const { return cfg.contrast_mode == EVSIM_CONTRAST_LOG; }
   bool magnitude() const { return cfg.events_per_crossing == EVSIM_EVENTS_MAGNITUDE; }
 
@@ -583,6 +592,8 @@ struct evsim_gpu_sim {
   ChainDesc desc() const {
     const int N = n_interp_eff();
     if (cfg.method == EVSIM_METHOD_DIFFERENCE_ONLY) return ChainDesc{0, 1, 1};
+    // difference_interp: warped difference frames 1..N, then d2 (endpoints)
+    if (diff_interp()) return ChainDesc{0, 1, N + (cfg.include_endpoints ? 1 : 0)};
     if (N == 0) return ChainDesc{0, 1, cfg.include_endpoints ? 1 : 0};
     if (cfg.include_endpoints) return ChainDesc{0, 1, N + 1};
     return ChainDesc{1, 1, std::max(0, N - 1)};
@@ -598,7 +609,7 @@ struct evsim_gpu_sim {
     rhead = 0;
     const bool band = band_y1 > 0;
     if (uses_flow()) {
-      flow.setup(w, h, preset, sparse_flow(), stream);
+      flow.setup(w, h, preset, splats(), stream);
       if (band && dense_flow()) flow.plan_band(band_y0, band_y1);
     }
     if (log_mode()) ref.ensure((size_t)w * h * sizeof(float), stream);
@@ -635,15 +646,21 @@ struct evsim_gpu_sim {
     CK(cudaStreamSynchronize(stream));
   }
 
-  // room for `pairs` pairs in one launch: ring of pairs + 1 frame slots
+  // room for `pairs` pairs in one launch: ring of pairs + kept_frames() slots
   void ensure_capacity(int pairs) {
     const size_t P = (size_t)w * h;
-    const int need_R = pairs + 1;
+    const int keep = kept_frames();
+    const int need_R = pairs + keep;
     if (need_R > R) {
-      // grow the ring; the previous frame (and its pyramid) moves to slot 0
+      // grow the ring; the kept frames move to slots 0 .. keep-1 (prev last)
+      const int have = std::min(n_seen, keep);  // kept frames that exist
       DevBuf nf;
       nf.ensure((size_t)need_R * P + 16, stream);
-      if (has_prev) CK(cudaMemcpyAsync(nf.p, frames.as<uint8_t>() + (size_t)rhead * P, P, cudaMemcpyDeviceToDevice, stream));
+      for (int j = 0; j < have; ++j) {
+        const int src = (rhead - (have - 1 - j) + R) % std::max(R, 1);
+        CK(cudaMemcpyAsync(nf.as<uint8_t>() + (size_t)(keep - have + j) * P, frames.as<uint8_t>() + (size_t)src * P,
+                           P, cudaMemcpyDeviceToDevice, stream));
+      }
       std::swap(frames.p, nf.p);
       std::swap(frames.n, nf.n);
       std::swap(frames.s, nf.s);
@@ -651,31 +668,42 @@ struct evsim_gpu_sim {
         DevBuf nq;
         nq.ensure((size_t)need_R * P * 4, stream);
         if (has_prev)
-          CK(cudaMemcpyAsync(nq.p, quads.as<uint32_t>() + (size_t)rhead * P, P * 4, cudaMemcpyDeviceToDevice, stream));
+          CK(cudaMemcpyAsync(nq.as<uint32_t>() + (size_t)(keep - 1) * P, quads.as<uint32_t>() + (size_t)rhead * P,
+                             P * 4, cudaMemcpyDeviceToDevice, stream));
         std::swap(quads.p, nq.p);
         std::swap(quads.n, nq.n);
         std::swap(quads.s, nq.s);
       }
+      if (diff_interp()) {
+        DevBuf nm;
+        nm.ensure((size_t)need_R * P + 16, stream);
+        if (n_seen >= 2)
+          CK(cudaMemcpyAsync(nm.as<uint8_t>() + (size_t)(keep - 1) * P, mags.as<uint8_t>() + (size_t)rhead * P, P,
+                             cudaMemcpyDeviceToDevice, stream));
+        std::swap(mags.p, nm.p);
+        std::swap(mags.n, nm.n);
+        std::swap(mags.s, nm.s);
+      }
       if (uses_flow()) {
-        // pyramid of prev: rebuilt from the frame below (cheap, exact)
+        // pyramid of prev (difference_interp: of prev's difference magnitude)
+        // rebuilt from the image below (cheap, exact)
         flow.ensure(need_R, std::max(pairs, 1), stream);
       }
-      const int old_head = rhead;
-      rhead = 0;
+      rhead = keep - 1;
       R = need_R;
-      if (uses_flow() && has_prev) {
-        PyramidParams pp = flow.pyramid_params(frames.as<uint8_t>(), P, dense_flow() ? quads.as<uint32_t>() : nullptr, 0);
+      if (uses_flow() && has_prev && (!diff_interp() || n_seen >= 2)) {
+        const uint8_t* src = diff_interp() ? mags.as<uint8_t>() : frames.as<uint8_t>();
+        PyramidParams pp = flow.pyramid_params(src, P, dense_flow() ? quads.as<uint32_t>() : nullptr, rhead);
         launch_pyramid(pp, 1, stream);
         CK_LAUNCH("pyramid");
       }
-      (void)old_head;
     }
     if (pairs > pair_cap) {
       if (uses_flow()) flow.ensure(R, pairs, stream);
       const int L = desc().n_links;
       const int64_t cap = magnitude() ? 0 : (int64_t)std::max(L, 1) * pairs * (int64_t)P;
       ev.ensure(L * pairs, magnitude(), std::max<int64_t>(cap, ev.capacity), stream);
-      if (sparse_flow()) {
+      if (splats()) {
         const int N = n_interp_eff();
         sel_masks.ensure((size_t)pairs * ev.n_words * 4, stream);
         sel_counts.ensure((size_t)pairs * ev.n_blocks * 4, stream);
@@ -685,8 +713,13 @@ struct evsim_gpu_sim {
         status.ensure((size_t)pairs * P, stream);
         claims.release();
         claims.ensure((size_t)pairs * N * P * 4, stream, true);
-        svals.release();
-        svals.ensure((size_t)pairs * N * P, stream);
+        if (diff_interp()) {
+          dvals.release();
+          dvals.ensure((size_t)pairs * N * P * 2, stream);
+        } else {
+          svals.release();
+          svals.ensure((size_t)pairs * N * P, stream);
+        }
         touched.release();
         touched.ensure((size_t)pairs * ((N + 31) / 32) * P * 4, stream, true);
       }
@@ -863,11 +896,28 @@ struct evsim_gpu_sim {
     if (uploaded) CK(cudaStreamWaitEvent(stream, uploaded, 0));
     else upload(pixels, F, base, on_device, stream);
     mark(EVSIM_STAGE_PYRAMID);
-    if (uses_flow()) {
+    if (diff_interp()) {
+      // difference magnitudes of the new frames that have a predecessor, and
+      // (for the sparse solver) their pyramids
+      const int j0 = n_seen == 0 ? 1 : 0;
+      const int slot0 = (base + j0) % R;
+      if (F - j0 > 0) {
+        launch_mags(Ring<const uint8_t>{frames.as<uint8_t>(), P}, Ring<uint8_t>{mags.as<uint8_t>(), P}, R, slot0,
+                    F - j0, P, stream);
+        CK_LAUNCH("mags");
+        ++launches;
+        if (uses_flow()) {
+          PyramidParams pp = flow.pyramid_params(mags.as<uint8_t>(), P, nullptr, slot0);
+          launch_pyramid(pp, F - j0, stream);
+          CK_LAUNCH("pyramid");
+          launches += 2 * flow.levels;
+        }
+      }
+    } else if (uses_flow()) {
       PyramidParams pp = flow.pyramid_params(frames.as<uint8_t>(), P, dense_flow() ? quads.as<uint32_t>() : nullptr, base);
       launch_pyramid(pp, F, stream);
       CK_LAUNCH("pyramid");
-      launches += flow.levels;
+      launches += flow.levels * (splats() ? 2 : 1);
     }
     if (!has_prev && log_mode()) {
       // warm-up frame: ref := L(frame0)
@@ -895,6 +945,12 @@ struct evsim_gpu_sim {
       } else if (sparse_flow()) {
         sparse_stage(r0, n_pairs, c);
         provider = kProvSparse;
+      } else if (diff_interp()) {
+        // difference_interp_events (simulate.cpp:212-285); pair 0 has no
+        // previous difference frame while the stream holds < 2 frames
+        c.skip_first = n_seen < 2;
+        if (di_flow()) sparse_stage(r0, n_pairs, c);
+        provider = kProvDiffInterp;
       }
       mark(EVSIM_STAGE_CHAIN);
       run_events(c, provider, pts.data(), h_seg, continue_call);
@@ -910,6 +966,7 @@ struct evsim_gpu_sim {
     rhead = (base + F - 1) % R;
     prev_t = ts[F - 1];
     has_prev = true;
+    n_seen += F;
   }
 
   // ---- streamed push: host frames in, host events out ---------------------
@@ -1053,6 +1110,10 @@ struct evsim_gpu_sim {
     sp.sel = cfg.selection_threshold > 0 ? cfg.selection_threshold : cfg.c_pos;  // types.hpp:122-124
     sp.sel_log = cfg.sel_log > 0.0f ? cfg.sel_log : cfg.c_pos_log;
     sp.lut = lut.as<float>();
+    sp.diff_mode = diff_interp();
+    sp.c_pos = cfg.c_pos;
+    sp.c_neg = cfg.c_neg;
+    sp.skip_first = c.skip_first;
     sp.masks = sel_masks.as<uint32_t>();
     sp.counts = sel_counts.as<uint32_t>();
     sp.points = points.as<uint32_t>();
@@ -1091,9 +1152,12 @@ struct evsim_gpu_sim {
     spl.touched = touched.as<uint32_t>();
     spl.P = P;
     spl.svals = svals.as<uint8_t>();
+    spl.diff_mode = diff_interp();
+    spl.dvals = dvals.as<int16_t>();
     launch_splat(spl, (int)std::min<int64_t>((int64_t)P * N, INT32_MAX), n_pairs, stream);
     CK_LAUNCH("splat");
     c.svals = svals.as<uint8_t>();
+    c.dvals = dvals.as<int16_t>();
     c.claims = claims.as<uint32_t>();
     c.touched = touched.as<uint32_t>();
     c.points = points.as<uint32_t>();
@@ -1207,8 +1271,6 @@ int evsim_gpu_create(const evsim_gpu_config* cfg, int device, evsim_gpu_sim** ou
   return guarded([&] {
     if (!cfg || !out) invalid("evsim_gpu_create: null argument");
     validate_config(*cfg);
-    if (cfg->method == EVSIM_METHOD_DIFFERENCE_INTERP)
-      runtime("evsim_gpu_create: difference_interp is outside the B200 hot path (SURVEY.md §8f)");
     validate_preset(resolve_preset(*cfg));
     int n = 0;
     CK(cudaGetDeviceCount(&n));
@@ -1359,6 +1421,7 @@ int evsim_gpu_reset(evsim_gpu_sim* sim) {
     sim->finish();
     // Simulator::reset  include/evsim/simulate.hpp:83-86
     sim->has_prev = false;
+    sim->n_seen = 0;
     sim->n_events = 0;
     sim->seg_t.clear();
     sim->seg_off.assign(1, 0);

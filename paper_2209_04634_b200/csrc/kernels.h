@@ -88,7 +88,7 @@ struct SparseLKParams {
 };
 
 // ---------------------------------------------------------------- chain
-enum ProviderKind { kProvNone = 0, kProvDenseGrid = 1, kProvDenseField = 2, kProvSparse = 3 };
+enum ProviderKind { kProvNone = 0, kProvDenseGrid = 1, kProvDenseField = 2, kProvSparse = 3, kProvDiffInterp = 4 };
 
 // Chain frame c (c = 0..n_links) of every pair is frame index start + c*step
 // (0 = prev, 1..N interpolated, N+1 = curr).
@@ -145,6 +145,8 @@ struct ChainParams {
   uint32_t* claims;        // [pair][N][P] keys (change << 24 | ~j)
   uint32_t* touched;       // [pair][ceil(N/32)][P] bits
   const uint8_t* svals;    // [pair][N][P] winning splat values (valid where touched)
+  const int16_t* dvals;    // difference_interp: [pair][N][P] winning signed differences
+  int skip_first;          // difference_interp: pair 0 has no previous difference frame
   const uint32_t* points;  // [pair][P]
   const int* n_points;     // [pair]
   size_t P;
@@ -206,6 +208,9 @@ struct SelectParams {
   int sel;
   float sel_log;
   const float* lut;
+  int diff_mode;          // difference_interp: active points of d1 = f[r0+z] - f[r0+z-1]
+  int c_pos, c_neg;       //   (simulate.cpp:78-87)
+  int skip_first;         //   pair 0 has no d1: selects nothing
   uint32_t* masks;        // [pair][n_words]
   uint32_t* counts;       // [pair][n_blocks]
   uint32_t* points;       // [pair][P]
@@ -225,6 +230,8 @@ struct SplatParams {
   uint32_t* claims;        // [pair][N][P]
   uint32_t* touched;       // [pair][ceil(N/32)][P]
   uint8_t* svals;          // [pair][N][P]
+  int diff_mode;           // difference_interp: signed d1 values, claims by |d1|
+  int16_t* dvals;          // [pair][N][P] (difference_interp)
   size_t P;
 };
 
@@ -240,6 +247,8 @@ void launch_offsets(const OffsetParams& p, cudaStream_t s);
 void launch_emit(const EmitParams& p, int64_t* segbase, cudaStream_t s);
 void launch_select(const SelectParams& p, int n_pairs, cudaStream_t s);
 void launch_init_ref(const uint8_t* frame, const float* lut, float* ref, int64_t n, cudaStream_t s);
+// mags[slot] = min(255, |f[slot] - f[slot-1]|) for n consecutive ring slots from slot0
+void launch_mags(Ring<const uint8_t> frames, Ring<uint8_t> mags, int R, int slot0, int n, size_t P, cudaStream_t s);
 void launch_sparse_lk(const SparseLKParams& p, int max_points, int n_pairs, cudaStream_t s);
 void launch_splat(const SplatParams& p, int max_items, int n_pairs, cudaStream_t s);
 void launch_unpack_events(const uint32_t* packed, const int64_t* seg_out, int64_t n, void* out24,

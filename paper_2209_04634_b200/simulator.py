@@ -358,6 +358,24 @@ def simulate_sparse(prev: Frame, curr: Frame, config: SimulatorConfig,
     return sparse_events_with_flow(prev, curr, estimator.estimate(prev, curr, pts), config)
 
 
+def simulate_difference(f0: Frame, f1: Frame, f2: Frame, config: SimulatorConfig,
+                        estimator: Optional[SparseFlowEstimator] = None) -> EventStream:
+    """simulate_difference (simulate.cpp:287-301): the difference_interp events
+    of (f1, f2] from the difference frames f1 - f0 and f2 - f1."""
+    config.validate()
+    _check_pair(f0, f1, "simulate_difference", empty_check=False)
+    _check_pair(f1, f2, "simulate_difference", empty_check=False)
+    if not (f0.timestamp < f1.timestamp < f2.timestamp):
+        raise InvalidArgument(1, "simulate_difference: timestamps must be strictly increasing")
+    if estimator is not None and not (isinstance(estimator, PyramidalLucasKanade)
+                                      and estimator.preset == config.preset()):
+        raise InvalidArgument(1, "simulate_difference: custom sparse estimators are not supported on the GPU path")
+    sim = Simulator(dataclasses.replace(config, method=Method.difference_interp))
+    sim.push_frame(f0)
+    sim.push_frame(f1)
+    return sim.push_frame(f2)
+
+
 # --------------------------------------------------------------------------- Simulator
 
 class Simulator:
@@ -377,6 +395,8 @@ class Simulator:
         self._config = dataclasses.replace(config)
         self._custom = (dense_flow is not None and not isinstance(dense_flow, PyramidalPatchFlow)) or \
                        (sparse_flow is not None and not isinstance(sparse_flow, PyramidalLucasKanade))
+        if self._custom and Method(config.method) == Method.difference_interp:
+            raise InvalidArgument(1, "Simulator: custom flow estimators are not supported for difference_interp")
         self._dense, self._sparse = dense_flow, sparse_flow
         self._lib = _lib.load()
         self._h = _vp()

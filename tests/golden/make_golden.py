@@ -113,7 +113,21 @@ def main():
                       events_per_crossing=1)
     out["log_dense_mag"] = dict(frames=frames, ts=ts, **cfg_arrays(cfg), **run_stream(R, cfg, frames, ts))
 
+    # 7. difference_interp (simulate.cpp:212-285, 334-341): sparse LK on the
+    # magnitude of consecutive difference frames, signed splats, thresholded
+    frames, ts = R.moving_disk(96, 72, 6, 6.0, 5.0, 100.0, 60, 220, 3)
+    cfg = make_config(Method.difference_interp)
+    out["diffinterp_disk"] = dict(frames=frames, ts=ts, **cfg_arrays(cfg), **run_stream(R, cfg, frames, ts))
+    cfg = make_config(Method.difference_interp, n_interp=4, c_pos=6, c_neg=-6, events_per_crossing=1)
+    out["diffinterp_disk_mag"] = dict(frames=frames, ts=ts, **cfg_arrays(cfg), **run_stream(R, cfg, frames, ts))
+    frames, ts = R.panning_texture(70, 52, 5, 2, -1, 20.0, 23)
+    cfg = make_config(Method.difference_interp, n_interp=6, c_pos=8, c_neg=-8, include_endpoints=0)
+    out["diffinterp_pan_noend"] = dict(frames=frames, ts=ts, **cfg_arrays(cfg), **run_stream(R, cfg, frames, ts))
+
+    only = sys.argv[1] if len(sys.argv) > 1 else ""
     for name, d in out.items():
+        if not name.startswith(only):
+            continue
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
         print(name, {k: v.shape for k, v in d.items() if hasattr(v, "shape") and v.ndim > 0 and v.size > 1})
 

@@ -13,7 +13,7 @@ from paper_2209_04634_b200.abi import Method, make_config
 
 def _cfgs():
     out = []
-    for m in (Method.difference_only, Method.dense, Method.sparse):
+    for m in (Method.difference_only, Method.dense, Method.sparse, Method.difference_interp):
         for mag in (0, 1):
             for incl in (1, 0):
                 for q in (0, 1):
@@ -24,7 +24,8 @@ def _cfgs():
 @pytest.mark.parametrize("m,mag,incl,q", _cfgs())
 def test_stream_linear_random_configs(oracle, reference, m, mag, incl, q):
     rng = np.random.default_rng(int(m) * 100 + mag * 10 + incl * 3 + q)
-    frames, ts = reference.panning_texture(53, 37, 3, int(rng.integers(-3, 4)), int(rng.integers(-2, 3)), 20.0,
+    frames, ts = reference.panning_texture(53, 37, 4 if m == Method.difference_interp else 3,
+                                           int(rng.integers(-3, 4)), int(rng.integers(-2, 3)), 20.0,
                                            int(rng.integers(1, 1000)))
     n = int(rng.integers(0, 7))
     cfg = make_config(m, n_interp=n, events_per_crossing=mag, include_endpoints=incl, flow_preset=q,
@@ -32,6 +33,15 @@ def test_stream_linear_random_configs(oracle, reference, m, mag, incl, q):
     so, sr = oracle.simulator(cfg), reference.simulator(cfg)
     for k in range(len(frames)):
         assert_same_events(so.push_frame(frames[k], ts[k]), sr.push_frame(frames[k], ts[k]), f"frame {k}")
+
+
+def test_difference_interp_moving_disk(oracle, reference):
+    frames, ts = reference.moving_disk(80, 64, 6, 7.0, 4.0, 60.0, 40, 230, 8)
+    for n in (0, 1, 5):
+        cfg = make_config(Method.difference_interp, n_interp=n, c_pos=10, c_neg=-10)
+        so, sr = oracle.simulator(cfg), reference.simulator(cfg)
+        for k in range(len(frames)):
+            assert_same_events(so.push_frame(frames[k], ts[k]), sr.push_frame(frames[k], ts[k]), f"N={n} frame {k}")
 
 
 @pytest.mark.parametrize("m", [Method.difference_only, Method.dense, Method.sparse])
