@@ -340,6 +340,8 @@ class Simulator {
       : config_(config), dense_(std::move(dense_flow)), sparse_(std::move(sparse_flow)) {
     config_.validate();
     if (!dense_ || !sparse_) throw std::invalid_argument("Simulator: flow estimators must not be null");
+    if (config_.method == Method::difference_interp)
+      throw std::invalid_argument("Simulator: custom flow estimators are not supported for difference_interp");
   }
 
   EventStream push_frame(const Frame& frame) {
@@ -380,6 +382,12 @@ class Simulator {
       all.append(collect(ev));
     }
     return all;
+  }
+
+  // Row band (evsim_gpu_set_row_band): emit only rows [y0, y1); stream start only.
+  void set_row_band(int y0, int y1) {
+    if (!h_) throw std::invalid_argument("set_row_band: not available with custom flow estimators");
+    detail::check(evsim_gpu_set_row_band(h_.get(), y0, y1));
   }
 
   const SimulatorConfig& config() const { return config_; }
@@ -437,5 +445,22 @@ class Simulator {
   std::shared_ptr<const SparseFlowEstimator> sparse_;
   std::unique_ptr<Frame> prev_;
 };
+
+// simulate_difference (simulate.hpp:48-55, simulate.cpp:287-301): the
+// difference_interp events of (f1, f2] from f1 - f0 and f2 - f1.
+inline EventStream simulate_difference(const Frame& f0, const Frame& f1, const Frame& f2,
+                                       const SimulatorConfig& config) {
+  config.validate();
+  if (f0.width != f1.width || f0.height != f1.height || f1.width != f2.width || f1.height != f2.height)
+    throw std::invalid_argument("simulate_difference: incompatible input frames");
+  if (!(f0.timestamp < f1.timestamp && f1.timestamp < f2.timestamp))
+    throw std::invalid_argument("simulate_difference: timestamps must be strictly increasing");
+  SimulatorConfig c = config;
+  c.method = Method::difference_interp;
+  Simulator sim(c);
+  sim.push_frame(f0);
+  sim.push_frame(f1);
+  return sim.push_frame(f2);
+}
 
 }  // namespace evsim_b200

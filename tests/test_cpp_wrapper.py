@@ -32,7 +32,8 @@ def test_cpp_header_compiles_and_host_semantics(binary):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("method,mode", [(Method.dense, 1), (Method.sparse, 0), (Method.difference_only, 1)])
+@pytest.mark.parametrize("method,mode", [(Method.dense, 1), (Method.sparse, 0), (Method.difference_only, 1),
+                                         (Method.difference_interp, 0)])
 def test_cpp_push_parity(binary, oracle, tmp_path, method, mode):
     from paper_2209_04634_b200 import scenes
     frames, ts = scenes.generate("c2", n_frames=5, width=120, height=90)
