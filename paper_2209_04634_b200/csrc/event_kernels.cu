@@ -178,6 +178,21 @@ __device__ __forceinline__ int frame_value(const ChainParams& p, const Prov& pro
   return prov.interp(p, pc, c, k);
 }
 
+// Position of the (r+1)-th set bit of m (r >= 0, r < popc(m)): a branch-free
+// binary search on popcounts.
+__device__ __forceinline__ int nth_set_bit(uint32_t m, int r) {
+  int pos = 0;
+  int c = __popc(m & 0xFFFFu);
+  if (r >= c) r -= c, m >>= 16, pos += 16;
+  c = __popc(m & 0xFFu);
+  if (r >= c) r -= c, m >>= 8, pos += 8;
+  c = __popc(m & 0xFu);
+  if (r >= c) r -= c, m >>= 4, pos += 4;
+  c = __popc(m & 0x3u);
+  if (r >= c) r -= c, m >>= 2, pos += 2;
+  return pos + (r >= (int)(m & 1u) ? 1 : 0);
+}
+
 __device__ __forceinline__ uint32_t pack_event(int x, int y, bool neg) {
   return (uint32_t)x | ((uint32_t)y << 16) | (neg ? 0x80000000u : 0u);
 }
@@ -1167,10 +1182,14 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
         if (lane >= o) incl += y;
       }
       const int T = __shfl_sync(kFull, incl, 31);
+      const int excl = incl - c;
       const uint32_t wi = (uint32_t)(wbeg + j);
       const int lrow = (int)(wi / (uint32_t)p.wpr);
       const int x0 = (int)(wi - (uint32_t)lrow * (uint32_t)p.wpr) * 32;
-      const int row = p.row0 + lrow;
+      // per word: output address of its slot 0 relative to the warp's slots,
+      // and its (x0, row) in one word (x < 2^16, row < 2^15)
+      const long long base = (long long)dst - excl;
+      const uint32_t xr = (uint32_t)x0 | ((uint32_t)(p.row0 + lrow) << 16);
       for (int q = lane; q - lane < T; q += 32) {
         // first lane l with incl[l] > q
         int lo = 0;
@@ -1180,17 +1199,14 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
           if (probe <= q) lo += step;
         }
         const int src = lo < 31 ? lo : 31;
-        const int src_incl = __shfl_sync(kFull, incl, src);
-        const int src_cnt = __shfl_sync(kFull, c, src);
+        const int sexcl = __shfl_sync(kFull, excl, src);
         const uint32_t m = __shfl_sync(kFull, all, src);
         const uint32_t pm = __shfl_sync(kFull, pos, src);
-        const long long d = __shfl_sync(kFull, (long long)dst, src);
-        const int sx0 = __shfl_sync(kFull, x0, src);
-        const int srow = __shfl_sync(kFull, row, src);
+        const long long sb = __shfl_sync(kFull, base, src);
+        const uint32_t sxr = __shfl_sync(kFull, xr, src);
         if (q < T) {
-          const int r = q - (src_incl - src_cnt);
-          const int bit = __fns(m, 0, r + 1);
-          p.out[d + r] = pack_event(sx0 + bit, srow, !((pm >> bit) & 1u));
+          const int bit = nth_set_bit(m, q - sexcl);
+          p.out[sb + q] = (sxr + (uint32_t)bit) | (((pm >> bit) & 1u) ? 0u : 0x80000000u);
         }
       }
     }
