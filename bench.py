@@ -54,6 +54,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c2")
     p.add_argument("--mode", default="log", choices=["log", "linear"])
+    p.add_argument("--preset", default="lq", choices=["lq", "hq"], help="flow preset (types.hpp:93: lq default)")
     p.add_argument("--frames", type=int, default=0, help="override sequence length")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -80,17 +81,19 @@ def workload(args, stream=0):
     frames, ts = scenes.generate(c, n_frames=n, stream=stream)
     cp, cn = scenes.LINEAR_THRESHOLDS[c.method]
     cfg = make_config(Method[c.method], n_interp=c.n_interp, c_pos=cp, c_neg=cn,
-                      contrast_mode=1 if args.mode == "log" else 0, c_pos_log=c.contrast, c_neg_log=-c.contrast)
+                      contrast_mode=1 if args.mode == "log" else 0, c_pos_log=c.contrast, c_neg_log=-c.contrast,
+                      flow_preset=1 if getattr(args, "preset", "lq") == "hq" else 0)
     return c, cfg, frames, ts
 
 
 def config_json(c, args, n_frames):
     return {
-        "workload": f"{c.name}: {c.width}x{c.height} u8, {c.method} (LK lq) N={c.n_interp}, "
+        "workload": f"{c.name}: {c.width}x{c.height} u8, {c.method} (LK {args.preset}) N={c.n_interp}, "
                     f"{args.mode} C={c.contrast if args.mode == 'log' else 'int Table I'}, "
                     f"{n_frames}-frame seeded synthetic sequence",
         "width": c.width, "height": c.height, "frames_per_step": n_frames, "n_interp": c.n_interp,
-        "method": c.method, "mode": args.mode, "flow_preset": "low_quality",
+        "method": c.method, "mode": args.mode,
+        "flow_preset": "high_quality" if args.preset == "hq" else "low_quality",
         "l2": "flushed before every step (256 MiB memset); device-resident inputs",
     }
 
