@@ -1485,11 +1485,12 @@ __global__ void resolve_kernel(SplatParams p) {
 
 // difference_interp's flow images: min(255, |f_j - f_(j-1)|) (simulate.cpp:226-229)
 __global__ void mags_kernel(Ring<const uint8_t> frames, Ring<uint8_t> mags, int R, int slot0, size_t P) {
-  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P) return;
   const int slot = (slot0 + (int)blockIdx.y) % R;
-  const int d = (int)frames.at(slot)[i] - (int)frames.at((slot - 1 + R) % R)[i];
-  mags.at(slot)[i] = (uint8_t)min(255, abs(d));
+  const uint8_t* a = frames.at((slot - 1 + R) % R);
+  const uint8_t* b = frames.at(slot);
+  uint8_t* m = mags.at(slot);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (size_t)gridDim.x * blockDim.x)
+    m[i] = (uint8_t)min(255, abs((int)b[i] - (int)a[i]));
 }
 
 __global__ void init_ref_kernel(const uint8_t* __restrict__ f, const float* __restrict__ lut, float* __restrict__ ref,
@@ -1644,7 +1645,8 @@ void launch_init_ref(const uint8_t* frame, const float* lut, float* ref, int64_t
 
 void launch_mags(Ring<const uint8_t> frames, Ring<uint8_t> mags, int R, int slot0, int n, size_t P, cudaStream_t s) {
   if (n <= 0) return;
-  mags_kernel<<<dim3((unsigned)((P + 255) / 256), n), 256, 0, s>>>(frames, mags, R, slot0, P);
+  const unsigned bx = (unsigned)std::min<size_t>((P + 255) / 256, (148 * 8 + n - 1) / n);
+  mags_kernel<<<dim3(std::max(bx, 1u), n), 256, 0, s>>>(frames, mags, R, slot0, P);
 }
 
 void launch_splat(const SplatParams& p, int max_items, int n_pairs, cudaStream_t s) {

@@ -211,6 +211,9 @@ struct FlowEngine {
   DevBuf qpyr[kMaxLevels];    // float4 quad images (4 bilinear taps per pixel), R slots
   DevBuf tex[kMaxLevels];     // sparse: float4 (value, gx, gy, 0) per pixel, R slots
   bool texels = false;
+  // dense with the warp-form solver at level 0: level 0 is read from the u8
+  // frame / quad rings, so its fp32 image and float4 quads are not written
+  bool u8_level0 = false;
   DevBuf tables[kMaxLevels];  // cx | cy | ix | wx | iy | wy
   DevBuf grid[kMaxLevels];    // per pair: pu | pv
   GridGeom geom[kMaxLevels]{};
@@ -351,6 +354,7 @@ struct FlowEngine {
       p.qpyr[l] = Ring<float4>{qpyr[l].as<float4>(), pl};
       p.tex[l] = Ring<float4>{texels ? tex[l].as<float4>() : nullptr, pl};
     }
+    p.u8_level0 = u8_level0 && quad_u8 != nullptr;
     p.frames = Ring<const uint8_t>{frames, P};
     p.quad_u8 = Ring<uint32_t>{quad_u8, P};
     p.R = R;
@@ -360,9 +364,15 @@ struct FlowEngine {
 
   // estimate_dense_flow's level loop, flow.cpp:268-275, for n_pairs pairs;
   // result = per-pair level-0 patch grids
-  int solve(int r0, int n_pairs, cudaStream_t s) {
+  // frames8 / quads8: the u8 frame and u8 quad rings (level 0 when u8_level0)
+  int solve(int r0, int n_pairs, const uint8_t* frames8, const uint32_t* quads8, cudaStream_t s) {
     for (int l = levels - 1; l >= 0; --l) {
       DenseLKParams p{};
+      if (l == 0 && u8_level0) {
+        p.u8 = 1;
+        p.prev8 = Ring<const uint8_t>{frames8, (size_t)w * h};
+        p.qcurr8 = Ring<const uint32_t>{quads8, (size_t)w * h};
+      }
       p.g = geom[l];
       p.has_coarse = l != levels - 1;
       if (p.has_coarse) p.coarse = geom[l + 1];
@@ -610,6 +620,10 @@ struct evsim_gpu_sim {
     const bool band = band_y1 > 0;
     if (uses_flow()) {
       flow.setup(w, h, preset, splats(), stream);
+      {
+        const int r = preset.radius;
+        flow.u8_level0 = dense_flow() && (r == 4 || r == 6) && w > 2 * r + 1 && h > 2 * r + 1;
+      }
       if (band && dense_flow()) flow.plan_band(band_y0, band_y1);
     }
     if (log_mode()) ref.ensure((size_t)w * h * sizeof(float), stream);
@@ -939,7 +953,7 @@ struct evsim_gpu_sim {
       int provider = kProvNone;
       if (dense_flow()) {
         // simulate_dense -> PyramidalPatchFlow -> dense_events_with_flow (simulate.cpp:130-143)
-        launches += flow.solve(r0, n_pairs, stream);
+        launches += flow.solve(r0, n_pairs, frames.as<uint8_t>(), quads.as<uint32_t>(), stream);
         c.g0 = flow.geom[0];
         provider = kProvDenseGrid;
       } else if (sparse_flow()) {
@@ -1528,7 +1542,7 @@ int evsim_gpu_dense_flow(const uint8_t* prev, const uint8_t* curr, int32_t w, in
     cfg.patch_radius = radius;
     Scratch s(cfg, w, h, prev, curr);
     s.pyramids();
-    s->flow.solve(0, 1, s->stream);
+    s->flow.solve(0, 1, s->frames.as<uint8_t>(), s->quads.as<uint32_t>(), s->stream);
     DevBuf field;
     field.ensure((size_t)w * h * 8, s->stream);
     launch_densify(s->flow.geom[0], field.as<float>(), field.as<float>() + (size_t)w * h, s->stream);

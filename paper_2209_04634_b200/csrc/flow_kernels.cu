@@ -19,39 +19,56 @@ namespace evsim_gpu {
 // replicate clamp — so a bilinear sample is one 16-byte gather.  Level 0 also
 // writes the u8 quad used by sample_u8 in the interpolation.
 __device__ __forceinline__ float level_value(const uint8_t* __restrict__ f0, const float* __restrict__ src,
-                                             LevelDims sd, int x, int y, bool level0) {
+                                             LevelDims sd, int x, int y, bool level0, bool from_u8) {
   if (level0) return (float)f0[(size_t)y * sd.w + x];
   // downsample  flow.cpp:30-42: 0.25f * (((a + b) + c) + d), odd edges replicate
   const int x0 = 2 * x, y0 = 2 * y;
   const int x1 = min(2 * x + 1, sd.w - 1);
   const int y1 = min(2 * y + 1, sd.h - 1);
+  if (from_u8) {  // level 1 straight from the u8 frame (level 0 = to_float of it)
+    const uint8_t* r0 = f0 + (size_t)y0 * sd.w;
+    const uint8_t* r1 = f0 + (size_t)y1 * sd.w;
+    return fmul(0.25f, fadd(fadd(fadd((float)r0[x0], (float)r0[x1]), (float)r1[x0]), (float)r1[x1]));
+  }
   const float* r0 = src + (size_t)y0 * sd.w;
   const float* r1 = src + (size_t)y1 * sd.w;
   return fmul(0.25f, fadd(fadd(fadd(r0[x0], r0[x1]), r1[x0]), r1[x1]));
 }
 
+constexpr int kPyrRows = 8;  // rows per block: fewer, longer-lived blocks (block launch rate bound)
+
 __global__ void pyramid_level_kernel(PyramidParams p, int l) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y;
   const LevelDims dd = p.dims[l];
   if (x >= dd.w) return;
   const int slot = (p.slot0 + (int)blockIdx.z) % p.R;
   const bool level0 = l == 0;
+  // u8_level0: level 0 lives only as the u8 frame / quad (the dense solver
+  // reads those); level 1 downsamples the bytes directly
+  const bool from_u8 = l == 1 && p.u8_level0;
   const uint8_t* f0 = p.frames.at(slot);
-  const float* src = level0 ? nullptr : p.pyr[l - 1].at(slot);
-  const int x1 = min(x + 1, dd.w - 1), y1 = min(y + 1, dd.h - 1);
+  const float* src = (level0 || from_u8) ? nullptr : p.pyr[l - 1].at(slot);
+  const int x1 = min(x + 1, dd.w - 1);
   // level-0 reads the u8 frame at the level's own coordinates
   const LevelDims rd = level0 ? dd : p.dims[l - 1];
-  const float a00 = level_value(f0, src, rd, x, y, level0);
-  const float a10 = level_value(f0, src, rd, x1, y, level0);
-  const float a01 = level_value(f0, src, rd, x, y1, level0);
-  const float a11 = level_value(f0, src, rd, x1, y1, level0);
-  const size_t i = (size_t)y * dd.w + x;
-  p.pyr[l].at(slot)[i] = a00;
-  p.qpyr[l].at(slot)[i] = make_float4(a00, a10, a01, a11);
-  if (level0 && p.quad_u8.base) {
-    p.quad_u8.at(slot)[i] =
-        (uint32_t)a00 | ((uint32_t)a10 << 8) | ((uint32_t)a01 << 16) | ((uint32_t)a11 << 24);
+  float* pyr = p.pyr[l].at(slot);
+  float4* qpyr = p.qpyr[l].at(slot);
+  uint32_t* qu8 = (level0 && p.quad_u8.base) ? p.quad_u8.at(slot) : nullptr;
+  const int yb = blockIdx.y * kPyrRows, ye = min(yb + kPyrRows, dd.h);
+  float a00 = level_value(f0, src, rd, x, yb, level0, from_u8);
+  float a10 = level_value(f0, src, rd, x1, yb, level0, from_u8);
+  for (int y = yb; y < ye; ++y) {
+    const int y1 = min(y + 1, dd.h - 1);
+    const float a01 = level_value(f0, src, rd, x, y1, level0, from_u8);
+    const float a11 = level_value(f0, src, rd, x1, y1, level0, from_u8);
+    const size_t i = (size_t)y * dd.w + x;
+    if (!(level0 && p.u8_level0)) {
+      pyr[i] = a00;
+      qpyr[i] = make_float4(a00, a10, a01, a11);
+    }
+    if (qu8) qu8[i] = (uint32_t)a00 | ((uint32_t)a10 << 8) | ((uint32_t)a01 << 16) | ((uint32_t)a11 << 24);
+    a00 = a01;  // the next row's top taps are this row's bottom taps
+    a10 = a11;
   }
 }
 
@@ -73,15 +90,18 @@ __global__ void build_quad_kernel(const uint8_t* __restrict__ src, uint32_t* __r
 // (gradients, flow.cpp:60-73), so a bilinear sample of all three is 4 loads.
 __global__ void texel_kernel(PyramidParams p, int l) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y;
   const LevelDims d = p.dims[l];
   if (x >= d.w) return;
   const int slot = (p.slot0 + (int)blockIdx.z) % p.R;
   const float* im = p.pyr[l].at(slot);
-  const float* r = im + (size_t)y * d.w;
-  const float gx = fmul(0.5f, fsub(r[min(x + 1, d.w - 1)], r[max(x - 1, 0)]));
-  const float gy = fmul(0.5f, fsub(im[(size_t)min(y + 1, d.h - 1) * d.w + x], im[(size_t)max(y - 1, 0) * d.w + x]));
-  p.tex[l].at(slot)[(size_t)y * d.w + x] = make_float4(r[x], gx, gy, 0.0f);
+  float4* tex = p.tex[l].at(slot);
+  const int yb = blockIdx.y * kPyrRows, ye = min(yb + kPyrRows, d.h);
+  for (int y = yb; y < ye; ++y) {
+    const float* r = im + (size_t)y * d.w;
+    const float gx = fmul(0.5f, fsub(r[min(x + 1, d.w - 1)], r[max(x - 1, 0)]));
+    const float gy = fmul(0.5f, fsub(im[(size_t)min(y + 1, d.h - 1) * d.w + x], im[(size_t)max(y - 1, 0) * d.w + x]));
+    tex[(size_t)y * d.w + x] = make_float4(r[x], gx, gy, 0.0f);
+  }
 }
 
 // sample() (flow.cpp:45-57) through a quad image: one 16-byte gather.
@@ -400,7 +420,7 @@ struct LKWarp {
 };
 static_assert(kLKThreads == 32 * kLKTileY, "one warp per tile row");
 
-template <int kR>
+template <int kR, bool kU8>
 __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams p) {
   using G = LKWarp<kR>;
   constexpr int D = G::D, P2 = G::P2, RPG = G::RPG, NG = G::NG, kPW = G::kPW, pitch = G::pitch;
@@ -412,8 +432,12 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
   GridGeom coarse = p.coarse;
   coarse.pu += z * coarse.pair_stride;
   coarse.pv += z * coarse.pair_stride;
-  const float* __restrict__ prev = p.prev.at((p.r0 + z) % p.R);
-  const float4* __restrict__ qcurr = p.qcurr.at((p.r0 + z + 1) % p.R);
+  // kU8 (level 0 of the dense path): prev = the u8 frame, curr = its u8 quad
+  // image — exactly the values to_float / the float quad would hold
+  const float* __restrict__ prev = kU8 ? nullptr : p.prev.at((p.r0 + z) % p.R);
+  const float4* __restrict__ qcurr = kU8 ? nullptr : p.qcurr.at((p.r0 + z + 1) % p.R);
+  const uint8_t* __restrict__ prev8 = kU8 ? p.prev8.at((p.r0 + z) % p.R) : nullptr;
+  const uint32_t* __restrict__ qcurr8 = kU8 ? p.qcurr8.at((p.r0 + z + 1) % p.R) : nullptr;
   const int w = g.w, h = g.h;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int i0 = blockIdx.x * kLKTileX, j0 = p.jt0 + blockIdx.y * kLKTileY;
@@ -429,8 +453,11 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
   float2* sY = sX + kPW * D;                                                        // [kPW][D] (y0*w, fy)
 
   for (int yy = warp; yy < rh; yy += kLKTileY) {
-    const float* src = prev + (size_t)clampi(ry0 + yy, 0, h - 1) * w;
-    for (int xx = lane; xx < rw; xx += 32) sP[yy * pitch + xx] = __ldg(src + clampi(rx0 + xx, 0, w - 1));
+    const size_t roff = (size_t)clampi(ry0 + yy, 0, h - 1) * w;
+    for (int xx = lane; xx < rw; xx += 32) {
+      const int sx = clampi(rx0 + xx, 0, w - 1);
+      sP[yy * pitch + xx] = kU8 ? u8f(__ldg(prev8 + roff + sx)) : __ldg(prev + roff + sx);
+    }
   }
   // this lane's patch: pl = lane & 7 of tile row `warp` (all four 8-lane parts agree)
   const int pl = lane & 7, part = lane >> 3;
@@ -518,7 +545,13 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
           const float2 Y = sY[j * D + (oy < D ? oy : 0)];
           fx[jj] = X.y;
           fy[jj] = Y.y;
-          q[jj] = __ldg(qcurr + (__float_as_int(Y.x) + __float_as_int(X.x)));
+          const int qi = __float_as_int(Y.x) + __float_as_int(X.x);
+          if (kU8) {
+            const uint32_t v = __ldg(qcurr8 + qi);
+            q[jj] = make_float4(byte_f<0>(v), byte_f<1>(v), byte_f<2>(v), byte_f<3>(v));
+          } else {
+            q[jj] = __ldg(qcurr + qi);
+          }
         }
 #pragma unroll
         for (int jj = 0; jj < kJB; ++jj) {
@@ -745,7 +778,7 @@ __global__ void __launch_bounds__(128) sparse_lk_kernel(SparseLKParams p) {
 void launch_pyramid(const PyramidParams& p, int n_frames, cudaStream_t s) {
   if (n_frames <= 0) return;
   for (int l = 0; l < p.levels; ++l) {
-    dim3 g((p.dims[l].w + 127) / 128, p.dims[l].h, n_frames);
+    dim3 g((p.dims[l].w + 127) / 128, (p.dims[l].h + kPyrRows - 1) / kPyrRows, n_frames);
     pyramid_level_kernel<<<g, 128, 0, s>>>(p, l);
     if (p.tex[l].base) texel_kernel<<<g, 128, 0, s>>>(p, l);
   }
@@ -764,16 +797,25 @@ void launch_dense_lk(const DenseLKParams& p, int n_pairs, cudaStream_t s) {
   const size_t sm = dense_lk_smem(r);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(dense_lk_warp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(dense_lk_warp_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(dense_lk_warp_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(dense_lk_warp_kernel<6, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(dense_lk_warp_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(dense_lk_warp_kernel<6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(dense_lk_tile_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(dense_lk_tile_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(dense_lk_tile_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
   const bool inside = p.g.w > 2 * r + 1 && p.g.h > 2 * r + 1;  // no template clamping
-  if (r == 4 && inside) dense_lk_warp_kernel<4><<<grid, kLKThreads, LKWarp<4>::floats * sizeof(float), s>>>(p);
-  else if (r == 6 && inside) dense_lk_warp_kernel<6><<<grid, kLKThreads, LKWarp<6>::floats * sizeof(float), s>>>(p);
+  if (p.u8 && !((r == 4 || r == 6) && inside)) return;  // host guarantees the warp form for u8 levels
+  if (r == 4 && inside && p.u8)
+    dense_lk_warp_kernel<4, true><<<grid, kLKThreads, LKWarp<4>::floats * sizeof(float), s>>>(p);
+  else if (r == 6 && inside && p.u8)
+    dense_lk_warp_kernel<6, true><<<grid, kLKThreads, LKWarp<6>::floats * sizeof(float), s>>>(p);
+  else if (r == 4 && inside)
+    dense_lk_warp_kernel<4, false><<<grid, kLKThreads, LKWarp<4>::floats * sizeof(float), s>>>(p);
+  else if (r == 6 && inside)
+    dense_lk_warp_kernel<6, false><<<grid, kLKThreads, LKWarp<6>::floats * sizeof(float), s>>>(p);
   else if (r == 4) dense_lk_tile_kernel<4><<<grid, kLKThreads, sm, s>>>(p);
   else if (r == 6) dense_lk_tile_kernel<6><<<grid, kLKThreads, sm, s>>>(p);
   else if (sm <= 200 * 1024) dense_lk_tile_kernel<0><<<grid, kLKThreads, sm, s>>>(p);

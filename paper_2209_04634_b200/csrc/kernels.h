@@ -40,6 +40,7 @@ struct PyramidParams {
   Ring<float4> qpyr[kMaxLevels];
   Ring<uint32_t> quad_u8;   // base may be null (no interpolation)
   Ring<float4> tex[kMaxLevels];  // sparse: per pixel (value, gx, gy, 0); base may be null
+  int u8_level0;            // level 0 not materialised as fp32 (dense: the solver reads the u8 frame / quad)
   int R, slot0;             // frame j of this launch is slot (slot0 + j) % R
 };
 
@@ -66,6 +67,9 @@ struct DenseLKParams {
   int has_coarse;
   Ring<const float> prev; // level images
   Ring<const float4> qcurr;
+  int u8;                  // level 0 from the u8 frame ring / u8 quad ring instead
+  Ring<const uint8_t> prev8;
+  Ring<const uint32_t> qcurr8;
   int R, r0;              // pair z: prev slot (r0+z)%R, curr slot (r0+z+1)%R
   int radius;
   int iterations;
