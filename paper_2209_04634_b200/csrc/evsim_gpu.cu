@@ -924,14 +924,14 @@ struct evsim_gpu_sim {
           PyramidParams pp = flow.pyramid_params(mags.as<uint8_t>(), P, nullptr, slot0);
           launch_pyramid(pp, F - j0, stream);
           CK_LAUNCH("pyramid");
-          launches += 2 * flow.levels;
+          launches += flow.levels;
         }
       }
     } else if (uses_flow()) {
       PyramidParams pp = flow.pyramid_params(frames.as<uint8_t>(), P, dense_flow() ? quads.as<uint32_t>() : nullptr, base);
       launch_pyramid(pp, F, stream);
       CK_LAUNCH("pyramid");
-      launches += flow.levels * (splats() ? 2 : 1);
+      launches += flow.levels;
     }
     if (!has_prev && log_mode()) {
       // warm-up frame: ref := L(frame0)

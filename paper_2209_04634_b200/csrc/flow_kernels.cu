@@ -55,8 +55,14 @@ __global__ void pyramid_level_kernel(PyramidParams p, int l) {
   float4* qpyr = p.qpyr[l].at(slot);
   uint32_t* qu8 = (level0 && p.quad_u8.base) ? p.quad_u8.at(slot) : nullptr;
   const int yb = blockIdx.y * kPyrRows, ye = min(yb + kPyrRows, dd.h);
+  // sparse: the template texels (value, gx, gy) of this level come out of
+  // the same pass — gradients (flow.cpp:60-73) from the row above / below and
+  // the left / right neighbours, all replicate-clamped
+  float4* tex = p.tex[l].base ? p.tex[l].at(slot) : nullptr;
+  const int xm = max(x - 1, 0);
   float a00 = level_value(f0, src, rd, x, yb, level0, from_u8);
   float a10 = level_value(f0, src, rd, x1, yb, level0, from_u8);
+  float up = tex ? level_value(f0, src, rd, x, max(yb - 1, 0), level0, from_u8) : 0.0f;
   for (int y = yb; y < ye; ++y) {
     const int y1 = min(y + 1, dd.h - 1);
     const float a01 = level_value(f0, src, rd, x, y1, level0, from_u8);
@@ -67,6 +73,11 @@ __global__ void pyramid_level_kernel(PyramidParams p, int l) {
       qpyr[i] = make_float4(a00, a10, a01, a11);
     }
     if (qu8) qu8[i] = (uint32_t)a00 | ((uint32_t)a10 << 8) | ((uint32_t)a01 << 16) | ((uint32_t)a11 << 24);
+    if (tex) {
+      const float left = level_value(f0, src, rd, xm, y, level0, from_u8);
+      tex[i] = make_float4(a00, fmul(0.5f, fsub(a10, left)), fmul(0.5f, fsub(a01, up)), 0.0f);
+      up = a00;
+    }
     a00 = a01;  // the next row's top taps are this row's bottom taps
     a10 = a11;
   }
@@ -83,25 +94,6 @@ __global__ void build_quad_kernel(const uint8_t* __restrict__ src, uint32_t* __r
   const uint8_t* r1 = src + (size_t)y1 * w;
   dst[(size_t)y * w + x] = (uint32_t)r0[x] | ((uint32_t)r0[x1] << 8) | ((uint32_t)r1[x] << 16) |
                            ((uint32_t)r1[x1] << 24);
-}
-
-// Template texels of one level for the sparse solver: (value, gx, gy, 0) per
-// pixel, gx / gy the reference's central differences with replicate borders
-// (gradients, flow.cpp:60-73), so a bilinear sample of all three is 4 loads.
-__global__ void texel_kernel(PyramidParams p, int l) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const LevelDims d = p.dims[l];
-  if (x >= d.w) return;
-  const int slot = (p.slot0 + (int)blockIdx.z) % p.R;
-  const float* im = p.pyr[l].at(slot);
-  float4* tex = p.tex[l].at(slot);
-  const int yb = blockIdx.y * kPyrRows, ye = min(yb + kPyrRows, d.h);
-  for (int y = yb; y < ye; ++y) {
-    const float* r = im + (size_t)y * d.w;
-    const float gx = fmul(0.5f, fsub(r[min(x + 1, d.w - 1)], r[max(x - 1, 0)]));
-    const float gy = fmul(0.5f, fsub(im[(size_t)min(y + 1, d.h - 1) * d.w + x], im[(size_t)max(y - 1, 0) * d.w + x]));
-    tex[(size_t)y * d.w + x] = make_float4(r[x], gx, gy, 0.0f);
-  }
 }
 
 // sample() (flow.cpp:45-57) through a quad image: one 16-byte gather.
@@ -780,7 +772,6 @@ void launch_pyramid(const PyramidParams& p, int n_frames, cudaStream_t s) {
   for (int l = 0; l < p.levels; ++l) {
     dim3 g((p.dims[l].w + 127) / 128, (p.dims[l].h + kPyrRows - 1) / kPyrRows, n_frames);
     pyramid_level_kernel<<<g, 128, 0, s>>>(p, l);
-    if (p.tex[l].base) texel_kernel<<<g, 128, 0, s>>>(p, l);
   }
 }
 
