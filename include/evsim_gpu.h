@@ -196,9 +196,36 @@ EVSIM_GPU_API int evsim_gpu_push_frame_async(evsim_gpu_sim* sim, const uint8_t* 
 EVSIM_GPU_API int evsim_gpu_sync(evsim_gpu_sim* sim, evsim_gpu_events* out);
 
 /* Copy the last push's events to host memory.
- * format 0: packed u32 records (4 B each); format 1: evsim_event (24 B).
+ * format 0: packed u32 records (4 B each); format 1: evsim_event (24 B);
+ * format 2: .evs records (13 B each: x u16, y u16, t u64, p i8, little
+ * endian; src/io.cpp:158-165), formatted on the device.
  * capacity is in records; returns INVALID_ARGUMENT if too small. */
 EVSIM_GPU_API int evsim_gpu_copy_events(evsim_gpu_sim* sim, void* host_dst, int64_t capacity, int32_t format);
+
+/* ---- data formats either side of the path ------------- */
+/* load_frames' pixel path (src/io.cpp:41-103): n_frames frames of w x h with
+ * `channels` (1 gray, 3 RGB) -> luma_bt601 -> resize_bilinear to tw x th
+ * ((0, 0) or (w, h) = no resize) -> dst (n_frames * tw * th bytes); host
+ * buffers.  Errors as the reference ("resize_bilinear: target must be
+ * positive"). */
+EVSIM_GPU_API int evsim_gpu_ingest_frames(const uint8_t* src, int32_t channels, int32_t width, int32_t height,
+                                          int32_t n_frames, int32_t target_width, int32_t target_height,
+                                          uint8_t* dst);
+/* write_events_binary / write_events_text (src/io.cpp:105-170) of the last
+ * push's events; records formatted on the device.  I/O errors return
+ * RUNTIME with the reference's message ("'<path>': cannot open for
+ * writing"). */
+EVSIM_GPU_API int evsim_gpu_write_events_binary(evsim_gpu_sim* sim, const char* path);
+EVSIM_GPU_API int evsim_gpu_write_events_text(evsim_gpu_sim* sim, const char* path);
+/* events_per_pixel_second (src/metrics.cpp:7-39): per-pixel counts on the
+ * device, the fp64 reduction in the reference's pixel order on the host. */
+EVSIM_GPU_API int evsim_gpu_events_per_pixel_second(const evsim_event* events, int64_t n, int32_t width,
+                                                    int32_t height, double duration, double* mean_rate,
+                                                    double* std_rate, uint64_t* total_events);
+/* accumulate (src/metrics.cpp:41-69): PixelClass per pixel (0 none,
+ * 1 positive, 2 negative, 3 both) over [t_start, t_end). */
+EVSIM_GPU_API int evsim_gpu_accumulate(const evsim_event* events, int64_t n, int32_t width, int32_t height,
+                                       int64_t t_start, int64_t t_end, uint8_t* classes);
 
 /* CUDA stream (cudaStream_t) the handle enqueues on, for event timing. */
 EVSIM_GPU_API void* evsim_gpu_stream(evsim_gpu_sim* sim);

@@ -252,3 +252,50 @@ class Reference(_Lib):
                                                           _i32(x0), _i32(y0), _i32(dx), _i32(dy),
                                                           ctypes.c_double(fps), _ptr(out), _ptr(ts)))
         return out, ts
+
+    # ---- frame ingestion, event files, metrics (src/io.cpp, src/metrics.cpp) --
+    def luma(self, rgb: np.ndarray) -> np.ndarray:
+        rgb = np.ascontiguousarray(rgb, np.uint8).reshape(-1, 3)
+        f = self.lib.evsim_ref_luma_bt601
+        f.restype = ctypes.c_uint8
+        return np.array([f(ctypes.c_uint8(r), ctypes.c_uint8(g), ctypes.c_uint8(b)) for r, g, b in rgb], np.uint8)
+
+    def resize_bilinear(self, frame: np.ndarray, tw: int, th: int) -> np.ndarray:
+        h, w = frame.shape
+        out = np.zeros((th, tw), np.uint8)
+        self._check(self.lib.evsim_ref_resize_bilinear(_ptr(np.ascontiguousarray(frame, np.uint8)), _i32(w),
+                                                       _i32(h), _i32(tw), _i32(th), _ptr(out)))
+        return out
+
+    @staticmethod
+    def _ev24(events: np.ndarray) -> np.ndarray:
+        from paper_2209_04634_b200.abi import EVENT_DTYPE
+        out = np.zeros(len(events), EVENT_DTYPE)
+        for k in ("x", "y", "t", "p"):
+            out[k] = events[k]
+        return out
+
+    def write_events_binary(self, events: np.ndarray, w: int, h: int, path: str) -> None:
+        ev = self._ev24(events)
+        self._check(self.lib.evsim_ref_write_events_binary(_ptr(ev), _i64(len(ev)), _i32(w), _i32(h),
+                                                           path.encode()))
+
+    def write_events_text(self, events: np.ndarray, w: int, h: int, path: str) -> None:
+        ev = self._ev24(events)
+        self._check(self.lib.evsim_ref_write_events_text(_ptr(ev), _i64(len(ev)), _i32(w), _i32(h), path.encode()))
+
+    def events_per_pixel_second(self, events: np.ndarray, w: int, h: int, duration: float):
+        ev = self._ev24(events)
+        out = np.zeros(3, np.float64)
+        tot = ctypes.c_uint64()
+        self._check(self.lib.evsim_ref_events_per_pixel_second(_ptr(ev), _i64(len(ev)), _i32(w), _i32(h),
+                                                               ctypes.c_double(duration), _ptr(out),
+                                                               ctypes.byref(tot)))
+        return float(out[0]), float(out[1]), float(out[2]), int(tot.value)
+
+    def accumulate(self, events: np.ndarray, w: int, h: int, t0: int, t1: int) -> np.ndarray:
+        ev = self._ev24(events)
+        out = np.zeros((h, w), np.uint8)
+        self._check(self.lib.evsim_ref_accumulate(_ptr(ev), _i64(len(ev)), _i32(w), _i32(h), _i64(t0), _i64(t1),
+                                                  _ptr(out)))
+        return out

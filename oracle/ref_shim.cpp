@@ -22,6 +22,8 @@
 #include <vector>
 
 #include "evsim/flow.hpp"
+#include "evsim/io.hpp"
+#include "evsim/metrics.hpp"
 #include "evsim/scenes.hpp"
 #include "evsim/simulate.hpp"
 
@@ -353,6 +355,57 @@ int evsim_ref_translating_square(int32_t w, int32_t h, int32_t n, int32_t size, 
                                  int32_t dx, int32_t dy, double fps, uint8_t* out, int64_t* ts) {
   return guarded([&] {
     copy_frames(evsim::scenes::translating_square(w, h, n, size, x0, y0, dx, dy, fps), out, ts);
+  });
+}
+
+}  // extern "C"
+
+// ---- frame ingestion, event files, metrics (io.cpp, metrics.cpp) ----------
+namespace {
+evsim::EventStream make_stream(const evsim_event* ev, int64_t n, int w, int h) {
+  evsim::EventStream s{w, h, {}};
+  s.events.resize(static_cast<std::size_t>(n));
+  if (n) std::memcpy(s.events.data(), ev, static_cast<std::size_t>(n) * sizeof(evsim_event));
+  return s;
+}
+}  // namespace
+
+extern "C" {
+
+uint8_t evsim_ref_luma_bt601(uint8_t r, uint8_t g, uint8_t b) { return evsim::luma_bt601(r, g, b); }
+
+int evsim_ref_resize_bilinear(const uint8_t* src, int32_t w, int32_t h, int32_t tw, int32_t th, uint8_t* dst) {
+  return guarded([&] {
+    const evsim::Frame f = make_frame(src, w, h, 0);
+    const evsim::Frame r = evsim::resize_bilinear(f, tw, th);
+    std::memcpy(dst, r.pixels.data(), r.pixels.size());
+  });
+}
+
+int evsim_ref_write_events_binary(const evsim_event* ev, int64_t n, int32_t w, int32_t h, const char* path) {
+  return guarded([&] { evsim::write_events_binary(make_stream(ev, n, w, h), path); });
+}
+
+int evsim_ref_write_events_text(const evsim_event* ev, int64_t n, int32_t w, int32_t h, const char* path) {
+  return guarded([&] { evsim::write_events_text(make_stream(ev, n, w, h), path); });
+}
+
+int evsim_ref_events_per_pixel_second(const evsim_event* ev, int64_t n, int32_t w, int32_t h, double duration,
+                                      double* out3, uint64_t* total) {
+  return guarded([&] {
+    const evsim::EventRateStats st = evsim::events_per_pixel_second(make_stream(ev, n, w, h), duration);
+    out3[0] = st.mean_rate;
+    out3[1] = st.std_rate;
+    out3[2] = st.duration;
+    *total = st.total_events;
+  });
+}
+
+int evsim_ref_accumulate(const evsim_event* ev, int64_t n, int32_t w, int32_t h, int64_t t0, int64_t t1,
+                         uint8_t* classes) {
+  return guarded([&] {
+    const evsim::AccumulatedFrame a = evsim::accumulate(make_stream(ev, n, w, h), t0, t1);
+    std::memcpy(classes, a.classes.data(), a.classes.size());
   });
 }
 

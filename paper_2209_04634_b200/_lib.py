@@ -35,6 +35,13 @@ _SIGS = {
     "evsim_gpu_push_frames_streamed": (
         ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _i32, _vp, _i64, ctypes.POINTER(CEvents)]),
     "evsim_gpu_max_batch": (ctypes.c_int, [_vp, _i32, _i32]),
+    "evsim_gpu_ingest_frames": (ctypes.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp]),
+    "evsim_gpu_write_events_binary": (ctypes.c_int, [_vp, ctypes.c_char_p]),
+    "evsim_gpu_write_events_text": (ctypes.c_int, [_vp, ctypes.c_char_p]),
+    "evsim_gpu_events_per_pixel_second": (
+        ctypes.c_int, [_vp, _i64, _i32, _i32, ctypes.c_double, ctypes.POINTER(ctypes.c_double),
+                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]),
+    "evsim_gpu_accumulate": (ctypes.c_int, [_vp, _i64, _i32, _i32, _i64, _i64, _vp]),
     "evsim_gpu_set_row_band": (ctypes.c_int, [_vp, _i32, _i32]),
     "evsim_gpu_sync": (ctypes.c_int, [_vp, ctypes.POINTER(CEvents)]),
     "evsim_gpu_copy_events": (ctypes.c_int, [_vp, _vp, _i64, _i32]),

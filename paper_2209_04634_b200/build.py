@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libevsim_gpu.so")
-SOURCES = ["evsim_gpu.cu", "flow_kernels.cu", "event_kernels.cu"]
+SOURCES = ["evsim_gpu.cu", "flow_kernels.cu", "event_kernels.cu", "io_kernels.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -1419,10 +1419,191 @@ int evsim_gpu_copy_events(evsim_gpu_sim* sim, void* host_dst, int64_t capacity, 
       CK_LAUNCH("unpack");
       CK(cudaMemcpyAsync(host_dst, tmp.p, (size_t)n * 24, cudaMemcpyDeviceToHost, sim->stream));
       CK(cudaStreamSynchronize(sim->stream));
+    } else if (format == 2) {
+      DevBuf tmp;
+      tmp.ensure((size_t)n * 13, sim->stream);
+      launch_evs_records(sim->ev.events.as<uint32_t>(), sim->ev.seg_out.as<int64_t>(), n, tmp.as<uint8_t>(),
+                         sim->stream);
+      CK_LAUNCH("evs");
+      CK(cudaMemcpyAsync(host_dst, tmp.p, (size_t)n * 13, cudaMemcpyDeviceToHost, sim->stream));
+      CK(cudaStreamSynchronize(sim->stream));
     } else {
       invalid("evsim_gpu_copy_events: unknown format");
     }
     CK(cudaStreamSynchronize(sim->stream));
+  });
+}
+
+// ---- data formats either side of the path ------------------
+
+namespace {
+struct TmpStream {
+  cudaStream_t s = nullptr;
+  TmpStream() { CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  ~TmpStream() {
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+};
+[[noreturn]] void io_fail(const std::string& path, const std::string& what) {
+  throw ApiError{EVSIM_GPU_RUNTIME, "'" + path + "': " + what};
+}
+}  // namespace
+
+int evsim_gpu_ingest_frames(const uint8_t* src, int32_t channels, int32_t w, int32_t h, int32_t n_frames,
+                            int32_t tw, int32_t th, uint8_t* dst) {
+  return guarded([&] {
+    if (!src || !dst || w <= 0 || h <= 0 || n_frames < 0) invalid("ingest_frames: malformed input");
+    if (channels != 1 && channels != 3) invalid("ingest_frames: channels must be 1 or 3");
+    const bool resize = !(tw == 0 && th == 0) && (tw != w || th != h);
+    if (resize && (tw <= 0 || th <= 0)) invalid("resize_bilinear: target must be positive");  // io.cpp:46-48
+    if (n_frames == 0) return;
+    CK(cudaSetDevice(0));
+    init_pool(0);
+    TmpStream ts;
+    const size_t P = (size_t)w * h, Q = resize ? (size_t)tw * th : P;
+    DevBuf in, gray, out;
+    in.ensure((size_t)n_frames * P * channels, ts.s);
+    CK(cudaMemcpyAsync(in.p, src, (size_t)n_frames * P * channels, cudaMemcpyHostToDevice, ts.s));
+    const uint8_t* g = in.as<uint8_t>();
+    if (channels == 3) {  // load_frames: luma of every pixel (io.cpp:86-90)
+      gray.ensure((size_t)n_frames * P, ts.s);
+      launch_luma(in.as<uint8_t>(), gray.as<uint8_t>(), (int64_t)(n_frames * P), ts.s);
+      CK_LAUNCH("luma");
+      g = gray.as<uint8_t>();
+    }
+    if (resize) {  // then resize_bilinear to the target (io.cpp:92-95)
+      out.ensure((size_t)n_frames * Q, ts.s);
+      launch_resize(g, w, h, out.as<uint8_t>(), tw, th, n_frames, ts.s);
+      CK_LAUNCH("resize");
+      g = out.as<uint8_t>();
+    }
+    CK(cudaMemcpyAsync(dst, g, (size_t)n_frames * Q, cudaMemcpyDeviceToHost, ts.s));
+    CK(cudaStreamSynchronize(ts.s));
+  });
+}
+
+int evsim_gpu_write_events_binary(evsim_gpu_sim* sim, const char* path) {
+  return guarded([&] {
+    if (!sim || !path) invalid("write_events_binary: null argument");
+    CK(cudaSetDevice(sim->device));
+    sim->finish();
+    const int64_t n = sim->n_events;
+    std::vector<uint8_t> buf(16 + (size_t)n * 13);
+    std::memcpy(buf.data(), "EVS1", 4);  // io.cpp:152-156
+    const uint16_t w16 = (uint16_t)sim->w, h16 = (uint16_t)sim->h;
+    const uint64_t cnt = (uint64_t)n;
+    for (int b = 0; b < 2; ++b) buf[4 + b] = (uint8_t)(w16 >> (8 * b)), buf[6 + b] = (uint8_t)(h16 >> (8 * b));
+    for (int b = 0; b < 8; ++b) buf[8 + b] = (uint8_t)(cnt >> (8 * b));
+    if (n) {
+      DevBuf tmp;
+      tmp.ensure((size_t)n * 13, sim->stream);
+      launch_evs_records(sim->ev.events.as<uint32_t>(), sim->ev.seg_out.as<int64_t>(), n, tmp.as<uint8_t>(),
+                         sim->stream);
+      CK_LAUNCH("evs");
+      CK(cudaMemcpyAsync(buf.data() + 16, tmp.p, (size_t)n * 13, cudaMemcpyDeviceToHost, sim->stream));
+      CK(cudaStreamSynchronize(sim->stream));
+    }
+    FILE* f = std::fopen(path, "wb");
+    if (!f) io_fail(path, "cannot open for writing");
+    const size_t wrote = std::fwrite(buf.data(), 1, buf.size(), f);
+    const bool ok = std::fclose(f) == 0 && wrote == buf.size();
+    if (!ok) io_fail(path, "write failed");
+  });
+}
+
+int evsim_gpu_write_events_text(evsim_gpu_sim* sim, const char* path) {
+  return guarded([&] {
+    if (!sim || !path) invalid("write_events_text: null argument");
+    CK(cudaSetDevice(sim->device));
+    sim->finish();
+    const int64_t n = sim->n_events;
+    std::vector<evsim_event> ev((size_t)n);
+    if (n) {
+      DevBuf tmp;
+      tmp.ensure((size_t)n * 24, sim->stream);
+      launch_unpack_events(sim->ev.events.as<uint32_t>(), sim->ev.seg_out.as<int64_t>(), n, tmp.p, sim->stream);
+      CK_LAUNCH("unpack");
+      CK(cudaMemcpyAsync(ev.data(), tmp.p, (size_t)n * 24, cudaMemcpyDeviceToHost, sim->stream));
+      CK(cudaStreamSynchronize(sim->stream));
+    }
+    FILE* f = std::fopen(path, "wb");
+    if (!f) io_fail(path, "cannot open for writing");
+    std::string line;  // io.cpp:105-126: "x,y,t,p\n", p as 1 / -1
+    bool ok = true;
+    for (const auto& e : ev) {
+      line = std::to_string(e.x) + ',' + std::to_string(e.y) + ',' + std::to_string(e.t) + ',' +
+             (e.p > 0 ? "1" : "-1") + '\n';
+      ok = ok && std::fwrite(line.data(), 1, line.size(), f) == line.size();
+    }
+    ok = std::fclose(f) == 0 && ok;
+    if (!ok) io_fail(path, "write failed");
+  });
+}
+
+int evsim_gpu_events_per_pixel_second(const evsim_event* ev, int64_t n, int32_t w, int32_t h, double duration,
+                                      double* mean, double* stddev, uint64_t* total) {
+  return guarded([&] {
+    // metrics.cpp:7-39
+    if (!(duration > 0.0)) invalid("events_per_pixel_second: duration must be > 0");
+    if (w <= 0 || h <= 0) invalid("events_per_pixel_second: stream resolution unknown");
+    if (n < 0 || (n > 0 && !ev)) invalid("events_per_pixel_second: malformed events");
+    CK(cudaSetDevice(0));
+    init_pool(0);
+    TmpStream ts;
+    const size_t P = (size_t)w * h;
+    std::vector<uint32_t> counts(P, 0);
+    if (n > 0) {
+      DevBuf dev, dc;
+      dev.ensure((size_t)n * sizeof(evsim_event), ts.s);
+      dc.ensure(P * 4, ts.s, true);
+      CK(cudaMemcpyAsync(dev.p, ev, (size_t)n * sizeof(evsim_event), cudaMemcpyHostToDevice, ts.s));
+      launch_event_counts(dev.as<evsim_event>(), n, w, dc.as<uint32_t>(), ts.s);
+      CK_LAUNCH("counts");
+      CK(cudaMemcpyAsync(counts.data(), dc.p, P * 4, cudaMemcpyDeviceToHost, ts.s));
+      CK(cudaStreamSynchronize(ts.s));
+    }
+    // the reduction keeps the reference's sequential fp64 order (it is not exact)
+    double sum = 0.0, sum_sq = 0.0;
+    for (size_t i = 0; i < P; ++i) {
+      const double rate = static_cast<double>(counts[i]) / duration;
+      sum += rate;
+      sum_sq += rate * rate;
+    }
+    const double np = static_cast<double>(P);
+    const double m = sum / np;
+    const double var = std::max(0.0, sum_sq / np - m * m);
+    if (mean) *mean = m;
+    if (stddev) *stddev = std::sqrt(var);
+    if (total) *total = (uint64_t)n;
+  });
+}
+
+int evsim_gpu_accumulate(const evsim_event* ev, int64_t n, int32_t w, int32_t h, int64_t t_start, int64_t t_end,
+                         uint8_t* classes) {
+  return guarded([&] {
+    // metrics.cpp:41-69
+    if (t_start >= t_end) invalid("accumulate: window must satisfy t_start < t_end");
+    if (w <= 0 || h <= 0) invalid("accumulate: stream resolution unknown");
+    if (n < 0 || (n > 0 && !ev) || !classes) invalid("accumulate: malformed events");
+    CK(cudaSetDevice(0));
+    init_pool(0);
+    TmpStream ts;
+    const size_t P = (size_t)w * h;
+    DevBuf dev, bits, out;
+    bits.ensure(P * 4, ts.s, true);
+    out.ensure(P, ts.s);
+    if (n > 0) {
+      dev.ensure((size_t)n * sizeof(evsim_event), ts.s);
+      CK(cudaMemcpyAsync(dev.p, ev, (size_t)n * sizeof(evsim_event), cudaMemcpyHostToDevice, ts.s));
+    }
+    launch_accumulate(n > 0 ? dev.as<evsim_event>() : nullptr, n, w, t_start, t_end, bits.as<uint32_t>(),
+                      out.as<uint8_t>(), (int64_t)P, ts.s);
+    CK_LAUNCH("accumulate");
+    CK(cudaMemcpyAsync(classes, out.p, P, cudaMemcpyDeviceToHost, ts.s));
+    CK(cudaStreamSynchronize(ts.s));
   });
 }
 

@@ -1,0 +1,118 @@
+// io_kernels.cu — the data formats either side of the path:
+// frame ingestion (BT.601 luma + bilinear resize, src/io.cpp:41-70), the
+// .evs event records (src/io.cpp:148-170) and the event metrics
+// (src/metrics.cpp:7-69), on the device.
+#include <algorithm>
+
+#include "evsim_device.cuh"
+#include "kernels.h"
+
+namespace evsim_gpu {
+
+namespace {
+
+// luma_bt601 (io.cpp:41-43): integer, exact
+__global__ void luma_kernel(const uint8_t* __restrict__ rgb, uint8_t* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = rgb[3 * i], g = rgb[3 * i + 1], b = rgb[3 * i + 2];
+    out[i] = (uint8_t)((299 * r + 587 * g + 114 * b + 500) / 1000);
+  }
+}
+
+// resize_bilinear (io.cpp:45-70): the reference's fp32 steps, lroundf
+__global__ void resize_kernel(const uint8_t* __restrict__ src, int w, int h, uint8_t* __restrict__ dst, int tw,
+                              int th) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  const int f = blockIdx.z;
+  if (x >= tw) return;
+  const uint8_t* s = src + (size_t)f * w * h;
+  const float sx_ratio = __fdiv_rn((float)w, (float)tw);
+  const float sy_ratio = __fdiv_rn((float)h, (float)th);
+  const float sy = clamp_ref(fsub(fmul(fadd((float)y, 0.5f), sy_ratio), 0.5f), 0.0f, (float)(h - 1));
+  const int y0 = (int)sy;
+  const int y1 = min(y0 + 1, h - 1);
+  const float fy = fsub(sy, (float)y0);
+  const float sx = clamp_ref(fsub(fmul(fadd((float)x, 0.5f), sx_ratio), 0.5f), 0.0f, (float)(w - 1));
+  const int x0 = (int)sx;
+  const int x1 = min(x0 + 1, w - 1);
+  const float fx = fsub(sx, (float)x0);
+  const uint8_t* r0 = s + (size_t)y0 * w;
+  const uint8_t* r1 = s + (size_t)y1 * w;
+  const float top = lerp_ref((float)r0[x0], (float)r0[x1], fx);
+  const float bot = lerp_ref((float)r1[x0], (float)r1[x1], fx);
+  dst[(size_t)f * tw * th + (size_t)y * tw + x] = (uint8_t)lroundf_ref(lerp_ref(top, bot, fy));
+}
+
+// .evs records (io.cpp:158-165): x u16, y u16, t u64, p i8, little endian, 13 B
+__global__ void evs_kernel(const uint32_t* __restrict__ packed, const int64_t* __restrict__ seg_out, int64_t n,
+                           uint8_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int S = (int)seg_out[0];
+  const int64_t* st = seg_out + 1;
+  const int64_t* so = seg_out + 1 + S;
+  int lo = 0, hi = S - 1;  // last segment with offset <= i
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (so[mid] <= i) lo = mid;
+    else hi = mid - 1;
+  }
+  const uint32_t e = packed[i];
+  const uint64_t t = (uint64_t)st[lo];
+  uint8_t* o = out + 13 * i;
+  o[0] = (uint8_t)(e & 0xFF);
+  o[1] = (uint8_t)((e >> 8) & 0xFF);
+  o[2] = (uint8_t)((e >> 16) & 0xFF);
+  o[3] = (uint8_t)((e >> 24) & 0x7F);
+#pragma unroll
+  for (int b = 0; b < 8; ++b) o[4 + b] = (uint8_t)(t >> (8 * b));
+  o[12] = (e >> 31) ? 0xFF : 0x01;
+}
+
+// per-pixel event counts of 24-byte evsim_event records
+__global__ void count_kernel(const evsim_event* __restrict__ ev, int64_t n, int w, uint32_t* __restrict__ counts) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&counts[(size_t)ev[i].y * w + ev[i].x], 1u);
+}
+
+// accumulate (metrics.cpp:41-69): polarity bits per pixel over [t0, t1);
+// none / positive / negative / both is order-independent, so an atomicOr
+// of (positive = 1, negative = 2) gives exactly the reference's class.
+__global__ void accumulate_kernel(const evsim_event* __restrict__ ev, int64_t n, int w, int64_t t0, int64_t t1,
+                                  uint32_t* __restrict__ bits) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const evsim_event e = ev[i];
+    if (e.t < t0 || e.t >= t1) continue;
+    atomicOr(&bits[(size_t)e.y * w + e.x], e.p > 0 ? 1u : 2u);
+  }
+}
+
+__global__ void classes_kernel(const uint32_t* __restrict__ bits, uint8_t* __restrict__ out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (uint8_t)bits[i];  // 0 none, 1 positive, 2 negative, 3 both (PixelClass)
+}
+
+unsigned grid_for(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
+
+}  // namespace
+
+void launch_luma(const uint8_t* rgb, uint8_t* out, int64_t n, cudaStream_t s) {
+  luma_kernel<<<grid_for(n), 256, 0, s>>>(rgb, out, n);
+}
+void launch_resize(const uint8_t* src, int w, int h, uint8_t* dst, int tw, int th, int n_frames, cudaStream_t s) {
+  resize_kernel<<<dim3((tw + 127) / 128, th, n_frames), 128, 0, s>>>(src, w, h, dst, tw, th);
+}
+void launch_evs_records(const uint32_t* packed, const int64_t* seg_out, int64_t n, uint8_t* out, cudaStream_t s) {
+  if (n > 0) evs_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(packed, seg_out, n, out);
+}
+void launch_event_counts(const evsim_event* ev, int64_t n, int w, uint32_t* counts, cudaStream_t s) {
+  if (n > 0) count_kernel<<<grid_for(n), 256, 0, s>>>(ev, n, w, counts);
+}
+void launch_accumulate(const evsim_event* ev, int64_t n, int w, int64_t t0, int64_t t1, uint32_t* bits,
+                       uint8_t* classes, int64_t P, cudaStream_t s) {
+  if (n > 0) accumulate_kernel<<<grid_for(n), 256, 0, s>>>(ev, n, w, t0, t1, bits);
+  classes_kernel<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(bits, classes, P);
+}
+
+}  // namespace evsim_gpu

@@ -13,6 +13,8 @@
 
 #include <cstdint>
 
+#include "evsim_gpu.h"
+
 namespace evsim_gpu {
 
 constexpr int kWarpsPerBlock = 8;  // chain / emit kernels: 256 threads
@@ -257,5 +259,13 @@ void launch_sparse_lk(const SparseLKParams& p, int max_points, int n_pairs, cuda
 void launch_splat(const SplatParams& p, int max_items, int n_pairs, cudaStream_t s);
 void launch_unpack_events(const uint32_t* packed, const int64_t* seg_out, int64_t n, void* out24,
                           cudaStream_t s);
+
+// io_kernels.cu — frame ingestion, .evs records, metrics
+void launch_luma(const uint8_t* rgb, uint8_t* out, int64_t n, cudaStream_t s);
+void launch_resize(const uint8_t* src, int w, int h, uint8_t* dst, int tw, int th, int n_frames, cudaStream_t s);
+void launch_evs_records(const uint32_t* packed, const int64_t* seg_out, int64_t n, uint8_t* out, cudaStream_t s);
+void launch_event_counts(const evsim_event* ev, int64_t n, int w, uint32_t* counts, cudaStream_t s);
+void launch_accumulate(const evsim_event* ev, int64_t n, int w, int64_t t0, int64_t t1, uint32_t* bits,
+                       uint8_t* classes, int64_t P, cudaStream_t s);
 
 }  // namespace evsim_gpu

@@ -433,6 +433,15 @@ class Simulator:
         out.events = unpack_events(packed, seg_t, seg_off)
         return out
 
+    def write_events_binary(self, path: str) -> None:
+        """write_events_binary (io.cpp:148-170) of the last push's events,
+        records formatted on the device."""
+        _lib.check(self._lib.evsim_gpu_write_events_binary(self._h, str(path).encode()))
+
+    def write_events_text(self, path: str) -> None:
+        """write_events_text (io.cpp:105-126) of the last push's events."""
+        _lib.check(self._lib.evsim_gpu_write_events_text(self._h, str(path).encode()))
+
     def set_row_band(self, y0: int, y1: int) -> None:
         """Emit only the events of rows [y0, y1) (evsim_gpu_set_row_band);
         (0, 0) = whole frame.  Stream start only; dense / difference_only."""
@@ -627,3 +636,59 @@ def push_frames_batched(sims: Sequence["Simulator"], frames: Sequence[np.ndarray
         r.width, r.height = w, h
         res.append(r)
     return res
+
+
+# --------------------------------------------------------------------------- data formats
+
+def ingest_frames(src: np.ndarray, target: Optional[tuple] = None) -> np.ndarray:
+    """load_frames' pixel path (io.cpp:41-103) on the GPU: (n, h, w) gray or
+    (n, h, w, 3) RGB u8 frames -> luma_bt601 -> resize_bilinear to
+    target = (width, height) -> (n, th, tw) u8."""
+    a = np.ascontiguousarray(src, dtype=np.uint8)
+    if a.ndim == 2:
+        a = a[None]
+    channels = 3 if a.ndim == 4 else 1
+    n, h, w = a.shape[:3]
+    tw, th = (w, h) if target is None else (int(target[0]), int(target[1]))
+    out = np.zeros((n, max(th, 0), max(tw, 0)), np.uint8)
+    lib = _lib.load()
+    _lib.check(lib.evsim_gpu_ingest_frames(_ptr(a), channels, w, h, n, tw, th, _ptr(out)))
+    return out
+
+
+@dataclasses.dataclass
+class EventRateStats:
+    """evsim::EventRateStats (metrics.hpp:9-14)."""
+    mean_rate: float
+    std_rate: float
+    duration: float
+    total_events: int
+
+
+def _ev24(stream: EventStream) -> np.ndarray:
+    ev = np.zeros(len(stream.events), EVENT_DTYPE)
+    for k in ("x", "y", "t", "p"):
+        ev[k] = stream.events[k]
+    return ev
+
+
+def events_per_pixel_second(stream: EventStream, duration: float) -> EventRateStats:
+    """events_per_pixel_second (metrics.cpp:7-39): counts on the GPU."""
+    ev = _ev24(stream)
+    m, s, t = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint64()
+    lib = _lib.load()
+    _lib.check(lib.evsim_gpu_events_per_pixel_second(_ptr(ev), len(ev), stream.width, stream.height,
+                                                     float(duration), ctypes.byref(m), ctypes.byref(s),
+                                                     ctypes.byref(t)))
+    return EventRateStats(m.value, s.value, float(duration), int(t.value))
+
+
+def accumulate(stream: EventStream, t_start: int, t_end: int) -> np.ndarray:
+    """accumulate (metrics.cpp:41-69): (height, width) PixelClass codes
+    (0 none, 1 positive, 2 negative, 3 both) over [t_start, t_end)."""
+    ev = _ev24(stream)
+    out = np.zeros((max(stream.height, 0), max(stream.width, 0)), np.uint8)
+    lib = _lib.load()
+    _lib.check(lib.evsim_gpu_accumulate(_ptr(ev), len(ev), stream.width, stream.height, int(t_start), int(t_end),
+                                        _ptr(out)))
+    return out

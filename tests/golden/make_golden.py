@@ -124,6 +124,22 @@ def main():
     cfg = make_config(Method.difference_interp, n_interp=6, c_pos=8, c_neg=-8, include_endpoints=0)
     out["diffinterp_pan_noend"] = dict(frames=frames, ts=ts, **cfg_arrays(cfg), **run_stream(R, cfg, frames, ts))
 
+    # 8. data formats either side of the path (io.cpp, metrics.cpp)
+    rgb = rng.integers(0, 256, size=(3, 23, 37, 3), dtype=np.uint8)
+    gray = np.stack([R.luma(f).reshape(23, 37) for f in rgb])
+    out["io_ingest"] = dict(rgb=rgb, gray=gray,
+                            down=np.stack([R.resize_bilinear(g, 29, 17) for g in gray]),
+                            up=np.stack([R.resize_bilinear(g, 50, 40) for g in gray]))
+    frames, ts = R.moving_disk(64, 48, 4, 7.0, 5.0, 60.0, 40, 230, 9)
+    cfg = make_config(Method.dense, n_interp=4)
+    sim = R.simulator(cfg)
+    evs = np.concatenate([sim.push_frame(frames[k], int(ts[k])) for k in range(len(frames))])
+    m = R.events_per_pixel_second(evs, 64, 48, 0.05)
+    t0, t1 = int(ts[1]), int(ts[3])
+    out["metrics"] = dict(ev_x=evs["x"].copy(), ev_y=evs["y"].copy(), ev_t=evs["t"].copy(), ev_p=evs["p"].copy(),
+                          rate=np.array(m[:3], np.float64), total=np.array(m[3], np.int64),
+                          window=np.array([t0, t1], np.int64), classes=R.accumulate(evs, 64, 48, t0, t1))
+
     only = sys.argv[1] if len(sys.argv) > 1 else ""
     for name, d in out.items():
         if not name.startswith(only):

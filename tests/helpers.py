@@ -11,8 +11,15 @@ from paper_2209_04634_b200.abi import CConfig
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
+NON_STREAM_FIXTURES = {"interp_random_flow", "io_ingest", "metrics"}
+
+
 def golden_names():
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+
+
+def stream_fixtures():
+    return [n for n in golden_names() if n not in NON_STREAM_FIXTURES]
 
 
 def load_golden(name):

@@ -5,7 +5,7 @@ count, and bit-exact on flow fields (north_star's 1e-3 px gate is implied).
 import numpy as np
 import pytest
 
-from helpers import (assert_events_equal, assert_same_events, golden_cfg, golden_names, load_golden,
+from helpers import (stream_fixtures, assert_events_equal, assert_same_events, golden_cfg, golden_names, load_golden,
                      run_oracle_stream)
 from paper_2209_04634_b200 import (FlowField, FlowPreset, Frame, SimulatorConfig, Simulator, SparseFlow,
                                    dense_events_with_flow, estimate_dense_flow, estimate_sparse_flow,
@@ -14,7 +14,7 @@ from paper_2209_04634_b200.abi import Method, make_config
 
 pytestmark = pytest.mark.gpu
 
-STREAM_FIXTURES = [n for n in golden_names() if n != "interp_random_flow"]
+STREAM_FIXTURES = stream_fixtures()
 
 
 def gpu_stream(cfg_c, frames, ts):

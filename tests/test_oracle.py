@@ -7,10 +7,10 @@
 import numpy as np
 import pytest
 
-from helpers import (assert_events_equal, golden_cfg, golden_names, load_golden, run_oracle_stream)
+from helpers import (stream_fixtures, assert_events_equal, golden_cfg, golden_names, load_golden, run_oracle_stream)
 from paper_2209_04634_b200.abi import Method, make_config
 
-STREAM_FIXTURES = [n for n in golden_names() if n != "interp_random_flow"]
+STREAM_FIXTURES = stream_fixtures()
 
 
 @pytest.mark.parametrize("name", STREAM_FIXTURES)
