@@ -483,10 +483,10 @@ __device__ __forceinline__ uint2 link_rule(const ChainParams& p, const float* s_
   return make_uint2(bp, bn);
 }
 
-template <int kW, int kNB, bool kClamp>
+template <int kW, int kNB, bool kClamp, int kBM>
 __device__ __forceinline__ unsigned dense_batch(const float4* s_kc, const uint32_t* qp, const uint32_t* qc,
                                                 uint32_t w, uint32_t kbias, float wm, float hm, const DenseWord* c,
-                                                int k0, int (&vals)[kW][4]) {
+                                                int k0, int (&vals)[kW][kBM]) {
   unsigned bad = 0;
 #pragma unroll
   for (int j = 0; j < kNB; ++j) {
@@ -494,14 +494,14 @@ __device__ __forceinline__ unsigned dense_batch(const float4* s_kc, const uint32
 #pragma unroll
     for (int q = 0; q < kW; ++q)
       vals[q][j] = dense_fast<kClamp>(qp, qc, w, kbias, wm, hm, c[q].xf, c[q].yf, c[q].u, c[q].v, kc, bad,
-                                      1u << (q * 4 + j));
+                                      1u << (q * kBM + j));
   }
   return bad;
 }
 
-template <bool kLog, bool kMag>
+template <bool kLog, bool kMag, int kB>
 __global__ void __launch_bounds__(256, 3) chain_dense_kernel(ChainParams p) {
-  constexpr int kW = 2, kB = 4;
+  constexpr int kW = 2;  // words per warp; kB links per batch (4, or 5 when it divides the interior links)
   extern __shared__ float4 s_dyn4[];
   __shared__ float s_lut[256];
   const int L = p.d.n_links, G = L * p.n_pairs, N = p.n_interp;
@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(256, 3) chain_dense_kernel(ChainParams p) {
       int l0 = 0;
       for (; l0 < n_int; l0 += kB) {
         const int nb = min(kB, n_int - l0);
-        int vals[kW][4];
+        int vals[kW][kB];
         unsigned bad;
         if (nb == kB) {
           bad = safe ? dense_batch<kW, kB, false>(s_kc, qp, qc, w, kbias, wm, hm, c, kfirst + l0, vals)
@@ -610,14 +610,14 @@ __global__ void __launch_bounds__(256, 3) chain_dense_kernel(ChainParams p) {
         } else {
           bad = 0;
           for (int j = 0; j < nb; ++j) {
-            int v1[kW][4];
+            int v1[kW][kB];
             bad |= (safe ? dense_batch<kW, 1, false>(s_kc, qp, qc, w, kbias, wm, hm, c, kfirst + l0 + j, v1)
                          : dense_batch<kW, 1, true>(s_kc, qp, qc, w, kbias, wm, hm, c, kfirst + l0 + j, v1))
                    << j;
 #pragma unroll
             for (int q = 0; q < kW; ++q)
 #pragma unroll
-              for (int jj = 0; jj < 4; ++jj)
+              for (int jj = 0; jj < kB; ++jj)
                 if (jj == j) vals[q][jj] = v1[q][0];
           }
         }
@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(256, 3) chain_dense_kernel(ChainParams p) {
           for (int q = 0; q < kW; ++q)
 #pragma unroll
             for (int j = 0; j < kB; ++j)
-              if ((bad >> (q * 4 + j)) & 1u)
+              if ((bad >> (q * kB + j)) & 1u)
                 vals[q][j] = dense_exact(p.nfb, p.oma, p.alpha, qp, qc, p.w, p.h, c[q].xf, c[q].yf, c[q].u, c[q].v,
                                        kfirst + l0 + j);
         }
@@ -1531,15 +1531,23 @@ static void launch_chain_mode(const ChainParams& p, cudaStream_t s) {
   }
 }
 
-template <bool kLog, bool kMag>
-static void launch_chain_dense(const ChainParams& p, size_t sm, cudaStream_t s) {
-  auto* k = chain_dense_kernel<kLog, kMag>;
+template <bool kLog, bool kMag, int kB>
+static void launch_chain_dense_b(const ChainParams& p, size_t sm, cudaStream_t s) {
+  auto* k = chain_dense_kernel<kLog, kMag, kB>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     attr = true;
   }
   k<<<p.n_blocks, 256, sm, s>>>(p);
+}
+
+template <bool kLog, bool kMag>
+static void launch_chain_dense(const ChainParams& p, size_t sm, cudaStream_t s) {
+  // batches of 5 links when they tile the interior links exactly and 4 do not
+  const int n_int = std::min(p.d.n_links, p.n_interp - p.d.start);
+  if (n_int % 5 == 0 && n_int % 4 != 0) launch_chain_dense_b<kLog, kMag, 5>(p, sm, s);
+  else launch_chain_dense_b<kLog, kMag, 4>(p, sm, s);
 }
 
 template <bool kLog, bool kMag>
