@@ -1014,8 +1014,29 @@ struct evsim_gpu_sim {
       h_seg2_cap = seg_need;
     }
     const size_t P = (size_t)w * h;
-    if (chunk <= 0) chunk = std::max(1, std::min(F, 32));
-    const int n_chunks = (F + chunk - 1) / chunk;
+    if (chunk <= 0) chunk = std::max(1, std::min(F, 48));
+    // chunk sizes: a quarter-size first chunk (its upload is not overlapped)
+    // and a quarter-size last one (its download is not), full ones between
+    std::vector<int> cfirst, csize;
+    {
+      const int c4 = std::max(1, chunk / 4);
+      int rem = F, at = 0;
+      auto add = [&](int n) {
+        cfirst.push_back(at);
+        csize.push_back(n);
+        at += n;
+        rem -= n;
+      };
+      if (rem > chunk) add(c4);
+      while (rem > chunk + c4) add(chunk);
+      if (rem > c4 && rem > 1) {
+        add(rem - c4);
+        add(c4);
+      } else {
+        add(rem);
+      }
+    }
+    const int n_chunks = (int)csize.size();
     std::vector<cudaEvent_t> up(n_chunks), done(n_chunks);
     for (int j = 0; j < n_chunks; ++j) {
       CK(cudaEventCreateWithFlags(&up[j], cudaEventDisableTiming));
@@ -1033,11 +1054,11 @@ struct evsim_gpu_sim {
       int sl = next_slot();
       for (int j = 0; j < n_chunks; ++j) {
         slot[j] = sl;
-        sl = (sl + std::min(chunk, F - j * chunk)) % R;
+        sl = (sl + csize[j]) % R;
       }
     }
     auto enqueue_upload = [&](int j) {
-      const int a = j * chunk, nf = std::min(chunk, F - a);
+      const int a = cfirst[j], nf = csize[j];
       upload(pixels + (size_t)a * P, nf, slot[j], false, s_in);
       CK(cudaEventRecord(up[j], s_in));
     };
@@ -1073,7 +1094,7 @@ struct evsim_gpu_sim {
     enqueue_upload(0);
     for (int j = 0; j < n_chunks; ++j) {
       if (j + 1 < n_chunks) enqueue_upload(j + 1);
-      const int a = j * chunk, nf = std::min(chunk, F - a);
+      const int a = cfirst[j], nf = csize[j];
       const bool had_prev = has_prev;
       if (!had_prev && nf == 1) {  // a warm-up chunk of one frame: no pairs, no segment table
         h_seg2[j & 1][0] = 0;
