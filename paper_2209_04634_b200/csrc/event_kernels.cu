@@ -1340,23 +1340,14 @@ __global__ void __launch_bounds__(256) select_mask_kernel(SelectParams p) {
 // pair publishes M.
 __global__ void __launch_bounds__(256) select_emit_kernel(SelectParams p) {
   __shared__ int s_warp[kWarpsPerBlock];
-  __shared__ int64_t s_warp64[kWarpsPerBlock];
+
   __shared__ uint32_t s_m[256];
   __shared__ int s_off[256];
   const int z = blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t* counts = p.counts + (size_t)z * p.n_blocks;
-  // prefix of this block and the total, over the pair's block counts
-  int64_t pre = 0, tot = 0;
-  for (int bb = threadIdx.x; bb < p.n_blocks; bb += blockDim.x) {
-    const int64_t c = counts[bb];
-    tot += c;
-    pre += bb < (int)blockIdx.x ? c : 0;
-  }
-  int64_t t_all, p_all;
-  block_exclusive_scan(tot, s_warp64, t_all);
-  block_exclusive_scan(pre, s_warp64, p_all);
-  if (blockIdx.x == 0 && threadIdx.x == 0) p.n_points[z] = (int)t_all;
+  // this block's offset and the pair's total (offsets_kernel over the counts)
+  const int64_t p_all = p.prefix[(size_t)z * p.n_blocks + blockIdx.x];
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.n_points[z] = (int)p.total[z];
   const uint32_t* masks = p.masks + (size_t)z * p.n_words;
   uint32_t* points = p.points + (size_t)z * p.P;
   const int64_t wbeg = (int64_t)blockIdx.x * p.words_per_block;
@@ -1644,6 +1635,8 @@ void launch_interp_frames(const ChainParams& p, uint8_t* out, cudaStream_t s) {
 void launch_select(const SelectParams& p, int n_pairs, cudaStream_t s) {
   if (n_pairs <= 0) return;
   select_mask_kernel<<<dim3(p.n_blocks, n_pairs), 256, 0, s>>>(p);
+  OffsetParams op{n_pairs, p.n_blocks, p.counts, p.prefix, p.total};
+  launch_offsets(op, s);
   select_emit_kernel<<<dim3(p.n_blocks, n_pairs), 256, 0, s>>>(p);
 }
 

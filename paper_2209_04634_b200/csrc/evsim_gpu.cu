@@ -514,7 +514,7 @@ struct evsim_gpu_sim {
   FlowEngine flow;
   EventEngine ev;
   // sparse (per pair)
-  DevBuf sel_masks, sel_counts, points, n_points, disp, status, claims, touched, svals, dvals;
+  DevBuf sel_masks, sel_counts, sel_prefix, sel_total, points, n_points, disp, status, claims, touched, svals, dvals;
 
   // last result
   int64_t* h_seg_out = nullptr;  // pinned
@@ -721,6 +721,8 @@ struct evsim_gpu_sim {
         const int N = n_interp_eff();
         sel_masks.ensure((size_t)pairs * ev.n_words * 4, stream);
         sel_counts.ensure((size_t)pairs * ev.n_blocks * 4, stream);
+        sel_prefix.ensure((size_t)pairs * ev.n_blocks * 8, stream);
+        sel_total.ensure((size_t)pairs * 8, stream);
         points.ensure((size_t)pairs * P * 4, stream);
         n_points.ensure((size_t)pairs * sizeof(int), stream, true);
         disp.ensure((size_t)pairs * P * sizeof(float2), stream);
@@ -1151,6 +1153,8 @@ struct evsim_gpu_sim {
     sp.skip_first = c.skip_first;
     sp.masks = sel_masks.as<uint32_t>();
     sp.counts = sel_counts.as<uint32_t>();
+    sp.prefix = sel_prefix.as<int64_t>();
+    sp.total = sel_total.as<int64_t>();
     sp.points = points.as<uint32_t>();
     sp.n_points = n_points.as<int>();
     sp.P = P;
@@ -1165,7 +1169,7 @@ struct evsim_gpu_sim {
     launch_sparse_lk(lk, (int)std::min<size_t>(P, INT32_MAX), n_pairs, stream);
     CK_LAUNCH("sparse_lk");
     splat_stage(r0, n_pairs, c);
-    launches += 5;  // select mask + emit, sparse LK, splat, resolve
+    launches += 6;  // select mask + offsets + emit, sparse LK, splat, resolve
     (void)N;
   }
 

@@ -219,6 +219,8 @@ struct SelectParams {
   int skip_first;         //   pair 0 has no d1: selects nothing
   uint32_t* masks;        // [pair][n_words]
   uint32_t* counts;       // [pair][n_blocks]
+  int64_t* prefix;        // [pair][n_blocks] exclusive prefix of counts
+  int64_t* total;         // [pair]
   uint32_t* points;       // [pair][P]
   int* n_points;          // [pair]
   size_t P;
