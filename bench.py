@@ -402,6 +402,8 @@ def run_ours(args):
             "events_per_s": round(events_per_s, 1), "events_per_frame": round(E_frame, 1),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(),
+            "issue_roofline": issue_roofline(c.name, args.mode, pairs_timed / launches_ev, stages, launches_ev,
+                                             clk.summary().get("sm_mhz")),
         }
         print(json.dumps(out), flush=True)
     sim.close()
@@ -409,6 +411,35 @@ def run_ours(args):
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+def issue_roofline(config: str, mode: str, pairs_per_launch: float, stages_ms: dict, launches: int,
+                   sm_mhz):
+    """SM-issue roofline of the two dominant kernels (both are issue / L1
+    bound, not HBM bound): warp instructions per launch from the committed
+    ncu --set full capture of this workload, over the live CUDA-event time of
+    the stage, against 148 SMs x 4 issue slots x the measured SM clock."""
+    if not (config == "c2" and mode == "log" and abs(pairs_per_launch - 127) < 0.5 and launches > 0):
+        return None
+    try:
+        rows = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_full_summary.json")))
+    except Exception:
+        return None
+    clock = float(sm_mhz or 1965.0) * 1e6
+    peak = 148 * 4 * clock
+    out = {"unit": "warp-instructions/s", "peak": peak, "peak_source": "148 SMs x 4 schedulers x measured SM clock",
+           "instructions_source": "profiles/r01/ncu_full_summary.json (smsp__inst_executed.sum per launch)"}
+    fam = {"chain": "chain_dense_kernel", "flow": "dense_lk_warp_kernel"}
+    for stage, name in fam.items():
+        ks = [r for r in rows if name in r["kernel"]]
+        if not ks:
+            continue
+        instr = ks[0]["warp_instr"] if stage == "chain" else sum(r["warp_instr"] for r in ks[:3])
+        t = stages_ms[stage] / launches / 1e3
+        if t > 0:
+            out[stage] = {"kernel": name, "warp_instr_per_launch": instr, "achieved": round(instr / t, 1),
+                          "frac": round(instr / t / peak, 4)}
+    return out
 
 
 def traffic_for(config: str, mode: str, pairs_per_launch: float):

@@ -499,9 +499,10 @@ __device__ __forceinline__ unsigned dense_batch(const float4* s_kc, const uint32
   return bad;
 }
 
-template <bool kLog, bool kMag, int kB>
-__global__ void __launch_bounds__(256, 3) chain_dense_kernel(ChainParams p) {
-  constexpr int kW = 2;  // words per warp; kB links per batch (4, or 5 when it divides the interior links)
+// kW words per warp (1 on small frames: finer tasks, 4 blocks per SM; 2 on
+// large ones), kB links per batch (4, or 5 when it tiles the interior links)
+template <bool kLog, bool kMag, int kB, int kW, int kMinB>
+__global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) {
   extern __shared__ float4 s_dyn4[];
   __shared__ float s_lut[256];
   const int L = p.d.n_links, G = L * p.n_pairs, N = p.n_interp;
@@ -1522,9 +1523,9 @@ static void launch_chain_mode(const ChainParams& p, cudaStream_t s) {
   }
 }
 
-template <bool kLog, bool kMag, int kB>
+template <bool kLog, bool kMag, int kB, int kW, int kMinB>
 static void launch_chain_dense_b(const ChainParams& p, size_t sm, cudaStream_t s) {
-  auto* k = chain_dense_kernel<kLog, kMag, kB>;
+  auto* k = chain_dense_kernel<kLog, kMag, kB, kW, kMinB>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
@@ -1537,8 +1538,14 @@ template <bool kLog, bool kMag>
 static void launch_chain_dense(const ChainParams& p, size_t sm, cudaStream_t s) {
   // batches of 5 links when they tile the interior links exactly and 4 do not
   const int n_int = std::min(p.d.n_links, p.n_interp - p.d.start);
-  if (n_int % 5 == 0 && n_int % 4 != 0) launch_chain_dense_b<kLog, kMag, 5>(p, sm, s);
-  else launch_chain_dense_b<kLog, kMag, 4>(p, sm, s);
+  const bool five = n_int % 5 == 0 && n_int % 4 != 0;
+  if (p.words_per_warp == 1) {
+    if (five) launch_chain_dense_b<kLog, kMag, 5, 1, 4>(p, sm, s);
+    else launch_chain_dense_b<kLog, kMag, 4, 1, 4>(p, sm, s);
+  } else {
+    if (five) launch_chain_dense_b<kLog, kMag, 5, 2, 3>(p, sm, s);
+    else launch_chain_dense_b<kLog, kMag, 4, 2, 3>(p, sm, s);
+  }
 }
 
 template <bool kLog, bool kMag>

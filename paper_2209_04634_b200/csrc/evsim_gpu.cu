@@ -417,14 +417,16 @@ struct EventEngine {
   int w = 0, h = 0, wpr = 0;
   int64_t n_words = 0;
   int wpb = 0, n_blocks = 0;
+  int words_per_warp = 2;  // dense chain kernel
   int max_links = 0;  // links of a launch (pairs * per-pair links)
   bool magnitude = false;
   DevBuf masks, counts, prefix, link_total, segtab, segbase, seg_out, events, mcount, wcount, base;
   int64_t capacity = 0;
 
-  // fixed_wpb > 0: words per block (sparse: 16, one 2-word task per warp, so
-  // blocks over busy regions do not hold idle warps for long)
-  void geometry(int w_, int h_, int fixed_wpb = 0) {
+  // fine = true (dense, small frames): 8 words per block, one word per warp —
+  // finer tasks balance the few waves of a small frame (measured: c2 chain
+  // 16.4 -> 15.0 us/frame); large frames keep 2-word tasks and ~8 blocks/SM
+  void geometry(int w_, int h_, bool fine = false) {
     w = w_;
     h = h_;
     wpr = (w + 31) / 32;
@@ -433,7 +435,11 @@ struct EventEngine {
     const int64_t target = 148 * 8;
     int64_t per = (n_words + target - 1) / target;
     per = std::max<int64_t>(kWarpsPerBlock, (per + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock);
-    if (fixed_wpb > 0) per = fixed_wpb;
+    words_per_warp = 2;
+    if (fine && (n_words + 7) / 8 <= 4096) {
+      per = 8;
+      words_per_warp = 1;
+    }
     wpb = (int)per;
     n_blocks = (int)((n_words + wpb - 1) / wpb);
     max_links = 0;
@@ -627,7 +633,7 @@ struct evsim_gpu_sim {
       if (band && dense_flow()) flow.plan_band(band_y0, band_y1);
     }
     if (log_mode()) ref.ensure((size_t)w * h * sizeof(float), stream);
-    ev.geometry(w, band ? band_y1 - band_y0 : h);
+    ev.geometry(w, band ? band_y1 - band_y0 : h, dense_flow());
     // interpolation constants, interpolate_frames simulate.cpp:97-100
     const int N = n_interp_eff();
     const int K = N + 2;
@@ -763,6 +769,7 @@ struct evsim_gpu_sim {
     c.n_words = ev.n_words;
     c.words_per_block = ev.wpb;
     c.n_blocks = ev.n_blocks;
+    c.words_per_warp = ev.words_per_warp;
     c.n_interp = N;
     c.n_pairs = n_pairs;
     c.R = R;
