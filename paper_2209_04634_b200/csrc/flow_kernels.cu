@@ -529,6 +529,7 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
       for (int jb = 0; jb < kPW; jb += kJB) {
         if (!((solved >> jb) & ((1u << kJB) - 1u))) continue;  // warp-uniform
         float4 q[kJB];
+        uint32_t q8[kJB];
         float fx[kJB], fy[kJB];
 #pragma unroll
         for (int jj = 0; jj < kJB; ++jj) {
@@ -538,20 +539,31 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
           fx[jj] = X.y;
           fy[jj] = Y.y;
           const int qi = __float_as_int(Y.x) + __float_as_int(X.x);
-          if (kU8) {
-            const uint32_t v = __ldg(qcurr8 + qi);
-            q[jj] = make_float4(byte_f<0>(v), byte_f<1>(v), byte_f<2>(v), byte_f<3>(v));
-          } else {
-            q[jj] = __ldg(qcurr + qi);
-          }
+          if (kU8) q8[jj] = __ldg(qcurr8 + qi);
+          else q[jj] = __ldg(qcurr + qi);
         }
 #pragma unroll
         for (int jj = 0; jj < kJB; ++jj) {
           const int j = jb + jj;
           const int o = __shfl_sync(kFull, tb, j) + (oy - kR) * pitch + (ox - kR);
           if (!on || !((solved >> j) & 1u)) continue;
-          const float4 a = q[jj];
-          const float smp = lerp_ref(lerp_ref(a.x, a.y, fx[jj]), lerp_ref(a.z, a.w, fx[jj]), fy[jj]);
+          float smp;
+          if (kU8) {
+            // the u8 quad as two fp32x2 pairs (a00, a01), (a10, a11): 2^23 + b
+            // via PRMT; b - a of biased taps is exact, f*(b-a) one FMUL2, the
+            // adds scalar (sample(), flow.cpp:54-56, rounding by rounding)
+            const uint32_t v = q8[jj];
+            const f32x2 B0 = pk2(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7540)),
+                                 __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7542)));
+            const f32x2 B1 = pk2(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7541)),
+                                 __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7543)));
+            const f32x2 A = sub2(B0, pk2(8388608.0f, 8388608.0f));
+            const f32x2 M = mul2(pk2(fx[jj], fx[jj]), sub2(B1, B0));
+            smp = lerp_ref(__fadd_rn(lo2(A), lo2(M)), __fadd_rn(hi2(A), hi2(M)), fy[jj]);
+          } else {
+            const float4 a = q[jj];
+            smp = lerp_ref(lerp_ref(a.x, a.y, fx[jj]), lerp_ref(a.z, a.w, fx[jj]), fy[jj]);
+          }
           const float res = fsub(smp, sP[o]);
           sB[j * G::S + lane] = fmul(sGx[o], res);
           sB[G::PO + j * G::S + lane] = fmul(sGy[o], res);
