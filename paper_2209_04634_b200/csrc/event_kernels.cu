@@ -702,7 +702,28 @@ __global__ void __launch_bounds__(256, 3) chain_sparse_kernel(ChainParams p) {
       ref[q] = kLog ? p.ref[c[q].pix] : 0.0f;
       before[q] = 0;
     }
+    // the per-pixel inputs of a pair (curr value, touched words) are loaded
+    // one pair ahead, so their latency overlaps the previous pair's links;
+    // prev of pair i+1 is curr of pair i
     int sp = p.r0 % p.R;
+    int nv0[kW], nvc[kW];
+    uint32_t ntw0[kW], ntw1[kW];
+    auto prefetch = [&](int i, int sc_i) {
+      const uint8_t* cur = p.frames.at(sc_i);
+      const uint32_t* tp = p.touched + (size_t)i * ((N + 31) >> 5) * P;
+#pragma unroll
+      for (int q = 0; q < kW; ++q) {
+        nvc[q] = cur[c[q].pix];
+        ntw0[q] = (c[q].valid && N > 0) ? tp[c[q].pix] : 0u;
+        ntw1[q] = (c[q].valid && N > 32) ? tp[P + c[q].pix] : 0u;
+      }
+    };
+    {
+      const uint8_t* pr = p.frames.at(sp);
+#pragma unroll
+      for (int q = 0; q < kW; ++q) nv0[q] = pr[c[q].pix];
+      if (p.n_pairs > 0) prefetch(0, sp + 1 == p.R ? 0 : sp + 1);
+    }
     for (int i = 0; i < p.n_pairs; ++i) {
       const int sc = sp + 1 == p.R ? 0 : sp + 1;
       PairCtx pc;
@@ -712,6 +733,17 @@ __global__ void __launch_bounds__(256, 3) chain_sparse_kernel(ChainParams p) {
       pc.skip = p.skip_empty && p.n_points[i] == 0;
       const uint8_t* svals = p.svals + (size_t)i * N * P;
       sp = sc;
+      int v0[kW], vc[kW];
+      uint32_t tw0[kW], tw1[kW], at0[kW], at1[kW];
+#pragma unroll
+      for (int q = 0; q < kW; ++q) {
+        v0[q] = nv0[q];
+        vc[q] = nvc[q];
+        tw0[q] = ntw0[q];
+        tw1[q] = ntw1[q];
+        nv0[q] = vc[q];
+      }
+      if (i + 1 < p.n_pairs) prefetch(i + 1, sc + 1 == p.R ? 0 : sc + 1);
       const int gbase = i * L;
       uint2 lm[kW];
       uint32_t lwc[kW], lcnt = 0;
@@ -737,14 +769,8 @@ __global__ void __launch_bounds__(256, 3) chain_sparse_kernel(ChainParams p) {
         for (int l = 0; l < L; ++l) flush(l);
         continue;
       }
-      int v0[kW], vc[kW];
-      uint32_t tw0[kW], tw1[kW], at0[kW], at1[kW];
 #pragma unroll
       for (int q = 0; q < kW; ++q) {
-        v0[q] = pc.prev[c[q].pix];
-        vc[q] = pc.curr[c[q].pix];
-        tw0[q] = (c[q].valid && N > 0) ? pc.touched[c[q].pix] : 0u;
-        tw1[q] = (c[q].valid && N > 32) ? pc.touched[P + c[q].pix] : 0u;
         at0[q] = __reduce_or_sync(kFull, tw0[q]);
         at1[q] = __reduce_or_sync(kFull, tw1[q]);
       }
