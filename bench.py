@@ -165,16 +165,56 @@ def run_reference(args):
 # ----------------------------------------------------------------------------- clocks
 
 class Clocks:
+    """SM clock and throttle reasons sampled DURING the timed region: an NVML
+    polling thread (every ~2 ms, so even a 20-ms region gets samples; one
+    sample is taken on entry and one on exit), or nvidia-smi when NVML is
+    unavailable."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, device):
         self.device = device
         self.proc = None
+        self.nvml = None
+        self.rows = []
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
 
+    def _sample(self):
+        import pynvml
+        h = self.handle
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        try:
+            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.rows.append((float(sm), float(mx), [n for n, bit in self.REASONS.items() if r & bit]))
+
+    def _poll(self):
+        while not self.stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                pass
+            self.stop.wait(0.002)
+
     def __enter__(self):
+        try:
+            import threading
+            import pynvml
+            pynvml.nvmlInit()
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self._nvml_index())
+            self.nvml = pynvml
+            self._sample()
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             os.makedirs(os.path.dirname(self.path), exist_ok=True)
             self.f = open(self.path, "w")
@@ -185,7 +225,24 @@ class Clocks:
             self.proc = None
         return self
 
+    def _nvml_index(self):
+        # CUDA_VISIBLE_DEVICES remaps CUDA ordinals; NVML sees all GPUs
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            ids = [v.strip() for v in vis.split(",") if v.strip()]
+            if self.device < len(ids) and ids[self.device].isdigit():
+                return int(ids[self.device])
+        return self.device
+
     def __exit__(self, *a):
+        if self.nvml:
+            self.stop.set()
+            self.thread.join(timeout=2)
+            try:
+                self._sample()
+            except Exception:
+                pass
+            return
         if self.proc:
             self.proc.terminate()
             try:
@@ -195,24 +252,28 @@ class Clocks:
             self.f.close()
 
     def summary(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        rows = []
-        for line in open(self.path):
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
-            except ValueError:
-                continue
+        rows = self.rows
+        src = "nvml"
+        if not self.nvml:
+            src = "nvidia-smi"
+            if not self.proc:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            rows = []
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+                    rows.append((float(parts[1]), float(parts[2]),
+                                 [names[i] for i in range(4) if parts[5 + i].lower().startswith("active")]))
+                except ValueError:
+                    continue
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, r in rows for i in range(4) if r[i].lower().startswith("active")})
-        loaded = [s for s, _, _ in rows]
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(m for _, m, _ in rows),
-                "reasons": reasons, "samples": len(rows)}
+        reasons = sorted({n for _, _, r in rows for n in r})
+        return {"sm_mhz": statistics.median(s for s, _, _ in rows), "sm_max_mhz": max(m for _, m, _ in rows),
+                "reasons": reasons, "samples": len(rows), "source": src}
 
 
 # ----------------------------------------------------------------------------- ours
