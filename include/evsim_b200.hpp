@@ -384,6 +384,17 @@ class Simulator {
     return all;
   }
 
+  // write_events_binary / write_events_text (io.hpp:30-36) of the last push's
+  // events, formatted on the device (library handle only).
+  void write_events_binary(const std::string& path) {
+    if (!h_) throw std::invalid_argument("write_events_binary: not available with custom flow estimators");
+    detail::check(evsim_gpu_write_events_binary(h_.get(), path.c_str()));
+  }
+  void write_events_text(const std::string& path) {
+    if (!h_) throw std::invalid_argument("write_events_text: not available with custom flow estimators");
+    detail::check(evsim_gpu_write_events_text(h_.get(), path.c_str()));
+  }
+
   // Row band (evsim_gpu_set_row_band): emit only rows [y0, y1); stream start only.
   void set_row_band(int y0, int y1) {
     if (!h_) throw std::invalid_argument("set_row_band: not available with custom flow estimators");
@@ -461,6 +472,67 @@ inline EventStream simulate_difference(const Frame& f0, const Frame& f1, const F
   sim.push_frame(f0);
   sim.push_frame(f1);
   return sim.push_frame(f2);
+}
+
+// ---- io.hpp / metrics.hpp (the data formats either side of the path) -------
+// luma_bt601 (io.cpp:41-43)
+inline std::uint8_t luma_bt601(std::uint8_t r, std::uint8_t g, std::uint8_t b) {
+  return static_cast<std::uint8_t>((299 * r + 587 * g + 114 * b + 500) / 1000);
+}
+
+// resize_bilinear (io.cpp:45-70), on the device
+inline Frame resize_bilinear(const Frame& src, int width, int height) {
+  if (width <= 0 || height <= 0) throw std::invalid_argument("resize_bilinear: target must be positive");
+  Frame dst(width, height, src.timestamp);
+  detail::check(evsim_gpu_ingest_frames(src.pixels.data(), 1, src.width, src.height, 1, width, height,
+                                        dst.pixels.data()));
+  return dst;
+}
+
+struct EventRateStats {  // metrics.hpp:9-14
+  double mean_rate = 0.0;
+  double std_rate = 0.0;
+  double duration = 0.0;
+  std::uint64_t total_events = 0;
+};
+
+enum class PixelClass : std::uint8_t { none = 0, positive = 1, negative = 2, both = 3 };
+
+struct AccumulatedFrame {  // metrics.hpp:19-27
+  int width = 0;
+  int height = 0;
+  time_us t_start = 0;
+  time_us t_end = 0;
+  std::vector<PixelClass> classes;
+  PixelClass at(int x, int y) const { return classes[static_cast<std::size_t>(y) * width + x]; }
+};
+
+// events_per_pixel_second (metrics.cpp:7-39): counts on the device
+inline EventRateStats events_per_pixel_second(const EventStream& stream, double duration) {
+  EventRateStats st;
+  detail::check(evsim_gpu_events_per_pixel_second(reinterpret_cast<const evsim_event*>(stream.events.data()),
+                                                  static_cast<int64_t>(stream.events.size()), stream.width,
+                                                  stream.height, duration, &st.mean_rate, &st.std_rate,
+                                                  &st.total_events));
+  st.duration = duration;
+  return st;
+}
+
+// accumulate (metrics.cpp:41-69), on the device
+inline AccumulatedFrame accumulate(const EventStream& stream, time_us t_start, time_us t_end) {
+  AccumulatedFrame f;
+  f.width = stream.width;
+  f.height = stream.height;
+  f.t_start = t_start;
+  f.t_end = t_end;
+  std::vector<std::uint8_t> cls(
+      static_cast<std::size_t>(stream.width > 0 ? stream.width : 0) * (stream.height > 0 ? stream.height : 0));
+  detail::check(evsim_gpu_accumulate(reinterpret_cast<const evsim_event*>(stream.events.data()),
+                                     static_cast<int64_t>(stream.events.size()), stream.width, stream.height,
+                                     t_start, t_end, cls.data()));
+  f.classes.resize(cls.size());
+  for (std::size_t i = 0; i < cls.size(); ++i) f.classes[i] = static_cast<PixelClass>(cls[i]);
+  return f;
 }
 
 }  // namespace evsim_b200

@@ -50,6 +50,8 @@ static int cpu_checks() {
   EXPECT(throws_msg<std::invalid_argument>([&] { ev::FlowPreset{0, 1, 1}.validate(); }) ==
          "FlowPreset: all fields must be >= 1");
   EXPECT(ev::sub_interval_end(0, 1100, 1, 4) == 275);
+  // luma_bt601  io.cpp:41-43 (values from the compiled reference)
+  EXPECT(ev::luma_bt601(10, 200, 30) == 124 && ev::luma_bt601(255, 255, 255) == 255);
   EXPECT(throws_msg<std::invalid_argument>([&] { ev::Frame(0, 3, 0); }) == "Frame: width and height must be positive");
   std::puts(fails ? "cpu checks FAILED" : "cpu checks ok");
   return fails ? 1 : 0;
@@ -82,6 +84,18 @@ static int gpu_run(const char* in, const char* out1, const char* out2) {
   std::ofstream o1(out1, std::ios::binary), o2(out2, std::ios::binary);
   o1.write(reinterpret_cast<const char*>(s1.events.data()), (std::streamsize)(s1.events.size() * sizeof(ev::Event)));
   o2.write(reinterpret_cast<const char*>(s2.events.data()), (std::streamsize)(s2.events.size() * sizeof(ev::Event)));
+  // io / metrics mirrors on the device: accumulate of the stream's own events
+  // classifies every pixel that received an event in the window
+  if (!s1.events.empty()) {
+    const auto acc = ev::accumulate(s1, s1.events.front().t, s1.events.back().t + 1);
+    std::size_t n_set = 0;
+    for (auto c : acc.classes) n_set += c != ev::PixelClass::none;
+    EXPECT(n_set > 0);
+    const auto st = ev::events_per_pixel_second(s1, 1.0);
+    EXPECT(st.total_events == s1.events.size() && st.mean_rate > 0.0);
+  }
+  const ev::Frame small = ev::resize_bilinear(frames[0], 17, 11);
+  EXPECT(small.width == 17 && small.height == 11 && small.pixels.size() == 187);
   std::printf("gpu run ok: %zu / %zu events\n", s1.events.size(), s2.events.size());
   return fails ? 1 : 0;
 }
