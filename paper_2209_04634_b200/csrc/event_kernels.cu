@@ -505,6 +505,10 @@ template <bool kLog, bool kMag, int kB, int kW, int kMinB>
 __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) {
   extern __shared__ float4 s_dyn4[];
   __shared__ float s_lut[256];
+  constexpr int kStage = 32 + kB;  // staged links of a warp: < 32 before a batch of kB
+  __shared__ uint2 s_stm[kWarpsPerBlock][kW][kStage];
+  __shared__ uint32_t s_stc[kWarpsPerBlock][kStage];
+  __shared__ uint32_t s_stw[kMag ? kWarpsPerBlock : 1][kW][kMag ? kStage : 1];
   const int L = p.d.n_links, G = L * p.n_pairs, N = p.n_interp;
   float4* s_kc = s_dyn4;                                       // [N + 2]
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_dyn4 + N + 2);  // [G]
@@ -571,34 +575,37 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
       }
       safe = __all_sync(kFull, safe);
       const int gbase = i * L;
-      // lane j collects link (l & 31) == j: its masks per word and its event
-      // count; every 32 links (and at the end) the lanes store / add them at once
-      uint2 lm[kW];
-      uint32_t lwc[kW], lcnt = 0;
-#pragma unroll
-      for (int q = 0; q < kW; ++q) lm[q] = make_uint2(0u, 0u), lwc[q] = 0u;
+      // lane 0 stages each link's masks (warp-uniform ballots) and event count
+      // in shared memory; once 32 or more links are staged (checked per batch)
+      // lane j stores / adds staged link j
+      int fbase = 0;
       auto step = [&](int l, int q, int val) {
         uint32_t ev;
         const uint2 m = link_rule<kLog, kMag>(p, s_lut, gbase + l, c[q], lane, val, ref[q], before[q], ev);
-        if (lane == (l & 31)) {
-          lm[q] = m;
-          if (kMag) lwc[q] = ev;
-          lcnt += ev;
+        if (lane == 0) {
+          s_stm[warp][q][l - fbase] = m;
+          if (kMag) s_stw[warp][q][l - fbase] = ev;
+          if (q == 0) s_stc[warp][l - fbase] = ev;
+          else s_stc[warp][l - fbase] += ev;
         }
       };
-      auto flush = [&](int l) {
-        if ((l & 31) != 31 && l != L - 1) return;
-        if (lane <= (l & 31)) {
-          const int g = gbase + (l & ~31) + lane;
+      auto flush = [&](int lend, bool force) {
+        const int n = lend - fbase;
+        if (n < 32 && !force) return;
+        __syncwarp();
+        for (int j = lane; j < n; j += 32) {
+          const int g = gbase + fbase + j;
 #pragma unroll
           for (int q = 0; q < kW; ++q) {
             if (!c[q].have) continue;
-            p.masks[(size_t)g * p.n_words + c[q].wi] = lm[q];
-            if (kMag) p.wcount[(size_t)g * p.n_words + c[q].wi] = lwc[q];
+            p.masks[(size_t)g * p.n_words + c[q].wi] = s_stm[warp][q][j];
+            if (kMag) p.wcount[(size_t)g * p.n_words + c[q].wi] = s_stw[warp][q][j];
           }
-          if (lcnt) atomicAdd(&s_cnt[g], lcnt);
+          const uint32_t cnt = s_stc[warp][j];
+          if (cnt) atomicAdd(&s_cnt[g], cnt);
         }
-        lcnt = 0;
+        __syncwarp();
+        fbase = lend;
       };
       int l0 = 0;
       for (; l0 < n_int; l0 += kB) {
@@ -636,15 +643,15 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
           if (j >= nb) break;
 #pragma unroll
           for (int q = 0; q < kW; ++q) step(l0 + j, q, vals[q][j]);
-          flush(l0 + j);
         }
+        flush(l0 + nb, false);
       }
       if (n_int < L) {  // the link into curr (include_endpoints)
         const uint8_t* curr = p.frames.at(sc);
 #pragma unroll
         for (int q = 0; q < kW; ++q) step(L - 1, q, (int)curr[c[q].pix]);
-        flush(L - 1);
       }
+      flush(L, true);
       sp = sc;
     }
     if (kLog) {
