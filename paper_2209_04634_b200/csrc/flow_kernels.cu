@@ -497,6 +497,9 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
   const int ry = lane / D, ox = lane - (lane / D) * D;
   const bool lane_on = lane < RPG * D;
   const int oxs = lane_on ? ox : 0;
+  int tbj[kPW];  // region offsets of the warp's patch centres
+#pragma unroll
+  for (int j = 0; j < kPW; ++j) tbj[j] = __shfl_sync(kFull, tb, j);
   for (int it = 0; it < p.iterations && solved; ++it) {
     // split tables for the warp's 8 patches (flow.cpp:45-53 on px + u, py + v; u, v finite)
 #pragma unroll
@@ -519,34 +522,43 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
     // = gg*RPG*D + lane): residual products gx*res, gy*res of the warp's 8
     // patches (flow.cpp:202-205), then 16 lanes = (patch, b1|b2) extend the
     // ordered fp64 sums by those k (flow.cpp:204-205, k order kept)
+    // the lane's column split of each patch is the same for every lane group
+    float fxj[kPW];
+    int xj[kPW];
+#pragma unroll
+    for (int j = 0; j < kPW; ++j) {
+      const float2 X = sX[j * D + oxs];
+      fxj[j] = X.y;
+      xj[j] = __float_as_int(X.x);
+    }
     double acc = 0.0;
 #pragma unroll 1
     for (int gg = 0; gg < NG; ++gg) {
       const int oy = gg * RPG + ry;
       const bool on = lane_on && oy < D;
+      const int oyc = oy < D ? oy : 0;  // lanes off the template compute in bounds, store nothing
+      const int loff = (oyc - kR) * pitch + (oxs - kR);
       constexpr int kJB = 4;  // patches per gather batch
-#pragma unroll 1
+#pragma unroll
       for (int jb = 0; jb < kPW; jb += kJB) {
         if (!((solved >> jb) & ((1u << kJB) - 1u))) continue;  // warp-uniform
         float4 q[kJB];
         uint32_t q8[kJB];
-        float fx[kJB], fy[kJB];
+        float fy[kJB];
 #pragma unroll
         for (int jj = 0; jj < kJB; ++jj) {
-          const int j = jb + jj;
-          const float2 X = sX[j * D + oxs];
-          const float2 Y = sY[j * D + (oy < D ? oy : 0)];
-          fx[jj] = X.y;
+          const float2 Y = sY[(jb + jj) * D + oyc];
           fy[jj] = Y.y;
-          const int qi = __float_as_int(Y.x) + __float_as_int(X.x);
+          const int qi = __float_as_int(Y.x) + xj[jb + jj];
           if (kU8) q8[jj] = __ldg(qcurr8 + qi);
           else q[jj] = __ldg(qcurr + qi);
         }
 #pragma unroll
         for (int jj = 0; jj < kJB; ++jj) {
           const int j = jb + jj;
-          const int o = __shfl_sync(kFull, tb, j) + (oy - kR) * pitch + (ox - kR);
-          if (!on || !((solved >> j) & 1u)) continue;
+          if (!((solved >> j) & 1u)) continue;  // warp-uniform
+          const int o = tbj[j] + loff;
+          const float fx = fxj[j];
           float smp;
           if (kU8) {
             // the u8 quad as two fp32x2 pairs (a00, a01), (a10, a11): 2^23 + b
@@ -558,15 +570,18 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
             const f32x2 B1 = pk2(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7541)),
                                  __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7543)));
             const f32x2 A = sub2(B0, pk2(8388608.0f, 8388608.0f));
-            const f32x2 M = mul2(pk2(fx[jj], fx[jj]), sub2(B1, B0));
+            const f32x2 M = mul2(pk2(fx, fx), sub2(B1, B0));
             smp = lerp_ref(__fadd_rn(lo2(A), lo2(M)), __fadd_rn(hi2(A), hi2(M)), fy[jj]);
           } else {
             const float4 a = q[jj];
-            smp = lerp_ref(lerp_ref(a.x, a.y, fx[jj]), lerp_ref(a.z, a.w, fx[jj]), fy[jj]);
+            smp = lerp_ref(lerp_ref(a.x, a.y, fx), lerp_ref(a.z, a.w, fx), fy[jj]);
           }
           const float res = fsub(smp, sP[o]);
-          sB[j * G::S + lane] = fmul(sGx[o], res);
-          sB[G::PO + j * G::S + lane] = fmul(sGy[o], res);
+          const float b1 = fmul(sGx[o], res), b2 = fmul(sGy[o], res);
+          if (on) {
+            sB[j * G::S + lane] = b1;
+            sB[G::PO + j * G::S + lane] = b2;
+          }
         }
       }
       __syncwarp();
