@@ -114,6 +114,34 @@ __device__ __forceinline__ float sample_quad_fast(const uint32_t* __restrict__ q
   return lerp_ref(top, bot, fy);
 }
 
+// ---- register pinning and 32-bit shared addressing for hot loops ----
+// A value passed through a shuffle cannot be rematerialised by ptxas, so a
+// ring base pointer or a constant used in a loop stays in one register
+// instead of being recomputed (64-bit folding, immediate moves) per use.
+template <typename T>
+__device__ __forceinline__ T pin(T v) {
+  static_assert(sizeof(T) == 4 || sizeof(T) == 8, "pin: 32- or 64-bit values");
+  if constexpr (sizeof(T) == 8) {
+    unsigned long long u;
+    memcpy(&u, &v, 8);
+    u = __shfl_sync(0xFFFFFFFFu, u, 0);
+    memcpy(&v, &u, 8);
+  } else {
+    unsigned u;
+    memcpy(&u, &v, 4);
+    u = __shfl_sync(0xFFFFFFFFu, u, 0);
+    memcpy(&v, &u, 4);
+  }
+  return v;
+}
+// ld.shared.f32 [a + kOff] (a: a shared-window byte address)
+template <int kOff>
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(kOff));
+  return v;
+}
+
 // ---- packed fp32x2 (sm_100 FADD2 / FMUL2): two independent IEEE fp32 ops per
 // instruction, each lane rounded exactly like its scalar counterpart ----
 typedef unsigned long long f32x2;

@@ -497,9 +497,14 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
   const int ry = lane / D, ox = lane - (lane / D) * D;
   const bool lane_on = lane < RPG * D;
   const int oxs = lane_on ? ox : 0;
-  int tbj[kPW];  // region offsets of the warp's patch centres
+  uint32_t tbj[kPW];  // region byte offsets of the warp's patch centres
 #pragma unroll
-  for (int j = 0; j < kPW; ++j) tbj[j] = __shfl_sync(kFull, tb, j);
+  for (int j = 0; j < kPW; ++j) tbj[j] = 4u * (uint32_t)__shfl_sync(kFull, tb, j);
+  // pinned: the shared window address of sP, the quad image, the 2^23 byte bias
+  const uint32_t s_addr = pin((uint32_t)__cvta_generic_to_shared(sP));
+  const float4* __restrict__ qcurr_p = kU8 ? nullptr : pin(qcurr);
+  const uint32_t* __restrict__ qcurr8_p = kU8 ? pin(qcurr8) : nullptr;
+  const uint32_t kMagic = pin(0x4B000000u);
   for (int it = 0; it < p.iterations && solved; ++it) {
     // split tables for the warp's 8 patches (flow.cpp:45-53 on px + u, py + v; u, v finite)
 #pragma unroll
@@ -537,7 +542,7 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
       const int oy = gg * RPG + ry;
       const bool on = lane_on && oy < D;
       const int oyc = oy < D ? oy : 0;  // lanes off the template compute in bounds, store nothing
-      const int loff = (oyc - kR) * pitch + (oxs - kR);
+      const uint32_t aoff = s_addr + 4u * (uint32_t)((oyc - kR) * pitch + (oxs - kR));
       constexpr int kJB = 4;  // patches per gather batch
 #pragma unroll
       for (int jb = 0; jb < kPW; jb += kJB) {
@@ -550,14 +555,14 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
           const float2 Y = sY[(jb + jj) * D + oyc];
           fy[jj] = Y.y;
           const int qi = __float_as_int(Y.x) + xj[jb + jj];
-          if (kU8) q8[jj] = __ldg(qcurr8 + qi);
-          else q[jj] = __ldg(qcurr + qi);
+          if (kU8) q8[jj] = __ldg(qcurr8_p + qi);
+          else q[jj] = __ldg(qcurr_p + qi);
         }
 #pragma unroll
         for (int jj = 0; jj < kJB; ++jj) {
           const int j = jb + jj;
           if (!((solved >> j) & 1u)) continue;  // warp-uniform
-          const int o = tbj[j] + loff;
+          const uint32_t ao = aoff + tbj[j];
           const float fx = fxj[j];
           float smp;
           if (kU8) {
@@ -565,10 +570,10 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
             // via PRMT; b - a of biased taps is exact, f*(b-a) one FMUL2, the
             // adds scalar (sample(), flow.cpp:54-56, rounding by rounding)
             const uint32_t v = q8[jj];
-            const f32x2 B0 = pk2(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7540)),
-                                 __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7542)));
-            const f32x2 B1 = pk2(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7541)),
-                                 __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7543)));
+            const f32x2 B0 = pk2(__uint_as_float(__byte_perm(v, kMagic, 0x7540)),
+                                 __uint_as_float(__byte_perm(v, kMagic, 0x7542)));
+            const f32x2 B1 = pk2(__uint_as_float(__byte_perm(v, kMagic, 0x7541)),
+                                 __uint_as_float(__byte_perm(v, kMagic, 0x7543)));
             const f32x2 A = sub2(B0, pk2(8388608.0f, 8388608.0f));
             const f32x2 M = mul2(pk2(fx, fx), sub2(B1, B0));
             smp = lerp_ref(__fadd_rn(lo2(A), lo2(M)), __fadd_rn(hi2(A), hi2(M)), fy[jj]);
@@ -576,8 +581,8 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
             const float4 a = q[jj];
             smp = lerp_ref(lerp_ref(a.x, a.y, fx), lerp_ref(a.z, a.w, fx), fy[jj]);
           }
-          const float res = fsub(smp, sP[o]);
-          const float b1 = fmul(sGx[o], res), b2 = fmul(sGy[o], res);
+          const float res = fsub(smp, lds_f32<0>(ao));
+          const float b1 = fmul(lds_f32<4 * G::plane>(ao), res), b2 = fmul(lds_f32<8 * G::plane>(ao), res);
           if (on) {
             sB[j * G::S + lane] = b1;
             sB[G::PO + j * G::S + lane] = b2;
