@@ -393,7 +393,7 @@ __device__ __forceinline__ int dense_fast(const uint32_t* __restrict__ qp, const
                                           uint32_t w, uint32_t kbias, float wm, float hm, float xf, float yf,
                                           float u, float v, float4 kc, unsigned& bad, unsigned bit) {
   const f32x2 NB = pk2(kc.x, kc.y);
-  f32x2 X = affine2(xf, NB, u), Y = affine2(yf, NB, v);
+  f32x2 X = affine2_est(xf, NB, u), Y = affine2_est(yf, NB, v);
   if (kClamp) {
     X = pk2(fminf(fmaxf(lo2(X), 0.0f), wm), fminf(fmaxf(hi2(X), 0.0f), wm));
     Y = pk2(fminf(fmaxf(lo2(Y), 0.0f), hm), fminf(fmaxf(hi2(Y), 0.0f), hm));
@@ -413,9 +413,9 @@ __device__ __forceinline__ int dense_fast(const uint32_t* __restrict__ qp, const
                         __uint_as_float(__byte_perm(vb, 0x4B000000u, 0x7542)));
   const f32x2 B11 = pk2(__uint_as_float(__byte_perm(va, 0x4B000000u, 0x7543)),
                         __uint_as_float(__byte_perm(vb, 0x4B000000u, 0x7543)));
-  const f32x2 top = lerpd2(sub2(B00, C23), sub2(B10, B00), FX);
-  const f32x2 bot = lerpd2(sub2(B01, C23), sub2(B11, B01), FX);
-  const f32x2 S = lerp2(top, bot, FY);
+  const f32x2 top = lerpd2_est(sub2(B00, C23), sub2(B10, B00), FX);
+  const f32x2 bot = lerpd2_est(sub2(B01, C23), sub2(B11, B01), FX);
+  const f32x2 S = lerp2_est(top, bot, FY);
   // s = RN64(RN64(oma*fp) + RN64(alpha*fc)); e below satisfies |e - s| < 6.2e-5
   // (see DenseProvider::interp), RN(e + c) adds < 1.6e-5.  If
   // floor(e + 0.5 -/+ 2e-4) agree, that floor is lround(s) = floor(s + 0.5).

@@ -199,6 +199,22 @@ __device__ __forceinline__ f32x2 affine2(float c, f32x2 st, float u) {
   return pk2(__fadd_rn(c, lo2(m)), __fadd_rn(c, hi2(m)));
 }
 
+// Estimate-only variants (dense_fast): the final adds as one FADD2.FTZ —
+// ptxas does not contract mul.f32x2 into add.ftz.f32x2.  Flushing a denormal
+// input / result moves a sample by < 255 * 2^-126, far inside the bounded
+// estimate's 2e-4 decision margin, so a decided lane is unaffected; these
+// must not be used where a result has to be exact.
+__device__ __forceinline__ f32x2 add2_ftz(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 lerp2_est(f32x2 a, f32x2 b, f32x2 f) { return add2_ftz(a, mul2(f, sub2(b, a))); }
+__device__ __forceinline__ f32x2 lerpd2_est(f32x2 a, f32x2 d, f32x2 f) { return add2_ftz(a, mul2(f, d)); }
+__device__ __forceinline__ f32x2 affine2_est(float c, f32x2 st, float u) {
+  return add2_ftz(pk2(c, c), mul2(st, pk2(u, u)));
+}
+
 // Two sample_u8 (simulate.cpp:10-26) through quad images at once: lane 0 =
 // (x.lo, y.lo) in qa, lane 1 = (x.hi, y.hi) in qb.  Finite coordinates only.
 __device__ __forceinline__ f32x2 sample_quad_pair(const uint32_t* __restrict__ qa, const uint32_t* __restrict__ qb,
