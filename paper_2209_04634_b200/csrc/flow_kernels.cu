@@ -444,11 +444,31 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
   float2* sX = reinterpret_cast<float2*>(smem + G::t_off) + warp * (2 * kPW * D);  // [kPW][D] (x0, fx)
   float2* sY = sX + kPW * D;                                                        // [kPW][D] (y0*w, fy)
 
-  for (int yy = warp; yy < rh; yy += kLKTileY) {
-    const size_t roff = (size_t)clampi(ry0 + yy, 0, h - 1) * w;
-    for (int xx = lane; xx < rw; xx += 32) {
-      const int sx = clampi(rx0 + xx, 0, w - 1);
-      sP[yy * pitch + xx] = kU8 ? u8f(__ldg(prev8 + roff + sx)) : __ldg(prev + roff + sx);
+  // u8 interior regions (no replicate clamp) of 4-byte aligned rows: aligned
+  // words, four taps each
+  const bool words = kU8 && (w & 3) == 0 && ((uintptr_t)prev8 & 3) == 0 && rx0 >= 0 && ry0 >= 0 &&
+                     rx0 + rw <= w && ry0 + rh <= h;
+  if (words) {
+    const int a0 = rx0 & ~3, nw = (rx0 + rw - a0 + 3) >> 2;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(prev8 + (size_t)ry0 * w + a0);
+    const int wpr = w >> 2;
+    for (int e = t; e < rh * nw; e += kLKThreads) {
+      const int yy = e / nw, wd = e - yy * nw;
+      const uint32_t q = __ldg(src + yy * wpr + wd);
+      const int xx = a0 - rx0 + 4 * wd;  // region column of byte 0 (>= -3)
+      float* dst = sP + yy * pitch + xx;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (xx + b >= 0 && xx + b < rw) dst[b] = __fsub_rn(__uint_as_float(__byte_perm(q, 0x4B000000u, 0x7540 + b)),
+                                                          8388608.0f);
+    }
+  } else {
+    for (int yy = warp; yy < rh; yy += kLKTileY) {
+      const size_t roff = (size_t)clampi(ry0 + yy, 0, h - 1) * w;
+      for (int xx = lane; xx < rw; xx += 32) {
+        const int sx = clampi(rx0 + xx, 0, w - 1);
+        sP[yy * pitch + xx] = kU8 ? u8f(__ldg(prev8 + roff + sx)) : __ldg(prev + roff + sx);
+      }
     }
   }
   // this lane's patch: pl = lane & 7 of tile row `warp` (all four 8-lane parts agree)
