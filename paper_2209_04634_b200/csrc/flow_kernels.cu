@@ -462,6 +462,22 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
         if (xx + b >= 0 && xx + b < rw) dst[b] = __fsub_rn(__uint_as_float(__byte_perm(q, 0x4B000000u, 0x7540 + b)),
                                                           8388608.0f);
     }
+  } else if (!kU8 && (w & 3) == 0 && ((uintptr_t)prev & 15) == 0 && rx0 >= 0 && ry0 >= 0 && rx0 + rw <= w &&
+             ry0 + rh <= h) {
+    // fp32 interior regions: aligned float4 loads
+    const int a0 = rx0 & ~3, nw = (rx0 + rw - a0 + 3) >> 2;
+    const float4* src = reinterpret_cast<const float4*>(prev + (size_t)ry0 * w + a0);
+    const int wpr = w >> 2;
+    for (int e = t; e < rh * nw; e += kLKThreads) {
+      const int yy = e / nw, wd = e - yy * nw;
+      const float4 q = __ldg(src + yy * wpr + wd);
+      const int xx = a0 - rx0 + 4 * wd;
+      float* dst = sP + yy * pitch + xx;
+      if (xx >= 0) dst[0] = q.x;
+      if (xx + 1 >= 0 && xx + 1 < rw) dst[1] = q.y;
+      if (xx + 2 >= 0 && xx + 2 < rw) dst[2] = q.z;
+      if (xx + 3 < rw) dst[3] = q.w;
+    }
   } else {
     for (int yy = warp; yy < rh; yy += kLKTileY) {
       const size_t roff = (size_t)clampi(ry0 + yy, 0, h - 1) * w;
