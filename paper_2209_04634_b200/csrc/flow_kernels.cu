@@ -83,6 +83,41 @@ __global__ void pyramid_level_kernel(PyramidParams p, int l) {
   }
 }
 
+// Level 0 of the dense path when it is only the u8 quad image (u8_level0,
+// no texels): four pixels per thread from one aligned word per row (the next
+// column's byte from the neighbouring lane), one 16-byte store per row.
+// Needs w % 4 == 0; same bytes as pyramid_level_kernel's qu8 output.
+__global__ void quad_level0_kernel(PyramidParams p) {
+  const int w = p.dims[0].w, h = p.dims[0].h;
+  const int slot = (p.slot0 + (int)blockIdx.z) % p.R;
+  const uint8_t* f = p.frames.at(slot);
+  uint32_t* q = p.quad_u8.at(slot);
+  const int x4 = 4 * (int)(blockIdx.x * blockDim.x + threadIdx.x);
+  const int lane = threadIdx.x & 31;
+  const bool in = x4 < w, last = x4 + 4 >= w;  // last: column x4 + 4 replicates x4 + 3
+  const int yb = blockIdx.y * kPyrRows, ye = min(yb + kPyrRows, h);
+  auto load = [&](int y, uint32_t& wd, uint32_t& nb) {
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(f + (size_t)y * w) + (x4 >> 2);
+    wd = in ? __ldg(row) : 0u;
+    uint32_t nx = __shfl_down_sync(kFull, wd, 1);
+    if (lane == 31 && !last) nx = __ldg(row + 1);
+    nb = last ? (wd >> 24) : (nx & 0xFFu);
+  };
+  uint32_t w0, n0, w1, n1;
+  load(yb, w0, n0);
+  for (int y = yb; y < ye; ++y) {
+    load(min(y + 1, h - 1), w1, n1);
+    if (in) {
+      const uint32_t t0 = __byte_perm(w0, n0, 0x0043), t1 = __byte_perm(w1, n1, 0x0043);
+      const uint4 o = make_uint4(__byte_perm(w0, w1, 0x5410), __byte_perm(w0, w1, 0x6521),
+                                 __byte_perm(w0, w1, 0x7632), __byte_perm(t0, t1, 0x5410));
+      *reinterpret_cast<uint4*>(q + (size_t)y * w + x4) = o;
+    }
+    w0 = w1;
+    n0 = n1;
+  }
+}
+
 // Quad image of a u8 frame only (stateless interpolation entry point).
 __global__ void build_quad_kernel(const uint8_t* __restrict__ src, uint32_t* __restrict__ dst, int w, int h) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -838,7 +873,14 @@ __global__ void __launch_bounds__(128) sparse_lk_kernel(SparseLKParams p) {
 void launch_pyramid(const PyramidParams& p, int n_frames, cudaStream_t s) {
   if (n_frames <= 0) return;
   for (int l = 0; l < p.levels; ++l) {
-    dim3 g((p.dims[l].w + 127) / 128, (p.dims[l].h + kPyrRows - 1) / kPyrRows, n_frames);
+    const int w = p.dims[l].w;
+    if (l == 0 && p.u8_level0 && p.quad_u8.base && !p.tex[0].base && (w & 3) == 0 &&
+        ((uintptr_t)p.frames.base & 3) == 0 && ((uintptr_t)p.quad_u8.base & 15) == 0) {
+      dim3 g((w / 4 + 127) / 128, (p.dims[0].h + kPyrRows - 1) / kPyrRows, n_frames);
+      quad_level0_kernel<<<g, 128, 0, s>>>(p);
+      continue;
+    }
+    dim3 g((w + 127) / 128, (p.dims[l].h + kPyrRows - 1) / kPyrRows, n_frames);
     pyramid_level_kernel<<<g, 128, 0, s>>>(p, l);
   }
 }
