@@ -1573,8 +1573,8 @@ static void launch_chain_dense(const ChainParams& p, size_t sm, cudaStream_t s) 
   const int n_int = std::min(p.d.n_links, p.n_interp - p.d.start);
   const bool five = n_int % 5 == 0 && n_int % 4 != 0;
   if (p.words_per_warp == 1) {
-    if (five) launch_chain_dense_b<kLog, kMag, 5, 1, 4>(p, sm, s);
-    else launch_chain_dense_b<kLog, kMag, 4, 1, 4>(p, sm, s);
+    if (five) launch_chain_dense_b<kLog, kMag, 5, 1, 3>(p, sm, s);
+    else launch_chain_dense_b<kLog, kMag, 4, 1, 3>(p, sm, s);
   } else {
     if (five) launch_chain_dense_b<kLog, kMag, 5, 2, 3>(p, sm, s);
     else launch_chain_dense_b<kLog, kMag, 4, 2, 3>(p, sm, s);
