@@ -1576,8 +1576,8 @@ static void launch_chain_dense(const ChainParams& p, size_t sm, cudaStream_t s) 
     if (five) launch_chain_dense_b<kLog, kMag, 5, 1, 3>(p, sm, s);
     else launch_chain_dense_b<kLog, kMag, 4, 1, 3>(p, sm, s);
   } else {
-    if (five) launch_chain_dense_b<kLog, kMag, 5, 2, 3>(p, sm, s);
-    else launch_chain_dense_b<kLog, kMag, 4, 2, 3>(p, sm, s);
+    if (five) launch_chain_dense_b<kLog, kMag, 5, 2, 2>(p, sm, s);
+    else launch_chain_dense_b<kLog, kMag, 4, 2, 2>(p, sm, s);
   }
 }
 
