@@ -1115,6 +1115,13 @@ __global__ void __launch_bounds__(1024) segbase_kernel(EmitParams p, int64_t* se
   }
 }
 
+// Predicated global store without a branch (the dense-word expansion's
+// per-lane "has an event" condition).
+__device__ __forceinline__ void st_global_if(uint32_t* ptr, uint32_t v, uint32_t cond) {
+  asm volatile("{.reg .pred q; setp.ne.u32 q, %2, 0; @q st.global.u32 [%0], %1;}" ::"l"(ptr), "r"(v), "r"(cond)
+               : "memory");
+}
+
 // ------------------------------------------------------------ emit kernel
 //
 // Writes every event once, in the reference's order (t, y, x, p).  The
@@ -1131,6 +1138,8 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
   __shared__ int s_item[256];
   __shared__ int64_t s_dst[256];
   __shared__ int s_nwork;
+  __shared__ uint4 s_wd[kWarpsPerBlock][32];      // dense-word expansion: (all, pos, x|row<<16, -)
+  __shared__ uint32_t* s_wptr[kWarpsPerBlock][32];  // and the word's first output record
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int S = *p.seg.n_segs;
@@ -1224,6 +1233,33 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
       // and its (x0, row) in one word (x < 2^16, row < 2^15)
       const long long base = (long long)dst - excl;
       const uint32_t xr = (uint32_t)x0 | ((uint32_t)(p.row0 + lrow) << 16);
+      const unsigned nzw = __ballot_sync(kFull, c > 0);
+      const int nnz = __popc(nzw);
+      if (T >= 5 * nnz && nnz >= 16) {
+        // dense words (>= 5 events each on average, most words non-empty):
+        // word by word with lanes = its pixels — rank = popc below the lane,
+        // one coalesced run per word, no per-event search; four independent
+        // words per step
+        s_wd[warp][lane] = make_uint4(all, all & ~pos, xr, 0u);  // (events, negative events, x0 | row << 16)
+        s_wptr[warp][lane] = p.out + dst;
+        __syncwarp();
+        const uint32_t bit = 1u << lane, below = bit - 1u;
+#pragma unroll 1
+        for (int k0 = 0; k0 < 32; k0 += 4) {
+          uint4 wd[4];
+          uint32_t* wp[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            wd[k] = s_wd[warp][k0 + k];
+            wp[k] = s_wptr[warp][k0 + k];
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k)  // x0 is a multiple of 32: x0 + lane = x0 | lane
+            st_global_if(wp[k] + __popc(wd[k].x & below), wd[k].z | (uint32_t)lane | ((wd[k].y >> lane) << 31),
+                         wd[k].x & bit);
+        }
+        __syncwarp();
+      } else
       for (int q = lane; q - lane < T; q += 32) {
         // first lane l with incl[l] > q
         int lo = 0;
