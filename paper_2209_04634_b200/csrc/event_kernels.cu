@@ -422,7 +422,7 @@ __device__ __forceinline__ int dense_fast(const uint32_t* __restrict__ qp, const
   const float e = __fmaf_rn(kc.z, lo2(S), __fmul_rn(kc.w, hi2(S)));
   const f32x2 T = add2_rz(add2(pk2(e, e), pk2(0.5f - 2e-4f, 0.5f + 2e-4f)), C23);
   if (__float_as_uint(lo2(T)) != __float_as_uint(hi2(T))) bad |= bit;
-  return __float_as_int(hi2(T)) - 0x4B000000;
+  return __float_as_int(hi2(T));  // kVB + value (the bias folds into the LUT address / cancels in differences)
 }
 
 // The exact reference expression for the lanes dense_fast cannot decide.
@@ -435,6 +435,9 @@ __device__ __noinline__ int dense_exact(const float2* nfb, const double* oma, co
   const double blend = dadd(dmul(__ldg(oma + k), (double)lo2(S)), dmul(__ldg(alpha + k), (double)hi2(S)));
   return lround_pos_fast(blend);
 }
+
+// chain values in the dense kernel carry this bias: the fp32 bits of 2^23 + v
+constexpr int kVB = 0x4B000000;
 
 struct DenseWord {
   bool have, valid;
@@ -483,6 +486,31 @@ __device__ __forceinline__ uint2 link_rule(const ChainParams& p, const float* s_
   return make_uint2(bp, bn);
 }
 
+// link_rule for single mode in the dense kernel, on biased values: the log
+// rule's LUT read folds the bias into the shared-window base (lut_b); lanes
+// past the row end hold ref = NaN (no comparison holds, ref never changes),
+// so validity needs no per-link test in log mode.  Event counts are taken
+// from the masks when they are flushed.
+template <bool kLog>
+__device__ __forceinline__ uint2 dense_rule(const ChainParams& p, uint32_t lut_b, const DenseWord& c, int val,
+                                            float& ref, int& before) {
+  bool pos, neg;
+  if (kLog) {
+    float lk;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(lk) : "r"(lut_b + ((uint32_t)val << 2)));
+    const float dd = fsub(lk, ref);
+    pos = dd > p.c_pos_log;  // c_pos_log > 0 > c_neg_log (validated): exclusive
+    neg = dd < p.c_neg_log;
+    if (pos || neg) ref = lk;
+  } else {
+    const int d = val - before;  // difference_frame, core.cpp:14-15 (biases cancel)
+    pos = d > p.c_pos && c.valid;  // threshold_events_into, core.cpp:31-43
+    neg = d < p.c_neg && c.valid;
+    before = val;
+  }
+  return make_uint2(__ballot_sync(kFull, pos), __ballot_sync(kFull, neg));
+}
+
 template <int kW, int kNB, bool kClamp, int kBM>
 __device__ __forceinline__ unsigned dense_batch(const float4* s_kc, const uint32_t* qp, const uint32_t* qc,
                                                 uint32_t w, uint32_t kbias, float wm, float hm, const DenseWord* c,
@@ -507,7 +535,7 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
   __shared__ float s_lut[256];
   constexpr int kStage = 32 + kB;  // staged links of a warp: < 32 before a batch of kB
   __shared__ uint2 s_stm[kWarpsPerBlock][kW][kStage];
-  __shared__ uint32_t s_stc[kWarpsPerBlock][kStage];
+  __shared__ uint32_t s_stc[kMag ? kWarpsPerBlock : 1][kMag ? kStage : 1];
   __shared__ uint32_t s_stw[kMag ? kWarpsPerBlock : 1][kW][kMag ? kStage : 1];
   const int L = p.d.n_links, G = L * p.n_pairs, N = p.n_interp;
   float4* s_kc = s_dyn4;                                       // [N + 2]
@@ -521,6 +549,7 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
   const uint32_t w = (uint32_t)p.w;
   const float wm = (float)(p.w - 1), hm = (float)(p.h - 1);
   const uint32_t kbias = 0u - 0x4B000000u * (w + 1u);
+  const uint32_t lut_b = pin((uint32_t)__cvta_generic_to_shared(s_lut) - ((uint32_t)kVB << 2));
   // link l joins chain frames start + l and start + l + 1; the first n_int
   // links end in an interpolated frame (k <= N), a last one (endpoints) in curr
   const int kfirst = p.d.start + 1;
@@ -545,7 +574,7 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
       c[q].pix = (uint32_t)c[q].y * w + (uint32_t)c[q].x;
       c[q].xf = (float)c[q].x;
       c[q].yf = (float)c[q].y;
-      ref[q] = kLog ? p.ref[c[q].pix] : 0.0f;
+      ref[q] = kLog ? (c[q].valid ? p.ref[c[q].pix] : __int_as_float(0x7FC00000)) : 0.0f;
       before[q] = 0;
     }
     int sp = p.r0 % p.R;
@@ -570,8 +599,9 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
         // monotone and the bounds are representable): no clamp needed
         safe = safe && fabsf(prov.u) <= fminf(c[q].xf, wm - c[q].xf) && fabsf(prov.v) <= fminf(c[q].yf, hm - c[q].yf);
         if (!kLog)
-          before[q] = p.d.start == 0 ? (int)p.frames.at(sp)[c[q].pix]
-                                     : dense_exact(p.nfb, p.oma, p.alpha, qp, qc, p.w, p.h, c[q].xf, c[q].yf, prov.u, prov.v, 1);
+          before[q] = kVB + (p.d.start == 0 ? (int)p.frames.at(sp)[c[q].pix]
+                                            : dense_exact(p.nfb, p.oma, p.alpha, qp, qc, p.w, p.h, c[q].xf, c[q].yf,
+                                                          prov.u, prov.v, 1));
       }
       safe = __all_sync(kFull, safe);
       const int gbase = i * L;
@@ -580,13 +610,20 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
       // lane j stores / adds staged link j
       int fbase = 0;
       auto step = [&](int l, int q, int val) {
-        uint32_t ev;
-        const uint2 m = link_rule<kLog, kMag>(p, s_lut, gbase + l, c[q], lane, val, ref[q], before[q], ev);
-        if (lane == 0) {
-          s_stm[warp][q][l - fbase] = m;
-          if (kMag) s_stw[warp][q][l - fbase] = ev;
-          if (q == 0) s_stc[warp][l - fbase] = ev;
-          else s_stc[warp][l - fbase] += ev;
+        if (kMag) {
+          uint32_t ev;
+          int bv = before[q] - kVB;
+          const uint2 m = link_rule<kLog, kMag>(p, s_lut, gbase + l, c[q], lane, val - kVB, ref[q], bv, ev);
+          before[q] = bv + kVB;
+          if (lane == 0) {
+            s_stm[warp][q][l - fbase] = m;
+            s_stw[warp][q][l - fbase] = ev;
+            if (q == 0) s_stc[warp][l - fbase] = ev;
+            else s_stc[warp][l - fbase] += ev;
+          }
+        } else {
+          const uint2 m = dense_rule<kLog>(p, lut_b, c[q], val, ref[q], before[q]);
+          if (lane == 0) s_stm[warp][q][l - fbase] = m;
         }
       };
       auto flush = [&](int lend, bool force) {
@@ -595,13 +632,16 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
         __syncwarp();
         for (int j = lane; j < n; j += 32) {
           const int g = gbase + fbase + j;
+          uint32_t cnt = 0;
 #pragma unroll
           for (int q = 0; q < kW; ++q) {
             if (!c[q].have) continue;
-            p.masks[(size_t)g * p.n_words + c[q].wi] = s_stm[warp][q][j];
+            const uint2 m = s_stm[warp][q][j];
+            p.masks[(size_t)g * p.n_words + c[q].wi] = m;
             if (kMag) p.wcount[(size_t)g * p.n_words + c[q].wi] = s_stw[warp][q][j];
+            else cnt += __popc(m.x | m.y);  // a pixel crosses one way or not at all
           }
-          const uint32_t cnt = s_stc[warp][j];
+          if (kMag) cnt = s_stc[warp][j];
           if (cnt) atomicAdd(&s_cnt[g], cnt);
         }
         __syncwarp();
@@ -635,21 +675,28 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
 #pragma unroll
             for (int j = 0; j < kB; ++j)
               if ((bad >> (q * kB + j)) & 1u)
-                vals[q][j] = dense_exact(p.nfb, p.oma, p.alpha, qp, qc, p.w, p.h, c[q].xf, c[q].yf, c[q].u, c[q].v,
-                                       kfirst + l0 + j);
+                vals[q][j] = kVB + dense_exact(p.nfb, p.oma, p.alpha, qp, qc, p.w, p.h, c[q].xf, c[q].yf, c[q].u,
+                                             c[q].v, kfirst + l0 + j);
         }
+        if (nb == kB) {
 #pragma unroll
-        for (int j = 0; j < kB; ++j) {
-          if (j >= nb) break;
+          for (int j = 0; j < kB; ++j)
 #pragma unroll
-          for (int q = 0; q < kW; ++q) step(l0 + j, q, vals[q][j]);
+            for (int q = 0; q < kW; ++q) step(l0 + j, q, vals[q][j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < kB; ++j) {
+            if (j >= nb) break;
+#pragma unroll
+            for (int q = 0; q < kW; ++q) step(l0 + j, q, vals[q][j]);
+          }
         }
         flush(l0 + nb, false);
       }
       if (n_int < L) {  // the link into curr (include_endpoints)
         const uint8_t* curr = p.frames.at(sc);
 #pragma unroll
-        for (int q = 0; q < kW; ++q) step(L - 1, q, (int)curr[c[q].pix]);
+        for (int q = 0; q < kW; ++q) step(L - 1, q, kVB + (int)curr[c[q].pix]);
       }
       flush(L, true);
       sp = sc;
