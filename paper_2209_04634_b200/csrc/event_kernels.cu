@@ -387,10 +387,13 @@ __global__ void __launch_bounds__(256, kMinBlocks) chain_kernel(ChainParams p) {
 
 // Rounded blend of chain frame k (simulate.cpp:108-116) at one pixel.
 //   X = x + (-fwd, bwd) * u, Y likewise: (prev sample, curr sample) as lanes.
-// kbias folds the 2^23 magic of both truncations out of the gather index.
+// The truncations use the magic 2^23 for X and my = 2^23 + m_y for Y
+// (ChainParams::magic_y); the gather index TY_bits * w + TX_bits then equals
+// y * w + x + qshift without wrapping, and qp / qc come pre-shifted by
+// -qshift elements, so the index costs one IMAD.
 template <bool kClamp>
 __device__ __forceinline__ int dense_fast(const uint32_t* __restrict__ qp, const uint32_t* __restrict__ qc,
-                                          uint32_t w, uint32_t kbias, float wm, float hm, float xf, float yf,
+                                          uint32_t w, float my, float wm, float hm, float xf, float yf,
                                           float u, float v, float4 kc, unsigned& bad, unsigned bit) {
   const f32x2 NB = pk2(kc.x, kc.y);
   f32x2 X = affine2_est(xf, NB, u), Y = affine2_est(yf, NB, v);
@@ -399,10 +402,11 @@ __device__ __forceinline__ int dense_fast(const uint32_t* __restrict__ qp, const
     Y = pk2(fminf(fmaxf(lo2(Y), 0.0f), hm), fminf(fmaxf(hi2(Y), 0.0f), hm));
   }
   const f32x2 C23 = pk2(8388608.0f, 8388608.0f);
-  const f32x2 TX = add2_rz(X, C23), TY = add2_rz(Y, C23);  // 2^23 + trunc
-  const f32x2 FX = sub2(X, sub2(TX, C23)), FY = sub2(Y, sub2(TY, C23));
-  const uint32_t ia = __float_as_uint(lo2(TY)) * w + __float_as_uint(lo2(TX)) + kbias;
-  const uint32_t ib = __float_as_uint(hi2(TY)) * w + __float_as_uint(hi2(TX)) + kbias;
+  const f32x2 CY = pk2(my, my);
+  const f32x2 TX = add2_rz(X, C23), TY = add2_rz(Y, CY);  // magic + trunc
+  const f32x2 FX = sub2(X, sub2(TX, C23)), FY = sub2(Y, sub2(TY, CY));
+  const uint32_t ia = __float_as_uint(lo2(TY)) * w + __float_as_uint(lo2(TX));
+  const uint32_t ib = __float_as_uint(hi2(TY)) * w + __float_as_uint(hi2(TX));
   const uint32_t va = __ldg(qp + ia), vb = __ldg(qc + ib);
   // taps as 2^23 + byte (PRMT); differences of biased taps are exact
   const f32x2 B00 = pk2(__uint_as_float(__byte_perm(va, 0x4B000000u, 0x7540)),
@@ -513,7 +517,7 @@ __device__ __forceinline__ uint2 dense_rule(const ChainParams& p, uint32_t lut_b
 
 template <int kW, int kNB, bool kClamp, int kBM>
 __device__ __forceinline__ unsigned dense_batch(const float4* s_kc, const uint32_t* qp, const uint32_t* qc,
-                                                uint32_t w, uint32_t kbias, float wm, float hm, const DenseWord* c,
+                                                uint32_t w, float my, float wm, float hm, const DenseWord* c,
                                                 int k0, int (&vals)[kW][kBM]) {
   unsigned bad = 0;
 #pragma unroll
@@ -521,7 +525,7 @@ __device__ __forceinline__ unsigned dense_batch(const float4* s_kc, const uint32
     const float4 kc = s_kc[k0 + j];
 #pragma unroll
     for (int q = 0; q < kW; ++q)
-      vals[q][j] = dense_fast<kClamp>(qp, qc, w, kbias, wm, hm, c[q].xf, c[q].yf, c[q].u, c[q].v, kc, bad,
+      vals[q][j] = dense_fast<kClamp>(qp, qc, w, my, wm, hm, c[q].xf, c[q].yf, c[q].u, c[q].v, kc, bad,
                                       1u << (q * kBM + j));
   }
   return bad;
@@ -548,7 +552,7 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t w = (uint32_t)p.w;
   const float wm = (float)(p.w - 1), hm = (float)(p.h - 1);
-  const uint32_t kbias = 0u - 0x4B000000u * (w + 1u);
+  const float my = p.magic_y;
   const uint32_t lut_b = pin((uint32_t)__cvta_generic_to_shared(s_lut) - ((uint32_t)kVB << 2));
   // link l joins chain frames start + l and start + l + 1; the first n_int
   // links end in an interpolated frame (k <= N), a last one (endpoints) in curr
@@ -582,6 +586,8 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
       const int sc = sp + 1 == p.R ? 0 : sp + 1;
       const uint32_t* qp = p.quads.at(sp);
       const uint32_t* qc = p.quads.at(sc);
+      const uint32_t* qbp = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(qp) - 4ull * p.qshift);
+      const uint32_t* qbc = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(qc) - 4ull * p.qshift);
       PairCtx pc{};
       pc.pu = p.g0.pu + (size_t)i * p.g0.pair_stride;
       pc.pv = p.g0.pv + (size_t)i * p.g0.pair_stride;
@@ -653,14 +659,14 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
         int vals[kW][kB];
         unsigned bad;
         if (nb == kB) {
-          bad = safe ? dense_batch<kW, kB, false>(s_kc, qp, qc, w, kbias, wm, hm, c, kfirst + l0, vals)
-                     : dense_batch<kW, kB, true>(s_kc, qp, qc, w, kbias, wm, hm, c, kfirst + l0, vals);
+          bad = safe ? dense_batch<kW, kB, false>(s_kc, qbp, qbc, w, my, wm, hm, c, kfirst + l0, vals)
+                     : dense_batch<kW, kB, true>(s_kc, qbp, qbc, w, my, wm, hm, c, kfirst + l0, vals);
         } else {
           bad = 0;
           for (int j = 0; j < nb; ++j) {
             int v1[kW][kB];
-            bad |= (safe ? dense_batch<kW, 1, false>(s_kc, qp, qc, w, kbias, wm, hm, c, kfirst + l0 + j, v1)
-                         : dense_batch<kW, 1, true>(s_kc, qp, qc, w, kbias, wm, hm, c, kfirst + l0 + j, v1))
+            bad |= (safe ? dense_batch<kW, 1, false>(s_kc, qbp, qbc, w, my, wm, hm, c, kfirst + l0 + j, v1)
+                         : dense_batch<kW, 1, true>(s_kc, qbp, qbc, w, my, wm, hm, c, kfirst + l0 + j, v1))
                    << j;
 #pragma unroll
             for (int q = 0; q < kW; ++q)
@@ -1129,6 +1135,28 @@ __global__ void __launch_bounds__(256) offsets_kernel(OffsetParams p) {
     carry += __shfl_sync(kFull, x, 31);
   }
   if (lane == 0) p.link_total[row] = carry;
+}
+
+// Few link rows (large frames, few pairs per launch: c5 has 33 rows of ~1.2k
+// blocks): one block per row, each thread a contiguous run of the row's
+// counts, one block scan — instead of one warp walking the row 32 at a time.
+__global__ void __launch_bounds__(256) offsets_row_kernel(OffsetParams p) {
+  __shared__ int64_t s_warp[32];
+  const int row = blockIdx.x;
+  const uint32_t* src = p.counts + (size_t)row * p.n_blocks;
+  int64_t* dst = p.prefix + (size_t)row * p.n_blocks;
+  const int per = (p.n_blocks + blockDim.x - 1) / blockDim.x;
+  const int b0 = min((int)threadIdx.x * per, p.n_blocks), b1 = min(b0 + per, p.n_blocks);
+  int64_t sum = 0;
+  for (int b = b0; b < b1; ++b) sum += src[b];
+  int64_t tot;
+  int64_t run = block_exclusive_scan(sum, s_warp, tot);
+  for (int b = b0; b < b1; ++b) {
+    const uint32_t c = src[b];
+    dst[b] = run;
+    run += c;
+  }
+  if (threadIdx.x == 0) p.link_total[row] = tot;
 }
 
 // Segment bases: exclusive scan of the segment totals (one block); also the
@@ -1729,7 +1757,8 @@ void launch_segments(const SegParams& p, cudaStream_t s) { segments_kernel<<<1, 
 
 void launch_offsets(const OffsetParams& p, cudaStream_t s) {
   if (p.n_rows <= 0) return;
-  offsets_kernel<<<(p.n_rows + kWarpsPerBlock - 1) / kWarpsPerBlock, 256, 0, s>>>(p);
+  if (p.n_rows < 4 * 148) offsets_row_kernel<<<p.n_rows, 256, 0, s>>>(p);
+  else offsets_kernel<<<(p.n_rows + kWarpsPerBlock - 1) / kWarpsPerBlock, 256, 0, s>>>(p);
 }
 
 // segbase_kernel then emit_kernel; segbase: [links] int64 scratch

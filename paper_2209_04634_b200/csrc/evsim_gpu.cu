@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <memory>
 #include <new>
 #include <stdexcept>
@@ -776,6 +777,25 @@ struct evsim_gpu_sim {
     c.r0 = r0;
     c.frames = Ring<const uint8_t>{frames.as<uint8_t>(), P};
     c.quads = Ring<const uint32_t>{quads.as<uint32_t>(), P};
+    {
+      // gather index of the dense chain: TY_bits * w + TX_bits with TX =
+      // 2^23 + x, TY = 2^23 + m_y + y (fp32 bits); it equals y * w + x +
+      // qshift without wrapping when qshift + P <= 2^32.  m_y = 0 almost
+      // always; otherwise the smallest m_y that wraps qshift below w (it
+      // exists for every frame the size checks accept)
+      const uint64_t M = 0x4B000000ull, w64 = (uint64_t)w;
+      uint64_t m = 0, K = (M * w64 + M) & 0xFFFFFFFFull;
+      // EVSIM_TEST_MAGIC_Y=1 forces the m_y > 0 form (tested on small frames)
+      const char* force = std::getenv("EVSIM_TEST_MAGIC_Y");
+      const uint64_t m_wrap = ((1ull << 32) - K + w64 - 1) / w64;
+      if (K + P > (1ull << 32) || (force && force[0] == '1' && m_wrap + (uint64_t)h <= (1ull << 23))) {
+        m = m_wrap;
+        K = (K + m * w64) & 0xFFFFFFFFull;
+      }
+      if (m + (uint64_t)h > (1ull << 23) || K + P > (1ull << 32)) runtime("push_frame: no gather bias for this frame size");
+      c.magic_y = (float)(8388608ull + m);
+      c.qshift = (uint32_t)K;
+    }
     const int K = N + 2;
     c.kc = consts.as<float4>();
     c.alpha = reinterpret_cast<const double*>(c.kc + K);

@@ -134,6 +134,8 @@ struct ChainParams {
   int R, r0;
   Ring<const uint8_t> frames;
   Ring<const uint32_t> quads;  // u8 quad images (dense provider)
+  float magic_y;               // dense chain: Y truncation magic 2^23 + m_y (exact integer float)
+  uint32_t qshift;             // dense chain: (bits(2^23 + m_y) * w + bits(2^23)) mod 2^32, + w*h <= 2^32
   // dense provider, grid form (level-0 patch grid + tables; per-pair pu/pv)
   GridGeom g0;
   // dense provider, field form (caller-supplied flow, single pair)

@@ -55,3 +55,24 @@ def test_random_streams(oracle, seed):
         got.append(sim.push_frames(frames[a:b], ts[a:b]).events)
         a = b
     assert_same_events(concat(got), exp, what=f"seed {seed}: {m.name} mode={mode} N={N} {w}x{h} n={n}")
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_dense_gather_bias_wrap_form(oracle, seed, monkeypatch):
+    """The dense chain's gather index with a non-zero Y magic (the form used
+    when qshift + P would exceed 2^32; forced here on small frames)."""
+    monkeypatch.setenv("EVSIM_TEST_MAGIC_Y", "1")
+    rng = np.random.default_rng(5000 + seed)
+    w = int(rng.choice([600, 640, 641, 700, 1000]))  # m_y < 2^23 needs w > ~512
+    h = int(rng.choice([3, 17, 40]))
+    n = int(rng.integers(2, 5))
+    mode = int(rng.integers(0, 2))
+    N = int(rng.choice([1, 5, 10]))
+    cfg = make_config(Method.dense, n_interp=N, contrast_mode=mode, include_endpoints=int(rng.integers(0, 2)),
+                      c_pos_log=0.1, c_neg_log=-0.1)
+    frames = _frames(rng, n, w, h)
+    ts = np.cumsum(rng.choice([1, 1000, 33333], size=n)).astype(np.int64)
+    exp = concat(run_oracle_stream(oracle, cfg, frames, ts))
+    sim = Simulator(SimulatorConfig.from_c(cfg))
+    got = sim.push_frames(frames, ts).events
+    assert_same_events(got, exp, what=f"seed {seed}: dense mode={mode} N={N} {w}x{h} n={n} (magic_y form)")
