@@ -246,7 +246,10 @@ enum {
   EVSIM_STAGE_EMIT = 5,    /* ordered event compaction                */
   EVSIM_N_STAGES = 6
 };
-/* enable != 0 starts per-stage event timing (and clears the totals). */
+/* enable != 0 starts per-stage event timing (and clears the totals).  While
+ * enabled, a dense push runs its stages serially on the handle's stream (the
+ * flow of the next sub-batch no longer overlaps the chain of the current one),
+ * so stage times add up to the push time. */
 EVSIM_GPU_API int evsim_gpu_set_profiling(evsim_gpu_sim* sim, int32_t enable);
 /* Accumulated device milliseconds per stage and number of timed pushes
  * since profiling was enabled (waits for queued work). */

@@ -366,7 +366,8 @@ struct FlowEngine {
   // estimate_dense_flow's level loop, flow.cpp:268-275, for n_pairs pairs;
   // result = per-pair level-0 patch grids
   // frames8 / quads8: the u8 frame and u8 quad rings (level 0 when u8_level0)
-  int solve(int r0, int n_pairs, const uint8_t* frames8, const uint32_t* quads8, cudaStream_t s) {
+  // pair_off: the pairs' first grid slot (sub-batches of one launch)
+  int solve(int r0, int n_pairs, const uint8_t* frames8, const uint32_t* quads8, cudaStream_t s, int pair_off = 0) {
     for (int l = levels - 1; l >= 0; --l) {
       DenseLKParams p{};
       if (l == 0 && u8_level0) {
@@ -375,8 +376,14 @@ struct FlowEngine {
         p.qcurr8 = Ring<const uint32_t>{quads8, (size_t)w * h};
       }
       p.g = geom[l];
+      p.g.pu += (size_t)pair_off * geom[l].pair_stride;
+      p.g.pv += (size_t)pair_off * geom[l].pair_stride;
       p.has_coarse = l != levels - 1;
-      if (p.has_coarse) p.coarse = geom[l + 1];
+      if (p.has_coarse) {
+        p.coarse = geom[l + 1];
+        p.coarse.pu += (size_t)pair_off * geom[l + 1].pair_stride;
+        p.coarse.pv += (size_t)pair_off * geom[l + 1].pair_stride;
+      }
       const size_t pl = (size_t)dims[l].w * dims[l].h;
       p.prev = Ring<const float>{pyr[l].as<float>(), pl};
       p.qcurr = Ring<const float4>{qpyr[l].as<float4>(), pl};
@@ -426,7 +433,8 @@ struct EventEngine {
 
   // fine = true (dense, small frames): 8 words per block, one word per warp —
   // finer tasks balance the few waves of a small frame (measured: c2 chain
-  // 16.4 -> 15.0 us/frame); large frames keep 2-word tasks and ~8 blocks/SM
+  // 16.4 -> 15.0 us/frame; 1080p c4 124 -> 112); 4K frames keep 2-word tasks
+  // and ~8 blocks/SM (c5: 815 vs 843 us/frame with 1-word tasks)
   void geometry(int w_, int h_, bool fine = false) {
     w = w_;
     h = h_;
@@ -437,7 +445,7 @@ struct EventEngine {
     int64_t per = (n_words + target - 1) / target;
     per = std::max<int64_t>(kWarpsPerBlock, (per + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock);
     words_per_warp = 2;
-    if (fine && (n_words + 7) / 8 <= 4096) {
+    if (fine && (n_words + 7) / 8 <= 8192) {
       per = 8;
       words_per_warp = 1;
     }
@@ -531,6 +539,12 @@ struct evsim_gpu_sim {
   bool pending = false;
   EmitParams last_emit{};
 
+  // dense flow / chain pipeline of one push: the flow of sub-batch b+1 runs
+  // on s_flow while the chain of sub-batch b runs on `stream` (the chain's
+  // per-pixel state orders the chains; the flows are independent)
+  cudaStream_t s_flow = nullptr;
+  std::vector<cudaEvent_t> pipe_ev;  // [0]: inputs ready; [1 + b]: flow of sub-batch b done
+
   // per-stage CUDA-event timing (evsim_gpu_set_profiling)
   using EvGroup = std::array<cudaEvent_t, EVSIM_N_STAGES + 1>;
   bool profiling = false;
@@ -545,6 +559,8 @@ struct evsim_gpu_sim {
     if (h_seg_out) cudaFreeHost(h_seg_out);
     for (auto& b : h_seg2)
       if (b) cudaFreeHost(b);
+    if (s_flow) cudaStreamSynchronize(s_flow), cudaStreamDestroy(s_flow);
+    for (auto e : pipe_ev) cudaEventDestroy(e);
     if (s_in) cudaStreamSynchronize(s_in), cudaStreamDestroy(s_in);
     if (s_out) cudaStreamSynchronize(s_out), cudaStreamDestroy(s_out);
     for (auto& g : ev_pool)
@@ -826,7 +842,10 @@ struct evsim_gpu_sim {
   // readback.  ts: n_pairs + 1 frame timestamps.
   // continue_call: this launch's events follow those of the previous launch of
   // the same call (streamed chunks); otherwise they start at offset 0.
-  void run_events(ChainParams& c, int provider, const int64_t* ts, int64_t* h_seg, bool continue_call = false) {
+  // sub: sub-batch boundaries (pairs) when the flow is pipelined (empty: one
+  // chain launch); the chain of sub-batch b waits for pipe_ev[1 + b]
+  void run_events(ChainParams& c, int provider, const int64_t* ts, int64_t* h_seg, bool continue_call = false,
+                  const std::vector<int>& sub = {}) {
     const int G = c.d.n_links * c.n_pairs;
     if (!continue_call) CK(cudaMemsetAsync(ev.base.p, 0, sizeof(int64_t), stream));
     SegParams sp{};
@@ -837,8 +856,30 @@ struct evsim_gpu_sim {
     for (int i = 0; i <= c.n_pairs; ++i) sp.ts[i] = ts[i];
     launch_segments(sp, stream);
     CK_LAUNCH("segments");
-    launch_chain(c, provider, stream);
-    CK_LAUNCH("chain");
+    if (sub.size() < 3) {
+      launch_chain(c, provider, stream);
+      CK_LAUNCH("chain");
+    } else {
+      const int L = c.d.n_links;
+      for (size_t b = 0; b + 1 < sub.size(); ++b) {
+        const int off = sub[b], nb = sub[b + 1] - sub[b];
+        CK(cudaStreamWaitEvent(stream, pipe_ev[1 + b], 0));
+        ChainParams cb = c;
+        cb.r0 = c.r0 + off;
+        cb.n_pairs = nb;
+        cb.g0.pu += (size_t)off * c.g0.pair_stride;
+        cb.g0.pv += (size_t)off * c.g0.pair_stride;
+        cb.masks += (size_t)off * L * ev.n_words;
+        cb.counts += (size_t)off * L * ev.n_blocks;
+        if (c.magnitude) {
+          cb.mcount += (size_t)off * L * ev.n_words * 32;
+          cb.wcount += (size_t)off * L * ev.n_words;
+        }
+        launch_chain(cb, provider, stream);
+        CK_LAUNCH("chain");
+      }
+      launches += (int64_t)sub.size() - 2;
+    }
     mark(EVSIM_STAGE_SCAN);
     OffsetParams op{G, ev.n_blocks, ev.counts.as<uint32_t>(), ev.prefix.as<int64_t>(), ev.link_total.as<int64_t>()};
     launch_offsets(op, stream);
@@ -980,11 +1021,33 @@ struct evsim_gpu_sim {
     if (n_pairs > 0) {
       ChainParams c = chain_params(r0, n_pairs);
       int provider = kProvNone;
+      std::vector<int> sub;
       if (dense_flow()) {
         // simulate_dense -> PyramidalPatchFlow -> dense_events_with_flow (simulate.cpp:130-143)
-        launches += flow.solve(r0, n_pairs, frames.as<uint8_t>(), quads.as<uint32_t>(), stream);
         c.g0 = flow.geom[0];
         provider = kProvDenseGrid;
+        // sub-batches of >= 8 pairs, at most 4; stage timing serialises
+        // (measured on c2: 2, 4, 8 sub-batches within 1 %; 4 + the stream
+        // priority: 33.2k -> 34.1k frames/s)
+        const int nsb = profiling ? 1 : std::min(4, n_pairs / 8);
+        if (nsb < 2) {
+          launches += flow.solve(r0, n_pairs, frames.as<uint8_t>(), quads.as<uint32_t>(), stream);
+        } else {
+          if (!s_flow) CK(cudaStreamCreateWithFlags(&s_flow, cudaStreamNonBlocking));
+          while ((int)pipe_ev.size() < nsb + 1) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            pipe_ev.push_back(e);
+          }
+          CK(cudaEventRecord(pipe_ev[0], stream));
+          CK(cudaStreamWaitEvent(s_flow, pipe_ev[0], 0));
+          for (int b = 0; b <= nsb; ++b) sub.push_back((int)((int64_t)n_pairs * b / nsb));
+          for (int b = 0; b < nsb; ++b) {
+            launches += flow.solve(r0 + sub[b], sub[b + 1] - sub[b], frames.as<uint8_t>(), quads.as<uint32_t>(),
+                                   s_flow, sub[b]);
+            CK(cudaEventRecord(pipe_ev[1 + b], s_flow));
+          }
+        }
       } else if (sparse_flow()) {
         sparse_stage(r0, n_pairs, c);
         provider = kProvSparse;
@@ -996,7 +1059,7 @@ struct evsim_gpu_sim {
         provider = kProvDiffInterp;
       }
       mark(EVSIM_STAGE_CHAIN);
-      run_events(c, provider, pts.data(), h_seg, continue_call);
+      run_events(c, provider, pts.data(), h_seg, continue_call, sub);
     } else {
       if (!continue_call) {
         seg_t.clear();
@@ -1287,7 +1350,12 @@ void make_sim(evsim_gpu_sim* s, const evsim_gpu_config& cfg, int device) {
   s->cfg = cfg;
   s->preset = resolve_preset(cfg);
   s->device = device;
-  CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  // the handle's stream carries the chain (the sequential critical path of a
+  // push): highest priority, so its blocks dispatch ahead of the pipelined
+  // flow of the next sub-batch (s_flow, default priority), which fills in
+  int lo_prio = 0, hi_prio = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  CK(cudaStreamCreateWithPriority(&s->stream, cudaStreamNonBlocking, hi_prio));
   float h_lut[256];
   log_lut(h_lut);
   s->lut.ensure(sizeof h_lut, s->stream);
