@@ -58,7 +58,7 @@ def parse():
     p.add_argument("--frames", type=int, default=0, help="override sequence length")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--chunk", type=int, default=0, help="e2e: frames per streamed chunk (0 = the library default, 48)")
+    p.add_argument("--chunk", type=int, default=0, help="e2e: frames per streamed chunk (0 = the library default, 64)")
     p.add_argument("--split", default="streams", choices=["streams", "bands"],
                    help="N>1: one camera stream per rank (weak scaling) or row bands of one stream (strong, c5)")
     p.add_argument("--batch", type=int, default=0,
@@ -451,7 +451,7 @@ def run_ours(args):
         e2e = {"value": round(frames_total / float(te.item()), 3), "unit": "frames/s",
                "h2d_bytes_per_step": n * P, "d2h_bytes_per_step": int(d2h),
                "api": f"evsim_gpu_push_frames_streamed (pinned host frames in, packed host events out, "
-                      f"chunks of ~{args.chunk or 48} frames: H2D / compute / D2H overlapped)"}
+                      f"chunks of ~{args.chunk or 64} frames: H2D / compute / D2H overlapped)"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

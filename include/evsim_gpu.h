@@ -176,7 +176,7 @@ EVSIM_GPU_API int evsim_gpu_push_frames_batched(evsim_gpu_sim* const* sims, int3
                                                 int32_t pixels_on_device, evsim_gpu_events* outs);
 
 /* Host frames in, host events out, overlapped: the frames are pushed in
- * chunks of about `chunk` frames (0 = 48; a quarter-size first and last
+ * chunks of about `chunk` frames (0 = 64; a quarter-size first and last
  * chunk); chunk j+1's upload and chunk j-1's event
  * download run on two copy streams while chunk j computes.  host_events
  * receives the packed records (format 0 of evsim_gpu_copy_events) of all
