@@ -211,6 +211,7 @@ struct FlowEngine {
   DevBuf pyr[kMaxLevels];     // fp32 level images, R slots
   DevBuf qpyr[kMaxLevels];    // float4 quad images (4 bilinear taps per pixel), R slots
   DevBuf tex[kMaxLevels];     // sparse: float4 (value, gx, gy, 0) per pixel, R slots
+  DevBuf tex8;                // sparse, level 0 from u8: packed texels (4 B per pixel), R slots
   bool texels = false;
   // dense with the warp-form solver at level 0: level 0 is read from the u8
   // frame / quad rings, so its fp32 image and float4 quads are not written
@@ -331,6 +332,10 @@ struct FlowEngine {
           tex[l].ensure((size_t)R_ * pl * sizeof(float4), s);
         }
       }
+      if (texels) {
+        tex8.release();
+        tex8.ensure((size_t)R_ * dims[0].w * dims[0].h * sizeof(uint32_t), s);
+      }
       R = R_;
     }
     if (pairs_ > pairs) {
@@ -355,7 +360,13 @@ struct FlowEngine {
       p.qpyr[l] = Ring<float4>{qpyr[l].as<float4>(), pl};
       p.tex[l] = Ring<float4>{texels ? tex[l].as<float4>() : nullptr, pl};
     }
-    p.u8_level0 = u8_level0 && quad_u8 != nullptr;
+    p.u8_level0 = (u8_level0 || texels) && quad_u8 != nullptr;
+    if (texels && p.u8_level0) {
+      // sparse: level 0 as the u8 quad + packed texels (the sparse solver
+      // decodes them exactly), no fp32 level-0 images
+      p.tex[0].base = nullptr;
+      p.tex8 = Ring<uint32_t>{tex8.as<uint32_t>(), P};
+    }
     p.frames = Ring<const uint8_t>{frames, P};
     p.quad_u8 = Ring<uint32_t>{quad_u8, P};
     p.R = R;
@@ -399,7 +410,9 @@ struct FlowEngine {
     return levels;
   }
 
-  SparseLKParams sparse_params(int r0) const {
+  // quads8: the u8 quad ring the pyramid pass wrote (level 0 then comes
+  // from it and the packed texels), or null (fp32 level 0)
+  SparseLKParams sparse_params(int r0, const uint32_t* quads8) const {
     SparseLKParams p{};
     p.levels = levels;
     for (int l = 0; l < levels; ++l) {
@@ -415,6 +428,11 @@ struct FlowEngine {
     p.radius = preset.radius;
     p.iterations = preset.iters;
     p.pair_stride = (size_t)w * h;
+    p.u8_level0 = quads8 != nullptr;
+    if (p.u8_level0) {
+      p.tex8 = Ring<const uint32_t>{tex8.as<uint32_t>(), (size_t)w * h};
+      p.qcurr8 = Ring<const uint32_t>{quads8, (size_t)w * h};
+    }
     return p;
   }
 };
@@ -701,7 +719,7 @@ struct evsim_gpu_sim {
       std::swap(frames.p, nf.p);
       std::swap(frames.n, nf.n);
       std::swap(frames.s, nf.s);
-      if (dense_flow()) {
+      if (uses_flow()) {  // u8 quads of level 0 (dense: frames; sparse / difference_interp: the pyramid source)
         DevBuf nq;
         nq.ensure((size_t)need_R * P * 4, stream);
         if (has_prev)
@@ -730,7 +748,7 @@ struct evsim_gpu_sim {
       R = need_R;
       if (uses_flow() && has_prev && (!diff_interp() || n_seen >= 2)) {
         const uint8_t* src = diff_interp() ? mags.as<uint8_t>() : frames.as<uint8_t>();
-        PyramidParams pp = flow.pyramid_params(src, P, dense_flow() ? quads.as<uint32_t>() : nullptr, rhead);
+        PyramidParams pp = flow.pyramid_params(src, P, quads.as<uint32_t>(), rhead);
         launch_pyramid(pp, 1, stream);
         CK_LAUNCH("pyramid");
       }
@@ -991,14 +1009,14 @@ struct evsim_gpu_sim {
         CK_LAUNCH("mags");
         ++launches;
         if (uses_flow()) {
-          PyramidParams pp = flow.pyramid_params(mags.as<uint8_t>(), P, nullptr, slot0);
+          PyramidParams pp = flow.pyramid_params(mags.as<uint8_t>(), P, quads.as<uint32_t>(), slot0);
           launch_pyramid(pp, F - j0, stream);
           CK_LAUNCH("pyramid");
           launches += flow.levels;
         }
       }
     } else if (uses_flow()) {
-      PyramidParams pp = flow.pyramid_params(frames.as<uint8_t>(), P, dense_flow() ? quads.as<uint32_t>() : nullptr, base);
+      PyramidParams pp = flow.pyramid_params(frames.as<uint8_t>(), P, quads.as<uint32_t>(), base);
       launch_pyramid(pp, F, stream);
       CK_LAUNCH("pyramid");
       launches += flow.levels;
@@ -1251,7 +1269,7 @@ struct evsim_gpu_sim {
     launch_select(sp, n_pairs, stream);
     CK_LAUNCH("select");
     // estimate_sparse_flow (flow.cpp:278-381)
-    SparseLKParams lk = flow.sparse_params(r0);
+    SparseLKParams lk = flow.sparse_params(r0, quads.as<uint32_t>());
     lk.points = points.as<uint32_t>();
     lk.n_points = n_points.as<int>();
     lk.disp = disp.as<float2>();
@@ -1807,7 +1825,7 @@ struct Scratch {
   evsim_gpu_sim* operator->() { return s.get(); }
   void pyramids() {
     PyramidParams pp = s->flow.pyramid_params(s->frames.as<uint8_t>(), (size_t)s->w * s->h,
-                                              s->dense_flow() ? s->quads.as<uint32_t>() : nullptr, 0);
+                                              s->uses_flow() ? s->quads.as<uint32_t>() : nullptr, 0);
     launch_pyramid(pp, 2, s->stream);
     CK_LAUNCH("pyramid");
   }
@@ -1884,7 +1902,7 @@ int evsim_gpu_sparse_flow(const uint8_t* prev, const uint8_t* curr, int32_t w, i
     ddisp.ensure((size_t)n_points * 8, s->stream);
     dst.ensure((size_t)n_points, s->stream);
     CK(cudaMemcpyAsync(dpts.p, idx.data(), (size_t)n_points * 4, cudaMemcpyHostToDevice, s->stream));
-    SparseLKParams lk = s->flow.sparse_params(0);
+    SparseLKParams lk = s->flow.sparse_params(0, s->quads.as<uint32_t>());
     lk.points = dpts.as<uint32_t>();
     lk.n_points = nullptr;
     lk.n_points_host = n_points;

@@ -59,10 +59,14 @@ __global__ void pyramid_level_kernel(PyramidParams p, int l) {
   // the same pass — gradients (flow.cpp:60-73) from the row above / below and
   // the left / right neighbours, all replicate-clamped
   float4* tex = p.tex[l].base ? p.tex[l].at(slot) : nullptr;
+  // sparse with a u8 level 0: the level-0 texels packed into one word
+  // (value, a10 - left, a01 - up: integers in [-255, 255], so gx = 0.5f *
+  // (a10 - left) is recovered exactly)
+  uint32_t* t8 = (level0 && p.tex8.base) ? p.tex8.at(slot) : nullptr;
   const int xm = max(x - 1, 0);
   float a00 = level_value(f0, src, rd, x, yb, level0, from_u8);
   float a10 = level_value(f0, src, rd, x1, yb, level0, from_u8);
-  float up = tex ? level_value(f0, src, rd, x, max(yb - 1, 0), level0, from_u8) : 0.0f;
+  float up = (tex || t8) ? level_value(f0, src, rd, x, max(yb - 1, 0), level0, from_u8) : 0.0f;
   for (int y = yb; y < ye; ++y) {
     const int y1 = min(y + 1, dd.h - 1);
     const float a01 = level_value(f0, src, rd, x, y1, level0, from_u8);
@@ -77,6 +81,11 @@ __global__ void pyramid_level_kernel(PyramidParams p, int l) {
       const float left = level_value(f0, src, rd, xm, y, level0, from_u8);
       tex[i] = make_float4(a00, fmul(0.5f, fsub(a10, left)), fmul(0.5f, fsub(a01, up)), 0.0f);
       up = a00;
+    } else if (t8) {
+      const float left = level_value(f0, src, rd, xm, y, level0, from_u8);
+      const uint32_t dx = (uint32_t)((int)a10 - (int)left) & 0x1FFu, dy = (uint32_t)((int)a01 - (int)up) & 0x1FFu;
+      t8[i] = (uint32_t)a00 | (dx << 8) | (dy << 17);
+      up = a00;
     }
     a00 = a01;  // the next row's top taps are this row's bottom taps
     a10 = a11;
@@ -87,11 +96,16 @@ __global__ void pyramid_level_kernel(PyramidParams p, int l) {
 // no texels): four pixels per thread from one aligned word per row (the next
 // column's byte from the neighbouring lane), one 16-byte store per row.
 // Needs w % 4 == 0; same bytes as pyramid_level_kernel's qu8 output.
+// kTex (sparse): also the packed level-0 texels (pyramid_level_kernel's t8
+// words): left neighbour from the previous lane's word, the row above
+// carried from the previous iteration (both replicate-clamped).
+template <bool kTex>
 __global__ void quad_level0_kernel(PyramidParams p) {
   const int w = p.dims[0].w, h = p.dims[0].h;
   const int slot = (p.slot0 + (int)blockIdx.z) % p.R;
   const uint8_t* f = p.frames.at(slot);
   uint32_t* q = p.quad_u8.at(slot);
+  uint32_t* t8 = kTex ? p.tex8.at(slot) : nullptr;
   const int x4 = 4 * (int)(blockIdx.x * blockDim.x + threadIdx.x);
   const int lane = threadIdx.x & 31;
   const bool in = x4 < w, last = x4 + 4 >= w;  // last: column x4 + 4 replicates x4 + 3
@@ -103,16 +117,36 @@ __global__ void quad_level0_kernel(PyramidParams p) {
     if (lane == 31 && !last) nx = __ldg(row + 1);
     nb = last ? (wd >> 24) : (nx & 0xFFu);
   };
-  uint32_t w0, n0, w1, n1;
+  uint32_t w0, n0, w1, n1, wm = 0u, nm;
   load(yb, w0, n0);
+  if (kTex) load(max(yb - 1, 0), wm, nm);
   for (int y = yb; y < ye; ++y) {
     load(min(y + 1, h - 1), w1, n1);
+    uint32_t pb = 0u;  // byte x4 - 1 of row y (replicate at x = 0)
+    if (kTex) {
+      const uint32_t prv = __shfl_up_sync(kFull, w0, 1);
+      if (lane == 0 && x4 > 0) pb = (uint32_t)__ldg(f + (size_t)y * w + x4 - 1);
+      else pb = x4 == 0 ? (w0 & 0xFFu) : (prv >> 24);
+    }
     if (in) {
       const uint32_t t0 = __byte_perm(w0, n0, 0x0043), t1 = __byte_perm(w1, n1, 0x0043);
       const uint4 o = make_uint4(__byte_perm(w0, w1, 0x5410), __byte_perm(w0, w1, 0x6521),
                                  __byte_perm(w0, w1, 0x7632), __byte_perm(t0, t1, 0x5410));
       *reinterpret_cast<uint4*>(q + (size_t)y * w + x4) = o;
+      if (kTex) {
+        uint32_t tw[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int v = (int)((w0 >> (8 * j)) & 0xFFu);
+          const int right = j < 3 ? (int)((w0 >> (8 * j + 8)) & 0xFFu) : (int)n0;
+          const int left = j > 0 ? (int)((w0 >> (8 * j - 8)) & 0xFFu) : (int)pb;
+          const int up = (int)((wm >> (8 * j)) & 0xFFu), down = (int)((w1 >> (8 * j)) & 0xFFu);
+          tw[j] = (uint32_t)v | (((uint32_t)(right - left) & 0x1FFu) << 8) | (((uint32_t)(down - up) & 0x1FFu) << 17);
+        }
+        *reinterpret_cast<uint4*>(t8 + (size_t)y * w + x4) = make_uint4(tw[0], tw[1], tw[2], tw[3]);
+      }
     }
+    if (kTex) wm = w0;
     w0 = w1;
     n0 = n1;
   }
@@ -789,6 +823,33 @@ __device__ __forceinline__ void sample_texel(const float4* __restrict__ tex, int
   val = lerp_ref(lerp_ref(q00.x, q10.x, t.fx), lerp_ref(q01.x, q11.x, t.fx), t.fy);
 }
 
+// Level 0 from u8 data: template positions are integral there (px = x:
+// the level ratio is 1), so sample() of the gradient images and of P is one
+// tap (lerp(a, b, 0) = a) — the packed texel; the residual's sample of curr
+// reads the u8 quad (bytes convert to the fp32 level values exactly).
+__device__ __forceinline__ void sample_texel8(const uint32_t* __restrict__ t8, int w, int h, float sx, float sy,
+                                              float& a, float& b, float& val) {
+  const int x = (int)clamp_ref(sx, 0.0f, (float)(w - 1));
+  const int y = (int)clamp_ref(sy, 0.0f, (float)(h - 1));
+  const uint32_t t = __ldg(t8 + (size_t)y * w + x);
+  val = (float)(t & 0xFFu);
+  a = fmul(0.5f, (float)((int)(t << 15) >> 23));
+  b = fmul(0.5f, (float)((int)(t << 6) >> 23));
+}
+
+__device__ __forceinline__ float sample_quad8(const uint32_t* __restrict__ q, int w, int h, float x, float y) {
+  x = clamp_ref(x, 0.0f, (float)(w - 1));
+  y = clamp_ref(y, 0.0f, (float)(h - 1));
+  const int x0 = (int)x;
+  const int y0 = (int)y;
+  const float fx = fsub(x, (float)x0);
+  const float fy = fsub(y, (float)y0);
+  const uint32_t a = __ldg(q + (size_t)y0 * w + x0);
+  const float top = lerp_ref((float)(a & 0xFFu), (float)((a >> 8) & 0xFFu), fx);
+  const float bot = lerp_ref((float)((a >> 16) & 0xFFu), (float)(a >> 24), fx);
+  return lerp_ref(top, bot, fy);
+}
+
 // estimate_sparse_flow's per-point loop (flow.cpp:309-380), one thread per point.
 __global__ void __launch_bounds__(128) sparse_lk_kernel(SparseLKParams p) {
   const int z = blockIdx.y;  // frame pair
@@ -811,8 +872,11 @@ __global__ void __launch_bounds__(128) sparse_lk_kernel(SparseLKParams p) {
     bool lost = false, solved_any = false;
     for (int l = p.levels - 1; l >= 0 && !lost; --l) {
       const int w = p.dims[l].w, h = p.dims[l].h;
-      const float4* T = p.tex[l].at(sp);
-      const float4* C = p.qcurr[l].at(sc);
+      const bool u8l = l == 0 && p.u8_level0;
+      const float4* T = u8l ? nullptr : p.tex[l].at(sp);
+      const float4* C = u8l ? nullptr : p.qcurr[l].at(sc);
+      const uint32_t* T8 = u8l ? p.tex8.at(sp) : nullptr;
+      const uint32_t* C8 = u8l ? p.qcurr8.at(sc) : nullptr;
       const float px = fsub(fmul(fadd((float)ptx, 0.5f), __fdiv_rn((float)w, w0)), 0.5f);
       const float py = fsub(fmul(fadd((float)pty, 0.5f), __fdiv_rn((float)h, h0)), 0.5f);
       if (l != p.levels - 1) {
@@ -824,7 +888,8 @@ __global__ void __launch_bounds__(128) sparse_lk_kernel(SparseLKParams p) {
         const float sy = fadd(py, (float)oy);
         for (int ox = -r; ox <= r; ++ox) {
           float a, b, tv;
-          sample_texel(T, w, h, fadd(px, (float)ox), sy, a, b, tv);
+          if (u8l) sample_texel8(T8, w, h, fadd(px, (float)ox), sy, a, b, tv);
+          else sample_texel(T, w, h, fadd(px, (float)ox), sy, a, b, tv);
           gxx = dadd(gxx, (double)fmul(a, a));
           gxy = dadd(gxy, (double)fmul(a, b));
           gyy = dadd(gyy, (double)fmul(b, b));
@@ -841,8 +906,15 @@ __global__ void __launch_bounds__(128) sparse_lk_kernel(SparseLKParams p) {
           for (int ox = -r; ox <= r; ++ox) {
             const float sx = fadd(px, (float)ox);
             float a, b, tv;
-            sample_texel(T, w, h, sx, sy, a, b, tv);
-            const float residual = fsub(sample_quadf(C, w, h, fadd(sx, u), syv), tv);
+            float smp;
+            if (u8l) {
+              sample_texel8(T8, w, h, sx, sy, a, b, tv);
+              smp = sample_quad8(C8, w, h, fadd(sx, u), syv);
+            } else {
+              sample_texel(T, w, h, sx, sy, a, b, tv);
+              smp = sample_quadf(C, w, h, fadd(sx, u), syv);
+            }
+            const float residual = fsub(smp, tv);
             b1 = dadd(b1, (double)fmul(a, residual));
             b2 = dadd(b2, (double)fmul(b, residual));
           }
@@ -875,9 +947,11 @@ void launch_pyramid(const PyramidParams& p, int n_frames, cudaStream_t s) {
   for (int l = 0; l < p.levels; ++l) {
     const int w = p.dims[l].w;
     if (l == 0 && p.u8_level0 && p.quad_u8.base && !p.tex[0].base && (w & 3) == 0 &&
-        ((uintptr_t)p.frames.base & 3) == 0 && ((uintptr_t)p.quad_u8.base & 15) == 0) {
+        ((uintptr_t)p.frames.base & 3) == 0 && ((uintptr_t)p.quad_u8.base & 15) == 0 &&
+        ((uintptr_t)p.tex8.base & 15) == 0) {
       dim3 g((w / 4 + 127) / 128, (p.dims[0].h + kPyrRows - 1) / kPyrRows, n_frames);
-      quad_level0_kernel<<<g, 128, 0, s>>>(p);
+      if (p.tex8.base) quad_level0_kernel<true><<<g, 128, 0, s>>>(p);
+      else quad_level0_kernel<false><<<g, 128, 0, s>>>(p);
       continue;
     }
     dim3 g((w + 127) / 128, (p.dims[l].h + kPyrRows - 1) / kPyrRows, n_frames);

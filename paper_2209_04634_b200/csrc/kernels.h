@@ -42,6 +42,7 @@ struct PyramidParams {
   Ring<float4> qpyr[kMaxLevels];
   Ring<uint32_t> quad_u8;   // base may be null (no interpolation)
   Ring<float4> tex[kMaxLevels];  // sparse: per pixel (value, gx, gy, 0); base may be null
+  Ring<uint32_t> tex8;           // sparse, u8 level 0: packed texels value | (2gx & 511) << 8 | (2gy & 511) << 17
   int u8_level0;            // level 0 not materialised as fp32 (dense: the solver reads the u8 frame / quad)
   int R, slot0;             // frame j of this launch is slot (slot0 + j) % R
 };
@@ -82,6 +83,9 @@ struct SparseLKParams {
   LevelDims dims[kMaxLevels];
   Ring<const float4> tex[kMaxLevels];    // prev: (value, gx, gy, 0) per pixel
   Ring<const float4> qcurr[kMaxLevels];  // curr: quad images
+  int u8_level0;                         // level 0 from the packed u8 texels / u8 quads below
+  Ring<const uint32_t> tex8;             // prev, level 0: packed (value, 2gx, 2gy)
+  Ring<const uint32_t> qcurr8;           // curr, level 0: u8 quads
   int R, r0;
   int w0, h0;
   int radius, iterations;
