@@ -514,12 +514,13 @@ def issue_roofline(config: str, mode: str, pairs_per_launch: float, stages_ms: d
 
 def traffic_for(config: str, mode: str, pairs_per_launch: float):
     """DRAM bytes (read + write) per launch of the event stage, from the
-    committed ncu --set full capture of the same workload, or None."""
+    committed ncu --set full capture of the same workload
+    (profiles/r01/traffic_<config>_<mode>.json), or None."""
     try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "r01", "traffic_c2_log.json")))
+        t = json.load(open(os.path.join(ROOT, "profiles", "r01", f"traffic_{config}_{mode}.json")))
     except Exception:
         return None
-    if config == "c2" and mode == "log" and abs(pairs_per_launch - 127) < 0.5:
+    if abs(pairs_per_launch - t.get("pairs_per_launch", -1)) < 0.5:
         return t["event_stage_dram_bytes_per_launch"]
     return None
 

@@ -58,6 +58,7 @@ def main(rep, outdir):
         per = {n: int((x["dram_rd_MB"] + x["dram_wr_MB"]) * 1e6) for n, x in parts.items()}
         json.dump({"source": f"{outdir}/ncu_full_summary.json (ncu --set full --clock-control none, one launch each)",
                    "workload": "c2 log, 128-frame push (127 pairs per launch), python bench.py --steps 3 --warmup 3",
+                   "pairs_per_launch": 127,
                    "event_stage_dram_bytes_per_launch": sum(per.values()), "per_kernel_dram_bytes": per},
                   open(os.path.join(outdir, "traffic_c2_log.json"), "w"), indent=1)
     for x in out:
