@@ -730,27 +730,34 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
 // the previous link ended in this pair's prev, or ref = L(frame0)).
 template <bool kLog, bool kMag>
 __global__ void __launch_bounds__(256, 3) chain_sparse_kernel(ChainParams p) {
+  // Work per word varies widely (only words near claimed pixels evaluate
+  // links), so warps take two-word tasks from a device counter instead of a
+  // static block partition (no block waits for its slowest warp); the
+  // (link, block) counts the emit needs are global atomics on the word's
+  // block, zeroed by the launch.
   constexpr int kW = 2;
-  extern __shared__ uint32_t s_cnt[];  // [G]
   __shared__ float s_lut[256];
-  const int L = p.d.n_links, G = L * p.n_pairs, N = p.n_interp;
-  for (int i = threadIdx.x; i < G; i += blockDim.x) s_cnt[i] = 0;
+  const int L = p.d.n_links, N = p.n_interp;
   if (kLog) s_lut[threadIdx.x] = p.lut[threadIdx.x];
   __syncthreads();
-  const int b = blockIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const size_t P = p.P;
   const int kfirst = p.d.start + 1;
-  const int64_t wbeg = (int64_t)b * p.words_per_block;
-  const int64_t wend = min(wbeg + p.words_per_block, p.n_words);
-  for (int64_t w0 = wbeg + warp; w0 < wend; w0 += kWarpsPerBlock * kW) {
+  const int64_t n_tasks = (p.n_words + kW - 1) / kW;
+  for (;;) {
+    int64_t task = 0;
+    if (lane == 0) task = (int64_t)atomicAdd(p.sched, 1u);
+    task = __shfl_sync(kFull, task, 0);
+    if (task >= n_tasks) break;
+    const int64_t w0 = task * kW;
+    const uint32_t blk = (uint32_t)(w0 / p.words_per_block);  // both words (words_per_block is even)
     DenseWord c[kW];
     float ref[kW];
     int before[kW];
 #pragma unroll
     for (int q = 0; q < kW; ++q) {
-      const int64_t wq = w0 + q * kWarpsPerBlock;
-      c[q].have = wq < wend;
+      const int64_t wq = w0 + q;
+      c[q].have = wq < p.n_words;
       c[q].wi = (uint32_t)wq;
       const int64_t ww = c[q].have ? wq : w0;
       const int row = (int)((uint32_t)ww / (uint32_t)p.wpr);
@@ -819,7 +826,7 @@ __global__ void __launch_bounds__(256, 3) chain_sparse_kernel(ChainParams p) {
             p.masks[(size_t)g * p.n_words + c[q].wi] = lm[q];
             if (kMag) p.wcount[(size_t)g * p.n_words + c[q].wi] = lwc[q];
           }
-          if (lcnt) atomicAdd(&s_cnt[g], lcnt);
+          if (lcnt) atomicAdd(&p.counts[(size_t)g * p.n_blocks + blk], lcnt);
         }
         lcnt = 0;
       };
@@ -953,8 +960,6 @@ __global__ void __launch_bounds__(256, 3) chain_sparse_kernel(ChainParams p) {
         if (c[q].valid) p.ref[c[q].pix] = ref[q];
     }
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < G; i += blockDim.x) p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
 }
 
 // ------------------------------------------------------------ difference_interp kernel
@@ -1699,13 +1704,14 @@ static void launch_chain_dense(const ChainParams& p, size_t sm, cudaStream_t s) 
 
 template <bool kLog, bool kMag>
 static void launch_chain_sparse(const ChainParams& p, size_t sm, cudaStream_t s) {
+  (void)sm;
   auto* k = chain_sparse_kernel<kLog, kMag>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    attr = true;
-  }
-  k<<<p.n_blocks, 256, sm, s>>>(p);
+  cudaMemsetAsync(p.counts, 0, (size_t)std::max(p.d.n_links * p.n_pairs, 1) * p.n_blocks * sizeof(uint32_t), s);
+  cudaMemsetAsync(p.sched, 0, sizeof(unsigned int), s);
+  // persistent: 3 resident blocks of 8 warps per SM take tasks until done
+  const int64_t tasks = (p.n_words + 1) / 2;
+  const int64_t blocks = std::min<int64_t>((tasks + kWarpsPerBlock - 1) / kWarpsPerBlock, 148 * 3);
+  k<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(p);
 }
 
 template <bool kMag>

@@ -446,7 +446,7 @@ struct EventEngine {
   int words_per_warp = 2;  // dense chain kernel
   int max_links = 0;  // links of a launch (pairs * per-pair links)
   bool magnitude = false;
-  DevBuf masks, counts, prefix, link_total, segtab, segbase, seg_out, events, mcount, wcount, base;
+  DevBuf masks, counts, prefix, link_total, segtab, segbase, seg_out, events, mcount, wcount, base, sched;
   int64_t capacity = 0;
 
   // fine = true (dense, small frames): 8 words per block, one word per warp —
@@ -486,6 +486,7 @@ struct EventEngine {
       segbase.ensure((size_t)max_links * sizeof(int64_t), s);
       seg_out.ensure((3 + 2 * (size_t)max_links) * sizeof(int64_t), s);
       base.ensure(sizeof(int64_t), s);
+      sched.ensure(sizeof(unsigned int), s);
       if (mag) {
         mcount.ensure((size_t)max_links * n_words * 32 * sizeof(uint16_t), s);
         wcount.ensure((size_t)max_links * n_words * sizeof(uint32_t), s);
@@ -853,6 +854,7 @@ struct evsim_gpu_sim {
     c.mcount = ev.mcount.as<uint16_t>();
     c.wcount = ev.wcount.as<uint32_t>();
     c.counts = ev.counts.as<uint32_t>();
+    c.sched = ev.sched.as<unsigned int>();
     return c;
   }
 

@@ -177,6 +177,7 @@ struct ChainParams {
   uint16_t* mcount;        // magnitude: [g][n_words*32]
   uint32_t* wcount;        // magnitude: [g][n_words]
   uint32_t* counts;        // [g][n_blocks] events per block
+  unsigned int* sched;     // sparse chain: device task counter (zeroed by the launch)
 };
 
 struct OffsetParams {
