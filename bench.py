@@ -498,13 +498,13 @@ def issue_roofline(config: str, mode: str, pairs_per_launch: float, stages_ms: d
     clock = float(sm_mhz or 1965.0) * 1e6
     peak = 148 * 4 * clock
     out = {"unit": "warp-instructions/s", "peak": peak, "peak_source": "148 SMs x 4 schedulers x measured SM clock",
-           "instructions_source": "profiles/r01/ncu_full_summary.json (smsp__inst_executed.sum per launch)"}
+           "instructions_source": "profiles/r01/ncu_full_summary.json (smsp__inst_executed.sum, every launch of one push)"}
     fam = {"chain": "chain_dense_kernel", "flow": "dense_lk_warp_kernel"}
     for stage, name in fam.items():
         ks = [r for r in rows if name in r["kernel"]]
         if not ks:
             continue
-        instr = ks[0]["warp_instr"] if stage == "chain" else sum(r["warp_instr"] for r in ks[:3])
+        instr = sum(r["warp_instr"] for r in ks)  # the capture holds every launch of one push
         t = stages_ms[stage] / launches / 1e3
         if t > 0:
             out[stage] = {"kernel": name, "warp_instr_per_launch": instr, "achieved": round(instr / t, 1),
