@@ -544,12 +544,7 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
   const int L = p.d.n_links, G = L * p.n_pairs, N = p.n_interp;
   float4* s_kc = s_dyn4;                                       // [N + 2]
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_dyn4 + N + 2);  // [G]
-  uint32_t* s_nzw = s_cnt + G;                                     // [G] when p.nzw
-  const bool nzw = p.nzw != nullptr;
-  for (int i = threadIdx.x; i < G; i += blockDim.x) {
-    s_cnt[i] = 0;
-    if (nzw) s_nzw[i] = 0;
-  }
+  for (int i = threadIdx.x; i < G; i += blockDim.x) s_cnt[i] = 0;
   for (int i = threadIdx.x; i < N + 2; i += blockDim.x) s_kc[i] = p.kc[i];
   if (kLog) s_lut[threadIdx.x] = p.lut[threadIdx.x];
   __syncthreads();
@@ -643,7 +638,7 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
         __syncwarp();
         for (int j = lane; j < n; j += 32) {
           const int g = gbase + fbase + j;
-          uint32_t cnt = 0, bits = 0;
+          uint32_t cnt = 0;
 #pragma unroll
           for (int q = 0; q < kW; ++q) {
             if (!c[q].have) continue;
@@ -651,9 +646,7 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
             p.masks[(size_t)g * p.n_words + c[q].wi] = m;
             if (kMag) p.wcount[(size_t)g * p.n_words + c[q].wi] = s_stw[warp][q][j];
             else cnt += __popc(m.x | m.y);  // a pixel crosses one way or not at all
-            if ((m.x | m.y) != 0u) bits |= 1u << (uint32_t)(c[q].wi - wbeg);
           }
-          if (nzw && bits) atomicOr(&s_nzw[g], bits);
           if (kMag) cnt = s_stc[warp][j];
           if (cnt) atomicAdd(&s_cnt[g], cnt);
         }
@@ -721,10 +714,7 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < G; i += blockDim.x) {
-    p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
-    if (nzw) p.nzw[(size_t)i * p.n_blocks + b] = s_nzw[i];
-  }
+  for (int i = threadIdx.x; i < G; i += blockDim.x) p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
 }
 
 // ------------------------------------------------------------ sparse chain kernel
@@ -1757,7 +1747,7 @@ void launch_chain(const ChainParams& p, int provider, cudaStream_t s) {
   }
   if (provider == kProvDenseGrid && p.kc) {
     const size_t sm = (size_t)(p.n_interp + 2) * sizeof(float4) +
-                      (size_t)std::max(p.d.n_links * p.n_pairs, 1) * sizeof(uint32_t) * (p.nzw ? 2 : 1);
+                      (size_t)std::max(p.d.n_links * p.n_pairs, 1) * sizeof(uint32_t);
     if (sm <= 96 * 1024) {
       if (p.log_mode) {
         if (p.magnitude) launch_chain_dense<true, true>(p, sm, s);

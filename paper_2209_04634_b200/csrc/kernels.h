@@ -178,8 +178,6 @@ struct ChainParams {
   uint32_t* wcount;        // magnitude: [g][n_words]
   uint32_t* counts;        // [g][n_blocks] events per block
   unsigned int* sched;     // sparse chain: device task counter (zeroed by the launch)
-  uint32_t* nzw;           // dense chain, words_per_block <= 32: [g][n_blocks] bit j = word j of the
-                           // block has events in link g (the emit's item list), or null
 };
 
 struct OffsetParams {
@@ -200,7 +198,6 @@ struct EmitParams {
   SegTable seg;
   const int64_t* prefix;
   const uint32_t* counts;  // [g][n_blocks] events per (link, block)
-  const uint32_t* nzw;     // [g][n_blocks] non-empty word bits (words_per_block <= 32), or null
   const int64_t* link_total;
   int64_t* seg_out;        // [0] = S, [1..S] seg_t, [1+S..1+2S] offsets (S+1); block 0
   int64_t* base;           // device scalar: output offset of this launch's first event;
