@@ -81,3 +81,20 @@ def test_full_sequence_one_batch_c2_log(oracle):
     exp = concat(run_oracle_stream(oracle, cfg, frames, ts))
     sim = Simulator(SimulatorConfig.from_c(cfg))
     assert_same_events(sim.push_frames(frames, ts).events, exp)
+
+
+@pytest.mark.parametrize("mode,mag,incl", [(1, 0, 1), (0, 0, 1), (1, 1, 1), (0, 1, 0), (1, 0, 0)])
+def test_pipelined_dense_push_matches_oracle(oracle, mode, mag, incl):
+    """A dense push of >= 16 pairs runs its flow in sub-batches on a second
+    stream, overlapping the previous sub-batch's chain (DESIGN.md §4.5a);
+    with stage timing on, the same push runs serially.  Both must equal the
+    oracle bit for bit."""
+    frames, ts = scenes.generate("c2", n_frames=41, width=100, height=76)
+    cfg = make_config(Method.dense, n_interp=6, contrast_mode=mode, events_per_crossing=mag,
+                      include_endpoints=incl, c_pos_log=0.1, c_neg_log=-0.12)
+    exp = concat(run_oracle_stream(oracle, cfg, frames, ts))
+    for profiling in (False, True):
+        sim = Simulator(SimulatorConfig.from_c(cfg))
+        sim.set_profiling(profiling)
+        got = [sim.push_frames(frames[:1], ts[:1]).events, sim.push_frames(frames[1:], ts[1:]).events]
+        assert_same_events(concat(got), exp, what=f"profiling={profiling}")
