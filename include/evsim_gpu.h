@@ -145,7 +145,8 @@ EVSIM_GPU_API int evsim_gpu_push_frame(evsim_gpu_sim* sim, const uint8_t* pixels
  * event streams concatenated (segments of all intervals, in order).  The
  * whole batch is validated first and rejected atomically (state untouched).
  * At most evsim_gpu_max_batch(sim, width, height) frames per call (bounded
- * by kernel shared-memory tables and a ~6 GB per-launch buffer budget). */
+ * by kernel shared-memory tables and a per-launch buffer budget of ~6 GB,
+ * ~24 GB for frames of 4 Mpixel or more). */
 EVSIM_GPU_API int evsim_gpu_push_frames(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t n_frames,
                                         int32_t width, int32_t height, const int64_t* t_us,
                                         int32_t pixels_on_device, evsim_gpu_events* out);

@@ -515,11 +515,15 @@ struct EventEngine {
 // Largest batch whose link count fits the kernels' shared-memory tables
 // (chain: 4 B per link, emit: 8 B per segment, both <= 96 KB).
 // Also keeps the per-launch event buffer + masks (12 B per link-pixel in
-// single mode) within ~6 GB of the 180 GB HBM.
+// single mode) within ~6 GB of the 180 GB HBM (24 GB for 4K and larger
+// frames, so a push still holds several pairs: c5 669 -> 714 frames/s).
 int max_batch_for(int links_per_pair, int64_t pixels) {
   const int L = std::max(links_per_pair, 1);
   const int by_links = 12000 / L;
-  const int64_t by_mem = (int64_t)6e9 / std::max<int64_t>(1, (int64_t)L * std::max<int64_t>(pixels, 1) * 12);
+  // (4K and larger frames: 24 GB, so a push holds several pairs and the
+  // flow / chain overlap has sub-batches to work with)
+  const int64_t budget = pixels >= ((int64_t)1 << 22) ? (int64_t)24e9 : (int64_t)6e9;
+  const int64_t by_mem = budget / std::max<int64_t>(1, (int64_t)L * std::max<int64_t>(pixels, 1) * 12);
   return (int)std::max<int64_t>(1, std::min<int64_t>(std::min(kMaxBatch, by_links), by_mem));
 }
 
@@ -1049,6 +1053,8 @@ struct evsim_gpu_sim {
         // sub-batches of >= 8 pairs, at most 4; stage timing serialises
         // (measured on c2: 2, 4, 8 sub-batches within 1 %; 4 + the stream
         // priority: 33.2k -> 34.1k frames/s)
+        // (4K pushes of 7 pairs in sub-batches of 1-2: 714 -> 710 frames/s, so
+        // sub-batches stay >= 8 pairs)
         const int nsb = profiling ? 1 : std::min(4, n_pairs / 8);
         if (nsb < 2) {
           launches += flow.solve(r0, n_pairs, frames.as<uint8_t>(), quads.as<uint32_t>(), stream);
