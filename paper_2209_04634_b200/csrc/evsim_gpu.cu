@@ -567,6 +567,11 @@ struct evsim_gpu_sim {
   // per-pixel state orders the chains; the flows are independent)
   cudaStream_t s_flow = nullptr;
   std::vector<cudaEvent_t> pipe_ev;  // [0]: inputs ready; [1 + b]: flow of sub-batch b done
+  // streamed call (dense): a chunk's pyramid and flow also run on s_flow,
+  // after its upload, so they overlap the previous chunk's chain and emit;
+  // each chunk's pairs use their own grid slots from pair_base
+  bool xchunk = false;
+  int pair_base = 0;
 
   // per-stage CUDA-event timing (evsim_gpu_set_profiling)
   using EvGroup = std::array<cudaEvent_t, EVSIM_N_STAGES + 1>;
@@ -880,7 +885,7 @@ struct evsim_gpu_sim {
     for (int i = 0; i <= c.n_pairs; ++i) sp.ts[i] = ts[i];
     launch_segments(sp, stream);
     CK_LAUNCH("segments");
-    if (sub.size() < 3) {
+    if (sub.empty()) {
       launch_chain(c, provider, stream);
       CK_LAUNCH("chain");
     } else {
@@ -999,9 +1004,11 @@ struct evsim_gpu_sim {
     const size_t P = (size_t)w * h;
     const int base = next_slot();  // ring slot of frame 0 of the batch
     const int n_pairs = has_prev ? F : F - 1;
+    const bool xc = xchunk && dense_flow() && uploaded && !profiling && s_flow;
+    cudaStream_t ps = xc ? s_flow : stream;  // upload wait + pyramid
     begin_group();
     mark(EVSIM_STAGE_UPLOAD);
-    if (uploaded) CK(cudaStreamWaitEvent(stream, uploaded, 0));
+    if (uploaded) CK(cudaStreamWaitEvent(ps, uploaded, 0));
     else upload(pixels, F, base, on_device, stream);
     mark(EVSIM_STAGE_PYRAMID);
     if (diff_interp()) {
@@ -1023,12 +1030,13 @@ struct evsim_gpu_sim {
       }
     } else if (uses_flow()) {
       PyramidParams pp = flow.pyramid_params(frames.as<uint8_t>(), P, quads.as<uint32_t>(), base);
-      launch_pyramid(pp, F, stream);
+      launch_pyramid(pp, F, ps);
       CK_LAUNCH("pyramid");
       launches += flow.levels;
     }
     if (!has_prev && log_mode()) {
       // warm-up frame: ref := L(frame0)
+      if (xc) CK(cudaStreamWaitEvent(stream, uploaded, 0));
       launch_init_ref(frames.as<uint8_t>() + (size_t)base * P, lut.as<float>(), ref.as<float>(), (int64_t)P, stream);
       CK_LAUNCH("init_ref");
       ++launches;
@@ -1049,6 +1057,9 @@ struct evsim_gpu_sim {
       if (dense_flow()) {
         // simulate_dense -> PyramidalPatchFlow -> dense_events_with_flow (simulate.cpp:130-143)
         c.g0 = flow.geom[0];
+        const int pb = xc ? pair_base : 0;  // this call's grid slots of the chunk
+        c.g0.pu += (size_t)pb * c.g0.pair_stride;
+        c.g0.pv += (size_t)pb * c.g0.pair_stride;
         provider = kProvDenseGrid;
         // sub-batches of >= 8 pairs, at most 4; stage timing serialises
         // (measured on c2: 2, 4, 8 sub-batches within 1 %; 4 + the stream
@@ -1056,21 +1067,24 @@ struct evsim_gpu_sim {
         // (4K pushes of 7 pairs in sub-batches of 1-2: 714 -> 710 frames/s, so
         // sub-batches stay >= 8 pairs)
         const int nsb = profiling ? 1 : std::min(4, n_pairs / 8);
-        if (nsb < 2) {
+        if (nsb < 2 && !xc) {
           launches += flow.solve(r0, n_pairs, frames.as<uint8_t>(), quads.as<uint32_t>(), stream);
         } else {
+          const int ns = std::max(nsb, 1);
           if (!s_flow) CK(cudaStreamCreateWithFlags(&s_flow, cudaStreamNonBlocking));
-          while ((int)pipe_ev.size() < nsb + 1) {
+          while ((int)pipe_ev.size() < ns + 1) {
             cudaEvent_t e;
             CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             pipe_ev.push_back(e);
           }
-          CK(cudaEventRecord(pipe_ev[0], stream));
-          CK(cudaStreamWaitEvent(s_flow, pipe_ev[0], 0));
-          for (int b = 0; b <= nsb; ++b) sub.push_back((int)((int64_t)n_pairs * b / nsb));
-          for (int b = 0; b < nsb; ++b) {
+          if (!xc) {  // (xc: the pyramid already ran on s_flow)
+            CK(cudaEventRecord(pipe_ev[0], stream));
+            CK(cudaStreamWaitEvent(s_flow, pipe_ev[0], 0));
+          }
+          for (int b = 0; b <= ns; ++b) sub.push_back((int)((int64_t)n_pairs * b / ns));
+          for (int b = 0; b < ns; ++b) {
             launches += flow.solve(r0 + sub[b], sub[b + 1] - sub[b], frames.as<uint8_t>(), quads.as<uint32_t>(),
-                                   s_flow, sub[b]);
+                                   s_flow, pb + sub[b]);
             CK(cudaEventRecord(pipe_ev[1 + b], s_flow));
           }
         }
@@ -1166,6 +1180,13 @@ struct evsim_gpu_sim {
     CK(cudaEventRecord(start, stream));
     CK(cudaStreamWaitEvent(s_in, start, 0));
     CK(cudaStreamWaitEvent(s_out, start, 0));
+    // dense: chunk j+1's pyramid + flow on s_flow overlap chunk j's chain
+    xchunk = dense_flow() && !profiling;
+    if (xchunk) {
+      if (!s_flow) CK(cudaStreamCreateWithFlags(&s_flow, cudaStreamNonBlocking));
+      CK(cudaStreamWaitEvent(s_flow, start, 0));
+    }
+    pair_base = 0;
     // ring slots of every chunk, as the pushes will assign them
     std::vector<int> slot(n_chunks);
     {
@@ -1219,11 +1240,14 @@ struct evsim_gpu_sim {
         h_seg2[j & 1][1] = 0;
       }
       enqueue(nullptr, nf, ts + a, false, up[j], h_seg2[j & 1], true);
+      pair_base += had_prev ? nf : nf - 1;
       CK(cudaEventRecord(done[j], stream));
       pending = false;
       if (j > 0) drain(j - 1);
     }
     drain(n_chunks - 1);
+    xchunk = false;
+    pair_base = 0;
     seg_off.push_back(copied);
     n_events = copied;
     CK(cudaStreamSynchronize(s_out));
