@@ -44,3 +44,21 @@ def test_batched_rejects_atomically(oracle):
     for (f, t), o in zip(seqs, outs):
         assert_same_events(o.events, concat(run_oracle_stream(oracle, cfg, f, t)))
     assert push_frames_batched([], [], []) == []
+
+
+@pytest.mark.parametrize("mode", [1, 0])
+def test_batched_streams_pipelined_dense(oracle, mode):
+    """Several handles pushing >= 16 pairs each: every handle's flow runs in
+    sub-batches on its own flow stream, all handles at once."""
+    n_streams, F = 3, 21
+    seqs = [scenes.generate("c4", n_frames=F, width=72, height=48, stream=s) for s in range(n_streams)]
+    cfg = make_config(Method.dense, n_interp=4, contrast_mode=mode, c_pos_log=0.1, c_neg_log=-0.1)
+    exp = [concat(run_oracle_stream(oracle, cfg, f, t)) for f, t in seqs]
+    sims = [Simulator(SimulatorConfig.from_c(cfg)) for _ in range(n_streams)]
+    got = [[] for _ in range(n_streams)]
+    for a, b in ((0, 1), (1, F)):
+        outs = push_frames_batched(sims, [f[a:b] for f, _ in seqs], [t[a:b] for _, t in seqs])
+        for i, o in enumerate(outs):
+            got[i].append(o.events)
+    for i in range(n_streams):
+        assert_same_events(concat(got[i]), exp[i], what=f"stream {i}")

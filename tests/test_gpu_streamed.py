@@ -81,3 +81,16 @@ def test_streamed_rejects_magnitude_and_bad_batches():
     # rejected atomically: the stream is untouched
     p, t, o = sim.push_frames_streamed(frames, ts, chunk=3)
     assert o[-1] == p.size
+
+
+@pytest.mark.parametrize("mode,chunk", [(1, 0), (0, 0), (1, 20), (0, 37)])
+def test_streamed_long_dense_pipelined(oracle, mode, chunk):
+    """Dense streamed calls long enough for flow sub-batches inside a chunk
+    and for the cross-chunk overlap: 45 frames in one chunk
+    (4 sub-batches) or in chunks of ~20 / ~37 frames."""
+    frames, ts = scenes.generate("c2", n_frames=45, width=100, height=76)
+    cfg = _cfg(Method.dense, mode)
+    exp = concat(run_oracle_stream(oracle, cfg, frames, ts))
+    sim = Simulator(SimulatorConfig.from_c(cfg))
+    packed, seg_t, seg_off = sim.push_frames_streamed(frames, ts, chunk=chunk)
+    assert_same_events(unpack_events(packed, seg_t, seg_off), exp)
