@@ -1689,19 +1689,15 @@ template <bool kLog, bool kMag>
 static void launch_chain_dense(const ChainParams& p, size_t sm, cudaStream_t s) {
   // the longest batch that tiles the interior links (more gathers in flight
   // per warp; measured on c2 N=10: batches of 10 vs 5, chain 12.7 -> 12.1
-  // us/frame), else batches of 4 with a remainder
+  // us/frame), else batches of 4 with a remainder.  One-word warp tasks
+  // (EventEngine::geometry), 3 blocks/SM at 80 regs (4 at 64 regs: c2 chain
+  // 12.6 -> 13.1; two-word tasks at 128 regs: c5 782 vs 707 µs/frame)
   const int n_int = std::min(p.d.n_links, p.n_interp - p.d.start);
   auto tiles = [&](int b) { return n_int > 0 && n_int % b == 0; };
-  if (p.words_per_warp == 1) {  // one-word tasks: 3 blocks/SM at 80 regs (4 at 64 regs: c2 chain 12.6 -> 13.1)
-    if (tiles(10)) launch_chain_dense_b<kLog, kMag, 10, 1, 3>(p, sm, s);
-    else if (tiles(8)) launch_chain_dense_b<kLog, kMag, 8, 1, 3>(p, sm, s);
-    else if (tiles(5) && !tiles(4)) launch_chain_dense_b<kLog, kMag, 5, 1, 3>(p, sm, s);
-    else launch_chain_dense_b<kLog, kMag, 4, 1, 3>(p, sm, s);
-  } else {
-    // (two-word tasks at 128 regs: batches of 8 measured slower on c5, 815 -> 870 us/frame)
-    if (tiles(5) && !tiles(4)) launch_chain_dense_b<kLog, kMag, 5, 2, 2>(p, sm, s);
-    else launch_chain_dense_b<kLog, kMag, 4, 2, 2>(p, sm, s);
-  }
+  if (tiles(10)) launch_chain_dense_b<kLog, kMag, 10, 1, 3>(p, sm, s);
+  else if (tiles(8)) launch_chain_dense_b<kLog, kMag, 8, 1, 3>(p, sm, s);
+  else if (tiles(5) && !tiles(4)) launch_chain_dense_b<kLog, kMag, 5, 1, 3>(p, sm, s);
+  else launch_chain_dense_b<kLog, kMag, 4, 1, 3>(p, sm, s);
 }
 
 template <bool kLog, bool kMag>

@@ -449,10 +449,9 @@ struct EventEngine {
   DevBuf masks, counts, prefix, link_total, segtab, segbase, seg_out, events, mcount, wcount, base, sched;
   int64_t capacity = 0;
 
-  // fine = true (dense, small frames): 8 words per block, one word per warp —
-  // finer tasks balance the few waves of a small frame (measured: c2 chain
-  // 16.4 -> 15.0 us/frame; 1080p c4 124 -> 112); 4K frames keep 2-word tasks
-  // and ~8 blocks/SM (c5: 815 vs 843 us/frame with 1-word tasks)
+  // fine = true (dense): one word per warp, 8 words per block on frames up
+  // to 1080p — finer tasks balance the few waves of a small frame (measured:
+  // c2 chain 16.4 -> 15.0 us/frame; 1080p c4 124 -> 112)
   void geometry(int w_, int h_, bool fine = false) {
     w = w_;
     h = h_;
@@ -463,9 +462,18 @@ struct EventEngine {
     int64_t per = (n_words + target - 1) / target;
     per = std::max<int64_t>(kWarpsPerBlock, (per + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock);
     words_per_warp = 2;
-    if (fine && (n_words + 7) / 8 <= 8192) {
-      per = 8;
+    if (fine) {
+      // one-word warp tasks; 8-word blocks up to 8192 blocks, beyond that
+      // ~45 blocks per SM (4K c5: 40-word blocks; chain 782 -> 707 and emit
+      // 220 -> 201 µs/frame against 224-word blocks of two-word tasks)
       words_per_warp = 1;
+      if ((n_words + 7) / 8 <= 8192) {
+        per = 8;
+      } else {
+        const int64_t t = 148 * 45;
+        per = (n_words + t - 1) / t;
+        per = std::max<int64_t>(kWarpsPerBlock, (per + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock);
+      }
     }
     wpb = (int)per;
     n_blocks = (int)((n_words + wpb - 1) / wpb);

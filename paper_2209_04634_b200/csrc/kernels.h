@@ -132,7 +132,7 @@ struct ChainParams {
   int64_t n_words;         // h * wpr
   int words_per_block;
   int n_blocks;
-  int words_per_warp;      // dense chain: 32-pixel words a warp evaluates together (1 or 2)
+  int words_per_warp;      // 32-pixel words a warp evaluates together (the dense chain: 1)
   int n_interp;            // N
   int n_pairs;
   int R, r0;
