@@ -1454,20 +1454,29 @@ __global__ void __launch_bounds__(256) select_mask_kernel(SelectParams p) {
   const int z = blockIdx.y;
   // sparse: (prev, curr) of the pair; difference_interp: (f[r0+z-1], f[r0+z]) = d1
   const int zoff = p.diff_mode ? -1 : 0;
-  const uint8_t* prev = p.frames.at((p.r0 + z + zoff + p.R) % p.R);
-  const uint8_t* curr = p.frames.at((p.r0 + z + 1 + zoff) % p.R);
+  auto wrap = [&](int s) {  // s in [0, 3R): s mod R without a division
+    if (s >= p.R) s -= p.R;
+    if (s >= p.R) s -= p.R;
+    return s;
+  };
+  const uint8_t* prev = p.frames.at(wrap(p.r0 % p.R + z + zoff + p.R));
+  const uint8_t* curr = p.frames.at(wrap(p.r0 % p.R + z + 1 + zoff));
   const bool none = p.diff_mode && p.skip_first && z == 0;
   uint32_t* masks = p.masks + (size_t)z * p.n_words;
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t wbeg = (int64_t)b * p.words_per_block;
   const int64_t wend = min(wbeg + p.words_per_block, p.n_words);
+  // (row, word column) of the warp's first word, then advanced incrementally
+  int row = (int)((uint32_t)(wbeg + warp) / (uint32_t)p.wpr);
+  int col = (int)(wbeg + warp - (int64_t)row * p.wpr);
   for (int64_t wi = wbeg + warp; wi < wend; wi += kWarpsPerBlock) {
-    const int row = (int)((uint32_t)wi / (uint32_t)p.wpr);
-    const int x = (int)(wi - (int64_t)row * p.wpr) * 32 + lane;
+    const int x = col * 32 + lane, wrow = row;
+    col += kWarpsPerBlock;
+    while (col >= p.wpr) col -= p.wpr, ++row;  // (rows of fewer than 8 words wrap more than once)
     bool take = false;
     if (x < p.w && !none) {
-      const size_t i = (size_t)row * p.w + x;
+      const size_t i = (size_t)wrow * p.w + x;
       const int a = prev[i], c = curr[i];
       if (p.diff_mode) {
         const int d = c - a;
