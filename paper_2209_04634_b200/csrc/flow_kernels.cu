@@ -851,7 +851,7 @@ __device__ __forceinline__ float sample_quad8(const uint32_t* __restrict__ q, in
 }
 
 // estimate_sparse_flow's per-point loop (flow.cpp:309-380), one thread per point.
-__global__ void __launch_bounds__(128) sparse_lk_kernel(SparseLKParams p) {
+__global__ void __launch_bounds__(128, 7) sparse_lk_kernel(SparseLKParams p) {
   const int z = blockIdx.y;  // frame pair
   const int64_t M = p.n_points ? (int64_t)p.n_points[z] : p.n_points_host;
   const uint32_t* points = p.points + z * p.pair_stride;
