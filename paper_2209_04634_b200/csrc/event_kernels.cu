@@ -1169,19 +1169,20 @@ __global__ void __launch_bounds__(256) offsets_row_kernel(OffsetParams p) {
 __global__ void __launch_bounds__(1024) segbase_kernel(EmitParams p, int64_t* segbase) {
   __shared__ int64_t s_warp[32];
   const int S = *p.seg.n_segs;
+  const int lo = p.seg_hi ? p.seg_lo : 0, hi = p.seg_hi ? p.seg_hi : S;  // (a sub-batch's segments)
   const int64_t b0 = *p.base;  // events of earlier launches of the same call
   __syncthreads();
   int64_t carry = b0;
-  for (int s0 = 0; s0 < S; s0 += blockDim.x) {
+  for (int s0 = lo; s0 < hi; s0 += blockDim.x) {
     const int s = s0 + threadIdx.x;
     int64_t tot = 0;
-    if (s < S) {
+    if (s < hi) {
       const int k0 = p.seg.seg_first[s], nk = p.seg.seg_nlinks[s];
       for (int k = k0; k < k0 + nk; ++k) tot += p.link_total[k];
     }
     int64_t chunk;
     const int64_t excl = block_exclusive_scan(tot, s_warp, chunk);
-    if (s < S) {
+    if (s < hi) {
       segbase[s] = carry + excl;
       p.seg_out[1 + s] = p.seg.seg_t[s];
       p.seg_out[1 + S + s] = carry + excl;
@@ -1230,10 +1231,11 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
   // events in earlier blocks; segments without events in this block are
   // dropped from the item list (their masks are never read)
   int n_nz = 0;
-  for (int s0 = 0; s0 < S; s0 += blockDim.x) {
+  const int slo = p.seg_hi ? p.seg_lo : 0, shi = p.seg_hi ? p.seg_hi : S;  // (a sub-batch's segments)
+  for (int s0 = slo; s0 < shi; s0 += blockDim.x) {
     const int s = s0 + threadIdx.x;
     int nz = 0;
-    if (s < S) {
+    if (s < shi) {
       const int k0 = p.seg.seg_first[s], nk = p.seg.seg_nlinks[s];
       int64_t o = segbase[s];
       uint32_t cnt = 0;

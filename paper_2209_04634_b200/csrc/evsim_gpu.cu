@@ -884,6 +884,7 @@ struct evsim_gpu_sim {
   void run_events(ChainParams& c, int provider, const int64_t* ts, int64_t* h_seg, bool continue_call = false,
                   const std::vector<int>& sub = {}) {
     const int G = c.d.n_links * c.n_pairs;
+    const int L = c.d.n_links;
     if (!continue_call) CK(cudaMemsetAsync(ev.base.p, 0, sizeof(int64_t), stream));
     SegParams sp{};
     sp.d = c.d;
@@ -893,35 +894,6 @@ struct evsim_gpu_sim {
     for (int i = 0; i <= c.n_pairs; ++i) sp.ts[i] = ts[i];
     launch_segments(sp, stream);
     CK_LAUNCH("segments");
-    if (sub.empty()) {
-      launch_chain(c, provider, stream);
-      CK_LAUNCH("chain");
-    } else {
-      const int L = c.d.n_links;
-      for (size_t b = 0; b + 1 < sub.size(); ++b) {
-        const int off = sub[b], nb = sub[b + 1] - sub[b];
-        CK(cudaStreamWaitEvent(stream, pipe_ev[1 + b], 0));
-        ChainParams cb = c;
-        cb.r0 = c.r0 + off;
-        cb.n_pairs = nb;
-        cb.g0.pu += (size_t)off * c.g0.pair_stride;
-        cb.g0.pv += (size_t)off * c.g0.pair_stride;
-        cb.masks += (size_t)off * L * ev.n_words;
-        cb.counts += (size_t)off * L * ev.n_blocks;
-        if (c.magnitude) {
-          cb.mcount += (size_t)off * L * ev.n_words * 32;
-          cb.wcount += (size_t)off * L * ev.n_words;
-        }
-        launch_chain(cb, provider, stream);
-        CK_LAUNCH("chain");
-      }
-      launches += (int64_t)sub.size() - 2;
-    }
-    mark(EVSIM_STAGE_SCAN);
-    OffsetParams op{G, ev.n_blocks, ev.counts.as<uint32_t>(), ev.prefix.as<int64_t>(), ev.link_total.as<int64_t>()};
-    launch_offsets(op, stream);
-    CK_LAUNCH("offsets");
-    mark(EVSIM_STAGE_EMIT);
     EmitParams ep{};
     ep.w = w;
     ep.h = h;
@@ -943,8 +915,69 @@ struct evsim_gpu_sim {
     ep.wcount = ev.wcount.as<uint32_t>();
     ep.capacity = ev.capacity;
     ep.out = ev.events.as<uint32_t>();
-    launch_emit(ep, ev.segbase.as<int64_t>(), stream);
-    CK_LAUNCH("emit");
+    // offsets + segment bases + emit of links [g0, g1) (segments = links when
+    // every link has its own timestamp)
+    auto emit_links = [&](int g0, int g1, bool range) {
+      OffsetParams op{g1 - g0, ev.n_blocks, ev.counts.as<uint32_t>() + (size_t)g0 * ev.n_blocks,
+                      ev.prefix.as<int64_t>() + (size_t)g0 * ev.n_blocks, ev.link_total.as<int64_t>() + g0};
+      launch_offsets(op, stream);
+      CK_LAUNCH("offsets");
+      mark(EVSIM_STAGE_EMIT);
+      EmitParams e = ep;
+      e.seg_lo = range ? g0 : 0;
+      e.seg_hi = range ? g1 : 0;
+      launch_emit(e, ev.segbase.as<int64_t>(), stream);
+      CK_LAUNCH("emit");
+    };
+    if (sub.empty()) {
+      launch_chain(c, provider, stream);
+      CK_LAUNCH("chain");
+      mark(EVSIM_STAGE_SCAN);
+      emit_links(0, G, false);
+    } else {
+      // every link its own timestamp (no collisions, one event per
+      // crossing): sub-batch b's events are emitted right after its chain,
+      // overlapping the next sub-batch's chain — a link's output offset only
+      // needs the totals of the links before it
+      // (not in the streamed call: its chunks already overlap the emit with
+      // the next chunk's flow, and per-sub-batch emits measured slower there)
+      bool split = !c.magnitude && !continue_call;
+      {
+        const int K = c.n_interp + 1;
+        auto stamp = [&](int i, int l) {
+          const int k = c.d.start + (l + 1) * c.d.step;
+          return k == K ? ts[i + 1] : sub_interval_end(ts[i], ts[i + 1], k, K);
+        };
+        int64_t tp = 0;
+        for (int g = 0; split && g < G; ++g) {
+          const int64_t t = stamp(g / L, g % L);
+          if (g > 0 && t == tp) split = false;
+          tp = t;
+        }
+      }
+      for (size_t b = 0; b + 1 < sub.size(); ++b) {
+        const int off = sub[b], nb = sub[b + 1] - sub[b];
+        CK(cudaStreamWaitEvent(stream, pipe_ev[1 + b], 0));
+        ChainParams cb = c;
+        cb.r0 = c.r0 + off;
+        cb.n_pairs = nb;
+        cb.g0.pu += (size_t)off * c.g0.pair_stride;
+        cb.g0.pv += (size_t)off * c.g0.pair_stride;
+        cb.masks += (size_t)off * L * ev.n_words;
+        cb.counts += (size_t)off * L * ev.n_blocks;
+        if (c.magnitude) {
+          cb.mcount += (size_t)off * L * ev.n_words * 32;
+          cb.wcount += (size_t)off * L * ev.n_words;
+        }
+        launch_chain(cb, provider, stream);
+        CK_LAUNCH("chain");
+        if (split) emit_links(off * L, (off + nb) * L, true);
+      }
+      launches += (int64_t)sub.size() - 2;
+      if (split) launches += 3 * ((int64_t)sub.size() - 2);
+      mark(EVSIM_STAGE_SCAN);
+      if (!split) emit_links(0, G, false);
+    }
     launches += 6;
     CK(cudaMemcpyAsync(h_seg, ev.seg_out.p, (3 + 2 * (size_t)G) * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
     last_emit = ep;

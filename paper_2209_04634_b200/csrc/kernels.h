@@ -195,6 +195,7 @@ struct EmitParams {
   int words_per_block;
   int n_blocks;
   int n_links;             // links of the launch (pairs * per-pair links)
+  int seg_lo, seg_hi;      // segments this launch emits: [seg_lo, seg_hi), or all when seg_hi == 0
   SegTable seg;
   const int64_t* prefix;
   const uint32_t* counts;  // [g][n_blocks] events per (link, block)
