@@ -56,7 +56,7 @@ def main(rep, outdir):
     def total(name):
         xs = [x for x in out if name in x["kernel"]]
         return int(sum(x["dram_rd_MB"] + x["dram_wr_MB"] for x in xs) * 1e6) if xs else None
-    per = {n: total(n) for n in ("chain_dense_kernel", "offsets_kernel", "segbase_kernel", "emit_kernel")}
+    per = {n: total(n) for n in ("chain_dense_kernel", "offsets", "segbase_kernel", "emit_kernel")}
     if all(v is not None for v in per.values()):
         json.dump({"source": f"{outdir}/ncu_full_summary.json (ncu --set full --clock-control none, every launch of one push)",
                    "workload": "c2 log, 128-frame push (127 pairs per launch), tools/profile_c2.sh",
