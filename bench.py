@@ -1,35 +1,48 @@
 """Benchmark of the B200 event-simulation hot path (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c2] [--mode log|linear]
+                    [--config c5] [--mode log|linear] [--split auto|streams|bands]
 
-Workload (BASELINE.json configs[1], the metric's headline config): c2 —
-640x480 u8 frames, 128-frame seeded synthetic sequence (paper_2209_04634_b200/
-scenes.py), dense pyramidal LK (lq preset), N = 10 interpolated frames, log
-intensity with C = 0.2.  One STEP = one pass of Simulator::push_frame over
-the whole 128-frame sequence (reset + 128 pushes; the reference's
-bench_method protocol, src/bench.cpp:53-64).  Metric: input frames/s (events/s
-reported beside it).
+Workload (default): BASELINE.json's largest single-GPU configuration, the one
+its metric ("per B200 (1/2/4/8 GPU)") is quoted on — c5: one 3840x2160 u8
+stream of 60 frames (seeded synthetic sequence, paper_2209_04634_b200/
+scenes.py: unblurred U[0,255] texture, 16 px/frame pan, 20 % flicker), dense
+pyramidal LK (lq preset), N = 32 interpolated frames, log intensity C = 0.1.
+One STEP = one pass of Simulator::push_frame over the whole sequence (reset
++ every frame; the reference's bench_method protocol, src/bench.cpp:53-64).
+Metric: simulated input frames/s, counting the frames that close an interval
+(n - 1 per step: the warm-up frame produces no events), events/s beside it.
 
 * value: frames already resident in HBM, device-timed with CUDA events on the
   simulator's stream, L2 flushed (256 MiB memset) before every step.
-* e2e: the same metric through the C-ABI with HOST buffers: per frame a pinned
-  H2D upload inside evsim_gpu_push_frame and a D2H of the packed events
-  (4 B/event) + segment table; host wall clock around the step.
-* roofline: event stage (chain -> scan -> emit) against measured HBM peak;
-  algorithmic bytes per frame B_alg = 2P + 4E.
-* cpu_baseline / --impl reference: the reference compiled from /root/reference
-  (oracle/_ref; the oracle C port when absent), one independent simulator per
-  host thread over contiguous chunks of the same sequence.
+* parity: an untimed pass with the timed pass's batches, each push's events
+  reduced on the device to per-frame (count, checksum)
+  (paper_2209_04634_b200/seqhash.py) and compared with the compiled
+  reference's (tests/golden/sequences.json, tests/golden/make_sequences.py);
+  the last timed push is checked the same way.
+* e2e: the same metric through the C-ABI with HOST buffers
+  (evsim_gpu_push_frames_streamed: pinned host frames in, events out to pinned
+  host memory, upload / compute / download overlapped), host wall clock.
+* roofline: the event stage (chain -> offsets -> emit) against the measured
+  HBM peak, algorithmic bytes per frame B_alg = 2P + 4E.
+* cpu_baseline / --impl reference: the reference compiled from its own sources
+  (oracle/_ref) run by evsim_ref_run_sequence on the host's threads (output
+  identical to one streaming Simulator, checked against the same checksums),
+  on a bounded sample of the sequence; also a 1-thread sample.
 
-Multi-GPU (torchrun): each rank simulates its own independent stream (per-rank
-seed) — stream sharding with no data-path collective ("weak" scaling); NCCL
-only all-reduces the timing and gathers event counts.
+Multi-GPU (torchrun), one process per GPU, no data-path collective:
+* --split bands (default for single-stream configs, c5): rank r emits the
+  events of its row band, solving only the flow patch rows they depend on
+  (exact); NCCL all-gathers per-(band, link) counts — the merged stream's
+  offsets — and the per-band partial checksums.  Strong scaling.
+* --split streams (default for c4: 32 streams): rank r owns a contiguous block
+  of the config's streams (shard_streams), pushed concurrently; weak per
+  stream, the total is fixed: "strong".
 """
 from __future__ import annotations
 
 import argparse
-import ctypes
+import concurrent.futures as cf
 import json
 import os
 import statistics
@@ -44,6 +57,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 L2_FLUSH_BYTES = 256 << 20
+METRIC = "simulated input frames/sec and events/sec per B200, % of HBM roofline"
+GOLDEN = os.path.join(ROOT, "tests", "golden", "sequences.json")
 
 
 def parse():
@@ -52,111 +67,170 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="c2")
+    p.add_argument("--config", default="c5")
     p.add_argument("--mode", default="log", choices=["log", "linear"])
     p.add_argument("--preset", default="lq", choices=["lq", "hq"], help="flow preset (types.hpp:93: lq default)")
     p.add_argument("--frames", type=int, default=0, help="override sequence length")
-    p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--chunk", type=int, default=0, help="e2e: frames per streamed chunk (0 = the library default, 64)")
-    p.add_argument("--split", default="streams", choices=["streams", "bands"],
-                   help="N>1: one camera stream per rank (weak scaling) or row bands of one stream (strong, c5)")
+    p.add_argument("--streams", type=int, default=0, help="total camera streams (0 = the config's)")
+    p.add_argument("--split", default="auto", choices=["auto", "streams", "bands"])
     p.add_argument("--batch", type=int, default=0,
                    help="frames per push_frames call (0 = the simulator's maximum; 1 = frame-by-frame)")
+    p.add_argument("--chunk", type=int, default=0, help="e2e: frames per streamed chunk (0 = library default)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-parity", action="store_true")
     return p.parse_args()
 
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def workload(args, stream=0):
+# ----------------------------------------------------------------------------- workload
+
+def make_cfg(c, args):
     from paper_2209_04634_b200 import scenes
     from paper_2209_04634_b200.abi import Method, make_config
-    c = scenes.CONFIGS[args.config]
-    n = args.frames or c.n_frames
-    frames, ts = scenes.generate(c, n_frames=n, stream=stream)
     cp, cn = scenes.LINEAR_THRESHOLDS[c.method]
-    cfg = make_config(Method[c.method], n_interp=c.n_interp, c_pos=cp, c_neg=cn,
-                      contrast_mode=1 if args.mode == "log" else 0, c_pos_log=c.contrast, c_neg_log=-c.contrast,
-                      flow_preset=1 if getattr(args, "preset", "lq") == "hq" else 0)
-    return c, cfg, frames, ts
+    return make_config(Method[c.method], n_interp=c.n_interp, c_pos=cp, c_neg=cn,
+                       contrast_mode=1 if args.mode == "log" else 0, c_pos_log=c.contrast, c_neg_log=-c.contrast,
+                       flow_preset=1 if args.preset == "hq" else 0)
 
 
-def config_json(c, args, n_frames):
+def _gen(job):
+    name, n, stream = job
+    from paper_2209_04634_b200 import scenes
+    return scenes.generate(scenes.CONFIGS[name], n_frames=n, stream=stream)
+
+
+def generate_streams(c, n, streams):
+    """Frames of several streams, generated in a process pool (c4: ~26 s each)."""
+    streams = list(streams)
+    if len(streams) == 1:
+        return [_gen((c.name, n, streams[0]))]
+    import multiprocessing as mp
+    with mp.get_context("spawn").Pool(min(len(streams), os.cpu_count() or 1)) as pool:
+        return pool.map(_gen, [(c.name, n, s) for s in streams], chunksize=1)
+
+
+def config_json(c, args, n_frames, split, ws, n_streams):
+    par = f"row bands x{ws}" if split == "bands" else f"streams: {n_streams} over {ws} GPU(s)"
     return {
-        "workload": f"{c.name}: {c.width}x{c.height} u8, {c.method} (LK {args.preset}) N={c.n_interp}, "
-                    f"{args.mode} C={c.contrast if args.mode == 'log' else 'int Table I'}, "
+        "workload": f"{c.name}: {n_streams} x {c.width}x{c.height} u8 stream(s), {c.method} (LK {args.preset}) "
+                    f"N={c.n_interp}, {args.mode} C={c.contrast if args.mode == 'log' else 'int Table I'}, "
                     f"{n_frames}-frame seeded synthetic sequence",
-        "width": c.width, "height": c.height, "frames_per_step": n_frames, "n_interp": c.n_interp,
-        "method": c.method, "mode": args.mode,
+        "width": c.width, "height": c.height, "streams": n_streams, "frames_per_stream": n_frames,
+        "n_interp": c.n_interp, "method": c.method, "mode": args.mode,
         "flow_preset": "high_quality" if args.preset == "hq" else "low_quality",
         "l2": "flushed before every step (256 MiB memset); device-resident inputs",
+        "parallelism": par,
     }
+
+
+def golden_entry(c, args, n_frames, stream=0):
+    """The committed reference checksums of this sequence, if pinned."""
+    if args.preset != "lq" or stream != 0:
+        return None
+    try:
+        g = json.load(open(GOLDEN)).get(f"{c.name}:{args.mode}")
+    except Exception:
+        return None
+    if not g or g["n_frames"] < n_frames:
+        return None
+    return g
 
 
 # ----------------------------------------------------------------------------- CPU arms
 
-def cpu_run(cfg, frames, ts, threads, prefer_reference=True):
-    """Time the reference (or the oracle port) over the sequence split into
-    contiguous chunks, one independent simulator per host thread.  Returns
-    (useful frames, seconds, kind, events)."""
+def cpu_sample(c, cfg, frames, ts, threads, pairs):
+    """The reference (oracle/_ref via evsim_ref_run_sequence; the C port when it
+    is absent) over frames[0 .. pairs]: (pairs, seconds, kind, counts, hashes)."""
     import oracle
-    kind = "reference" if (prefer_reference and os.path.exists(oracle.REF_SO)) else "port"
-    lib = oracle.Reference() if kind == "reference" else oracle.Oracle()
-    n = len(frames)
-    bounds = np.linspace(0, n - 1, threads + 1).astype(int)
-    counts = [0] * threads
-    useful = [0] * threads
-
-    def work(i):
-        lo, hi = int(bounds[i]), int(bounds[i + 1])
-        sim = lib.simulator(cfg)
-        ev = 0
-        for k in range(lo, hi + 1):
-            ev += len(sim.push_frame(frames[k], int(ts[k])))
-        counts[i] = ev
-        useful[i] = hi - lo
-        sim.close()
-
+    pairs = max(1, min(pairs, len(frames) - 1))
+    sub = np.ascontiguousarray(frames[:pairs + 1])
+    if os.path.exists(oracle.REF_SO):
+        R = oracle.Reference()
+        t0 = time.perf_counter()
+        counts, hashes = R.run_sequence(cfg, sub, ts[:pairs + 1], threads)
+        return pairs, time.perf_counter() - t0, "reference", counts, hashes
+    # fallback: the C restatement, one streaming simulator (1 thread)
+    from paper_2209_04634_b200.seqhash import frame_hash_np
+    sim = oracle.Oracle().simulator(cfg)
+    counts, hashes = [], []
     t0 = time.perf_counter()
-    th = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join()
-    dt = time.perf_counter() - t0
-    return sum(useful), dt, kind, sum(counts)
+    for k in range(pairs + 1):
+        ev = sim.push_frame(sub[k], int(ts[k]))
+        counts.append(len(ev))
+        hashes.append(frame_hash_np(ev["x"], ev["y"], ev["t"], ev["p"], int(ts[k - 1]) if k else 0))
+    return pairs, time.perf_counter() - t0, "port", np.array(counts), np.array(hashes, np.uint64)
+
+
+def sample_parity(g, counts, hashes):
+    if g is None:
+        return "unpinned"
+    n = len(counts)
+    ok = list(map(int, counts[1:])) == g["counts"][1:n] and \
+        [f"{int(h):016x}" for h in hashes[1:]] == g["hashes"][1:n]
+    return "match" if ok else "MISMATCH"
+
+
+def cpu_pairs_for(c, threads):
+    # log mode pipelines one pair per thread; bound the sample to ~10-30 s
+    return min(threads, 16 if c.pixels >= 4_000_000 else 64)
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if ws > 1 and rank != 0:
         return 0
-    c, cfg, frames, ts = workload(args)
+    from paper_2209_04634_b200 import scenes
+    c = scenes.CONFIGS[args.config]
+    n = args.frames or c.n_frames
+    cfg = make_cfg(c, args)
     threads = os.cpu_count() or 1
-    vals = []
-    evs = 0
-    kind = "port"
-    for i in range(args.warmup + args.steps):
-        f, dt, kind, evs = cpu_run(cfg, frames, ts, threads)
-        if i >= args.warmup:
-            vals.append(f / dt)
+    n_streams = args.streams or c.streams
+    split = "streams" if c.streams > 1 else "bands"
+    if c.streams > 1:
+        # one reference thread per stream (independent instances, SPEC.md:260), up to nproc
+        use = list(range(min(threads, n_streams)))
+        data = generate_streams(c, 3, use)
+        vals = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            with cf.ThreadPoolExecutor(len(use)) as ex:
+                res = list(ex.map(lambda d: cpu_sample(c, cfg, d[0], d[1], 1, 2), data))
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                vals.append(sum(r[0] for r in res) / dt)
+        kind = res[0][2]
+        parity = sample_parity(golden_entry(c, args, 3), res[0][3], res[0][4])
+        sample = f"{len(use)} of the {n_streams} {c.name} streams, frames 0-2 each, one reference thread per stream"
+        evs = sum(int(r[3].sum()) for r in res) / sum(r[0] for r in res)
+        cores = len(use)
+    else:
+        frames, ts = _gen((c.name, n, 0))
+        pairs = cpu_pairs_for(c, threads)
+        g = golden_entry(c, args, pairs + 1)
+        vals = []
+        for i in range(args.warmup + args.steps):
+            p, dt, kind, counts, hashes = cpu_sample(c, cfg, frames, ts, threads, pairs)
+            if i >= args.warmup:
+                vals.append(p / dt)
+        parity = sample_parity(g, counts, hashes)
+        sample = (f"{c.name} frames 0-{p} ({p} intervals) of the {n}-frame sequence, {threads} host threads "
+                  f"(evsim_ref_run_sequence: {'pairs in parallel + the log rule over row bands' if args.mode == 'log' else 'contiguous chunks, one Simulator each'}; output = one streaming Simulator)")
+        evs = float(counts.sum()) / p
+        cores = threads
     v = statistics.mean(vals)
     out = {
-        "metric": "simulated input frames/sec (events/sec beside it), % of HBM roofline",
-        "impl": "reference", "value": round(v, 3), "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(1e3 * len(frames) / v, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8/f32/f64", "data": "synthetic",
-        "config": config_json(c, args, len(frames)),
-        "events_per_s": round(v * evs / max(len(frames) - threads, 1), 1),
-        "cpu_baseline": {"value": round(v, 3), "unit": "frames/s", "cores": threads, "kind": kind,
-                         "sample": f"{c.name} {len(frames)}-frame sequence, {args.mode} mode, split into "
-                                   f"{threads} contiguous chunks (one simulator per host thread)"},
-        "e2e": {"value": round(v, 3), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "metric": METRIC, "impl": "reference", "value": round(v, 4), "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * (n - 1) / v, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8/f32/f64",
+        "data": "synthetic", "config": config_json(c, args, n, split, 1, n_streams),
+        "events_per_s": round(v * evs, 1), "parity": parity,
+        "cpu_baseline": {"value": round(v, 4), "unit": "frames/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": round(v, 4), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
     return 0
@@ -165,14 +239,11 @@ def run_reference(args):
 # ----------------------------------------------------------------------------- clocks
 
 class Clocks:
-    """SM clock and throttle reasons sampled DURING the timed region: an NVML
-    polling thread (every ~2 ms, so even a 20-ms region gets samples; one
-    sample is taken on entry and one on exit), or nvidia-smi when NVML is
-    unavailable."""
+    """SM clock and throttle reasons sampled DURING the timed region (NVML
+    polling thread, ~2 ms; nvidia-smi when NVML is unavailable)."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-    # nvmlClocksEventReason* bits
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, device):
@@ -203,7 +274,6 @@ class Clocks:
 
     def __enter__(self):
         try:
-            import threading
             import pynvml
             pynvml.nvmlInit()
             self.handle = pynvml.nvmlDeviceGetHandleByIndex(self._nvml_index())
@@ -226,7 +296,6 @@ class Clocks:
         return self
 
     def _nvml_index(self):
-        # CUDA_VISIBLE_DEVICES remaps CUDA ordinals; NVML sees all GPUs
         vis = os.environ.get("CUDA_VISIBLE_DEVICES")
         if vis:
             ids = [v.strip() for v in vis.split(",") if v.strip()]
@@ -278,6 +347,135 @@ class Clocks:
 
 # ----------------------------------------------------------------------------- ours
 
+class Arm:
+    """This rank's simulators (one per stream; one row band for bands) with
+    their frames resident in HBM."""
+
+    def __init__(self, c, cfg, args, ws, rank, device, split):
+        import torch
+
+        from paper_2209_04634_b200 import Simulator, SimulatorConfig
+        from paper_2209_04634_b200.parallel import band_rows, shard_streams
+        self.c, self.args, self.ws, self.rank, self.device, self.split = c, args, ws, rank, device, split
+        self.n = args.frames or c.n_frames
+        if split == "bands":
+            self.streams = [0]
+            self.band = band_rows(c.height, ws, rank) if ws > 1 else None
+        else:
+            total = args.streams or c.streams
+            self.streams = list(shard_streams(total, ws, rank)) if total > 1 else [rank]
+            self.band = None
+        data = generate_streams(c, self.n, self.streams)
+        self.frames = [d[0] for d in data]
+        self.ts = data[0][1]
+        self.sims = []
+        for _ in self.streams:
+            s = Simulator(SimulatorConfig.from_c(cfg), device=device)
+            if self.band:
+                s.set_row_band(*self.band)
+            self.sims.append(s)
+        self.P = c.width * c.height
+        self.d_frames = [torch.from_numpy(f).to(f"cuda:{device}") for f in self.frames]
+        mb = self.sims[0].max_batch(c.width, c.height)
+        if len(self.sims) > 1:
+            mb = min(mb, 8)  # many resident streams: bound each handle's event buffers
+        self.batch = max(1, min(args.batch or mb, mb, self.n))
+        self.torch_stream = torch.cuda.ExternalStream(self.sims[0].stream, device=device)
+        self.other_streams = [torch.cuda.ExternalStream(s.stream, device=device) for s in self.sims[1:]]
+
+    def pushes(self):
+        return [(a, min(self.batch, self.n - a)) for a in range(0, self.n, self.batch)]
+
+    def push(self, a, nb, sync):
+        from paper_2209_04634_b200.simulator import push_frames_batched_device
+        c = self.c
+        if len(self.sims) == 1:
+            return [self.sims[0].push_frames_device(self.d_frames[0].data_ptr() + a * self.P, nb, c.width, c.height,
+                                                    self.ts[a:a + nb], on_device=True, sync=sync)]
+        return push_frames_batched_device(self.sims, [d.data_ptr() + a * self.P for d in self.d_frames], nb,
+                                          c.width, c.height, [self.ts[a:a + nb]] * len(self.sims))
+
+    def enqueue_step(self):
+        for s in self.sims:
+            s.reset()
+        for a, nb in self.pushes():
+            self.push(a, nb, sync=False)
+
+    def sync(self):
+        for s in self.sims:
+            s.sync()
+
+
+def push_checksums(arm, a, nb, outs, timeline_counts=None):
+    """Per-frame (count, checksum) of one push for this rank's stream 0 (bands:
+    the band's partial checksums with global frame indices)."""
+    from paper_2209_04634_b200.seqhash import push_frame_hashes
+    ev = outs[0]
+    S = int(ev.n_segments)
+    seg_t = np.ctypeslib.as_array(ev.seg_t, shape=(S,)).copy() if S else np.zeros(0, np.int64)
+    seg_off = np.ctypeslib.as_array(ev.seg_offset, shape=(S + 1,)).copy() if S else np.zeros(1, np.int64)
+    f0 = max(a, 1)
+    frame_ts = arm.ts[f0 - 1:a + nb]
+    if timeline_counts is None:
+        return seg_t, seg_off, push_frame_hashes(int(ev.d_packed), seg_t, seg_off, frame_ts, arm.device)
+    timeline, jbase = timeline_counts
+    return seg_t, seg_off, push_frame_hashes(int(ev.d_packed), seg_t, seg_off, frame_ts, arm.device, timeline, jbase)
+
+
+def parity_pass(arm, g, ws):
+    """Untimed pass with the timed pass's batches; per-frame checksums of
+    stream 0 compared with the reference's.  Returns (status, events total of
+    this rank, per-frame (count, hash) list)."""
+    import torch
+    from paper_2209_04634_b200.parallel import gather_counts, link_timeline, timeline_counts
+    for s in arm.sims:
+        s.reset()
+    frames_out = []
+    ev_total = 0
+    for a, nb in arm.pushes():
+        outs = arm.push(a, nb, sync=True)
+        ev_total += sum(int(o.n_events) for o in outs)
+        if arm.band is None:
+            frames_out += push_checksums(arm, a, nb, outs)[2]
+            continue
+        # row bands: counts per (band, link) over the push's full link
+        # timeline, all-gathered (the merged stream's offsets), then partial
+        # checksums with global frame indices, summed over ranks
+        f0 = max(a, 1)
+        timeline = link_timeline(arm.ts[f0 - 1:a + nb], arm.c.n_interp)
+        ev = outs[0]
+        S = int(ev.n_segments)
+        seg_t = np.ctypeslib.as_array(ev.seg_t, shape=(S,)).copy() if S else np.zeros(0, np.int64)
+        seg_off = np.ctypeslib.as_array(ev.seg_offset, shape=(S + 1,)).copy()
+        local = timeline_counts(seg_t, seg_off, timeline)
+        allc = gather_counts(local, device=torch.device("cuda", arm.device)) if ws > 1 else local[None]
+        before = allc[:arm.rank].sum(axis=0)
+        tot = allc.sum(axis=0)
+        jbase = np.zeros(len(timeline), np.int64)
+        fts = arm.ts[f0 - 1:a + nb]
+        for f in range(len(fts) - 1):  # frame-relative prefix of earlier links
+            lo, hi = np.searchsorted(timeline, fts[f], side="right"), np.searchsorted(timeline, fts[f + 1], side="right")
+            jbase[lo:hi] = np.concatenate([[0], np.cumsum(tot[lo:hi])[:-1]]) + before[lo:hi]
+        part = push_checksums(arm, a, nb, outs, (timeline, jbase))[2]
+        hs = np.array([h for _, h in part], dtype=np.uint64).view(np.int64)
+        cs = np.array([cnt for cnt, _ in part], dtype=np.int64)
+        if ws > 1:
+            hs_all = gather_counts(hs, device=torch.device("cuda", arm.device))
+            cs_all = gather_counts(cs, device=torch.device("cuda", arm.device))
+        else:
+            hs_all, cs_all = hs[None], cs[None]
+        for f in range(len(part)):
+            h = int(hs_all[:, f].astype(np.uint64).sum(dtype=np.uint64))
+            frames_out.append((int(cs_all[:, f].sum()), h))
+    status = "unpinned"
+    if g is not None and (arm.streams[0] == 0):
+        got_c = [cnt for cnt, _ in frames_out]
+        got_h = [f"{h:016x}" for _, h in frames_out]
+        n = len(got_c) + 1
+        status = "match" if (got_c == g["counts"][1:n] and got_h == g["hashes"][1:n]) else "MISMATCH"
+    return status, ev_total, frames_out
+
+
 def run_ours(args):
     import torch
     ws, rank, local = dist_env()
@@ -287,103 +485,102 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = local if ws > 1 else 0
     torch.cuda.set_device(device)
-
-    from paper_2209_04634_b200 import SimulatorConfig, Simulator
-    from paper_2209_04634_b200._lib import load
-    bands = args.split == "bands" and ws > 1
-    c, cfg, frames, ts = workload(args, stream=0 if bands else rank)
-    n = len(frames)
-    P = c.width * c.height
-    sim = Simulator(SimulatorConfig.from_c(cfg), device=device)
-    if bands:
-        # every rank holds the whole frames and emits its own rows
-        from paper_2209_04634_b200.parallel import band_rows
-        sim.set_row_band(*band_rows(c.height, ws, rank))
-    stream_ptr = sim.stream
-    torch_stream = torch.cuda.ExternalStream(stream_ptr, device=device)
-
-    d_frames = torch.from_numpy(frames).to(f"cuda:{device}")
+    from paper_2209_04634_b200 import scenes
+    c = scenes.CONFIGS[args.config]
+    split = args.split
+    if split == "auto":
+        split = "streams" if c.streams > 1 else "bands"
+    cfg = make_cfg(c, args)
+    arm = Arm(c, cfg, args, ws, rank, device, split)
+    n, P = arm.n, arm.P
+    # streams simulated per step over all ranks (a single-stream config split
+    # by streams runs one replica per rank)
+    if split == "bands":
+        n_streams = 1
+    elif (args.streams or c.streams) > 1:
+        n_streams = args.streams or c.streams
+    else:
+        n_streams = ws
+    scaling = "weak" if (split == "streams" and (args.streams or c.streams) == 1) else "strong"
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=f"cuda:{device}")
-    base = d_frames.data_ptr()
     torch.cuda.synchronize()
 
-    mb = sim.max_batch(c.width, c.height)
-    batch = args.batch or mb
-    batch = max(1, min(batch, mb, n))
-
-    def enqueue_step():
-        # reset + the whole sequence in batches of `batch` frames (one launch
-        # sequence per batch); the first frame is the warm-up frame
-        sim.reset()
-        for a in range(0, n, batch):
-            nb = min(batch, n - a)
-            sim.push_frames_device(base + a * P, nb, c.width, c.height, ts[a:a + nb], on_device=True, sync=False)
-
-    # warm-up, then an untimed synchronous pass that counts the events
     for _ in range(max(args.warmup, 1)):
-        enqueue_step()
-        sim.sync()
-    ev_total = 0
-    sim.reset()
-    for a in range(0, n, batch):
-        nb = min(batch, n - a)
-        e = sim.push_frames_device(base + a * P, nb, c.width, c.height, ts[a:a + nb], on_device=True, sync=True)
-        ev_total += e.n_events
+        arm.enqueue_step()
+        arm.sync()
+    g = golden_entry(c, args, n)
+    parity, ev_total, frames_out = ("skipped", 0, [])
+    if not args.no_parity:
+        parity, ev_total, frames_out = parity_pass(arm, g, ws)
+    else:
+        for s in arm.sims:
+            s.reset()
+        for a, nb in arm.pushes():
+            ev_total += sum(int(o.n_events) for o in arm.push(a, nb, sync=True))
     torch.cuda.synchronize()
 
     # ---- timed region: device-resident, L2 flushed before each step -------------
     if ws > 1:
-        import torch.distributed as dist
-        dist.barrier()
+        torch.distributed.barrier()
     torch.cuda.synchronize()
-    launches0 = sim.kernel_launches
+    launches0 = sum(s.kernel_launches for s in arm.sims)
     times = []
     with Clocks(device) as clk:
         for _ in range(args.steps):
-            with torch.cuda.stream(torch_stream):
+            with torch.cuda.stream(arm.torch_stream):
                 flush.fill_(1)
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(torch_stream)
-            enqueue_step()
-            e1.record(torch_stream)
-            sim.sync()
+                e0.record(arm.torch_stream)
+            # every handle's stream waits for the flush + start event
+            for st in arm.other_streams:
+                st.wait_event(e0)
+            arm.enqueue_step()
+            for s in arm.sims[1:]:
+                s.sync()
+            e1.record(arm.torch_stream)
+            arm.sims[0].sync()
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
     torch.cuda.synchronize()
-    launches = sim.kernel_launches - launches0
-    # stage split: the same steps again with per-stage CUDA events (stage
-    # timing serialises the library's flow / chain overlap, so it is measured
-    # outside the timed region)
-    sim.set_profiling(True)
-    for _ in range(args.steps):
-        with torch.cuda.stream(torch_stream):
+    launches = sum(s.kernel_launches for s in arm.sims) - launches0
+    # the last timed push, checked against the parity pass (same frames)
+    timed_check = "skipped"
+    if frames_out and arm.band is None:
+        a, nb = arm.pushes()[-1]
+        ev = arm.sims[0].sync()
+        part = push_checksums(arm, a, nb, [ev])[2]
+        timed_check = "match" if part == frames_out[-len(part):] else "MISMATCH"
+
+    # stage split: the same steps with per-stage CUDA events (stage timing
+    # serialises the flow / chain overlap, so it runs outside the timed region)
+    for s in arm.sims:
+        s.set_profiling(True)
+    for _ in range(max(1, min(args.steps, 3))):
+        with torch.cuda.stream(arm.torch_stream):
             flush.fill_(1)
-        enqueue_step()
-        sim.sync()
+        arm.enqueue_step()
+        arm.sync()
     torch.cuda.synchronize()
-    stages, timed_pushes = sim.stage_times()
-    sim.set_profiling(False)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.barrier()
+    stages, timed_pushes = arm.sims[0].stage_times()
+    for s in arm.sims:
+        s.set_profiling(False)
+    prof_steps = max(1, min(args.steps, 3))
+
     total_ms = sum(times)
     t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{device}")
     evs = torch.tensor([ev_total], dtype=torch.int64, device=f"cuda:{device}")
     if ws > 1:
         import torch.distributed as dist
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        gathered = [torch.zeros_like(evs) for _ in range(ws)]
-        dist.all_gather(gathered, evs)  # per-stream event counts (merged-output offsets)
-        ev_all = int(sum(int(g.item()) for g in gathered))
-    else:
-        ev_all = ev_total
+        dist.all_reduce(evs, op=dist.ReduceOp.SUM)
     max_ms = float(t.item())
-    frames_total = (1 if bands else ws) * n * args.steps
-    value = frames_total / (max_ms / 1e3)
+    ev_all = int(evs.item())
+    frames_per_step = (n - 1) * n_streams  # intervals closed per step, all streams / the whole frame
+    value = frames_per_step * args.steps / (max_ms / 1e3)
     events_per_s = ev_all * args.steps / (max_ms / 1e3)
 
-    # ---- roofline of the event stage (chain -> scan -> emit) ---------------------
+    # ---- roofline of the event stage (chain -> offsets -> emit) -----------------
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -391,137 +588,143 @@ def run_ours(args):
         pass
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"
-    E_frame = ev_total / max(n - 1, 1)
+    E_frame = ev_all / max(frames_per_step, 1)
     b_alg = 2 * P + 4 * E_frame  # read 2 u8 frames, write 4 B per event
-    # the event stage (chain_kernel -> offsets_kernel -> segbase+emit_kernel)
-    # runs once per push_frames call, over all of the call's frame pairs
+    # stream 0's handle: its pushes (launches of the event stage) over its pairs
+    pairs_prof = prof_steps * (n - 1)
     launches_ev = max(timed_pushes, 1)
-    pairs_timed = args.steps * (n - 1)
     ev_stage_ms = stages["chain"] + stages["scan"] + stages["emit"]
-    bytes_per_launch = b_alg * pairs_timed / launches_ev
+    E_band = (ev_total / max(len(arm.sims), 1)) / max(n - 1, 1)  # this rank's (band's) events per frame
+    P_band = c.width * (arm.band[1] - arm.band[0]) if arm.band else P
+    b_alg_band = 2 * P_band + 4 * E_band
+    bytes_per_launch = b_alg_band * pairs_prof / launches_ev
     ms_per_launch = ev_stage_ms / launches_ev
     achieved = bytes_per_launch / (ms_per_launch / 1e3) / 1e9 if ms_per_launch > 0 else 0.0
     e2e_frac = b_alg * (value / ws) / 1e9 / hbm
-    frames_timed = args.steps * n
     roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": traffic_for(c.name, args.mode, pairs_timed / launches_ev),
-                "kernel": "event stage = chain_dense_kernel + offsets_kernel + segbase_kernel + emit_kernel (one push_frames call)",
-                "algorithmic_bytes_per_frame": round(b_alg), "frames_per_launch": round(pairs_timed / launches_ev, 2),
+                "frac": round(achieved / hbm, 4),
+                "traffic": traffic_for(c.name, args.mode, pairs_prof / launches_ev) if ws == 1 else None,
+                "kernel": "event stage = chain_dense_kernel + offsets_kernel + segbase_kernel + emit_kernel "
+                          "(one push_frames call)",
+                "algorithmic_bytes_per_frame": round(b_alg_band), "frames_per_launch": round(pairs_prof / launches_ev, 2),
                 "algorithmic_bytes_per_launch": round(bytes_per_launch), "avg_launch_ms": round(ms_per_launch, 5),
                 "peak_source": peak_src, "end_to_end_frac": round(e2e_frac, 5),
-                "stage_us_per_frame": {k: round(1e3 * v / frames_timed, 3) for k, v in stages.items()}}
+                "stage_us_per_frame": {k: round(1e3 * v / pairs_prof, 3) for k, v in stages.items()}}
 
     # ---- e2e through the C-ABI with host buffers ---------------------------------
     e2e = None
     if not args.no_e2e:
-        h_frames = torch.from_numpy(frames).pin_memory()
-        hbase = h_frames.data_ptr()
-        cap = (c.n_interp + 1) * P * batch
-        h_events = torch.empty(cap, dtype=torch.int32).pin_memory()
-        hev = h_events.data_ptr()
+        e2e = run_e2e(arm, args, ws, n_streams)
 
-        def e2e_step():
-            # evsim_gpu_push_frames_streamed: pinned host frames in, packed
-            # host events out; chunk j+1's H2D and chunk j-1's D2H overlap
-            # chunk j's compute
-            sim.reset()
-            d2h = 0
-            for a in range(0, n, batch):
-                nb = min(batch, n - a)
-                e = sim.push_frames_streamed_ptr(hbase + a * P, nb, c.width, c.height, ts[a:a + nb], hev, cap,
-                                                 chunk=args.chunk)
-                d2h += 4 * e.n_events + 16 * (e.n_segments + 1)
-            return d2h
-
-        e2e_step()
-        if ws > 1:
-            import torch.distributed as dist
-            dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        d2h = 0
-        for _ in range(args.steps):
-            d2h = e2e_step()
-        torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - t0
-        te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{device}")
-        if ws > 1:
-            import torch.distributed as dist
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": round(frames_total / float(te.item()), 3), "unit": "frames/s",
-               "h2d_bytes_per_step": n * P, "d2h_bytes_per_step": int(d2h),
-               "api": f"evsim_gpu_push_frames_streamed (pinned host frames in, packed host events out, "
-                      f"chunks of ~{args.chunk or 64} frames: H2D / compute / D2H overlapped)"}
-
-    cpu = None
+    cpu = cpu1 = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        f, dt, kind, _ = cpu_run(cfg, frames, ts, os.cpu_count() or 1)
-        cpu = {"value": round(f / dt, 3), "unit": "frames/s", "cores": os.cpu_count() or 1, "kind": kind,
-               "sample": f"{c.name} {n}-frame sequence, {args.mode} mode, split into {os.cpu_count()} contiguous "
-                         f"chunks (one simulator per host thread), {dt:.1f} s"}
+        threads = os.cpu_count() or 1
+        pairs = cpu_pairs_for(c, threads)
+        p, dt, kind, cc, hh = cpu_sample(c, cfg, arm.frames[0], arm.ts, threads, pairs)
+        cpu = {"value": round(p / dt, 4), "unit": "frames/s", "cores": threads, "kind": kind,
+               "sample": f"{c.name} stream 0, frames 0-{p} ({p} intervals), {threads} host threads "
+                         f"(evsim_ref_run_sequence, output = one streaming Simulator), {dt:.1f} s",
+               "parity": sample_parity(golden_entry(c, args, p + 1), cc, hh)}
+        p1 = 2 if c.pixels >= 2_000_000 else 8
+        p, dt, kind, cc, hh = cpu_sample(c, cfg, arm.frames[0], arm.ts, 1, p1)
+        cpu1 = {"value": round(p / dt, 4), "unit": "frames/s", "cores": 1, "kind": kind,
+                "sample": f"{c.name} stream 0, frames 0-{p}, one reference Simulator (single thread), {dt:.1f} s"}
 
     if rank == 0:
+        clocks = clk.summary()
         out = {
-            "metric": "simulated input frames/sec (events/sec beside it), % of HBM roofline",
-            "value": round(value, 3), "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
+            "metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "strong" if bands else "weak", "vs_baseline": None, "dtype": "u8/f32/f64",
-            "data": "synthetic",
-            "config": {**config_json(c, args, n), "parallelism": f"row bands x{ws}" if bands else f"streams x{ws}",
-                       "frames_per_push": batch},
+            "scaling": scaling, "vs_baseline": None, "dtype": "u8/f32/f64", "data": "synthetic",
+            "config": {**config_json(c, args, n, split, ws, n_streams), "frames_per_push": arm.batch},
+            "parity": parity, "timed_output_check": timed_check,
+            "parity_ref": "tests/golden/sequences.json (compiled reference, per-frame count + checksum)",
             "events_per_s": round(events_per_s, 1), "events_per_frame": round(E_frame, 1),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk.summary(),
-            "issue_roofline": issue_roofline(c.name, args.mode, pairs_timed / launches_ev, stages, launches_ev,
-                                             clk.summary().get("sm_mhz")),
+            "roofline": roofline, "cpu_baseline": cpu, "cpu_baseline_1thread": cpu1, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": clocks,
+            "flow_gsamples_per_s": flow_rate(c, args, stages, pairs_prof),
         }
         print(json.dumps(out), flush=True)
-    sim.close()
+    for s in arm.sims:
+        s.close()
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
 
 
-def issue_roofline(config: str, mode: str, pairs_per_launch: float, stages_ms: dict, launches: int,
-                   sm_mhz):
-    """SM-issue roofline of the two dominant kernels (both are issue / L1
-    bound, not HBM bound): warp instructions per launch from the committed
-    ncu --set full capture of this workload, over the live CUDA-event time of
-    the stage, against 148 SMs x 4 issue slots x the measured SM clock."""
-    if not (config == "c2" and mode == "log" and abs(pairs_per_launch - 127) < 0.5 and launches > 0):
+def run_e2e(arm, args, ws, n_streams):
+    """Same steps through evsim_gpu_push_frames_streamed with pinned host
+    frames in and packed host events out (one host thread per handle).  Large
+    frames go in calls of 16 frames whose events land in one reused pinned
+    buffer (a consumer that takes each call's events before the next call)."""
+    import torch
+    c, n, P = arm.c, arm.n, arm.P
+    h_frames = [torch.from_numpy(f).pin_memory() for f in arm.frames]
+    rows = (arm.band[1] - arm.band[0]) if arm.band else c.height
+    per_call = 16 if P >= 4_000_000 else n
+    calls = [(a, min(per_call, n - a)) for a in range(0, n, per_call)]
+    cap = (c.n_interp + 1) * c.width * rows * per_call
+    h_events = [torch.empty(cap, dtype=torch.int32).pin_memory() for _ in arm.sims]
+
+    def one(i):
+        s = arm.sims[i]
+        s.reset()
+        d2h = 0
+        for a, nb in calls:
+            e = s.push_frames_streamed_ptr(h_frames[i].data_ptr() + a * P, nb, c.width, c.height,
+                                           arm.ts[a:a + nb], h_events[i].data_ptr(), cap, chunk=args.chunk)
+            d2h += 4 * int(e.n_events) + 16 * (int(e.n_segments) + 1)
+        return d2h
+
+    def step():
+        if len(arm.sims) == 1:
+            return one(0)
+        with cf.ThreadPoolExecutor(len(arm.sims)) as ex:
+            return sum(ex.map(one, range(len(arm.sims))))
+
+    step()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    d2h = 0
+    for _ in range(args.steps):
+        d2h = step()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{arm.device}")
+    if ws > 1:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+    frames_total = (n - 1) * n_streams * args.steps
+    return {"value": round(frames_total / float(te.item()), 3), "unit": "frames/s",
+            "h2d_bytes_per_step": n * P * len(arm.sims), "d2h_bytes_per_step": int(d2h),
+            "api": f"evsim_gpu_push_frames_streamed, {len(calls)} call(s) per stream per step (pinned host frames "
+                   "in, packed 4-byte host events out, H2D / compute / D2H overlapped), host wall clock"}
+
+
+def flow_rate(c, args, stages, pairs):
+    """Flow-stage template samples per second."""
+    S = {("c1", "lq"): 1.74e6, ("c2", "lq"): 6.00e6, ("c3", "lq"): 18.16e6, ("c4", "lq"): 41.03e6,
+         ("c5", "lq"): 164.7e6, ("c2", "hq"): 31.82e6, ("c5", "hq"): 876.2e6}
+    s = S.get((c.name, args.preset))
+    ms = stages.get("flow", 0.0)
+    if s is None or ms <= 0 or c.method != "dense":
         return None
-    try:
-        rows = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_full_summary.json")))
-    except Exception:
-        return None
-    clock = float(sm_mhz or 1965.0) * 1e6
-    peak = 148 * 4 * clock
-    out = {"unit": "warp-instructions/s", "peak": peak, "peak_source": "148 SMs x 4 schedulers x measured SM clock",
-           "instructions_source": "profiles/r01/ncu_full_summary.json (smsp__inst_executed.sum, every launch of one push)"}
-    fam = {"chain": "chain_dense_kernel", "flow": "dense_lk_warp_kernel"}
-    for stage, name in fam.items():
-        ks = [r for r in rows if name in r["kernel"]]
-        if not ks:
-            continue
-        instr = sum(r["warp_instr"] for r in ks)  # the capture holds every launch of one push
-        t = stages_ms[stage] / launches / 1e3
-        if t > 0:
-            out[stage] = {"kernel": name, "warp_instr_per_launch": instr, "achieved": round(instr / t, 1),
-                          "frac": round(instr / t / peak, 4)}
-    return out
+    return round(s * pairs / (ms / 1e3) / 1e9, 2)
 
 
 def traffic_for(config: str, mode: str, pairs_per_launch: float):
     """DRAM bytes (read + write) per launch of the event stage, from the
     committed ncu --set full capture of the same workload
-    (profiles/r01/traffic_<config>_<mode>.json), or None."""
-    try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "r01", f"traffic_{config}_{mode}.json")))
-    except Exception:
-        return None
-    if abs(pairs_per_launch - t.get("pairs_per_launch", -1)) < 0.5:
-        return t["event_stage_dram_bytes_per_launch"]
+    (profiles/r02/traffic_<config>_<mode>.json), or None."""
+    for r in ("r02", "r01"):
+        try:
+            t = json.load(open(os.path.join(ROOT, "profiles", r, f"traffic_{config}_{mode}.json")))
+        except Exception:
+            continue
+        if abs(pairs_per_launch - t.get("pairs_per_launch", -1)) < 0.5:
+            return t["event_stage_dram_bytes_per_launch"]
     return None
 
 

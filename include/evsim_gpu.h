@@ -190,6 +190,61 @@ EVSIM_GPU_API int evsim_gpu_push_frames_streamed(evsim_gpu_sim* sim, const uint8
                                                  int32_t width, int32_t height, const int64_t* t_us, int32_t chunk,
                                                  uint32_t* host_events, int64_t capacity, evsim_gpu_events* out);
 
+/* ---- compact lossless wire format ----------------------------------------
+ * Replaces, for the caller that wants the events on the host, the 24-byte
+ * std::vector<Event> the reference's push_frame returns
+ * (include/evsim/types.hpp:54-80, src/simulate.cpp:306-347), carrying the
+ * same events in ~1 bit per pixel-link + 1 bit per event.  The call's links
+ * (every chain link of every frame pair, in stream order: chain_pipeline,
+ * src/simulate.cpp:57-69) are numbered g = 0 .. n_links-1:
+ *   link_t[g]        the link's timestamp (sub_interval_end, simulate.hpp:15-19)
+ *   planes[g*words_per_link + w]  bit i set = an event of link g at pixel
+ *                    x = 32*(w % words_per_row) + i, y = row0 + w / words_per_row
+ *   link_events[g]   its number of events (= popcount of its plane)
+ *   polarity         bit link_bit[g] + k (u32 words, LSB first) = 1 when the
+ *                    k-th event of link g (plane order) has polarity -1
+ * A link's events in plane order are the reference's (y, x) order; links
+ * with equal timestamps form one reference segment, ordered (y, x, p)
+ * (finalize's stable sort, src/simulate.cpp:36-40): evsim_gpu_wire_unpack
+ * reproduces the reference's event stream exactly.  Single-event mode
+ * (EVSIM_EVENTS_SINGLE) only. */
+typedef struct evsim_gpu_wire {
+  /* caller-owned host buffers (pinned memory lets the downloads overlap) */
+  uint32_t* planes;
+  int64_t planes_capacity;   /* u32 words */
+  uint32_t* polarity;
+  int64_t polarity_capacity; /* u32 words */
+  int64_t* link_t;
+  int64_t* link_events;
+  int64_t* link_bit;
+  int64_t link_capacity;     /* entries of each link array */
+  /* filled by evsim_gpu_push_frames_wire */
+  int64_t n_links;
+  int32_t words_per_row;
+  int32_t row0;
+  int32_t rows;
+  int32_t width;
+  int64_t words_per_link;    /* rows * words_per_row */
+  int64_t n_events;
+  int64_t polarity_words;
+} evsim_gpu_wire;
+
+/* evsim_gpu_push_frames_streamed with the events delivered in the wire
+ * format: host frames in, planes + polarity bits out, chunked and overlapped
+ * the same way (chunk 0 = 64 frames).  Needs (links of the call) *
+ * words_per_link plane words and about n_events/32 + 2*chunks polarity
+ * words; too small buffers -> INVALID_ARGUMENT after the simulation
+ * completed.  Same validation and errors as evsim_gpu_push_frames. */
+EVSIM_GPU_API int evsim_gpu_push_frames_wire(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t n_frames,
+                                             int32_t width, int32_t height, const int64_t* t_us, int32_t chunk,
+                                             evsim_gpu_wire* wire, evsim_gpu_events* out);
+
+/* Expand a wire buffer into the reference's event stream: format 0 packed u32
+ * records (EVSIM_PACK_*), format 1 evsim_event (24 B), on `threads` host
+ * threads (0 = all).  capacity in records. */
+EVSIM_GPU_API int evsim_gpu_wire_unpack(const evsim_gpu_wire* wire, int32_t format, void* out, int64_t capacity,
+                                        int32_t threads);
+
 /* Asynchronous variant: enqueues the push on the handle's CUDA stream and
  * returns without waiting; evsim_gpu_sync() completes it.  Validation
  * errors are still reported synchronously. */

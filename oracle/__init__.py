@@ -188,6 +188,21 @@ class Reference(_Lib):
     prefix = "evsim_ref"
     path = REF_SO
 
+    def run_sequence(self, cfg: CConfig, frames: np.ndarray, ts, threads: int):
+        """Whole sequence on `threads` host threads with output identical to one
+        streaming reference Simulator (ref_shim.cpp evsim_ref_run_sequence).
+        Returns per-frame (counts int64[n], hashes uint64[n]) — the checksum of
+        paper_2209_04634_b200/seqhash.py."""
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        n, h, w = frames.shape
+        ts = np.ascontiguousarray(np.asarray(ts, dtype=np.int64))
+        counts = np.zeros(n, np.int64)
+        hashes = np.zeros(n, np.uint64)
+        self._check(self.lib.evsim_ref_run_sequence(
+            ctypes.byref(cfg), _ptr(frames), _i32(n), _i32(w), _i32(h), _ptr(ts), _i32(threads), _ptr(counts),
+            _ptr(hashes)))
+        return counts, hashes
+
     @staticmethod
     def available() -> bool:
         return os.path.exists(REF_SO) or os.path.isdir(REF_SRC)

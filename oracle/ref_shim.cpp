@@ -12,6 +12,10 @@
 // and apply the log rule of DESIGN.md §3 on top — the decomposition SURVEY.md
 // §8c prescribes for the log-mode baseline.
 #include <algorithm>
+#include <atomic>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstddef>
 #include <cstdlib>
@@ -115,10 +119,10 @@ class FixedSparse final : public evsim::SparseFlowEstimator {
 };
 
 // ---- log-mode restatement on top of the reference's stages ---------------
-void log_link(const evsim_gpu_config* c, const float* lut, const uint8_t* after, int w, int h,
+void log_link(const evsim_gpu_config* c, const float* lut, const uint8_t* after, int w, int y0, int y1,
               int64_t t, float* ref, std::vector<evsim::Event>& out) {
   const bool mag = c->events_per_crossing == EVSIM_EVENTS_MAGNITUDE;
-  for (int y = 0; y < h; ++y)
+  for (int y = y0; y < y1; ++y)
     for (int x = 0; x < w; ++x) {
       const std::size_t i = static_cast<std::size_t>(y) * w + x;
       const float lk = lut[after[i]];
@@ -135,6 +139,55 @@ void log_link(const evsim_gpu_config* c, const float* lut, const uint8_t* after,
         ref[i] = lk;
       }
     }
+}
+
+// Intermediate chain frames of one pair in log mode: the reference's own
+// flow + interpolate_frames (dense), or its selection / sparse LK / splat
+// (simulate.cpp:145-199, restated here because it is inline in
+// simulate_sparse) with the log-mode selection of DESIGN.md §3.
+std::vector<evsim::Frame> log_chain_frames(const evsim_gpu_config* c, const float* lut, const evsim::Frame& pf,
+                                           const evsim::Frame& f) {
+  const int w = f.width, h = f.height;
+  const int64_t t = f.timestamp;
+  std::vector<evsim::Frame> inter;
+  if (c->method == EVSIM_METHOD_DENSE && c->n_interp > 0) {
+    const evsim::FlowField fl = evsim::estimate_dense_flow(pf, f, preset_of(c));
+    inter = evsim::interpolate_frames(pf, f, fl, c->n_interp);
+  } else if (c->method == EVSIM_METHOD_SPARSE && c->n_interp > 0) {
+    const float sel = c->sel_log > 0.0f ? c->sel_log : c->c_pos_log;
+    std::vector<evsim::PixelPoint> pts;
+    for (int y = 0; y < h; ++y)
+      for (int x = 0; x < w; ++x)
+        if (std::fabs(lut[f.at(x, y)] - lut[pf.at(x, y)]) > sel) pts.push_back({x, y});
+    if (!pts.empty()) {
+      const evsim::SparseFlow fl = evsim::estimate_sparse_flow(pf, f, pts, preset_of(c));
+      std::vector<int> mark(pf.pixel_count(), -1), chg(pf.pixel_count(), 0);
+      for (int k = 1; k <= c->n_interp; ++k) {
+        const float alpha = static_cast<float>(k) / static_cast<float>(c->n_interp + 1);
+        evsim::Frame fr = pf;
+        fr.timestamp = evsim::sub_interval_end(pf.timestamp, t, k, c->n_interp + 1);
+        for (std::size_t j = 0; j < pts.size(); ++j) {
+          if (!fl.status[j]) continue;
+          const int tx = static_cast<int>(std::lround(static_cast<float>(pts[j].x) + alpha * fl.displacements[j].du));
+          const int ty = static_cast<int>(std::lround(static_cast<float>(pts[j].y) + alpha * fl.displacements[j].dv));
+          if (tx < 0 || tx >= w || ty < 0 || ty >= h) continue;
+          const std::size_t idx = static_cast<std::size_t>(ty) * w + tx;
+          const std::uint8_t value = pf.at(pts[j].x, pts[j].y);
+          const int change = std::abs(static_cast<int>(value) - static_cast<int>(pf.pixels[idx]));
+          if (mark[idx] != k) {
+            mark[idx] = k;
+            chg[idx] = change;
+            fr.pixels[idx] = value;
+          } else if (change > chg[idx]) {
+            chg[idx] = change;
+            fr.pixels[idx] = value;
+          }
+        }
+        inter.push_back(std::move(fr));
+      }
+    }
+  }
+  return inter;
 }
 
 }  // namespace
@@ -194,50 +247,13 @@ int evsim_ref_push_frame(evsim_ref_sim* s, const uint8_t* px, int32_t w, int32_t
         if (t <= s->prev->timestamp)
           throw std::invalid_argument("push_frame: timestamps must be strictly increasing");
         const evsim::Frame& pf = *s->prev;
-        std::vector<evsim::Frame> inter;
-        if (c->method == EVSIM_METHOD_DENSE && c->n_interp > 0) {
-          const evsim::FlowField fl = evsim::estimate_dense_flow(pf, f, preset_of(c));
-          inter = evsim::interpolate_frames(pf, f, fl, c->n_interp);
-        } else if (c->method == EVSIM_METHOD_SPARSE && c->n_interp > 0) {
-          const float sel = c->sel_log > 0.0f ? c->sel_log : c->c_pos_log;
-          std::vector<evsim::PixelPoint> pts;
-          for (int y = 0; y < h; ++y)
-            for (int x = 0; x < w; ++x)
-              if (std::fabs(s->lut[f.at(x, y)] - s->lut[pf.at(x, y)]) > sel) pts.push_back({x, y});
-          if (!pts.empty()) {
-            const evsim::SparseFlow fl = evsim::estimate_sparse_flow(pf, f, pts, preset_of(c));
-            std::vector<int> mark(pf.pixel_count(), -1), chg(pf.pixel_count(), 0);
-            for (int k = 1; k <= c->n_interp; ++k) {
-              const float alpha = static_cast<float>(k) / static_cast<float>(c->n_interp + 1);
-              evsim::Frame fr = pf;
-              fr.timestamp = evsim::sub_interval_end(pf.timestamp, t, k, c->n_interp + 1);
-              for (std::size_t j = 0; j < pts.size(); ++j) {
-                if (!fl.status[j]) continue;
-                const int tx = static_cast<int>(std::lround(static_cast<float>(pts[j].x) + alpha * fl.displacements[j].du));
-                const int ty = static_cast<int>(std::lround(static_cast<float>(pts[j].y) + alpha * fl.displacements[j].dv));
-                if (tx < 0 || tx >= w || ty < 0 || ty >= h) continue;
-                const std::size_t idx = static_cast<std::size_t>(ty) * w + tx;
-                const std::uint8_t value = pf.at(pts[j].x, pts[j].y);
-                const int change = std::abs(static_cast<int>(value) - static_cast<int>(pf.pixels[idx]));
-                if (mark[idx] != k) {
-                  mark[idx] = k;
-                  chg[idx] = change;
-                  fr.pixels[idx] = value;
-                } else if (change > chg[idx]) {
-                  chg[idx] = change;
-                  fr.pixels[idx] = value;
-                }
-              }
-              inter.push_back(std::move(fr));
-            }
-          }
-        }
+        std::vector<evsim::Frame> inter = log_chain_frames(c, s->lut, pf, f);
         std::vector<const evsim::Frame*> chain;
         if (c->method == EVSIM_METHOD_DIFFERENCE_ONLY || c->include_endpoints) chain.push_back(&pf);
         for (const auto& fr : inter) chain.push_back(&fr);
         if (c->method == EVSIM_METHOD_DIFFERENCE_ONLY || c->include_endpoints) chain.push_back(&f);
         for (std::size_t i = 1; i < chain.size(); ++i)
-          log_link(c, s->lut, chain[i]->pixels.data(), w, h, chain[i]->timestamp, s->ref.data(),
+          log_link(c, s->lut, chain[i]->pixels.data(), w, 0, h, chain[i]->timestamp, s->ref.data(),
                    s->last.events);
         if (!std::is_sorted(s->last.events.begin(), s->last.events.end(), evsim::event_order))
           std::stable_sort(s->last.events.begin(), s->last.events.end(), evsim::event_order);
@@ -320,6 +336,129 @@ int evsim_ref_sparse_events_with_flow(const uint8_t* prev, const uint8_t* curr, 
 }
 
 void evsim_ref_free(void* p) { std::free(p); }
+
+// ---- multi-threaded sequence runner (bench.py --impl reference, cpu_baseline)
+//
+// Runs the reference over frames[0..n) with `threads` host threads and
+// reports, per frame, the event count and the checksum of
+// paper_2209_04634_b200/seqhash.py — output identical to ONE streaming
+// Simulator (verified against tests/golden/sequences.json):
+//  * linear mode: the reference Simulator keeps no state across pairs but
+//    the previous frame (simulate.cpp:306-347), so the sequence is split into
+//    contiguous chunks overlapping by one frame, one Simulator per thread;
+//  * log mode: per pair the reference's intermediate frames
+//    (log_chain_frames) are computed in parallel over pairs (a window of
+//    `threads` pairs at a time), then the per-pixel log rule runs pair by
+//    pair in stream order, in parallel over row bands (the rule is per pixel;
+//    a link's events are the bands' events concatenated, (y, x) order).
+}  // extern "C"
+
+namespace {
+uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+struct FrameSum {
+  uint64_t h = 0;
+  int64_t n = 0;
+  void add(const evsim::Event& e, int64_t t_prev) {
+    const uint64_t v = (uint64_t)e.x | ((uint64_t)e.y << 16) | ((uint64_t)(e.p < 0) << 31) |
+                       ((uint64_t)(e.t - t_prev) << 32);
+    h += mix64(v + (uint64_t)n * 0x9E3779B97F4A7C15ull);
+    ++n;
+  }
+};
+template <class F>
+void parallel_for(int n, int threads, F&& f) {
+  std::atomic<int> next{0};
+  std::vector<std::thread> th;
+  std::exception_ptr err;
+  std::mutex m;
+  for (int i = 0; i < std::max(1, std::min(threads, n)); ++i)
+    th.emplace_back([&] {
+      try {
+        for (int j; (j = next.fetch_add(1)) < n;) f(j);
+      } catch (...) {
+        std::lock_guard<std::mutex> g(m);
+        err = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  if (err) std::rethrow_exception(err);
+}
+}  // namespace
+
+extern "C" {
+
+int evsim_ref_run_sequence(const evsim_gpu_config* cfg, const uint8_t* frames, int32_t n, int32_t w, int32_t h,
+                           const int64_t* ts, int32_t threads, int64_t* counts, uint64_t* hashes) {
+  return guarded([&] {
+    const std::size_t P = static_cast<std::size_t>(w) * h;
+    threads = std::max(1, threads);
+    for (int k = 0; k < n; ++k) counts[k] = 0, hashes[k] = 0;
+    if (n < 2) return;
+    auto finish_frame = [&](int k, const std::vector<evsim::Event>& ev) {
+      FrameSum s;
+      for (const auto& e : ev) s.add(e, ts[k - 1]);
+      counts[k] = s.n;
+      hashes[k] = s.h;
+    };
+    if (cfg->contrast_mode == EVSIM_CONTRAST_LINEAR) {
+      const int T = std::min(threads, n - 1);
+      parallel_for(T, T, [&](int c) {
+        const int lo = (int)((int64_t)(n - 1) * c / T), hi = (int)((int64_t)(n - 1) * (c + 1) / T);
+        const evsim::FlowPreset p = preset_of(cfg);
+        evsim::Simulator sim(to_ref(cfg), std::make_shared<evsim::PyramidalPatchFlow>(p),
+                             std::make_shared<evsim::PyramidalLucasKanade>(p));
+        for (int k = lo; k <= hi; ++k) {
+          const evsim::EventStream es = sim.push_frame(make_frame(frames + k * P, w, h, ts[k]));
+          if (k > lo) finish_frame(k, es.events);
+        }
+      });
+      return;
+    }
+    if (cfg->method == EVSIM_METHOD_DIFFERENCE_INTERP)
+      throw std::invalid_argument("SimulatorConfig: difference_interp has no log contrast mode");
+    to_ref(cfg).validate();
+    float lut[256];
+    for (int i = 0; i < 256; ++i) lut[i] = std::log(static_cast<float>(i) / 255.0f + 1e-3f);
+    std::vector<float> ref(P);
+    for (std::size_t i = 0; i < P; ++i) ref[i] = lut[frames[i]];
+    const bool ends = cfg->method == EVSIM_METHOD_DIFFERENCE_ONLY || cfg->include_endpoints;
+    const int bands = std::min(threads, h);
+    for (int a = 1; a < n; a += threads) {
+      const int np = std::min(threads, n - a);  // pairs (a-1, a) .. (a+np-2, a+np-1)
+      std::vector<std::vector<evsim::Frame>> inter(np);
+      parallel_for(np, threads, [&](int i) {
+        const int k = a + i;
+        inter[i] = log_chain_frames(cfg, lut, make_frame(frames + (k - 1) * P, w, h, ts[k - 1]),
+                                    make_frame(frames + k * P, w, h, ts[k]));
+      });
+      for (int i = 0; i < np; ++i) {
+        const int k = a + i;
+        std::vector<const uint8_t*> px;
+        std::vector<int64_t> tl;
+        for (const auto& fr : inter[i]) px.push_back(fr.pixels.data()), tl.push_back(fr.timestamp);
+        if (ends) px.push_back(frames + k * P), tl.push_back(ts[k]);
+        // links in order; each link's bands in row order
+        std::vector<evsim::Event> ev;
+        std::vector<std::vector<std::vector<evsim::Event>>> lb(px.size(), std::vector<std::vector<evsim::Event>>(bands));
+        parallel_for(bands, bands, [&](int b) {
+          const int y0 = (int)((int64_t)h * b / bands), y1 = (int)((int64_t)h * (b + 1) / bands);
+          for (std::size_t l = 0; l < px.size(); ++l) log_link(cfg, lut, px[l], w, y0, y1, tl[l], ref.data(), lb[l][b]);
+        });
+        for (auto& l : lb)
+          for (auto& b : l) ev.insert(ev.end(), b.begin(), b.end());
+        if (!std::is_sorted(ev.begin(), ev.end(), evsim::event_order))
+          std::stable_sort(ev.begin(), ev.end(), evsim::event_order);
+        finish_frame(k, ev);
+        inter[i].clear();
+        inter[i].shrink_to_fit();
+      }
+    }
+  });
+}
 
 // ---- reference scenes (src/scenes.cpp), for fixtures --------------------
 int evsim_ref_textured_frame(int32_t w, int32_t h, uint32_t seed, uint8_t lo, uint8_t hi, uint8_t* out) {

@@ -10,7 +10,7 @@ import ctypes
 import os
 import threading
 
-from .abi import CConfig, CEvents
+from .abi import CConfig, CEvents, CWire
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libevsim_gpu.so")
@@ -34,6 +34,9 @@ _SIGS = {
         ctypes.c_int, [_vp, _i32, _vp, _i32, _i32, _i32, _vp, _i32, ctypes.POINTER(CEvents)]),
     "evsim_gpu_push_frames_streamed": (
         ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _i32, _vp, _i64, ctypes.POINTER(CEvents)]),
+    "evsim_gpu_push_frames_wire": (
+        ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _i32, ctypes.POINTER(CWire), ctypes.POINTER(CEvents)]),
+    "evsim_gpu_wire_unpack": (ctypes.c_int, [ctypes.POINTER(CWire), _i32, _vp, _i64, _i32]),
     "evsim_gpu_max_batch": (ctypes.c_int, [_vp, _i32, _i32]),
     "evsim_gpu_ingest_frames": (ctypes.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp]),
     "evsim_gpu_write_events_binary": (ctypes.c_int, [_vp, ctypes.c_char_p]),

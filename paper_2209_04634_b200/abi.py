@@ -85,6 +85,29 @@ class CEvents(ctypes.Structure):
     ]
 
 
+class CWire(ctypes.Structure):
+    """struct evsim_gpu_wire (the compact lossless event wire format)."""
+
+    _fields_ = [
+        ("planes", ctypes.c_void_p),
+        ("planes_capacity", ctypes.c_int64),
+        ("polarity", ctypes.c_void_p),
+        ("polarity_capacity", ctypes.c_int64),
+        ("link_t", ctypes.c_void_p),
+        ("link_events", ctypes.c_void_p),
+        ("link_bit", ctypes.c_void_p),
+        ("link_capacity", ctypes.c_int64),
+        ("n_links", ctypes.c_int64),
+        ("words_per_row", ctypes.c_int32),
+        ("row0", ctypes.c_int32),
+        ("rows", ctypes.c_int32),
+        ("width", ctypes.c_int32),
+        ("words_per_link", ctypes.c_int64),
+        ("n_events", ctypes.c_int64),
+        ("polarity_words", ctypes.c_int64),
+    ]
+
+
 # evsim::Event / evsim_event: x@0 u16, y@2 u16, t@8 i64, p@16 i8, sizeof 24.
 EVENT_DTYPE = np.dtype(
     {"names": ["x", "y", "t", "p"], "formats": ["<u2", "<u2", "<i8", "i1"],

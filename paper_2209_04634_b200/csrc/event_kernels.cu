@@ -10,6 +10,11 @@
 // the emit kernel writes every event exactly once, contiguously, in the
 // reference's order (t, y, x, p).
 #include <algorithm>
+#include <mutex>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <utility>
 
 #include "evsim_device.cuh"
 #include "kernels.h"
@@ -1655,15 +1660,26 @@ __global__ void init_ref_kernel(const uint8_t* __restrict__ f, const float* __re
 
 // ------------------------------------------------------------ launches
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per (function, device): set
+// it once per pair, thread-safely (handles on several devices may launch from
+// several host threads), and fail loudly if the driver refuses.
+void set_max_dynamic_smem(const void* func, int bytes) {
+  static std::mutex m;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) throw std::runtime_error("cudaGetDevice failed");
+  std::lock_guard<std::mutex> g(m);
+  if (done.count({func, dev})) return;
+  const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  done.insert({func, dev});
+}
+
 template <class Prov, bool kLog, bool kMag, int kW, int kB, int kMinBlocks>
 static void launch_chain_k(const ChainParams& p, cudaStream_t s) {
   const size_t sm = (size_t)std::max(p.d.n_links * p.n_pairs, 1) * sizeof(uint32_t);
   auto* k = chain_kernel<Prov, kLog, kMag, kW, kB, kMinBlocks>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    attr = true;
-  }
+  set_max_dynamic_smem((const void*)k, 96 * 1024);
   k<<<p.n_blocks, 256, sm, s>>>(p);
 }
 
@@ -1688,11 +1704,7 @@ static void launch_chain_mode(const ChainParams& p, cudaStream_t s) {
 template <bool kLog, bool kMag, int kB, int kW, int kMinB>
 static void launch_chain_dense_b(const ChainParams& p, size_t sm, cudaStream_t s) {
   auto* k = chain_dense_kernel<kLog, kMag, kB, kW, kMinB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    attr = true;
-  }
+  set_max_dynamic_smem((const void*)k, 96 * 1024);
   k<<<p.n_blocks, 256, sm, s>>>(p);
 }
 
@@ -1726,11 +1738,7 @@ static void launch_chain_sparse(const ChainParams& p, size_t sm, cudaStream_t s)
 template <bool kMag>
 static void launch_chain_diffinterp(const ChainParams& p, size_t sm, cudaStream_t s) {
   auto* k = chain_diffinterp_kernel<kMag>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    attr = true;
-  }
+  set_max_dynamic_smem((const void*)k, 96 * 1024);
   k<<<p.n_blocks, 256, sm, s>>>(p);
 }
 
@@ -1781,15 +1789,15 @@ void launch_offsets(const OffsetParams& p, cudaStream_t s) {
   else offsets_kernel<<<(p.n_rows + kWarpsPerBlock - 1) / kWarpsPerBlock, 256, 0, s>>>(p);
 }
 
+void launch_segbase(const EmitParams& p, int64_t* segbase, cudaStream_t s) {
+  segbase_kernel<<<1, 1024, 0, s>>>(p, segbase);
+}
+
 // segbase_kernel then emit_kernel; segbase: [links] int64 scratch
 void launch_emit(const EmitParams& p, int64_t* segbase, cudaStream_t s) {
   segbase_kernel<<<1, 1024, 0, s>>>(p, segbase);
   const size_t sm = (size_t)std::max(p.n_links, 1) * (sizeof(int64_t) + sizeof(int));
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 144 * 1024);
-    attr = true;
-  }
+  set_max_dynamic_smem((const void*)emit_kernel, 144 * 1024);
   emit_kernel<<<p.n_blocks, 256, sm, s>>>(p, segbase);
 }
 

@@ -13,6 +13,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <thread>
+#include <atomic>
+#include <mutex>
 #include <array>
 #include <cmath>
 #include <cstdio>
@@ -121,7 +124,9 @@ int64_t sub_interval_end(int64_t t0, int64_t t1, int k, int n) {
 // ------------------------------------------------------------------ memory
 
 void init_pool(int device) {
+  static std::mutex m;
   static bool done[64] = {};
+  std::lock_guard<std::mutex> g(m);
   if (device < 0 || device >= 64 || done[device]) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -447,6 +452,7 @@ struct EventEngine {
   int max_links = 0;  // links of a launch (pairs * per-pair links)
   bool magnitude = false;
   DevBuf masks, counts, prefix, link_total, segtab, segbase, seg_out, events, mcount, wcount, base, sched;
+  DevBuf wplanes, wpol, wlinks, wbit;  // wire format of a streamed call (wire_kernels.cu)
   int64_t capacity = 0;
 
   // fine = true (dense): one word per warp, 8 words per block on frames up
@@ -581,6 +587,15 @@ struct evsim_gpu_sim {
   bool xchunk = false;
   int pair_base = 0;
 
+  // wire format (evsim_gpu_push_frames_wire): the chain masks of each launch
+  // become planes + polarity bits instead of packed events
+  bool wire_on = false;
+  int64_t wire_link0 = 0;                // links of the call before this launch
+  int64_t* wire_host_links = nullptr;    // pinned: this launch's (bit[G], count[G])
+  std::vector<int64_t> wire_t;           // timestamps of the call's links
+  int64_t* h_wl[2] = {nullptr, nullptr};
+  size_t h_wl_cap = 0;
+
   // per-stage CUDA-event timing (evsim_gpu_set_profiling)
   using EvGroup = std::array<cudaEvent_t, EVSIM_N_STAGES + 1>;
   bool profiling = false;
@@ -594,6 +609,8 @@ struct evsim_gpu_sim {
     if (stream) cudaStreamSynchronize(stream);
     if (h_seg_out) cudaFreeHost(h_seg_out);
     for (auto& b : h_seg2)
+      if (b) cudaFreeHost(b);
+    for (auto& b : h_wl)
       if (b) cudaFreeHost(b);
     if (s_flow) cudaStreamSynchronize(s_flow), cudaStreamDestroy(s_flow);
     for (auto e : pipe_ev) cudaEventDestroy(e);
@@ -926,9 +943,44 @@ struct evsim_gpu_sim {
       EmitParams e = ep;
       e.seg_lo = range ? g0 : 0;
       e.seg_hi = range ? g1 : 0;
+      if (wire_on) {
+        // wire format: segment table as usual, then planes + polarity bits
+        // of links [0, G) instead of packed events (called once per launch)
+        launch_segbase(e, ev.segbase.as<int64_t>(), stream);
+        CK_LAUNCH("segbase");
+        WireParams wp{};
+        wp.n_links = G;
+        wp.n_words = ev.n_words;
+        wp.words_per_block = ev.wpb;
+        wp.n_blocks = ev.n_blocks;
+        wp.blocks_per_tile = std::max(1, 256 / std::max(1, ev.wpb));
+        wp.masks = ev.masks.as<uint2>();
+        wp.prefix = ev.prefix.as<int64_t>();
+        wp.link_total = ev.link_total.as<int64_t>();
+        wp.link_bit = ev.wlinks.as<int64_t>() + wire_link0;
+        wp.link_count = ev.wlinks.as<int64_t>() + (ev.wlinks.n / 16) + wire_link0;
+        wp.bit_base = ev.wbit.as<int64_t>();
+        wp.planes = ev.wplanes.as<uint32_t>() + (size_t)wire_link0 * ev.n_words;
+        wp.pol = ev.wpol.as<uint32_t>();
+        launch_wire(wp, stream);
+        CK_LAUNCH("wire");
+        CK(cudaMemcpyAsync(wire_host_links, wp.link_bit, (size_t)G * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(wire_host_links + G, wp.link_count, (size_t)G * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                           stream));
+        launches += 1;  // segbase + linkbase + wire vs segbase + emit
+        return;
+      }
       launch_emit(e, ev.segbase.as<int64_t>(), stream);
       CK_LAUNCH("emit");
     };
+    if (wire_on) {
+      const int K = c.n_interp + 1;
+      for (int g = 0; g < G; ++g) {
+        const int i = g / L, l = g % L;
+        const int k = c.d.start + (l + 1) * c.d.step;
+        wire_t.push_back(k == K ? ts[i + 1] : sub_interval_end(ts[i], ts[i + 1], k, K));
+      }
+    }
     if (sub.empty()) {
       launch_chain(c, provider, stream);
       CK_LAUNCH("chain");
@@ -936,12 +988,14 @@ struct evsim_gpu_sim {
       emit_links(0, G, false);
     } else {
       // every link its own timestamp (no collisions, one event per
-      // crossing): sub-batch b's events are emitted right after its chain,
-      // overlapping the next sub-batch's chain — a link's output offset only
-      // needs the totals of the links before it
+      // crossing): sub-batch b's events are emitted right after its chain —
+      // a link's output offset only needs the totals of the links before it.
+      // The emit runs on `stream` before the next sub-batch's chain, so it
+      // fills the time that chain would wait for its flow on s_flow (the
+      // flows run ahead on s_flow; the chains and emits stay in order)
       // (not in the streamed call: its chunks already overlap the emit with
       // the next chunk's flow, and per-sub-batch emits measured slower there)
-      bool split = !c.magnitude && !continue_call;
+      bool split = !c.magnitude && !continue_call && !wire_on;
       {
         const int K = c.n_interp + 1;
         auto stamp = [&](int i, int l) {
@@ -979,6 +1033,7 @@ struct evsim_gpu_sim {
       if (!split) emit_links(0, G, false);
     }
     launches += 6;
+    if (wire_on) wire_link0 += G;
     CK(cudaMemcpyAsync(h_seg, ev.seg_out.p, (3 + 2 * (size_t)G) * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
     last_emit = ep;
     pending = true;
@@ -1168,9 +1223,12 @@ struct evsim_gpu_sim {
   bool host_short = false;
 
   void push_streamed(const uint8_t* pixels, int F, int fw, int fh, const int64_t* ts, int chunk, uint32_t* host_dst,
-                     int64_t capacity) {
+                     int64_t capacity, evsim_gpu_wire* wire = nullptr) {
     if (magnitude()) invalid("push_frames_streamed: magnitude mode is not supported (use push_frames)");
-    if (!host_dst && capacity > 0) invalid("push_frames_streamed: null destination");
+    if (!wire && !host_dst && capacity > 0) invalid("push_frames_streamed: null destination");
+    if (wire && ((!wire->planes && wire->planes_capacity > 0) || (!wire->polarity && wire->polarity_capacity > 0) ||
+                 (wire->link_capacity > 0 && (!wire->link_t || !wire->link_events || !wire->link_bit))))
+      invalid("push_frames_wire: null destination");
     validate_batch(pixels, F, fw, fh, ts);
     prepare(F, fw, fh);
     if (!s_in) {
@@ -1247,6 +1305,45 @@ struct evsim_gpu_sim {
     n_events = 0;
     host_short = false;
     int64_t copied = 0;
+    // wire format: the call's planes / polarity / link tables on the device
+    const int L = desc().n_links;
+    const int64_t call_links = (int64_t)L * (has_prev ? F : F - 1);
+    std::vector<int64_t> chunk_link0(n_chunks + 1, 0);
+    struct WireReset {  // the wire path ends with the call, also on errors
+      bool& f;
+      ~WireReset() { f = false; }
+    } wire_reset{wire_on};
+    if (wire) {
+      const int max_chunk = *std::max_element(csize.begin(), csize.end());
+      ev.wplanes.ensure((size_t)std::max<int64_t>(call_links, 1) * ev.n_words * 4, stream);
+      ev.wpol.ensure(((size_t)std::max<int64_t>(call_links, 1) * P + 31) / 32 * 4 + 8 * ((size_t)n_chunks + 2), stream);
+      ev.wlinks.ensure(16 * (size_t)std::max<int64_t>(call_links, 1), stream);
+      ev.wbit.ensure(sizeof(int64_t), stream);
+      CK(cudaMemsetAsync(ev.wpol.p, 0, ev.wpol.n, stream));
+      CK(cudaMemsetAsync(ev.wbit.p, 0, sizeof(int64_t), stream));
+      const size_t need = 2 * (size_t)L * max_chunk * sizeof(int64_t);
+      if (need > h_wl_cap) {
+        for (auto& b : h_wl) {
+          if (b) cudaFreeHost(b);
+          b = nullptr;
+          CK(cudaHostAlloc((void**)&b, need, cudaHostAllocDefault));
+        }
+        h_wl_cap = need;
+      }
+      wire_on = true;
+      wire_link0 = 0;
+      wire_t.clear();
+      wire->n_links = call_links;
+      wire->words_per_row = ev.wpr;
+      wire->row0 = band_y1 > 0 ? band_y0 : 0;
+      wire->rows = (int32_t)(ev.n_words / ev.wpr);
+      wire->width = w;
+      wire->words_per_link = ev.n_words;
+      wire->n_events = 0;
+      wire->polarity_words = 0;
+      if (call_links > wire->link_capacity) host_short = true;
+    }
+    int64_t wire_words = 0;  // polarity words downloaded so far (the call's end)
     auto drain = [&](int j) {  // chunk j's segment table and events to the host
       CK(cudaEventSynchronize(done[j]));
       const int64_t* hs = h_seg2[j & 1];
@@ -1258,6 +1355,34 @@ struct evsim_gpu_sim {
           seg_t.push_back(hs[1 + q]);
           seg_off.push_back(a);
         }
+      }
+      if (wire) {
+        // chunk j's links: planes, then the polarity words its bits span
+        const int64_t g0 = chunk_link0[j], G = chunk_link0[j + 1] - g0;
+        if (G > 0 && !host_short) {
+          const int64_t* bits = h_wl[j & 1];
+          const int64_t* cnts = bits + G;
+          const int64_t wlo = bits[0] >> 5;  // chunk starts are u32-aligned
+          const int64_t whi = (bits[G - 1] + cnts[G - 1] + 31) >> 5;
+          const int64_t pw = (g0 + G) * ev.n_words;
+          if (pw > wire->planes_capacity || whi > wire->polarity_capacity) {
+            host_short = true;
+          } else {
+            for (int64_t g = 0; g < G; ++g) {
+              wire->link_bit[g0 + g] = bits[g];
+              wire->link_events[g0 + g] = cnts[g];
+            }
+            CK(cudaStreamWaitEvent(s_out, done[j], 0));
+            CK(cudaMemcpyAsync(wire->planes + g0 * ev.n_words, ev.wplanes.as<uint32_t>() + g0 * ev.n_words,
+                               (size_t)G * ev.n_words * 4, cudaMemcpyDeviceToHost, s_out));
+            if (whi > wlo)
+              CK(cudaMemcpyAsync(wire->polarity + wlo, ev.wpol.as<uint32_t>() + wlo, (size_t)(whi - wlo) * 4,
+                                 cudaMemcpyDeviceToHost, s_out));
+            wire_words = std::max(wire_words, whi);
+          }
+        }
+        copied = hi;
+        return;
       }
       if (hi > lo) {
         if (hi <= capacity && !host_short) {
@@ -1280,8 +1405,10 @@ struct evsim_gpu_sim {
         h_seg2[j & 1][0] = 0;
         h_seg2[j & 1][1] = 0;
       }
+      wire_host_links = h_wl[j & 1];
       enqueue(nullptr, nf, ts + a, false, up[j], h_seg2[j & 1], true);
       pair_base += had_prev ? nf : nf - 1;
+      chunk_link0[j + 1] = chunk_link0[j] + (int64_t)L * (had_prev ? nf : nf - 1);
       CK(cudaEventRecord(done[j], stream));
       pending = false;
       if (j > 0) drain(j - 1);
@@ -1289,6 +1416,13 @@ struct evsim_gpu_sim {
     drain(n_chunks - 1);
     xchunk = false;
     pair_base = 0;
+    if (wire) {
+      wire_on = false;
+      if (!host_short)
+        for (int64_t g = 0; g < call_links; ++g) wire->link_t[g] = wire_t[(size_t)g];
+      wire->n_events = copied;
+      wire->polarity_words = wire_words;
+    }
     seg_off.push_back(copied);
     n_events = copied;
     CK(cudaStreamSynchronize(s_out));
@@ -1307,6 +1441,7 @@ struct evsim_gpu_sim {
       cudaEventDestroy(done[j]);
     }
     cudaEventDestroy(start);
+    if (host_short && wire) invalid("push_frames_wire: destination too small");
     if (host_short) invalid("push_frames_streamed: destination too small (events stay on the device; see copy_events)");
   }
 
@@ -1432,6 +1567,133 @@ struct evsim_gpu_sim {
     out->d_packed = ev.events.as<uint32_t>();
   }
 };
+
+// ====================================================================== wire unpack
+// Expands evsim_gpu_wire (include/evsim_gpu.h) into the reference's event
+// stream.  Runs of links with equal timestamps form one segment, ordered
+// (y, x, p) with duplicates (finalize's stable sort, src/simulate.cpp:36-40):
+// per pixel the segment's negative events, then its positive ones.  Segments
+// are independent, so threads take segments (long single-link segments are
+// split into word ranges, their event offsets from per-range popcounts).
+namespace {
+
+struct WireOut {
+  int format;
+  void* out;
+  void put(int64_t i, uint32_t x, uint32_t y, bool neg, int64_t t) const {
+    if (format == 0) {
+      static_cast<uint32_t*>(out)[i] = x | (y << 16) | (neg ? 0x80000000u : 0u);
+    } else {
+      evsim_event& e = static_cast<evsim_event*>(out)[i];
+      e.x = (uint16_t)x;
+      e.y = (uint16_t)y;
+      e.t = t;
+      e.p = neg ? -1 : 1;
+    }
+  }
+};
+
+inline bool pol_bit(const uint32_t* pol, int64_t b) { return (pol[b >> 5] >> (b & 31)) & 1u; }
+
+}  // namespace
+
+void wire_unpack(const evsim_gpu_wire& wr, int format, void* out, int threads) {
+  const int64_t G = wr.n_links, W = wr.words_per_link;
+  const int wpr = wr.words_per_row;
+  const WireOut o{format, out};
+  // segments: runs of equal link_t
+  std::vector<int64_t> seg_first, ev_base;
+  int64_t tot = 0;
+  for (int64_t g = 0; g < G; ++g) {
+    if (g == 0 || wr.link_t[g] != wr.link_t[g - 1]) {
+      seg_first.push_back(g);
+      ev_base.push_back(tot);
+    }
+    tot += wr.link_events[g];
+  }
+  seg_first.push_back(G);
+  ev_base.push_back(tot);
+  // work items: (segment, word range); single-link segments in ranges of
+  // ~64k words with their own event offsets
+  struct Item {
+    int64_t seg, w0, w1, base, bit;
+  };
+  std::vector<Item> items;
+  const int64_t span = 1 << 16;
+  for (size_t sgi = 0; sgi + 1 < seg_first.size(); ++sgi) {
+    const int64_t g0 = seg_first[sgi], g1 = seg_first[sgi + 1];
+    if (g1 - g0 > 1 || W <= span) {
+      items.push_back({(int64_t)sgi, 0, W, ev_base[sgi], wr.link_bit[g0]});
+      continue;
+    }
+    const uint32_t* pl = wr.planes + g0 * W;
+    int64_t base = ev_base[sgi], bit = wr.link_bit[g0];
+    for (int64_t w0 = 0; w0 < W; w0 += span) {
+      const int64_t w1 = std::min(W, w0 + span);
+      items.push_back({(int64_t)sgi, w0, w1, base, bit});
+      int64_t c = 0;
+      for (int64_t w = w0; w < w1; ++w) c += __builtin_popcount(pl[w]);
+      base += c;
+      bit += c;
+    }
+  }
+  auto run = [&](const Item& it) {
+    const int64_t g0 = seg_first[(size_t)it.seg], g1 = seg_first[(size_t)it.seg + 1];
+    const int64_t t = wr.link_t[g0];
+    int64_t i = it.base;
+    if (g1 - g0 == 1) {
+      const uint32_t* pl = wr.planes + g0 * W;
+      int64_t b = it.bit;
+      for (int64_t w = it.w0; w < it.w1; ++w) {
+        uint32_t m = pl[w];
+        if (!m) continue;
+        const uint32_t y = (uint32_t)(wr.row0 + w / wpr), x0 = (uint32_t)(32 * (w % wpr));
+        while (m) {
+          const int bitpos = __builtin_ctz(m);
+          m &= m - 1;
+          o.put(i++, x0 + (uint32_t)bitpos, y, pol_bit(wr.polarity, b++), t);
+        }
+      }
+      return;
+    }
+    // several links share the timestamp: per pixel, negatives then positives
+    std::vector<int64_t> cur(g1 - g0);
+    for (int64_t g = g0; g < g1; ++g) cur[g - g0] = wr.link_bit[g];
+    for (int64_t w = 0; w < W; ++w) {
+      uint32_t any = 0;
+      for (int64_t g = g0; g < g1; ++g) any |= wr.planes[g * W + w];
+      if (!any) continue;
+      int nneg[32] = {}, npos[32] = {};
+      for (int64_t g = g0; g < g1; ++g) {
+        uint32_t m = wr.planes[g * W + w];
+        while (m) {
+          const int bitpos = __builtin_ctz(m);
+          m &= m - 1;
+          if (pol_bit(wr.polarity, cur[g - g0]++)) ++nneg[bitpos];
+          else ++npos[bitpos];
+        }
+      }
+      const uint32_t y = (uint32_t)(wr.row0 + w / wpr), x0 = (uint32_t)(32 * (w % wpr));
+      for (int b = 0; b < 32; ++b) {
+        for (int q = 0; q < nneg[b]; ++q) o.put(i++, x0 + (uint32_t)b, y, true, t);
+        for (int q = 0; q < npos[b]; ++q) o.put(i++, x0 + (uint32_t)b, y, false, t);
+      }
+    }
+  };
+  int T = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
+  T = (int)std::min<int64_t>(T, (int64_t)items.size());
+  if (T <= 1) {
+    for (const auto& it : items) run(it);
+    return;
+  }
+  std::atomic<size_t> next{0};
+  std::vector<std::thread> th;
+  for (int k = 0; k < T; ++k)
+    th.emplace_back([&] {
+      for (size_t j; (j = next.fetch_add(1)) < items.size();) run(items[j]);
+    });
+  for (auto& x : th) x.join();
+}
 
 // ====================================================================== C-ABI
 
@@ -1580,6 +1842,31 @@ int evsim_gpu_push_frames_streamed(evsim_gpu_sim* sim, const uint8_t* pixels, in
       throw;
     }
     sim->fill_out(out);
+  });
+}
+
+int evsim_gpu_push_frames_wire(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t n_frames, int32_t width,
+                               int32_t height, const int64_t* t_us, int32_t chunk, evsim_gpu_wire* wire,
+                               evsim_gpu_events* out) {
+  return guarded([&] {
+    if (!sim) invalid("evsim_gpu_push_frames_wire: null simulator");
+    if (!wire) invalid("evsim_gpu_push_frames_wire: null wire descriptor");
+    try {
+      sim->push_streamed(pixels, n_frames, width, height, t_us, chunk, nullptr, 0, wire);
+    } catch (...) {
+      sim->fill_out(out);
+      throw;
+    }
+    sim->fill_out(out);
+  });
+}
+
+int evsim_gpu_wire_unpack(const evsim_gpu_wire* wire, int32_t format, void* out, int64_t capacity, int32_t threads) {
+  return guarded([&] {
+    if (!wire || (!out && capacity > 0)) invalid("evsim_gpu_wire_unpack: null argument");
+    if (format != 0 && format != 1) invalid("evsim_gpu_wire_unpack: format must be 0 (packed) or 1 (evsim_event)");
+    if (capacity < wire->n_events) invalid("evsim_gpu_wire_unpack: destination too small");
+    wire_unpack(*wire, format, out, threads);
   });
 }
 

@@ -970,17 +970,11 @@ void launch_dense_lk(const DenseLKParams& p, int n_pairs, cudaStream_t s) {
   dim3 grid((p.g.ncx + kLKTileX - 1) / kLKTileX, (p.jt1 - p.jt0 + kLKTileY - 1) / kLKTileY, n_pairs);
   const int r = p.radius;
   const size_t sm = dense_lk_smem(r);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(dense_lk_warp_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(dense_lk_warp_kernel<6, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(dense_lk_warp_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(dense_lk_warp_kernel<6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(dense_lk_tile_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(dense_lk_tile_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(dense_lk_tile_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
+  for (const void* f : {(const void*)dense_lk_warp_kernel<4, false>, (const void*)dense_lk_warp_kernel<6, false>,
+                        (const void*)dense_lk_warp_kernel<4, true>, (const void*)dense_lk_warp_kernel<6, true>,
+                        (const void*)dense_lk_tile_kernel<0>, (const void*)dense_lk_tile_kernel<4>,
+                        (const void*)dense_lk_tile_kernel<6>})
+    set_max_dynamic_smem(f, 200 * 1024);
   const bool inside = p.g.w > 2 * r + 1 && p.g.h > 2 * r + 1;  // no template clamping
   if (p.u8 && !((r == 4 || r == 6) && inside)) return;  // host guarantees the warp form for u8 levels
   if (r == 4 && inside && p.u8)

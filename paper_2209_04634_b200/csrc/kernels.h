@@ -211,6 +211,23 @@ struct EmitParams {
   uint32_t* out;
 };
 
+// wire format (wire_kernels.cu)
+struct WireParams {
+  int n_links;               // links of the launch
+  int64_t n_words;
+  int words_per_block;       // the chain's block geometry
+  int n_blocks;
+  int blocks_per_tile;       // chain blocks per wire CTA (<= 256 words)
+  const uint2* masks;        // [g][n_words] (pos, neg)
+  const int64_t* prefix;     // [g][n_blocks] exclusive event prefix within the link
+  const int64_t* link_total; // [g]
+  int64_t* link_bit;         // [g] out: first polarity bit of link g (call-wide numbering)
+  int64_t* link_count;       // [g] out: events of link g
+  int64_t* bit_base;         // device scalar: the call's next free polarity bit (advanced)
+  uint32_t* planes;          // [g][n_words] out
+  uint32_t* pol;             // the call's polarity words (zeroed at the call start)
+};
+
 // ---------------------------------------------------------------- sparse
 struct SelectParams {
   int w, h, wpr;
@@ -259,9 +276,14 @@ void launch_dense_lk(const DenseLKParams& p, int n_pairs, cudaStream_t s);
 void launch_densify(const GridGeom& g, float* du, float* dv, cudaStream_t s);
 void launch_interp_frames(const ChainParams& p, uint8_t* out, cudaStream_t s);
 void launch_segments(const SegParams& p, cudaStream_t s);
+// per-(function, device) MaxDynamicSharedMemorySize, thread-safe; throws
+// std::runtime_error if the driver refuses
+void set_max_dynamic_smem(const void* func, int bytes);
 void launch_chain(const ChainParams& p, int provider, cudaStream_t s);
 void launch_offsets(const OffsetParams& p, cudaStream_t s);
 void launch_emit(const EmitParams& p, int64_t* segbase, cudaStream_t s);
+void launch_segbase(const EmitParams& p, int64_t* segbase, cudaStream_t s);
+void launch_wire(const WireParams& p, cudaStream_t s);
 void launch_select(const SelectParams& p, int n_pairs, cudaStream_t s);
 void launch_init_ref(const uint8_t* frame, const float* lut, float* ref, int64_t n, cudaStream_t s);
 // mags[slot] = min(255, |f[slot] - f[slot-1]|) for n consecutive ring slots from slot0

@@ -161,6 +161,37 @@ def band_input_halo(plan: BandPlan, radius: int) -> int:
     return max(lo, hi)
 
 
+def link_timeline(ts: Sequence[int], n_interp: int, include_endpoints: bool = True) -> np.ndarray:
+    """Every distinct link timestamp of a push over frames ts (dense / sparse /
+    difference_only chains: chain_pipeline, simulate.cpp:57-69, with
+    sub_interval_end, simulate.hpp:15-19), ascending.  Every rank derives the
+    same timeline from the timestamps alone, so per-band counts over it line
+    up even where a band has no events (the device reports only the segments
+    that hold events)."""
+    K = n_interp + 1
+    out = []
+    for i in range(len(ts) - 1):
+        t0, t1 = int(ts[i]), int(ts[i + 1])
+        ks = range(1, K + 1) if include_endpoints or n_interp == 0 else range(2, K)
+        for k in ks:
+            out.append(t1 if k == K else t0 + (k * (t1 - t0) + K - 1) // K)
+    return np.unique(np.asarray(out, np.int64))
+
+
+def timeline_counts(seg_t: Sequence[int], seg_off: Sequence[int], timeline: np.ndarray) -> np.ndarray:
+    """Events per timeline entry from a push's segment table (seg_t: the
+    non-empty segments' timestamps, seg_off: their offsets + total); 0 where
+    the band has no segment.  The vector every rank all-gathers."""
+    seg_t = np.asarray(seg_t, np.int64)
+    out = np.zeros(len(timeline), np.int64)
+    if len(seg_t):
+        idx = np.searchsorted(timeline, seg_t)
+        if np.any(idx >= len(timeline)) or np.any(timeline[np.minimum(idx, len(timeline) - 1)] != seg_t):
+            raise ValueError("timeline_counts: a segment timestamp is not on the timeline")
+        out[idx] = np.diff(np.asarray(seg_off, np.int64))
+    return out
+
+
 def band_offsets(seg_counts: np.ndarray, rank: int) -> np.ndarray:
     """Output offsets of `rank`'s events per segment in the merged stream.
 

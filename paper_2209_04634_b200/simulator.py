@@ -26,7 +26,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _lib
-from .abi import (EVENT_DTYPE, CConfig, CEvents, ContrastMode, EventsPerCrossing, FlowQuality, Method,
+from .abi import (EVENT_DTYPE, CConfig, CEvents, CWire, ContrastMode, EventsPerCrossing, FlowQuality, Method,
                   unpack_events)
 from ._lib import EvsimError, InvalidArgument
 
@@ -504,6 +504,18 @@ class Simulator:
                                                             ctypes.byref(ev)))
         return ev
 
+    def push_frames_wire(self, frames: np.ndarray, timestamps, chunk: int = 0,
+                         wire: Optional["WireBuffer"] = None) -> "WireBuffer":
+        """Host frames in, the events in the compact wire format out
+        (evsim_gpu_push_frames_wire; include/evsim_gpu.h): one plane bit per
+        pixel-link + one polarity bit per event.  WireBuffer.unpack() gives
+        the packed / 24-byte stream push_frames would return."""
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        F, h, w = frames.shape
+        if wire is None:
+            wire = WireBuffer.for_call(self, F, w, h)
+        return wire.run(self, frames.ctypes.data, F, w, h, timestamps, chunk)
+
     def push_frames_device(self, pixels_ptr: int, n_frames: int, width: int, height: int, timestamps,
                            on_device: bool = True, sync: bool = True) -> Optional[CEvents]:
         """Device-resident batched push (no event download)."""
@@ -597,6 +609,84 @@ class Simulator:
             pass
 
 
+class WireBuffer:
+    """Host buffers of evsim_gpu_wire (pinned when torch is available, so the
+    downloads overlap the compute) sized for one call of F frames."""
+
+    def __init__(self, n_links: int, words_per_link: int, max_events: int, pinned: bool = True):
+        def buf(n, dt):
+            if pinned:
+                try:
+                    import torch
+                    t = torch.empty(max(int(n), 1), dtype={np.uint32: torch.int32, np.int64: torch.int64}[dt])
+                    t = t.pin_memory()
+                    self._keep.append(t)
+                    return t.numpy().view(dt)
+                except Exception:
+                    pass
+            return np.zeros(max(int(n), 1), dt)
+        self._keep = []
+        self.planes = buf(n_links * words_per_link, np.uint32)
+        self.polarity = buf(max_events // 32 + 64 + 2 * n_links, np.uint32)
+        self.link_t = buf(n_links, np.int64)
+        self.link_events = buf(n_links, np.int64)
+        self.link_bit = buf(n_links, np.int64)
+        self.c = CWire()
+
+    @classmethod
+    def for_call(cls, sim: "Simulator", F: int, w: int, h: int, rows: Optional[int] = None) -> "WireBuffer":
+        links = max(1, sim.config.n_interp + 1) * F
+        rows = h if rows is None else rows
+        wpl = rows * ((w + 31) // 32)
+        return cls(links, wpl, links * rows * w)
+
+    def run(self, sim, pixels_ptr: int, F: int, w: int, h: int, timestamps, chunk: int = 0) -> "WireBuffer":
+        ts = np.ascontiguousarray(np.asarray(timestamps, dtype=np.int64))
+        c = self.c
+        c.planes, c.planes_capacity = self.planes.ctypes.data, self.planes.size
+        c.polarity, c.polarity_capacity = self.polarity.ctypes.data, self.polarity.size
+        c.link_t, c.link_events, c.link_bit = (self.link_t.ctypes.data, self.link_events.ctypes.data,
+                                               self.link_bit.ctypes.data)
+        c.link_capacity = self.link_t.size
+        ev = CEvents()
+        _lib.check(sim._lib.evsim_gpu_push_frames_wire(sim._h, _vp(pixels_ptr), F, w, h, _ptr(ts), int(chunk),
+                                                       ctypes.byref(c), ctypes.byref(ev)))
+        return self
+
+    @property
+    def n_events(self) -> int:
+        return int(self.c.n_events)
+
+    @property
+    def bytes(self) -> int:
+        """Host bytes the call delivered (planes + polarity words + link tables)."""
+        c = self.c
+        return 4 * int(c.n_links) * int(c.words_per_link) + 4 * int(c.polarity_words) + 24 * int(c.n_links)
+
+    def unpack(self, fmt: int = 0, threads: int = 0) -> np.ndarray:
+        """The reference's event stream: packed u32 records (fmt 0) or
+        evsim::Event records (fmt 1, EVENT_DTYPE)."""
+        n = self.n_events
+        out = np.zeros(max(n, 1), np.uint32 if fmt == 0 else EVENT_DTYPE)
+        _lib.check(_lib.load().evsim_gpu_wire_unpack(ctypes.byref(self.c), fmt, _ptr(out), n, int(threads)))
+        return out[:n]
+
+    def segments(self) -> tuple:
+        """(seg_t, seg_offset) of the unpacked stream: links with equal
+        timestamps merged, empty segments dropped."""
+        L = int(self.c.n_links)
+        t = self.link_t[:L]
+        e = self.link_events[:L]
+        if L == 0:
+            return np.zeros(0, np.int64), np.zeros(1, np.int64)
+        starts = np.concatenate([[True], t[1:] != t[:-1]])
+        seg_t = t[starts]
+        cnt = np.add.reduceat(e, np.nonzero(starts)[0])
+        keep = cnt > 0
+        off = np.concatenate([[0], np.cumsum(cnt[keep])]).astype(np.int64)
+        return seg_t[keep].astype(np.int64), off
+
+
 def concatenate(streams: Sequence[EventStream]) -> EventStream:
     if not streams:
         return EventStream(0, 0)
@@ -636,6 +726,23 @@ def push_frames_batched(sims: Sequence["Simulator"], frames: Sequence[np.ndarray
         r.width, r.height = w, h
         res.append(r)
     return res
+
+
+def push_frames_batched_device(sims: Sequence["Simulator"], pixel_ptrs: Sequence[int], n_frames: int, width: int,
+                               height: int, timestamps, on_device: bool = True) -> list:
+    """Raw-pointer form of push_frames_batched (frames already in device or
+    pinned host memory): returns one CEvents per simulator (device-resident
+    events, valid until that handle's next push)."""
+    n = len(sims)
+    ts = [np.ascontiguousarray(np.asarray(t, dtype=np.int64)) for t in timestamps]
+    lib = sims[0]._lib
+    hs = (ctypes.c_void_p * n)(*[s._h.value for s in sims])
+    px = (ctypes.c_void_p * n)(*[int(p) for p in pixel_ptrs])
+    tp = (ctypes.c_void_p * n)(*[t.ctypes.data for t in ts])
+    outs = (CEvents * n)()
+    _lib.check(lib.evsim_gpu_push_frames_batched(hs, n, px, n_frames, width, height, tp, 1 if on_device else 0,
+                                                 outs))
+    return list(outs)
 
 
 # --------------------------------------------------------------------------- data formats (SURVEY.md §8f)

@@ -98,3 +98,23 @@ def test_pipelined_dense_push_matches_oracle(oracle, mode, mag, incl):
         sim.set_profiling(profiling)
         got = [sim.push_frames(frames[:1], ts[:1]).events, sim.push_frames(frames[1:], ts[1:]).events]
         assert_same_events(concat(got), exp, what=f"profiling={profiling}")
+
+
+@pytest.mark.parametrize("where", [9, 10, 39])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_pipelined_push_with_one_colliding_pair(oracle, where, mode):
+    """Sub-batched pushes (41 frames -> 4 flow sub-batches of 10 pairs) emit
+    per sub-batch only when every link has its own timestamp; one pair with
+    dt < K (equal sub-interval stamps, finalize's stable sort,
+    simulate.cpp:36-40) at the last pair of a sub-batch, the first pair of the
+    next, or the last pair of the push must switch that off.  Single mode."""
+    frames, ts = scenes.generate("c2", n_frames=41, width=100, height=76)
+    ts = ts.copy()
+    gap = np.full(40, 33333, np.int64)
+    gap[where] = 2 + (where % 2)  # 2-3 us < K = 7
+    ts[1:] = np.cumsum(gap)
+    cfg = make_config(Method.dense, n_interp=6, contrast_mode=mode, c_pos_log=0.1, c_neg_log=-0.12)
+    exp = concat(run_oracle_stream(oracle, cfg, frames, ts))
+    sim = Simulator(SimulatorConfig.from_c(cfg))
+    got = [sim.push_frames(frames[:1], ts[:1]).events, sim.push_frames(frames[1:], ts[1:]).events]
+    assert_same_events(concat(got), exp)

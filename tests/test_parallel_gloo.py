@@ -61,21 +61,30 @@ def _band_worker(rank, world, port, out_dir):
     from oracle import Oracle
     from paper_2209_04634_b200 import scenes
     from paper_2209_04634_b200.abi import Method, make_config
-    from paper_2209_04634_b200.parallel import gather_counts
+    from paper_2209_04634_b200.parallel import gather_counts, link_timeline, timeline_counts
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    frames, ts = scenes.generate("c5", n_frames=2, width=96, height=64)
+    frames, ts = scenes.generate("c5", n_frames=3, width=96, height=64)
+    frames = frames.copy()
+    frames[:, 8:, :] = 128  # texture in the top rows only: band 1 is static ...
+    frames[2, 50, 7] = 250  # ... but for one pixel in the last frame (events on some links only)
     cfg = make_config(Method.dense, n_interp=6, contrast_mode=1, c_pos_log=0.1, c_neg_log=-0.1)
     sim = Oracle().simulator(cfg)
     sim.push_frame(frames[0], ts[0])
-    full = sim.push_frame(frames[1], ts[1])
+    full = np.concatenate([sim.push_frame(frames[1], ts[1]), sim.push_frame(frames[2], ts[2])])
     y0, y1 = band_rows(64, world, rank)
     mine = full[(full["y"] >= y0) & (full["y"] < y1)]  # this band's device output (rows [y0, y1))
-    seg_t = np.unique(full["t"])
-    local = np.array([(mine["t"] == t).sum() for t in seg_t], np.int64)
+    # what a band handle reports: only the segments that hold events, so the
+    # bands' segment tables differ in length; counts go over the common
+    # link timeline every rank derives from the timestamps
+    seg_t, first = np.unique(mine["t"], return_index=True)
+    seg_off = np.append(first, len(mine))
+    timeline = link_timeline(ts, 6)
+    local = timeline_counts(seg_t, seg_off, timeline)
     counts = gather_counts(local)
+    np.save(os.path.join(out_dir, f"nseg_{rank}.npy"), np.array([len(seg_t)]))
     np.save(os.path.join(out_dir, f"band_{rank}.npy"), mine)
     np.save(os.path.join(out_dir, f"bandcounts_{rank}.npy"), counts)
     if rank == 0:
@@ -109,6 +118,8 @@ def test_row_bands_gloo_world2(tmp_path):
     bands = [np.load(tmp_path / f"band_{r}.npy") for r in range(2)]
     counts = np.load(tmp_path / "bandcounts_0.npy")
     assert np.array_equal(counts, np.load(tmp_path / "bandcounts_1.npy"))
+    n0, n1 = (int(np.load(tmp_path / f"nseg_{r}.npy")[0]) for r in range(2))
+    assert n0 != n1  # the bands' own segment tables differ in length
     merged = merge_band_events(bands, counts)
     for f in ("x", "y", "t", "p"):
         assert np.array_equal(merged[f], full[f])
