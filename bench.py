@@ -78,6 +78,9 @@ def parse():
     p.add_argument("--chunk", type=int, default=0, help="e2e: frames per streamed chunk (0 = library default)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-e2e-extra", action="store_true", help="skip the one-step e2e lines of the other formats")
+    p.add_argument("--e2e-format", default="auto", choices=["auto", "wire", "packed", "event24"],
+                   help="host event format of e2e (auto: wire when it is smaller than packed records)")
     p.add_argument("--no-parity", action="store_true")
     return p.parse_args()
 
@@ -177,7 +180,7 @@ def sample_parity(g, counts, hashes):
 
 def cpu_pairs_for(c, threads):
     # log mode pipelines one pair per thread; bound the sample to ~10-30 s
-    return min(threads, 16 if c.pixels >= 4_000_000 else 64)
+    return min(threads, 8 if c.pixels >= 4_000_000 else 64)
 
 
 def run_reference(args):
@@ -208,6 +211,7 @@ def run_reference(args):
         sample = f"{len(use)} of the {n_streams} {c.name} streams, frames 0-2 each, one reference thread per stream"
         evs = sum(int(r[3].sum()) for r in res) / sum(r[0] for r in res)
         cores = len(use)
+        sample_pairs = sum(r[0] for r in res)
     else:
         frames, ts = _gen((c.name, n, 0))
         pairs = cpu_pairs_for(c, threads)
@@ -222,10 +226,11 @@ def run_reference(args):
                   f"(evsim_ref_run_sequence: {'pairs in parallel + the log rule over row bands' if args.mode == 'log' else 'contiguous chunks, one Simulator each'}; output = one streaming Simulator)")
         evs = float(counts.sum()) / p
         cores = threads
+        sample_pairs = p
     v = statistics.mean(vals)
     out = {
         "metric": METRIC, "impl": "reference", "value": round(v, 4), "unit": "frames/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * (n - 1) / v, 3),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sample_pairs / v, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8/f32/f64",
         "data": "synthetic", "config": config_json(c, args, n, split, 1, n_streams),
         "events_per_s": round(v * evs, 1), "parity": parity,
@@ -613,8 +618,18 @@ def run_ours(args):
 
     # ---- e2e through the C-ABI with host buffers ---------------------------------
     e2e = None
+    e2e_other = {}
     if not args.no_e2e:
-        e2e = run_e2e(arm, args, ws, n_streams)
+        fmt = args.e2e_format
+        if fmt == "auto":
+            fmt = "wire" if wire_is_smaller(c, E_frame) else "packed"
+        e2e = run_e2e(arm, args, ws, n_streams, fmt, args.steps)
+        # the other host formats, one step each (bounded: the 24-byte records
+        # of c5 are 1.6-3.8 GB per frame)
+        for other in ("packed", "wire", "event24"):
+            if other != fmt and not args.no_e2e_extra:
+                r = run_e2e(arm, args, ws, n_streams, other, 1, max_calls=1 if other == "event24" else None)
+                e2e_other[other] = {k: r[k] for k in ("value", "unit", "d2h_bytes_per_step")}
 
     cpu = cpu1 = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -641,6 +656,7 @@ def run_ours(args):
             "parity_ref": "tests/golden/sequences.json (compiled reference, per-frame count + checksum)",
             "events_per_s": round(events_per_s, 1), "events_per_frame": round(E_frame, 1),
             "roofline": roofline, "cpu_baseline": cpu, "cpu_baseline_1thread": cpu1, "e2e": e2e,
+            "e2e_other_formats": e2e_other,
             "gpu_launches": int(launches), "clocks": clocks,
             "flow_gsamples_per_s": flow_rate(c, args, stages, pairs_prof),
         }
@@ -653,28 +669,56 @@ def run_ours(args):
     return 0
 
 
-def run_e2e(arm, args, ws, n_streams):
-    """Same steps through evsim_gpu_push_frames_streamed with pinned host
-    frames in and packed host events out (one host thread per handle).  Large
-    frames go in calls of 16 frames whose events land in one reused pinned
-    buffer (a consumer that takes each call's events before the next call)."""
+def run_e2e(arm, args, ws, n_streams, fmt, steps, max_calls=None):
+    """Steps through the public C-ABI with pinned host frames in and the
+    events on the host (one host thread per handle), host wall clock:
+      wire    evsim_gpu_push_frames_wire: planes + polarity bits (lossless,
+              evsim_gpu_wire_unpack gives the reference's stream)
+      packed  evsim_gpu_push_frames_streamed: packed 4-byte records
+      event24 evsim_gpu_push_frames + evsim_gpu_copy_events format 1: the
+              reference's 24-byte evsim::Event records
+    The sequence goes in calls of at most max_batch frames whose events land
+    in one reused host buffer (a consumer that takes each call's events
+    before the next call); max_calls bounds the sample."""
     import torch
+
+    from paper_2209_04634_b200.simulator import WireBuffer
     c, n, P = arm.c, arm.n, arm.P
     h_frames = [torch.from_numpy(f).pin_memory() for f in arm.frames]
     rows = (arm.band[1] - arm.band[0]) if arm.band else c.height
-    per_call = 16 if P >= 4_000_000 else n
-    calls = [(a, min(per_call, n - a)) for a in range(0, n, per_call)]
+    # a streamed / device call holds <= max_batch frames; a wire call's launches
+    # are chunks of <= max_batch pairs, so one call can take the sequence
+    per_call = n if fmt == "wire" else min(n, arm.sims[0].max_batch(c.width, c.height))
+    calls = [(a, min(per_call, n - a)) for a in range(0, n, per_call)][:max_calls]
+    pairs_per_step = sum(nb for _, nb in calls) - 1
     cap = (c.n_interp + 1) * c.width * rows * per_call
-    h_events = [torch.empty(cap, dtype=torch.int32).pin_memory() for _ in arm.sims]
+    bufs = []
+    for s in arm.sims:
+        if fmt == "wire":
+            bufs.append(WireBuffer.for_call(s, per_call, c.width, c.height, rows=rows))
+        elif fmt == "packed":
+            bufs.append(torch.empty(cap, dtype=torch.int32).pin_memory())
+        else:
+            bufs.append(None)
 
     def one(i):
         s = arm.sims[i]
         s.reset()
         d2h = 0
         for a, nb in calls:
-            e = s.push_frames_streamed_ptr(h_frames[i].data_ptr() + a * P, nb, c.width, c.height,
-                                           arm.ts[a:a + nb], h_events[i].data_ptr(), cap, chunk=args.chunk)
-            d2h += 4 * int(e.n_events) + 16 * (int(e.n_segments) + 1)
+            ptr = h_frames[i].data_ptr() + a * P
+            if fmt == "wire":
+                bufs[i].run(s, ptr, nb, c.width, c.height, arm.ts[a:a + nb], chunk=args.chunk)
+                d2h += bufs[i].bytes
+            elif fmt == "packed":
+                e = s.push_frames_streamed_ptr(ptr, nb, c.width, c.height, arm.ts[a:a + nb], bufs[i].data_ptr(),
+                                               cap, chunk=args.chunk)
+                d2h += 4 * int(e.n_events) + 16 * (int(e.n_segments) + 1)
+            else:
+                e = s.push_frames_device(ptr, nb, c.width, c.height, arm.ts[a:a + nb], on_device=False, sync=True)
+                ev = np.empty(max(int(e.n_events), 1), dtype=[("b", "V24")])
+                s.copy_events(ev.ctypes.data, int(e.n_events), 1)
+                d2h += 24 * int(e.n_events) + 16 * (int(e.n_segments) + 1)
         return d2h
 
     def step():
@@ -689,18 +733,28 @@ def run_e2e(arm, args, ws, n_streams):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     d2h = 0
-    for _ in range(args.steps):
+    for _ in range(steps):
         d2h = step()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{arm.device}")
     if ws > 1:
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-    frames_total = (n - 1) * n_streams * args.steps
+    frames_total = pairs_per_step * n_streams * steps
+    api = {"wire": "evsim_gpu_push_frames_wire (pinned host frames in; event planes + polarity bits out, lossless: "
+                   "evsim_gpu_wire_unpack reproduces the reference stream)",
+           "packed": "evsim_gpu_push_frames_streamed (pinned host frames in, packed 4-byte host events out)",
+           "event24": "evsim_gpu_push_frames + evsim_gpu_copy_events(format 1): 24-byte evsim::Event records"}[fmt]
     return {"value": round(frames_total / float(te.item()), 3), "unit": "frames/s",
-            "h2d_bytes_per_step": n * P * len(arm.sims), "d2h_bytes_per_step": int(d2h),
-            "api": f"evsim_gpu_push_frames_streamed, {len(calls)} call(s) per stream per step (pinned host frames "
-                   "in, packed 4-byte host events out, H2D / compute / D2H overlapped), host wall clock"}
+            "h2d_bytes_per_step": sum(nb for _, nb in calls) * P * len(arm.sims), "d2h_bytes_per_step": int(d2h),
+            "format": fmt, "api": f"{api}; {len(calls)} call(s) of <= {per_call} frames per stream per step, "
+                                  "H2D / compute / D2H overlapped, host wall clock"}
+
+
+def wire_is_smaller(c, events_per_frame):
+    """Wire bytes (1 bit per pixel-link + 1 per event) below packed (4 B per event)?"""
+    links = c.n_interp + 1
+    return links * c.width * c.height / 8 + events_per_frame / 8 < 4 * events_per_frame
 
 
 def flow_rate(c, args, stages, pairs):

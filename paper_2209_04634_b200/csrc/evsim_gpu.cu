@@ -541,6 +541,16 @@ int max_batch_for(int links_per_pair, int64_t pixels) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(std::min(kMaxBatch, by_links), by_mem));
 }
 
+// Frames per wire call (evsim_gpu_push_frames_wire): its launches are
+// chunks of <= max_batch_for pairs, so only the frame ring, the flow grids
+// and the call's planes + polarity bits grow with F (~12 B per pixel per
+// frame + 2 bits per pixel-link), kept within ~24 GB.
+int max_wire_frames(int links_per_pair, int64_t pixels) {
+  const int64_t L = std::max(links_per_pair, 1);
+  const int64_t per_frame = std::max<int64_t>(pixels, 1) * 12 + L * std::max<int64_t>(pixels, 1) / 4;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(kMaxBatch, (int64_t)24e9 / per_frame));
+}
+
 }  // namespace
 
 // ====================================================================== handle
@@ -560,6 +570,7 @@ struct evsim_gpu_sim {
   int rhead = 0;  // ring slot of the previous frame
   int R = 0;      // ring slots allocated
   int pair_cap = 0;
+  int launch_cap = 0;
   int band_y0 = 0, band_y1 = 0;  // row band of the events (0, 0 = the whole frame)
 
   DevBuf frames, quads, mags, lut, ref, consts;
@@ -692,6 +703,7 @@ struct evsim_gpu_sim {
     h = h_;
     R = 0;
     pair_cap = 0;
+    launch_cap = 0;
     rhead = 0;
     const bool band = band_y1 > 0;
     if (uses_flow()) {
@@ -736,8 +748,12 @@ struct evsim_gpu_sim {
     CK(cudaStreamSynchronize(stream));
   }
 
-  // room for `pairs` pairs in one launch: ring of pairs + kept_frames() slots
-  void ensure_capacity(int pairs) {
+  // room for `pairs` pairs in one call (ring of pairs + kept_frames() slots,
+  // flow grids per pair) whose launches hold at most `launch_pairs` pairs
+  // (chain masks, tables, splat buffers; 0 = pairs) and whose events need
+  // `event_cap` device records (-1 = every link-pixel of the call)
+  void ensure_capacity(int pairs, int launch_pairs = 0, int64_t event_cap = -1) {
+    if (launch_pairs <= 0) launch_pairs = pairs;
     const size_t P = (size_t)w * h;
     const int keep = kept_frames();
     const int need_R = pairs + keep;
@@ -790,9 +806,12 @@ struct evsim_gpu_sim {
     }
     if (pairs > pair_cap) {
       if (uses_flow()) flow.ensure(R, pairs, stream);
-      const int L = desc().n_links;
-      const int64_t cap = magnitude() ? 0 : (int64_t)std::max(L, 1) * pairs * (int64_t)P;
-      ev.ensure(L * pairs, magnitude(), std::max<int64_t>(cap, ev.capacity), stream);
+      pair_cap = pairs;
+    }
+    const int L = desc().n_links;
+    if (launch_pairs > launch_cap) {
+      ev.ensure(L * launch_pairs, magnitude(), 0, stream);
+      const int pairs = launch_pairs;
       if (splats()) {
         const int N = n_interp_eff();
         sel_masks.ensure((size_t)pairs * ev.n_words * 4, stream);
@@ -822,9 +841,11 @@ struct evsim_gpu_sim {
         CK(cudaHostAlloc((void**)&h_seg_out, seg_need, cudaHostAllocDefault));
         h_seg_cap = seg_need;
       }
-      pair_cap = pairs;
+      launch_cap = launch_pairs;
     }
-    if (magnitude() && ev.capacity == 0) ev.grow((int64_t)std::max(desc().n_links, 1) * pairs * (int64_t)P, stream);
+    if (event_cap < 0) event_cap = (int64_t)std::max(L, 1) * pairs * (int64_t)P;
+    // (magnitude mode grows the buffer on demand, finish())
+    if (!magnitude() || ev.capacity == 0) ev.grow(event_cap, stream);
   }
 
   // ---- chain params --------------------------------------------------------
@@ -1042,7 +1063,7 @@ struct evsim_gpu_sim {
   // ---- push ----------------------------------------------------------------
   // Simulator::push_frame (src/simulate.cpp:306-347) applied to F frames in
   // order; the whole batch is validated first and rejected atomically.
-  void validate_batch(const uint8_t* pixels, int F, int fw, int fh, const int64_t* ts) const {
+  void validate_batch(const uint8_t* pixels, int F, int fw, int fh, const int64_t* ts, bool wire = false) const {
     if (F < 1) invalid("push_frames: n_frames must be >= 1");
     if (fw <= 0 || fh <= 0 || !pixels || !ts) invalid("push_frame: malformed frame");
     if (has_prev) {
@@ -1056,12 +1077,13 @@ struct evsim_gpu_sim {
       invalid("push_frame: frames of 2^24 pixels or more are not supported by the sparse method");
     if ((int64_t)fw * fh >= (int64_t)1 << 31) invalid("push_frame: frame too large");
     const int L = desc().n_links;
-    const int fmax = max_batch_for(L, (int64_t)fw * fh);
+    const int fmax = wire ? max_wire_frames(L, (int64_t)fw * fh) : max_batch_for(L, (int64_t)fw * fh);
     if (F > fmax) invalid("push_frames: batch too large (max " + std::to_string(fmax) + ")");
   }
 
-  // device state for F more frames of one call
-  void prepare(int F, int fw, int fh) {
+  // device state for F more frames of one call (launches of <= launch_pairs
+  // pairs, event_cap device event records; see ensure_capacity)
+  void prepare(int F, int fw, int fh, int launch_pairs = 0, int64_t event_cap = -1) {
     CK(cudaSetDevice(device));
     // A queued single-mode result is superseded (stream order keeps the
     // device buffers consistent); magnitude mode may need a re-emit.
@@ -1071,7 +1093,7 @@ struct evsim_gpu_sim {
     }
     if (!has_prev && (fw != w || fh != h)) allocate(fw, fh);
     const int n_pairs = has_prev ? F : F - 1;
-    ensure_capacity(std::max(n_pairs, 1));
+    ensure_capacity(std::max(n_pairs, 1), launch_pairs, event_cap);
   }
 
   // ring slot of the first frame of the next push
@@ -1229,22 +1251,10 @@ struct evsim_gpu_sim {
     if (wire && ((!wire->planes && wire->planes_capacity > 0) || (!wire->polarity && wire->polarity_capacity > 0) ||
                  (wire->link_capacity > 0 && (!wire->link_t || !wire->link_events || !wire->link_bit))))
       invalid("push_frames_wire: null destination");
-    validate_batch(pixels, F, fw, fh, ts);
-    prepare(F, fw, fh);
-    if (!s_in) {
-      CK(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
-      CK(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
-    }
-    const size_t seg_need = (3 + 2 * (size_t)ev.max_links) * sizeof(int64_t);
-    if (seg_need > h_seg2_cap) {
-      for (auto& b : h_seg2) {
-        if (b) cudaFreeHost(b);
-        b = nullptr;
-        CK(cudaHostAlloc((void**)&b, seg_need, cudaHostAllocDefault));
-      }
-      h_seg2_cap = seg_need;
-    }
-    const size_t P = (size_t)w * h;
+    validate_batch(pixels, F, fw, fh, ts, wire != nullptr);
+    // a wire call may hold more frames than one launch: its chunks are
+    // launches of <= max_batch_for pairs
+    if (wire) chunk = std::min(chunk > 0 ? chunk : 64, max_batch_for(desc().n_links, (int64_t)fw * fh));
     if (chunk <= 0) chunk = std::max(1, std::min(F, 64));  // c2 e2e: 32 -> 27.7k, 48 -> 28.3k, 64 -> 29.1k frames/s
     // chunk sizes: a quarter-size first chunk (its upload is not overlapped)
     // and a quarter-size last one (its download is not), full ones between
@@ -1267,6 +1277,21 @@ struct evsim_gpu_sim {
         add(rem);
       }
     }
+    prepare(F, fw, fh, *std::max_element(csize.begin(), csize.end()), wire ? 0 : -1);
+    if (!s_in) {
+      CK(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+    }
+    const size_t seg_need = (3 + 2 * (size_t)ev.max_links) * sizeof(int64_t);
+    if (seg_need > h_seg2_cap) {
+      for (auto& b : h_seg2) {
+        if (b) cudaFreeHost(b);
+        b = nullptr;
+        CK(cudaHostAlloc((void**)&b, seg_need, cudaHostAllocDefault));
+      }
+      h_seg2_cap = seg_need;
+    }
+    const size_t P = (size_t)w * h;
     const int n_chunks = (int)csize.size();
     std::vector<cudaEvent_t> up(n_chunks), done(n_chunks);
     for (int j = 0; j < n_chunks; ++j) {
@@ -1434,6 +1459,8 @@ struct evsim_gpu_sim {
       t[0] = S;
       for (int q = 0; q < S; ++q) t[1 + q] = seg_t[q], t[1 + S + q] = seg_off[q];
       t[1 + 2 * S] = copied;
+      // (the call may hold more segments than one launch's table)
+      if ((3 + 2 * (size_t)S) * sizeof(int64_t) > ev.seg_out.n) ev.seg_out.ensure((3 + 2 * (size_t)S) * sizeof(int64_t), stream);
       CK(cudaMemcpy(ev.seg_out.p, t.data(), (2 + 2 * (size_t)S) * sizeof(int64_t), cudaMemcpyHostToDevice));
     }
     for (int j = 0; j < n_chunks; ++j) {

@@ -550,6 +550,11 @@ class Simulator:
     def copy_packed(self, dst_ptr: int, capacity: int) -> None:
         _lib.check(self._lib.evsim_gpu_copy_events(self._h, _vp(dst_ptr), capacity, 0))
 
+    def copy_events(self, dst_ptr: int, capacity: int, fmt: int) -> None:
+        """evsim_gpu_copy_events: the last push's events to host memory in
+        format 0 (packed), 1 (evsim_event, 24 B) or 2 (.evs, 13 B)."""
+        _lib.check(self._lib.evsim_gpu_copy_events(self._h, _vp(dst_ptr), capacity, int(fmt)))
+
     @property
     def stream(self) -> int:
         return self._lib.evsim_gpu_stream(self._h) or 0

@@ -126,13 +126,18 @@ def test_sequence_streamed_call_matches_reference(key):
     from paper_2209_04634_b200.seqhash import frame_hash_packed_np
     name, mode = key.split(":")
     frames, ts = _frames(name)
+    c = scenes.CONFIGS[name]
     sim = Simulator(SimulatorConfig.from_c(_cfg(name, mode)))
-    packed, seg_t, seg_off = sim.push_frames_streamed(frames, ts, chunk=24)
-    sim.close()
+    mb = sim.max_batch(c.width, c.height)
     got = []
-    for f in range(1, len(frames)):
-        a = int(np.searchsorted(seg_t, ts[f - 1], side="right"))
-        b = int(np.searchsorted(seg_t, ts[f], side="right"))
-        lo, hi = int(seg_off[a]), int(seg_off[b])
-        got.append((hi - lo, frame_hash_packed_np(packed[lo:hi], seg_t[a:b], seg_off[a:b + 1] - lo, int(ts[f - 1]))))
+    for a0 in range(0, len(frames), mb):  # calls of at most max_batch frames, chunks of 24 inside
+        a1 = min(len(frames), a0 + mb)
+        packed, seg_t, seg_off = sim.push_frames_streamed(frames[a0:a1], ts[a0:a1], chunk=24)
+        for f in range(max(a0, 1), a1):
+            a = int(np.searchsorted(seg_t, ts[f - 1], side="right"))
+            b = int(np.searchsorted(seg_t, ts[f], side="right"))
+            lo, hi = int(seg_off[a]), int(seg_off[b])
+            got.append((hi - lo, frame_hash_packed_np(packed[lo:hi], seg_t[a:b], seg_off[a:b + 1] - lo,
+                                                      int(ts[f - 1]))))
+    sim.close()
     _check(key, got)

@@ -116,3 +116,20 @@ def test_wire_continues_a_stream():
              b.push_frames(frames[12:15], ts[12:15]).events,
              b.push_frames_wire(frames[15:], ts[15:]).unpack(fmt=1)]
     assert_same_events(np.concatenate(parts), exp)
+
+
+def test_wire_call_longer_than_a_launch():
+    """A wire call may hold more frames than max_batch: its chunks are
+    launches of <= max_batch pairs (events never need one device buffer)."""
+    frames, ts = scenes.generate("c5", n_frames=21, width=1280, height=800)
+    cfg = make_config(Method.dense, n_interp=32, contrast_mode=1, c_pos_log=0.1, c_neg_log=-0.1)
+    a = Simulator(SimulatorConfig.from_c(cfg))
+    mb = a.max_batch(1280, 800)
+    assert mb < 21
+    exp = a.push_frames(frames, ts)  # (split into max_batch calls by the wrapper)
+    b = Simulator(SimulatorConfig.from_c(cfg))
+    wire = b.push_frames_wire(frames, ts)
+    assert wire.n_events == len(exp.events)
+    packed = wire.unpack(fmt=0)
+    seg_t, seg_off = wire.segments()
+    assert_same_events(unpack_events(packed, seg_t, seg_off), exp.events)
