@@ -10,6 +10,7 @@
 // the emit kernel writes every event exactly once, contiguously, in the
 // reference's order (t, y, x, p).
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <set>
 #include <stdexcept>
@@ -1408,6 +1409,82 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
   }
 }
 
+// ------------------------------------------------------------ emit (single-link segments)
+//
+// The common case — every link its own timestamp, one event per crossing:
+// segment g is link g, its events are the set bits of its masks in word
+// order (threshold_events_into's (y, x) scan, src/core.cpp:21-46).  One CTA
+// per (tile of chain blocks, link): a thread per 32-pixel word, a block scan
+// of the words' popcounts gives each word's slot, the thread writes its
+// events into shared memory, and the CTA streams the tile's contiguous run
+// out with 16-byte stores.  The tile starts at segbase[g] + the chain's
+// per-(link, block) exclusive prefix.
+//
+// Two ways to fill the staging buffer, chosen per tile: sparse tiles loop
+// over each word's set bits in its own thread; dense tiles (>= `lanes_from`
+// events per word on average) go word by word with lanes = the word's
+// pixels — rank = popc(mask below the lane), so a word's events land on
+// consecutive shared-memory banks (no conflicts) and the cost is fixed per
+// word instead of per event.
+__global__ void __launch_bounds__(256) emit_single_kernel(EmitParams p, const int64_t* __restrict__ segbase,
+                                                          int blocks_per_tile, int g0, int lanes_from) {
+  __shared__ uint32_t s_ev[256 * 32];
+  __shared__ uint4 s_wd[256];
+  __shared__ int s_warp[kWarpsPerBlock];
+  const int S = *p.seg.n_segs;
+  if (p.seg_out[1 + 2 * S] > p.capacity) return;  // host grows the buffer and re-emits
+  const int g = g0 + blockIdx.y;
+  const int b0 = blockIdx.x * blocks_per_tile;
+  const int64_t w0 = (int64_t)b0 * p.words_per_block;
+  const int64_t w1 = min(w0 + (int64_t)blocks_per_tile * p.words_per_block, p.n_words);
+  const int64_t w = w0 + threadIdx.x;
+  uint32_t all = 0, neg = 0;
+  if (w < w1) {
+    const uint2 m = p.masks[(size_t)g * p.n_words + w];
+    all = m.x | m.y;
+    neg = m.y;
+  }
+  int total;
+  const int excl = block_exclusive_scan(__popc(all), s_warp, total);
+  if (total == 0) return;  // uniform
+  const uint32_t row = (uint32_t)w / (uint32_t)p.wpr;
+  const uint32_t xy = ((uint32_t)w - row * (uint32_t)p.wpr) * 32u | ((uint32_t)(p.row0 + (int)row) << 16);
+  if (total < lanes_from * (int)(w1 - w0)) {
+    if (all) {
+      uint32_t m = all;
+      uint32_t* o = s_ev + excl;
+      do {
+        const int b = __ffs(m) - 1;
+        m &= m - 1u;
+        *o++ = (xy + (uint32_t)b) | (((neg >> b) & 1u) << 31);
+      } while (m);
+    }
+  } else {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    s_wd[threadIdx.x] = make_uint4(all, neg, (uint32_t)excl, xy);
+    __syncwarp();
+    const uint32_t bit = 1u << lane, below = bit - 1u;
+    const uint4* wd = s_wd + warp * 32;
+#pragma unroll 4
+    for (int k = 0; k < 32; ++k) {
+      const uint4 d = wd[k];
+      if (d.x & bit) s_ev[d.z + __popc(d.x & below)] = (d.w | (uint32_t)lane) | ((d.y << (31 - lane)) & 0x80000000u);
+    }
+  }
+  __syncthreads();
+  uint32_t* dst = p.out + segbase[g] + p.prefix[(size_t)g * p.n_blocks + b0];
+  const int head = min(total, (int)((4u - (uint32_t)(((uintptr_t)dst >> 2) & 3u)) & 3u));  // to a 16-byte boundary
+  if ((int)threadIdx.x < head) dst[threadIdx.x] = s_ev[threadIdx.x];
+  const int nv = (total - head) >> 2;
+  uint4* dv = reinterpret_cast<uint4*>(dst + head);
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    const int e = head + 4 * i;
+    dv[i] = make_uint4(s_ev[e], s_ev[e + 1], s_ev[e + 2], s_ev[e + 3]);
+  }
+  const int t0 = head + 4 * nv;
+  if ((int)threadIdx.x < total - t0) dst[t0 + threadIdx.x] = s_ev[t0 + threadIdx.x];
+}
+
 // ------------------------------------------------------------ unpack
 // Packed record -> evsim::Event layout (24 B: x@0 y@2 t@8 p@16).
 __global__ void unpack_kernel(const uint32_t* __restrict__ packed, const int64_t* __restrict__ seg_out, int64_t n,
@@ -1799,6 +1876,24 @@ void launch_emit(const EmitParams& p, int64_t* segbase, cudaStream_t s) {
   const size_t sm = (size_t)std::max(p.n_links, 1) * (sizeof(int64_t) + sizeof(int));
   set_max_dynamic_smem((const void*)emit_kernel, 144 * 1024);
   emit_kernel<<<p.n_blocks, 256, sm, s>>>(p, segbase);
+}
+
+// segbase_kernel then emit_single_kernel over links [g0, g1) (every link
+// its own segment, single mode); false when the geometry does not fit a tile
+bool launch_emit_single(const EmitParams& p, int64_t* segbase, int g0, int g1, cudaStream_t s) {
+  if (p.magnitude || p.words_per_block > 256 || g1 <= g0) return false;
+  segbase_kernel<<<1, 1024, 0, s>>>(p, segbase);
+  const int bpt = std::max(1, 256 / p.words_per_block);
+  const int tiles = (p.n_blocks + bpt - 1) / bpt;
+  // EVSIM_EMIT_LANES: average events per word from which a tile goes word by
+  // word (0 = always; default 33 = never: measured slower at every density,
+  // c5 log 161 vs 253 us/frame, c5 linear 252 vs 307, c2 log 1.41 vs 2.45)
+  static const int lanes_from = [] {
+    const char* e = std::getenv("EVSIM_EMIT_LANES");
+    return e ? std::atoi(e) : 33;
+  }();
+  emit_single_kernel<<<dim3((unsigned)tiles, (unsigned)(g1 - g0)), 256, 0, s>>>(p, segbase, bpt, g0, lanes_from);
+  return true;
 }
 
 void launch_unpack_events(const uint32_t* packed, const int64_t* seg_out, int64_t n, void* out24,

@@ -601,6 +601,12 @@ struct evsim_gpu_sim {
   // wire format (evsim_gpu_push_frames_wire): the chain masks of each launch
   // become planes + polarity bits instead of packed events
   bool wire_on = false;
+  // EVSIM_EMIT_LEGACY=1: the general (segment, word) emit for every launch
+  // (A/B measurement and tests of both paths)
+  bool emit_legacy = [] {
+    const char* e = std::getenv("EVSIM_EMIT_LEGACY");
+    return e && e[0] == '1';
+  }();
   int64_t wire_link0 = 0;                // links of the call before this launch
   int64_t* wire_host_links = nullptr;    // pinned: this launch's (bit[G], count[G])
   std::vector<int64_t> wire_t;           // timestamps of the call's links
@@ -955,6 +961,20 @@ struct evsim_gpu_sim {
     ep.out = ev.events.as<uint32_t>();
     // offsets + segment bases + emit of links [g0, g1) (segments = links when
     // every link has its own timestamp)
+    // every link its own timestamp (no finalize() run spans two links) and
+    // one event per crossing: segment g = link g, tile-staged emit
+    bool single = !c.magnitude;
+    {
+      const int K = c.n_interp + 1;
+      int64_t tp = 0;
+      for (int g = 0; single && g < G; ++g) {
+        const int i = g / L, l = g % L;
+        const int k = c.d.start + (l + 1) * c.d.step;
+        const int64_t t = k == K ? ts[i + 1] : sub_interval_end(ts[i], ts[i + 1], k, K);
+        if (g > 0 && t == tp) single = false;
+        tp = t;
+      }
+    }
     auto emit_links = [&](int g0, int g1, bool range) {
       OffsetParams op{g1 - g0, ev.n_blocks, ev.counts.as<uint32_t>() + (size_t)g0 * ev.n_blocks,
                       ev.prefix.as<int64_t>() + (size_t)g0 * ev.n_blocks, ev.link_total.as<int64_t>() + g0};
@@ -991,7 +1011,8 @@ struct evsim_gpu_sim {
         launches += 1;  // segbase + linkbase + wire vs segbase + emit
         return;
       }
-      launch_emit(e, ev.segbase.as<int64_t>(), stream);
+      if (!(single && !emit_legacy && launch_emit_single(e, ev.segbase.as<int64_t>(), g0, g1, stream)))
+        launch_emit(e, ev.segbase.as<int64_t>(), stream);
       CK_LAUNCH("emit");
     };
     if (wire_on) {
@@ -1016,20 +1037,7 @@ struct evsim_gpu_sim {
       // flows run ahead on s_flow; the chains and emits stay in order)
       // (not in the streamed call: its chunks already overlap the emit with
       // the next chunk's flow, and per-sub-batch emits measured slower there)
-      bool split = !c.magnitude && !continue_call && !wire_on;
-      {
-        const int K = c.n_interp + 1;
-        auto stamp = [&](int i, int l) {
-          const int k = c.d.start + (l + 1) * c.d.step;
-          return k == K ? ts[i + 1] : sub_interval_end(ts[i], ts[i + 1], k, K);
-        };
-        int64_t tp = 0;
-        for (int g = 0; split && g < G; ++g) {
-          const int64_t t = stamp(g / L, g % L);
-          if (g > 0 && t == tp) split = false;
-          tp = t;
-        }
-      }
+      const bool split = single && !continue_call && !wire_on;
       for (size_t b = 0; b + 1 < sub.size(); ++b) {
         const int off = sub[b], nb = sub[b + 1] - sub[b];
         CK(cudaStreamWaitEvent(stream, pipe_ev[1 + b], 0));

@@ -282,6 +282,9 @@ void set_max_dynamic_smem(const void* func, int bytes);
 void launch_chain(const ChainParams& p, int provider, cudaStream_t s);
 void launch_offsets(const OffsetParams& p, cudaStream_t s);
 void launch_emit(const EmitParams& p, int64_t* segbase, cudaStream_t s);
+// every link of [g0, g1) its own segment, single mode: segbase + the
+// tile-staged emit; false (nothing launched) when it does not apply
+bool launch_emit_single(const EmitParams& p, int64_t* segbase, int g0, int g1, cudaStream_t s);
 void launch_segbase(const EmitParams& p, int64_t* segbase, cudaStream_t s);
 void launch_wire(const WireParams& p, cudaStream_t s);
 void launch_select(const SelectParams& p, int n_pairs, cudaStream_t s);

@@ -21,7 +21,8 @@ WANT = {"dur_ms": "gpu__time_duration.sum", "dram_rd_MB": "dram__bytes_read.sum"
         "lsu_pct": "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
         "fp64_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
         "grid": "launch__grid_size", "block": "launch__block_size"}
-SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}
+SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
+         "ns": 1e-6, "us": 1e-3, "ms": 1.0, "second": 1e3, "s": 1e3}
 
 
 def main(rep, outdir):
