@@ -1415,21 +1415,16 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
 // segment g is link g, its events are the set bits of its masks in word
 // order (threshold_events_into's (y, x) scan, src/core.cpp:21-46).  One CTA
 // per (tile of chain blocks, link): a thread per 32-pixel word, a block scan
-// of the words' popcounts gives each word's slot, the thread writes its
-// events into shared memory, and the CTA streams the tile's contiguous run
-// out with 16-byte stores.  The tile starts at segbase[g] + the chain's
-// per-(link, block) exclusive prefix.
-//
-// Two ways to fill the staging buffer, chosen per tile: sparse tiles loop
-// over each word's set bits in its own thread; dense tiles (>= `lanes_from`
-// events per word on average) go word by word with lanes = the word's
-// pixels — rank = popc(mask below the lane), so a word's events land on
-// consecutive shared-memory banks (no conflicts) and the cost is fixed per
-// word instead of per event.
+// of the words' popcounts gives each word's slot, the thread expands its set
+// bits into shared memory (highest pixel first with FLO, written back to
+// front), and one thread streams the tile's contiguous run to
+// global memory with a TMA bulk copy (cp.async.bulk smem -> global); the
+// staging buffer is offset so it has the destination's alignment mod 16 B,
+// the < 16-byte head and tail go out as plain stores.  The tile starts at
+// segbase[g] + the chain's per-(link, block) exclusive prefix.
 __global__ void __launch_bounds__(256) emit_single_kernel(EmitParams p, const int64_t* __restrict__ segbase,
-                                                          int blocks_per_tile, int g0, int lanes_from) {
-  __shared__ uint32_t s_ev[256 * 32];
-  __shared__ uint4 s_wd[256];
+                                                          int blocks_per_tile, int g0) {
+  __shared__ __align__(16) uint32_t s_ev[256 * 32 + 4];
   __shared__ int s_warp[kWarpsPerBlock];
   const int S = *p.seg.n_segs;
   if (p.seg_out[1 + 2 * S] > p.capacity) return;  // host grows the buffer and re-emits
@@ -1447,42 +1442,39 @@ __global__ void __launch_bounds__(256) emit_single_kernel(EmitParams p, const in
   int total;
   const int excl = block_exclusive_scan(__popc(all), s_warp, total);
   if (total == 0) return;  // uniform
-  const uint32_t row = (uint32_t)w / (uint32_t)p.wpr;
-  const uint32_t xy = ((uint32_t)w - row * (uint32_t)p.wpr) * 32u | ((uint32_t)(p.row0 + (int)row) << 16);
-  if (total < lanes_from * (int)(w1 - w0)) {
-    if (all) {
-      uint32_t m = all;
-      uint32_t* o = s_ev + excl;
-      do {
-        const int b = __ffs(m) - 1;
-        m &= m - 1u;
-        *o++ = (xy + (uint32_t)b) | (((neg >> b) & 1u) << 31);
-      } while (m);
-    }
-  } else {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    s_wd[threadIdx.x] = make_uint4(all, neg, (uint32_t)excl, xy);
-    __syncwarp();
-    const uint32_t bit = 1u << lane, below = bit - 1u;
-    const uint4* wd = s_wd + warp * 32;
-#pragma unroll 4
-    for (int k = 0; k < 32; ++k) {
-      const uint4 d = wd[k];
-      if (d.x & bit) s_ev[d.z + __popc(d.x & below)] = (d.w | (uint32_t)lane) | ((d.y << (31 - lane)) & 0x80000000u);
-    }
+  uint32_t* dst = p.out + segbase[g] + p.prefix[(size_t)g * p.n_blocks + b0];
+  const int shift = (int)(((uintptr_t)dst >> 2) & 3u);  // dst alignment mod 16 B, in events
+  if (all) {
+    // descending pixels (FLO = the highest set bit), written back to front;
+    // n1 = neg rotated right by 1, so rotr(n1, b) holds pixel b's polarity
+    // at bit 31
+    const uint32_t row = (uint32_t)w / (uint32_t)p.wpr;
+    const uint32_t xy = ((uint32_t)w - row * (uint32_t)p.wpr) * 32u | ((uint32_t)(p.row0 + (int)row) << 16);
+    const uint32_t n1 = __funnelshift_r(neg, neg, 1);
+    uint32_t m = all;
+    uint32_t* o = s_ev + shift + excl + __popc(all) - 1;
+    do {
+      uint32_t b;
+      asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(m));  // FLO: the highest set bit
+      m ^= 1u << b;
+      *o-- = (xy + b) | (__funnelshift_r(n1, n1, b) & 0x80000000u);
+    } while (m);
   }
   __syncthreads();
-  uint32_t* dst = p.out + segbase[g] + p.prefix[(size_t)g * p.n_blocks + b0];
-  const int head = min(total, (int)((4u - (uint32_t)(((uintptr_t)dst >> 2) & 3u)) & 3u));  // to a 16-byte boundary
-  if ((int)threadIdx.x < head) dst[threadIdx.x] = s_ev[threadIdx.x];
-  const int nv = (total - head) >> 2;
-  uint4* dv = reinterpret_cast<uint4*>(dst + head);
-  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
-    const int e = head + 4 * i;
-    dv[i] = make_uint4(s_ev[e], s_ev[e + 1], s_ev[e + 2], s_ev[e + 3]);
+  const int head = min(total, (4 - shift) & 3);
+  const int nbody = (total - head) & ~3;
+  if ((int)threadIdx.x < head) dst[threadIdx.x] = s_ev[shift + threadIdx.x];
+  const int t0 = head + nbody;
+  if ((int)threadIdx.x >= 32 && (int)threadIdx.x - 32 < total - t0)
+    dst[t0 + threadIdx.x - 32] = s_ev[shift + t0 + threadIdx.x - 32];
+  if (threadIdx.x == 0 && nbody > 0) {
+    const uint32_t src = (uint32_t)__cvta_generic_to_shared(s_ev + shift + head);
+    asm volatile("fence.proxy.async.shared::cta;\n"
+                 "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                 "cp.async.bulk.commit_group;\n"
+                 "cp.async.bulk.wait_group.read 0;\n" ::"l"(dst + head), "r"(src), "r"(nbody * 4)
+                 : "memory");
   }
-  const int t0 = head + 4 * nv;
-  if ((int)threadIdx.x < total - t0) dst[t0 + threadIdx.x] = s_ev[t0 + threadIdx.x];
 }
 
 // ------------------------------------------------------------ unpack
@@ -1885,14 +1877,7 @@ bool launch_emit_single(const EmitParams& p, int64_t* segbase, int g0, int g1, c
   segbase_kernel<<<1, 1024, 0, s>>>(p, segbase);
   const int bpt = std::max(1, 256 / p.words_per_block);
   const int tiles = (p.n_blocks + bpt - 1) / bpt;
-  // EVSIM_EMIT_LANES: average events per word from which a tile goes word by
-  // word (0 = always; default 33 = never: measured slower at every density,
-  // c5 log 161 vs 253 us/frame, c5 linear 252 vs 307, c2 log 1.41 vs 2.45)
-  static const int lanes_from = [] {
-    const char* e = std::getenv("EVSIM_EMIT_LANES");
-    return e ? std::atoi(e) : 33;
-  }();
-  emit_single_kernel<<<dim3((unsigned)tiles, (unsigned)(g1 - g0)), 256, 0, s>>>(p, segbase, bpt, g0, lanes_from);
+  emit_single_kernel<<<dim3((unsigned)tiles, (unsigned)(g1 - g0)), 256, 0, s>>>(p, segbase, bpt, g0);
   return true;
 }
 
