@@ -82,6 +82,7 @@ def parse():
     p.add_argument("--e2e-format", default="auto", choices=["auto", "wire", "packed", "event24"],
                    help="host event format of e2e (auto: wire when it is smaller than packed records)")
     p.add_argument("--no-parity", action="store_true")
+    p.add_argument("--force-band", action="store_true", help=argparse.SUPPRESS)
     return p.parse_args()
 
 
@@ -365,7 +366,9 @@ class Arm:
         self.n = args.frames or c.n_frames
         if split == "bands":
             self.streams = [0]
-            self.band = band_rows(c.height, ws, rank) if ws > 1 else None
+            # (--force-band: the band path at N = 1 — one band = the frame — to
+            # exercise the placement / merged-output check on one GPU)
+            self.band = band_rows(c.height, ws, rank) if (ws > 1 or args.force_band) else None
         else:
             total = args.streams or c.streams
             self.streams = list(shard_streams(total, ws, rank)) if total > 1 else [rank]
@@ -387,6 +390,31 @@ class Arm:
         self.batch = max(1, min(args.batch or mb, mb, self.n))
         self.torch_stream = torch.cuda.ExternalStream(self.sims[0].stream, device=device)
         self.other_streams = [torch.cuda.ExternalStream(s.stream, device=device) for s in self.sims[1:]]
+
+    def merged_buffer(self, ws, need):
+        """Rank 0's merged-output buffer (every band's events, placed by
+        each rank) as a device address in this process: allocated once at the
+        push's upper bound (every link-pixel an event) and mapped into the
+        other ranks with CUDA IPC."""
+        import torch
+        if getattr(self, "_merged", None) is None:
+            cap = (self.c.n_interp + 1) * self.P * self.batch
+            handle = [None]
+            if self.rank == 0:
+                self._merged_t = torch.empty(cap, dtype=torch.int32, device=f"cuda:{self.device}")
+                self._merged = self._merged_t.data_ptr()
+                if ws > 1:
+                    from paper_2209_04634_b200.parallel import share_buffer
+                    handle = [share_buffer(self._merged)]
+            if ws > 1:
+                torch.distributed.broadcast_object_list(handle, src=0)
+                if self.rank != 0:
+                    from paper_2209_04634_b200.parallel import open_shared
+                    self._merged = open_shared(handle[0], self.device)
+            self._merged_cap = cap
+        if need > self._merged_cap:
+            raise RuntimeError("merged output larger than its bound")
+        return self._merged
 
     def pushes(self):
         return [(a, min(self.batch, self.n - a)) for a in range(0, self.n, self.batch)]
@@ -432,7 +460,8 @@ def parity_pass(arm, g, ws):
     stream 0 compared with the reference's.  Returns (status, events total of
     this rank, per-frame (count, hash) list)."""
     import torch
-    from paper_2209_04634_b200.parallel import gather_counts, link_timeline, timeline_counts
+    from paper_2209_04634_b200.parallel import gather_counts, link_timeline, segment_dst_offsets, timeline_counts
+    from paper_2209_04634_b200.seqhash import push_frame_hashes
     for s in arm.sims:
         s.reset()
     frames_out = []
@@ -444,8 +473,9 @@ def parity_pass(arm, g, ws):
             frames_out += push_checksums(arm, a, nb, outs)[2]
             continue
         # row bands: counts per (band, link) over the push's full link
-        # timeline, all-gathered (the merged stream's offsets), then partial
-        # checksums with global frame indices, summed over ranks
+        # timeline, all-gathered over NCCL (the merged stream's offsets);
+        # every rank places its events into rank 0's buffer (CUDA IPC over
+        # NVLink, evsim_gpu_place_events); rank 0 checks the merged stream
         f0 = max(a, 1)
         timeline = link_timeline(arm.ts[f0 - 1:a + nb], arm.c.n_interp)
         ev = outs[0]
@@ -454,24 +484,20 @@ def parity_pass(arm, g, ws):
         seg_off = np.ctypeslib.as_array(ev.seg_offset, shape=(S + 1,)).copy()
         local = timeline_counts(seg_t, seg_off, timeline)
         allc = gather_counts(local, device=torch.device("cuda", arm.device)) if ws > 1 else local[None]
-        before = allc[:arm.rank].sum(axis=0)
-        tot = allc.sum(axis=0)
-        jbase = np.zeros(len(timeline), np.int64)
-        fts = arm.ts[f0 - 1:a + nb]
-        for f in range(len(fts) - 1):  # frame-relative prefix of earlier links
-            lo, hi = np.searchsorted(timeline, fts[f], side="right"), np.searchsorted(timeline, fts[f + 1], side="right")
-            jbase[lo:hi] = np.concatenate([[0], np.cumsum(tot[lo:hi])[:-1]]) + before[lo:hi]
-        part = push_checksums(arm, a, nb, outs, (timeline, jbase))[2]
-        hs = np.array([h for _, h in part], dtype=np.uint64).view(np.int64)
-        cs = np.array([cnt for cnt, _ in part], dtype=np.int64)
+        merged_ptr = arm.merged_buffer(ws, int(allc.sum()))
+        arm.sims[0].place_events(merged_ptr, segment_dst_offsets(allc, arm.rank, timeline, seg_t))
+        arm.sims[0].sync()
         if ws > 1:
-            hs_all = gather_counts(hs, device=torch.device("cuda", arm.device))
-            cs_all = gather_counts(cs, device=torch.device("cuda", arm.device))
-        else:
-            hs_all, cs_all = hs[None], cs[None]
-        for f in range(len(part)):
-            h = int(hs_all[:, f].astype(np.uint64).sum(dtype=np.uint64))
-            frames_out.append((int(cs_all[:, f].sum()), h))
+            torch.distributed.barrier()
+        if arm.rank == 0:
+            tot = allc.sum(axis=0)
+            m_off = np.concatenate([[0], np.cumsum(tot)]).astype(np.int64)
+            keep = tot > 0
+            frames_out += push_frame_hashes(merged_ptr, timeline[keep],
+                                            np.concatenate([m_off[:-1][keep], [m_off[-1]]]),
+                                            arm.ts[f0 - 1:a + nb], arm.device)
+        if ws > 1:
+            torch.distributed.barrier()
     status = "unpinned"
     if g is not None and (arm.streams[0] == 0):
         got_c = [cnt for cnt, _ in frames_out]

@@ -245,6 +245,25 @@ EVSIM_GPU_API int evsim_gpu_push_frames_wire(evsim_gpu_sim* sim, const uint8_t* 
 EVSIM_GPU_API int evsim_gpu_wire_unpack(const evsim_gpu_wire* wire, int32_t format, void* out, int64_t capacity,
                                         int32_t threads);
 
+/* ---- multi-GPU merged output ------------------------------
+ * One process per GPU; each rank's handle emits its row band (or its
+ * streams).  The reference's single stream is, per timestamp, band 0's
+ * events, then band 1's, ... (event order (t, y, x, p),
+ * include/evsim/types.hpp:64-69, src/simulate.cpp:36-40); an all-gather of
+ * per-(band, segment) counts gives every band's offset in it.
+ * evsim_gpu_place_events copies the last push's segment s (the
+ * evsim_gpu_events table) to dst + dst_offset[s] records — dst in this GPU's
+ * or a peer GPU's memory (NVLink P2P; across processes via the CUDA IPC
+ * calls below) — on the handle's stream (evsim_gpu_sync waits). */
+EVSIM_GPU_API int evsim_gpu_place_events(evsim_gpu_sim* sim, uint32_t* dst, const int64_t* dst_offset,
+                                         int32_t n_segments);
+/* CUDA IPC of a device buffer: the 64-byte handle of dptr (cudaIpcGetMemHandle),
+ * and the mapping of a peer process's buffer into this one (opened with lazy
+ * peer access). */
+EVSIM_GPU_API int evsim_gpu_ipc_handle(const void* dptr, void* handle64);
+EVSIM_GPU_API int evsim_gpu_ipc_open(int32_t device, const void* handle64, void** dptr);
+EVSIM_GPU_API int evsim_gpu_ipc_close(int32_t device, void* dptr);
+
 /* Asynchronous variant: enqueues the push on the handle's CUDA stream and
  * returns without waiting; evsim_gpu_sync() completes it.  Validation
  * errors are still reported synchronously. */

@@ -37,6 +37,10 @@ _SIGS = {
     "evsim_gpu_push_frames_wire": (
         ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _i32, ctypes.POINTER(CWire), ctypes.POINTER(CEvents)]),
     "evsim_gpu_wire_unpack": (ctypes.c_int, [ctypes.POINTER(CWire), _i32, _vp, _i64, _i32]),
+    "evsim_gpu_place_events": (ctypes.c_int, [_vp, _vp, _vp, _i32]),
+    "evsim_gpu_ipc_handle": (ctypes.c_int, [_vp, _vp]),
+    "evsim_gpu_ipc_open": (ctypes.c_int, [_i32, _vp, ctypes.POINTER(_vp)]),
+    "evsim_gpu_ipc_close": (ctypes.c_int, [_i32, _vp]),
     "evsim_gpu_max_batch": (ctypes.c_int, [_vp, _i32, _i32]),
     "evsim_gpu_ingest_frames": (ctypes.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp]),
     "evsim_gpu_write_events_binary": (ctypes.c_int, [_vp, ctypes.c_char_p]),

@@ -573,7 +573,7 @@ struct evsim_gpu_sim {
   int launch_cap = 0;
   int band_y0 = 0, band_y1 = 0;  // row band of the events (0, 0 = the whole frame)
 
-  DevBuf frames, quads, mags, lut, ref, consts;
+  DevBuf frames, quads, mags, lut, ref, consts, place_tab;
   FlowEngine flow;
   EventEngine ev;
   // sparse (per pair)
@@ -1902,6 +1902,69 @@ int evsim_gpu_wire_unpack(const evsim_gpu_wire* wire, int32_t format, void* out,
     if (format != 0 && format != 1) invalid("evsim_gpu_wire_unpack: format must be 0 (packed) or 1 (evsim_event)");
     if (capacity < wire->n_events) invalid("evsim_gpu_wire_unpack: destination too small");
     wire_unpack(*wire, format, out, threads);
+  });
+}
+
+int evsim_gpu_place_events(evsim_gpu_sim* sim, uint32_t* dst, const int64_t* dst_offset, int32_t n_segments) {
+  return guarded([&] {
+    if (!sim || (!dst && n_segments > 0) || (!dst_offset && n_segments > 0))
+      invalid("evsim_gpu_place_events: null argument");
+    CK(cudaSetDevice(sim->device));
+    sim->finish();
+    const int S = (int)sim->seg_t.size();
+    if (n_segments != S) invalid("evsim_gpu_place_events: n_segments must equal the last push's segment count");
+    if (S == 0) return;
+    {  // a peer GPU's buffer in this process: enable P2P (IPC mappings are opened with it)
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, dst) == cudaSuccess && at.type == cudaMemoryTypeDevice &&
+          at.device != sim->device) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "cudaDeviceEnablePeerAccess");
+        cudaGetLastError();
+      }
+    }
+    std::vector<int64_t> tab(2 * (size_t)S + 1);
+    int64_t max_len = 0;
+    for (int q = 0; q <= S; ++q) tab[q] = sim->seg_off[q];
+    for (int q = 0; q < S; ++q) {
+      tab[S + 1 + q] = dst_offset[q];
+      max_len = std::max(max_len, sim->seg_off[q + 1] - sim->seg_off[q]);
+    }
+    sim->place_tab.ensure(tab.size() * sizeof(int64_t), sim->stream);
+    CK(cudaMemcpyAsync(sim->place_tab.p, tab.data(), tab.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
+                       sim->stream));
+    const int64_t* d = sim->place_tab.as<int64_t>();
+    launch_place(sim->ev.events.as<uint32_t>(), d, d + S + 1, S, max_len, dst, sim->stream);
+    CK_LAUNCH("place");
+    ++sim->launches;
+    CK(cudaStreamSynchronize(sim->stream));  // tab is a stack buffer of this call
+  });
+}
+
+int evsim_gpu_ipc_handle(const void* dptr, void* handle64) {
+  return guarded([&] {
+    if (!dptr || !handle64) invalid("evsim_gpu_ipc_handle: null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)));
+    std::memcpy(handle64, &h, sizeof(h));
+  });
+}
+
+int evsim_gpu_ipc_open(int32_t device, const void* handle64, void** dptr) {
+  return guarded([&] {
+    if (!handle64 || !dptr) invalid("evsim_gpu_ipc_open: null argument");
+    CK(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    CK(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int evsim_gpu_ipc_close(int32_t device, void* dptr) {
+  return guarded([&] {
+    CK(cudaSetDevice(device));
+    if (dptr) CK(cudaIpcCloseMemHandle(dptr));
   });
 }
 

@@ -116,3 +116,30 @@ void launch_accumulate(const evsim_event* ev, int64_t n, int w, int64_t t0, int6
 }
 
 }  // namespace evsim_gpu
+
+namespace evsim_gpu {
+
+// ------------------------------------------------------------ merged output
+// Segment s of a push (records [off[s], off[s+1]) of its packed stream) to
+// dst + dst_off[s]: one block row per segment, 4096 records per block,
+// coalesced on both sides.  dst may be peer memory (NVLink P2P / CUDA IPC):
+// the ranks of a multi-GPU run place their bands / streams into rank 0's
+// merged buffer at the offsets an all-gather of counts gave.
+__global__ void place_kernel(const uint32_t* __restrict__ src, const int64_t* __restrict__ off,
+                             const int64_t* __restrict__ dst_off, uint32_t* __restrict__ dst) {
+  const int s = blockIdx.y;
+  const int64_t a = off[s], n = off[s + 1] - a;
+  uint32_t* d = dst + dst_off[s];
+  for (int64_t i = (int64_t)blockIdx.x * 4096 + threadIdx.x; i < n && i < (int64_t)(blockIdx.x + 1) * 4096;
+       i += blockDim.x)
+    d[i] = src[a + i];
+}
+
+void launch_place(const uint32_t* src, const int64_t* off, const int64_t* dst_off, int n_segs, int64_t max_len,
+                  uint32_t* dst, cudaStream_t s) {
+  if (n_segs <= 0 || max_len <= 0) return;
+  const unsigned gx = (unsigned)((max_len + 4095) / 4096);
+  place_kernel<<<dim3(gx, (unsigned)n_segs), 256, 0, s>>>(src, off, dst_off, dst);
+}
+
+}  // namespace evsim_gpu

@@ -287,6 +287,9 @@ void launch_emit(const EmitParams& p, int64_t* segbase, cudaStream_t s);
 bool launch_emit_single(const EmitParams& p, int64_t* segbase, int g0, int g1, cudaStream_t s);
 void launch_segbase(const EmitParams& p, int64_t* segbase, cudaStream_t s);
 void launch_wire(const WireParams& p, cudaStream_t s);
+// segment s of a packed stream ([off[s], off[s+1])) to dst + dst_off[s] (dst may be peer memory)
+void launch_place(const uint32_t* src, const int64_t* off, const int64_t* dst_off, int n_segs, int64_t max_len,
+                  uint32_t* dst, cudaStream_t s);
 void launch_select(const SelectParams& p, int n_pairs, cudaStream_t s);
 void launch_init_ref(const uint8_t* frame, const float* lut, float* ref, int64_t n, cudaStream_t s);
 // mags[slot] = min(255, |f[slot] - f[slot-1]|) for n consecutive ring slots from slot0

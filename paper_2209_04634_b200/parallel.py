@@ -220,3 +220,45 @@ def merge_band_events(band_events: Sequence[np.ndarray], seg_counts: np.ndarray)
             out[offs[s]:offs[s] + n] = ev[pos:pos + n]
             pos += n
     return out
+
+
+# ----------------------------------------------------------------------------- merged output on the device
+
+def segment_dst_offsets(all_counts: np.ndarray, rank: int, timeline: np.ndarray, seg_t: Sequence[int],
+                        base: int = 0) -> np.ndarray:
+    """Where this rank's non-empty segments (seg_t) go in the merged stream:
+    all_counts is the (world, len(timeline)) all-gather of timeline_counts;
+    merged order = timestamp-major, band (or stream) minor."""
+    offs = band_offsets(all_counts, rank) + int(base)
+    idx = np.searchsorted(timeline, np.asarray(seg_t, np.int64))
+    return offs[idx].astype(np.int64)
+
+
+def share_buffer(ptr: int) -> bytes:
+    """64-byte CUDA IPC handle of a device allocation (evsim_gpu_ipc_handle),
+    to broadcast to the other ranks."""
+    import ctypes
+
+    from . import _lib
+    h = (ctypes.c_char * 64)()
+    _lib.check(_lib.load().evsim_gpu_ipc_handle(ctypes.c_void_p(ptr), h))
+    return bytes(h)
+
+
+def open_shared(handle: bytes, device: int) -> int:
+    """Map a peer process's buffer (share_buffer) into this one: its device
+    address here (evsim_gpu_ipc_open, lazy peer access)."""
+    import ctypes
+
+    from . import _lib
+    out = ctypes.c_void_p()
+    h = (ctypes.c_char * 64).from_buffer_copy(handle)
+    _lib.check(_lib.load().evsim_gpu_ipc_open(device, h, ctypes.byref(out)))
+    return int(out.value)
+
+
+def close_shared(ptr: int, device: int) -> None:
+    import ctypes
+
+    from . import _lib
+    _lib.check(_lib.load().evsim_gpu_ipc_close(device, ctypes.c_void_p(ptr)))

@@ -550,6 +550,13 @@ class Simulator:
     def copy_packed(self, dst_ptr: int, capacity: int) -> None:
         _lib.check(self._lib.evsim_gpu_copy_events(self._h, _vp(dst_ptr), capacity, 0))
 
+    def place_events(self, dst_ptr: int, dst_offsets) -> None:
+        """evsim_gpu_place_events: segment s of the last push to
+        dst + dst_offsets[s] records (device memory of this or a peer GPU,
+        e.g. rank 0's merged buffer opened with parallel.open_shared)."""
+        off = np.ascontiguousarray(np.asarray(dst_offsets, dtype=np.int64))
+        _lib.check(self._lib.evsim_gpu_place_events(self._h, _vp(dst_ptr), _ptr(off), int(off.size)))
+
     def copy_events(self, dst_ptr: int, capacity: int, fmt: int) -> None:
         """evsim_gpu_copy_events: the last push's events to host memory in
         format 0 (packed), 1 (evsim_event, 24 B) or 2 (.evs, 13 B)."""

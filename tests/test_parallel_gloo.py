@@ -85,6 +85,10 @@ def _band_worker(rank, world, port, out_dir):
     local = timeline_counts(seg_t, seg_off, timeline)
     counts = gather_counts(local)
     np.save(os.path.join(out_dir, f"nseg_{rank}.npy"), np.array([len(seg_t)]))
+    # where evsim_gpu_place_events puts this band's segments in rank 0's buffer
+    from paper_2209_04634_b200.parallel import segment_dst_offsets
+    np.save(os.path.join(out_dir, f"dst_{rank}.npy"), segment_dst_offsets(counts, rank, timeline, seg_t))
+    np.save(os.path.join(out_dir, f"segoff_{rank}.npy"), seg_off)
     np.save(os.path.join(out_dir, f"band_{rank}.npy"), mine)
     np.save(os.path.join(out_dir, f"bandcounts_{rank}.npy"), counts)
     if rank == 0:
@@ -121,6 +125,15 @@ def test_row_bands_gloo_world2(tmp_path):
     n0, n1 = (int(np.load(tmp_path / f"nseg_{r}.npy")[0]) for r in range(2))
     assert n0 != n1  # the bands' own segment tables differ in length
     merged = merge_band_events(bands, counts)
+    # the device placement's arithmetic: each band's segment s at dst[s]
+    placed = np.zeros(len(full), full.dtype)
+    for r in range(2):
+        dst = np.load(tmp_path / f"dst_{r}.npy")
+        off = np.load(tmp_path / f"segoff_{r}.npy")
+        for q in range(len(dst)):
+            placed[dst[q]:dst[q] + off[q + 1] - off[q]] = bands[r][off[q]:off[q + 1]]
+    for f in ("x", "y", "t", "p"):
+        assert np.array_equal(placed[f], full[f])
     for f in ("x", "y", "t", "p"):
         assert np.array_equal(merged[f], full[f])
     assert band_offsets(counts, 0)[0] == 0
