@@ -194,22 +194,24 @@ def run_reference(args):
     cfg = make_cfg(c, args)
     threads = os.cpu_count() or 1
     n_streams = args.streams or c.streams
-    split = "streams" if c.streams > 1 else "bands"
-    if c.streams > 1:
+    split = "streams" if n_streams > 1 else "bands"
+    if n_streams > 1:
         # one reference thread per stream (independent instances), up to nproc
         use = list(range(min(threads, n_streams)))
-        data = generate_streams(c, 3, use)
+        nf = 3 if c.pixels >= 1_000_000 else n
+        data = generate_streams(c, nf, use)
         vals = []
         for i in range(args.warmup + args.steps):
             t0 = time.perf_counter()
             with cf.ThreadPoolExecutor(len(use)) as ex:
-                res = list(ex.map(lambda d: cpu_sample(c, cfg, d[0], d[1], 1, 2), data))
+                res = list(ex.map(lambda d: cpu_sample(c, cfg, d[0], d[1], 1, nf - 1), data))
             dt = time.perf_counter() - t0
             if i >= args.warmup:
                 vals.append(sum(r[0] for r in res) / dt)
         kind = res[0][2]
-        parity = sample_parity(golden_entry(c, args, 3), res[0][3], res[0][4])
-        sample = f"{len(use)} of the {n_streams} {c.name} streams, frames 0-2 each, one reference thread per stream"
+        parity = sample_parity(golden_entry(c, args, nf), res[0][3], res[0][4])
+        sample = (f"{len(use)} of the {n_streams} {c.name} streams, frames 0-{nf - 1} each, one reference thread "
+                  f"per stream")
         evs = sum(int(r[3].sum()) for r in res) / sum(r[0] for r in res)
         cores = len(use)
         sample_pairs = sum(r[0] for r in res)
@@ -520,7 +522,7 @@ def run_ours(args):
     c = scenes.CONFIGS[args.config]
     split = args.split
     if split == "auto":
-        split = "streams" if c.streams > 1 else "bands"
+        split = "streams" if (args.streams or c.streams) > 1 else "bands"
     cfg = make_cfg(c, args)
     arm = Arm(c, cfg, args, ws, rank, device, split)
     n, P = arm.n, arm.P
