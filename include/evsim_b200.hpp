@@ -38,6 +38,21 @@ struct Frame {
   std::size_t pixel_count() const { return static_cast<std::size_t>(width) * static_cast<std::size_t>(height); }
 };
 
+// Signed per-pixel intensity delta (types.hpp:33-46)
+struct DifferenceFrame {
+  int width = 0;
+  int height = 0;
+  time_us t_start = 0;
+  time_us t_end = 0;
+  std::vector<std::int16_t> values;
+
+  DifferenceFrame() = default;
+  DifferenceFrame(int w, int h, time_us t0, time_us t1)
+      : width(w), height(h), t_start(t0), t_end(t1), values(static_cast<std::size_t>(w) * static_cast<std::size_t>(h), 0) {}
+  std::int16_t& at(int x, int y) { return values[static_cast<std::size_t>(y) * width + x]; }
+  std::int16_t at(int x, int y) const { return values[static_cast<std::size_t>(y) * width + x]; }
+};
+
 struct Event {
   std::uint16_t x = 0;
   std::uint16_t y = 0;
@@ -65,6 +80,16 @@ enum class Method { difference_only, dense, sparse, difference_interp };
 enum class FlowQuality { low_quality, high_quality };
 enum class EventsPerCrossing { single, magnitude };
 enum class ContrastMode { linear, log };  // extension (BASELINE.json configs)
+
+inline const char* method_name(Method m) {  // types.hpp:133-142
+  switch (m) {
+    case Method::difference_only: return "difference_only";
+    case Method::dense: return "dense";
+    case Method::sparse: return "sparse";
+    case Method::difference_interp: return "difference_interp";
+  }
+  return "?";
+}
 
 struct SimulatorConfig {
   Method method = Method::difference_only;
@@ -137,6 +162,38 @@ inline void check(int rc) {
 inline void SimulatorConfig::validate() const {
   const evsim_gpu_config c = to_c();
   detail::check(evsim_gpu_config_validate(&c));
+}
+
+// ---- core.hpp:8-19 -------------------------------------------------------------
+inline DifferenceFrame difference_frame(const Frame& prev, const Frame& curr) {
+  if (prev.width != curr.width || prev.height != curr.height)
+    throw std::invalid_argument("difference_frame: incompatible input frames (" + std::to_string(prev.width) + "x" +
+                                std::to_string(prev.height) + " vs " + std::to_string(curr.width) + "x" +
+                                std::to_string(curr.height) + ")");
+  DifferenceFrame d(prev.width, prev.height, prev.timestamp, curr.timestamp);
+  if (!d.values.empty())
+    detail::check(evsim_gpu_difference_frame(prev.pixels.data(), curr.pixels.data(), prev.width, prev.height,
+                                             d.values.data()));
+  return d;
+}
+
+inline void threshold_events_into(const DifferenceFrame& diff, const SimulatorConfig& config, time_us event_time,
+                                  std::vector<Event>& out) {
+  const evsim_gpu_config c = config.to_c();
+  int64_t n = 0;
+  detail::check(evsim_gpu_threshold_events(diff.values.data(), diff.width, diff.height, &c, event_time, nullptr, 0, &n));
+  const std::size_t at = out.size();
+  out.resize(at + static_cast<std::size_t>(n));
+  if (n)
+    detail::check(evsim_gpu_threshold_events(diff.values.data(), diff.width, diff.height, &c, event_time,
+                                             reinterpret_cast<evsim_event*>(out.data() + at), n, &n));
+}
+
+inline std::vector<Event> threshold_events(const DifferenceFrame& diff, const SimulatorConfig& config,
+                                           time_us event_time) {
+  std::vector<Event> out;
+  threshold_events_into(diff, config, event_time, out);
+  return out;
 }
 
 // ---- flow.hpp:9-110 ----------------------------------------------------------
@@ -322,6 +379,43 @@ inline EventStream sparse_events_with_flow(const Frame& prev, const Frame& curr,
                                              reinterpret_cast<const float*>(flow.displacements.data()),
                                              flow.status.data(), &c, ev, cap, n);
   });
+}
+
+// simulate_dense (simulate.hpp:37-39, simulate.cpp:129-142): the flow from
+// the estimator (default: PyramidalPatchFlow of config.flow_preset, on the
+// GPU), interpolation and events on the GPU.
+inline EventStream simulate_dense(const Frame& prev, const Frame& curr, const SimulatorConfig& config,
+                                  const DenseFlowEstimator& estimator) {
+  config.validate();
+  check_pair(prev, curr, "simulate_dense");
+  if (config.n_interp == 0) return dense_events_with_flow(prev, curr, FlowField(prev.width, prev.height), config);
+  return dense_events_with_flow(prev, curr, estimator.estimate(prev, curr), config);
+}
+inline EventStream simulate_dense(const Frame& prev, const Frame& curr, const SimulatorConfig& config) {
+  return simulate_dense(prev, curr, config, PyramidalPatchFlow(flow_preset(config.flow_preset)));
+}
+
+// simulate_sparse (simulate.hpp:44-46, simulate.cpp:144-201): selection as
+// the reference, the tracks from the estimator (default PyramidalLucasKanade
+// on the GPU), splat + chain on the GPU.
+inline EventStream simulate_sparse(const Frame& prev, const Frame& curr, const SimulatorConfig& config,
+                                   const SparseFlowEstimator& estimator) {
+  config.validate();
+  check_pair(prev, curr, "simulate_sparse");
+  const int select = config.effective_selection_threshold();
+  if (select <= 0) throw std::invalid_argument("simulate_sparse: selection threshold must be > 0");
+  std::vector<PixelPoint> points;
+  for (int y = 0; y < prev.height; ++y)
+    for (int x = 0; x < prev.width; ++x) {
+      const int d = static_cast<int>(curr.at(x, y)) - static_cast<int>(prev.at(x, y));
+      if ((d < 0 ? -d : d) > select) points.push_back({x, y});
+    }
+  SparseFlow flow;
+  if (!points.empty() && config.n_interp > 0) flow = estimator.estimate(prev, curr, points);
+  return sparse_events_with_flow(prev, curr, flow, config);
+}
+inline EventStream simulate_sparse(const Frame& prev, const Frame& curr, const SimulatorConfig& config) {
+  return simulate_sparse(prev, curr, config, PyramidalLucasKanade(flow_preset(config.flow_preset)));
 }
 
 // ---- simulate.hpp:60-94 ------------------------------------------------------

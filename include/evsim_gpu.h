@@ -293,6 +293,20 @@ EVSIM_GPU_API int evsim_gpu_ingest_frames(const uint8_t* src, int32_t channels, 
  * writing"). */
 EVSIM_GPU_API int evsim_gpu_write_events_binary(evsim_gpu_sim* sim, const char* path);
 EVSIM_GPU_API int evsim_gpu_write_events_text(evsim_gpu_sim* sim, const char* path);
+/* difference_frame (include/evsim/core.hpp:8, src/core.cpp:5-19): values[i]
+ * = curr[i] - prev[i] as int16 over w*h pixels (the caller checks that the
+ * two frames have one size; the reference's message is "difference_frame:
+ * incompatible input frames (WxH vs WxH)"). */
+EVSIM_GPU_API int evsim_gpu_difference_frame(const uint8_t* prev, const uint8_t* curr, int32_t width, int32_t height,
+                                             int16_t* values);
+/* threshold_events / threshold_events_into (include/evsim/core.hpp:14-19,
+ * src/core.cpp:21-52): the events of a difference frame's values, scan
+ * order, every event at event_time; single or magnitude mode from the
+ * config, which is validated first (INVALID with the reference's messages).
+ * events == NULL (or capacity too small) only reports *n_events. */
+EVSIM_GPU_API int evsim_gpu_threshold_events(const int16_t* values, int32_t width, int32_t height,
+                                             const evsim_gpu_config* config, int64_t event_time, evsim_event* events,
+                                             int64_t capacity, int64_t* n_events);
 /* events_per_pixel_second (src/metrics.cpp:7-39): per-pixel counts on the
  * device, the fp64 reduction in the reference's pixel order on the host. */
 EVSIM_GPU_API int evsim_gpu_events_per_pixel_second(const evsim_event* events, int64_t n, int32_t width,

@@ -36,12 +36,17 @@ class OracleError(RuntimeError):
 
 
 def build(ref: bool | None = None) -> None:
-    """Compile the C restatement (and, when /root/reference exists, the reference)."""
+    """Compile the C restatement (and, when /root/reference exists, the
+    reference and the reference's own unit suites against the drop-in:
+    oracle/Makefile `refsuite`, after the CUDA library is built)."""
     targets = ["all"]
     if ref is None:
         ref = os.path.isdir(REF_SRC)
     if ref:
         targets.append("ref")
+        gpu_so = os.path.join(os.path.dirname(HERE), "paper_2209_04634_b200", "libevsim_gpu.so")
+        if os.path.exists(gpu_so):
+            targets.append("refsuite")
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 

@@ -12,7 +12,7 @@ from .simulator import (EventRateStats, accumulate, events_per_pixel_second, ing
                         SparseFlowEstimator, dense_events_with_flow, estimate_dense_flow, estimate_sparse_flow,
                         flow_preset, interpolate_frames, push_frames_batched, simulate_dense, simulate_difference,
                         simulate_sparse,
-                        sparse_events_with_flow)
+                        sparse_events_with_flow, DifferenceFrame, difference_frame, threshold_events)
 
 __all__ = [
     "EventRateStats", "accumulate", "events_per_pixel_second", "ingest_frames",
@@ -21,4 +21,5 @@ __all__ = [
     "PyramidalPatchFlow", "SimulatorConfig", "Simulator", "SparseFlow", "SparseFlowEstimator",
     "dense_events_with_flow", "estimate_dense_flow", "estimate_sparse_flow", "flow_preset", "interpolate_frames",
     "push_frames_batched", "simulate_dense", "simulate_difference", "simulate_sparse", "sparse_events_with_flow",
+    "DifferenceFrame", "difference_frame", "threshold_events",
 ]

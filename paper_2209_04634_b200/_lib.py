@@ -49,6 +49,9 @@ _SIGS = {
         ctypes.c_int, [_vp, _i64, _i32, _i32, ctypes.c_double, ctypes.POINTER(ctypes.c_double),
                        ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]),
     "evsim_gpu_accumulate": (ctypes.c_int, [_vp, _i64, _i32, _i32, _i64, _i64, _vp]),
+    "evsim_gpu_difference_frame": (ctypes.c_int, [_vp, _vp, _i32, _i32, _vp]),
+    "evsim_gpu_threshold_events": (
+        ctypes.c_int, [_vp, _i32, _i32, ctypes.POINTER(CConfig), _i64, _vp, _i64, ctypes.POINTER(_i64)]),
     "evsim_gpu_set_row_band": (ctypes.c_int, [_vp, _i32, _i32]),
     "evsim_gpu_sync": (ctypes.c_int, [_vp, ctypes.POINTER(CEvents)]),
     "evsim_gpu_copy_events": (ctypes.c_int, [_vp, _vp, _i64, _i32]),

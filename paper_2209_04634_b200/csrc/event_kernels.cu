@@ -10,11 +10,13 @@
 // the emit kernel writes every event exactly once, contiguously, in the
 // reference's order (t, y, x, p).
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <mutex>
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <utility>
 
 #include "evsim_device.cuh"
@@ -435,6 +437,44 @@ __device__ __forceinline__ int dense_fast(const uint32_t* __restrict__ qp, const
   return __float_as_int(hi2(T));  // kVB + value (the bias folds into the LUT address / cancels in differences)
 }
 
+// dense_fast on the fp32 lerp quads (a00, a10 - a00, a01, a11 - a01) of the
+// frames: one 16-byte gather per sample, no byte unpack, and each sample's
+// three lerps as FFMA — an estimate, like e.  The positions X, Y and their
+// splits are the reference's exactly (as above).  Bound (u = 2^-17, half an
+// ulp in [128, 256)): the reference's fp32 sample (simulate.cpp:10-26) is
+// within 5u of the exact bilinear value (2u per row lerp, + the rounded
+// difference, product and sum), this one within 3u, so |fp - fp_ref| <= 8u
+// = 6.1e-5, the same for fc; with the fp32 weights (|oma_f - oma| <= 2^-25,
+// oma + alpha = 1) and e's two fp32 roundings, |e - s| <= 255 * 2^-24 + 8u
+// + 2u < 9.2e-5, and RN(e + 0.5 -/+ 2e-4) adds < 1.6e-5: inside the 2e-4
+// decision margin, so a decided lane rounds exactly like the reference.
+template <bool kClamp>
+__device__ __forceinline__ int dense_fast(const float4* __restrict__ qp, const float4* __restrict__ qc,
+                                          uint32_t w, float my, float wm, float hm, float xf, float yf,
+                                          float u, float v, float4 kc, unsigned& bad, unsigned bit) {
+  const f32x2 NB = pk2(kc.x, kc.y);
+  f32x2 X = affine2_est(xf, NB, u), Y = affine2_est(yf, NB, v);
+  if (kClamp) {
+    X = pk2(fminf(fmaxf(lo2(X), 0.0f), wm), fminf(fmaxf(hi2(X), 0.0f), wm));
+    Y = pk2(fminf(fmaxf(lo2(Y), 0.0f), hm), fminf(fmaxf(hi2(Y), 0.0f), hm));
+  }
+  const f32x2 C23 = pk2(8388608.0f, 8388608.0f);
+  const f32x2 CY = pk2(my, my);
+  const f32x2 TX = add2_rz(X, C23), TY = add2_rz(Y, CY);  // magic + trunc
+  const f32x2 FX = sub2(X, sub2(TX, C23)), FY = sub2(Y, sub2(TY, CY));
+  const uint32_t ia = __float_as_uint(lo2(TY)) * w + __float_as_uint(lo2(TX));
+  const uint32_t ib = __float_as_uint(hi2(TY)) * w + __float_as_uint(hi2(TX));
+  const float4 A = __ldg(qp + ia), B = __ldg(qc + ib);
+  const float ta = __fmaf_rn(lo2(FX), A.y, A.x), ba = __fmaf_rn(lo2(FX), A.w, A.z);
+  const float tb = __fmaf_rn(hi2(FX), B.y, B.x), bb = __fmaf_rn(hi2(FX), B.w, B.z);
+  const float sa = __fmaf_rn(lo2(FY), __fsub_rn(ba, ta), ta);
+  const float sb = __fmaf_rn(hi2(FY), __fsub_rn(bb, tb), tb);
+  const float e = __fmaf_rn(kc.z, sa, __fmul_rn(kc.w, sb));
+  const f32x2 T = add2_rz(add2(pk2(e, e), pk2(0.5f - 2e-4f, 0.5f + 2e-4f)), C23);
+  if (__float_as_uint(lo2(T)) != __float_as_uint(hi2(T))) bad |= bit;
+  return __float_as_int(hi2(T));
+}
+
 // The exact reference expression for the lanes dense_fast cannot decide.
 __device__ __noinline__ int dense_exact(const float2* nfb, const double* oma, const double* alpha,
                                         const uint32_t* qp, const uint32_t* qc, int w, int h, float xf, float yf,
@@ -447,7 +487,7 @@ __device__ __noinline__ int dense_exact(const float2* nfb, const double* oma, co
 }
 
 // chain values in the dense kernel carry this bias: the fp32 bits of 2^23 + v
-constexpr int kVB = 0x4B000000;
+constexpr int kVB = kChainBias;
 
 struct DenseWord {
   bool have, valid;
@@ -521,14 +561,31 @@ __device__ __forceinline__ uint2 dense_rule(const ChainParams& p, uint32_t lut_b
   return make_uint2(__ballot_sync(kFull, pos), __ballot_sync(kFull, neg));
 }
 
-template <int kW, int kNB, bool kClamp, int kBM>
-__device__ __forceinline__ unsigned dense_batch(const float4* s_kc, const uint32_t* qp, const uint32_t* qc,
+// dense_rule for log single mode as level thresholds: the
+// reference state is always a LUT level L[r] (init_ref sets L(frame0), an
+// event sets L(v)), and fsub(L[v], L[r]) is monotone in v, so d > c_pos <=>
+// v > hi[r] and d < c_neg <=> v < lo[r] (host table lthr, biased like val).
+// The lane keeps its level's (hi, lo) and value; only lanes that fired
+// reload them (one 8-byte LDS) — no LUT read and no fp32 subtraction per
+// link.  Padding lanes hold (INT_MAX, INT_MIN): they never fire.
+__device__ __forceinline__ uint2 dense_rule_th(uint32_t th_b, int val, int& thh, int& thl, int& vr) {
+  const bool pos = val > thh, neg = val < thl;
+  const unsigned bp = __ballot_sync(kFull, pos), bn = __ballot_sync(kFull, neg);
+  if (pos || neg) {
+    asm("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(thh), "=r"(thl) : "r"(th_b + ((uint32_t)val << 3)));
+    vr = val;
+  }
+  return make_uint2(bp, bn);
+}
+
+template <int kW, int kNB, bool kClamp, int kBM, class Q>
+__device__ __forceinline__ unsigned dense_batch(const ChainParams& p, const Q* qp, const Q* qc,
                                                 uint32_t w, float my, float wm, float hm, const DenseWord* c,
                                                 int k0, int (&vals)[kW][kBM]) {
   unsigned bad = 0;
 #pragma unroll
   for (int j = 0; j < kNB; ++j) {
-    const float4 kc = s_kc[k0 + j];
+    const float4 kc = p.kcp[k0 + j];
 #pragma unroll
     for (int q = 0; q < kW; ++q)
       vals[q][j] = dense_fast<kClamp>(qp, qc, w, my, wm, hm, c[q].xf, c[q].yf, c[q].u, c[q].v, kc, bad,
@@ -539,20 +596,23 @@ __device__ __forceinline__ unsigned dense_batch(const float4* s_kc, const uint32
 
 // kW words per warp (1 on small frames: finer tasks, 4 blocks per SM; 2 on
 // large ones), kB links per batch (4, or 5 when it tiles the interior links)
-template <bool kLog, bool kMag, int kB, int kW, int kMinB>
+template <bool kLog, bool kMag, int kB, int kW, int kMinB, bool kF4>
 __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) {
+  using Q = std::conditional_t<kF4, float4, uint32_t>;
+  constexpr bool kTh = kLog && !kMag;  // log single mode: level thresholds (dense_rule_th)
   extern __shared__ float4 s_dyn4[];
   __shared__ float s_lut[256];
+  __shared__ int2 s_th[kTh ? 256 : 1];
   constexpr int kStage = 32 + kB;  // staged links of a warp: < 32 before a batch of kB
   __shared__ uint2 s_stm[kWarpsPerBlock][kW][kStage];
   __shared__ uint32_t s_stc[kMag ? kWarpsPerBlock : 1][kMag ? kStage : 1];
   __shared__ uint32_t s_stw[kMag ? kWarpsPerBlock : 1][kW][kMag ? kStage : 1];
   const int L = p.d.n_links, G = L * p.n_pairs, N = p.n_interp;
-  float4* s_kc = s_dyn4;                                       // [N + 2]
+  // (the chain constants come from the kernel parameters, p.kcp)
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_dyn4 + N + 2);  // [G]
   for (int i = threadIdx.x; i < G; i += blockDim.x) s_cnt[i] = 0;
-  for (int i = threadIdx.x; i < N + 2; i += blockDim.x) s_kc[i] = p.kc[i];
   if (kLog) s_lut[threadIdx.x] = p.lut[threadIdx.x];
+  if (kTh) s_th[threadIdx.x] = make_int2(p.lthr[threadIdx.x].x, p.lthr[threadIdx.x].y);  // (hi, lo) of level threadIdx.x
   __syncthreads();
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -560,6 +620,7 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
   const float wm = (float)(p.w - 1), hm = (float)(p.h - 1);
   const float my = p.magic_y;
   const uint32_t lut_b = pin((uint32_t)__cvta_generic_to_shared(s_lut) - ((uint32_t)kVB << 2));
+  const uint32_t th_b = pin((uint32_t)__cvta_generic_to_shared(s_th) - ((uint32_t)kVB << 3));
   // link l joins chain frames start + l and start + l + 1; the first n_int
   // links end in an interpolated frame (k <= N), a last one (endpoints) in curr
   const int kfirst = p.d.start + 1;
@@ -570,6 +631,7 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
     DenseWord c[kW];
     float ref[kW];
     int before[kW];
+    int thh[kW], thl[kW], vr[kW];  // kTh: the level's (hi, lo) and biased value
 #pragma unroll
     for (int q = 0; q < kW; ++q) {
       const int64_t wq = w0 + q * kWarpsPerBlock;
@@ -586,6 +648,23 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
       c[q].yf = (float)c[q].y;
       ref[q] = kLog ? (c[q].valid ? p.ref[c[q].pix] : __int_as_float(0x7FC00000)) : 0.0f;
       before[q] = 0;
+      if constexpr (kTh) {
+        thh[q] = INT_MAX;
+        thl[q] = INT_MIN;
+        vr[q] = kVB;
+        if (c[q].valid) {
+          // the level r with L[r] == ref (ref is always a LUT value): the
+          // largest r with L[r] <= ref, L strictly increasing
+          int r = 0;
+#pragma unroll
+          for (int st = 128; st >= 1; st >>= 1)
+            if (s_lut[r + st] <= ref[q]) r += st;
+          const int2 t = s_th[r];
+          thh[q] = t.x;
+          thl[q] = t.y;
+          vr[q] = kVB + r;
+        }
+      }
     }
     int sp = p.r0 % p.R;
     for (int i = 0; i < p.n_pairs; ++i) {
@@ -594,6 +673,16 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
       const uint32_t* qc = p.quads.at(sc);
       const uint32_t* qbp = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(qp) - 4ull * p.qshift);
       const uint32_t* qbc = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(qc) - 4ull * p.qshift);
+      // the gathers' rings (fp32 lerp quads or u8 quads), pre-shifted by -qshift elements
+      const Q* gbp;
+      const Q* gbc;
+      if constexpr (kF4) {
+        gbp = reinterpret_cast<const float4*>(reinterpret_cast<uintptr_t>(p.quadf.at(sp)) - 16ull * p.qshift);
+        gbc = reinterpret_cast<const float4*>(reinterpret_cast<uintptr_t>(p.quadf.at(sc)) - 16ull * p.qshift);
+      } else {
+        gbp = qbp;
+        gbc = qbc;
+      }
       PairCtx pc{};
       pc.pu = p.g0.pu + (size_t)i * p.g0.pair_stride;
       pc.pv = p.g0.pv + (size_t)i * p.g0.pair_stride;
@@ -633,6 +722,9 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
             if (q == 0) s_stc[warp][l - fbase] = ev;
             else s_stc[warp][l - fbase] += ev;
           }
+        } else if constexpr (kTh) {
+          const uint2 m = dense_rule_th(th_b, val, thh[q], thl[q], vr[q]);
+          if (lane == 0) s_stm[warp][q][l - fbase] = m;
         } else {
           const uint2 m = dense_rule<kLog>(p, lut_b, c[q], val, ref[q], before[q]);
           if (lane == 0) s_stm[warp][q][l - fbase] = m;
@@ -665,14 +757,14 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
         int vals[kW][kB];
         unsigned bad;
         if (nb == kB) {
-          bad = safe ? dense_batch<kW, kB, false>(s_kc, qbp, qbc, w, my, wm, hm, c, kfirst + l0, vals)
-                     : dense_batch<kW, kB, true>(s_kc, qbp, qbc, w, my, wm, hm, c, kfirst + l0, vals);
+          bad = safe ? dense_batch<kW, kB, false>(p, gbp, gbc, w, my, wm, hm, c, kfirst + l0, vals)
+                     : dense_batch<kW, kB, true>(p, gbp, gbc, w, my, wm, hm, c, kfirst + l0, vals);
         } else {
           bad = 0;
           for (int j = 0; j < nb; ++j) {
             int v1[kW][kB];
-            bad |= (safe ? dense_batch<kW, 1, false>(s_kc, qbp, qbc, w, my, wm, hm, c, kfirst + l0 + j, v1)
-                         : dense_batch<kW, 1, true>(s_kc, qbp, qbc, w, my, wm, hm, c, kfirst + l0 + j, v1))
+            bad |= (safe ? dense_batch<kW, 1, false>(p, gbp, gbc, w, my, wm, hm, c, kfirst + l0 + j, v1)
+                         : dense_batch<kW, 1, true>(p, gbp, gbc, w, my, wm, hm, c, kfirst + l0 + j, v1))
                    << j;
 #pragma unroll
             for (int q = 0; q < kW; ++q)
@@ -716,11 +808,44 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
     if (kLog) {
 #pragma unroll
       for (int q = 0; q < kW; ++q)
-        if (c[q].valid) p.ref[c[q].pix] = ref[q];
+        if (c[q].valid) p.ref[c[q].pix] = kTh ? s_lut[vr[q] - kVB] : ref[q];
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < G; i += blockDim.x) p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
+}
+
+// ------------------------------------------------------------ lerp quads
+// The dense chain's gather image of a frame: per pixel (a00, a10 - a00, a01,
+// a11 - a01) in fp32 — the four taps sample_u8 reads at (x0, y0)
+// (simulate.cpp:10-26, replicate clamp) with the row differences formed
+// (exactly: integers).  One column per thread, kLQRows rows per block (the
+// row below's taps are the next row's top taps), one 16-byte store per pixel.
+constexpr int kLQRows = 8;
+__global__ void __launch_bounds__(256) lerp_quad_kernel(Ring<const uint8_t> frames, Ring<float4> out, int w, int h,
+                                                        int R, int slot0) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= w) return;
+  const int slot = (slot0 + (int)blockIdx.z) % R;
+  const uint8_t* __restrict__ f = frames.at(slot);
+  float4* __restrict__ q = out.at(slot);
+  const int x1 = min(x + 1, w - 1);
+  const int yb = blockIdx.y * kLQRows, ye = min(yb + kLQRows, h);
+  float a00 = (float)__ldg(f + (size_t)yb * w + x), a10 = (float)__ldg(f + (size_t)yb * w + x1);
+  for (int y = yb; y < ye; ++y) {
+    const size_t r1 = (size_t)min(y + 1, h - 1) * w;
+    const float a01 = (float)__ldg(f + r1 + x), a11 = (float)__ldg(f + r1 + x1);
+    q[(size_t)y * w + x] = make_float4(a00, a10 - a00, a01, a11 - a01);
+    a00 = a01;
+    a10 = a11;
+  }
+}
+
+void launch_lerp_quads(Ring<const uint8_t> frames, Ring<float4> out, int w, int h, int R, int slot0, int n_frames,
+                       cudaStream_t s) {
+  if (n_frames <= 0) return;
+  dim3 g((w + 255) / 256, (h + kLQRows - 1) / kLQRows, n_frames);
+  lerp_quad_kernel<<<g, 256, 0, s>>>(frames, out, w, h, R, slot0);
 }
 
 // ------------------------------------------------------------ sparse chain kernel
@@ -760,6 +885,7 @@ __global__ void __launch_bounds__(256, 3) chain_sparse_kernel(ChainParams p) {
     DenseWord c[kW];
     float ref[kW];
     int before[kW];
+    int thh[kW], thl[kW], vr[kW];  // kTh: the level's (hi, lo) and biased value
 #pragma unroll
     for (int q = 0; q < kW; ++q) {
       const int64_t wq = w0 + q;
@@ -1317,7 +1443,7 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
       const int T = __shfl_sync(kFull, incl, 31);
       const int excl = incl - c;
       const uint32_t wi = (uint32_t)(wbeg + j);
-      const int lrow = (int)(wi / (uint32_t)p.wpr);
+      const int lrow = (int)p.wdiv.div(wi);
       const int x0 = (int)(wi - (uint32_t)lrow * (uint32_t)p.wpr) * 32;
       // per word: output address of its slot 0 relative to the warp's slots,
       // and its (x0, row) in one word (x < 2^16, row < 2^15)
@@ -1383,7 +1509,7 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
       const int sij = item / nw;
       const int sj = s_list[sij];
       const uint32_t wij = (uint32_t)(wbeg + (item - sij * nw));
-      const int lrow = (int)(wij / (uint32_t)p.wpr);
+      const int lrow = (int)p.wdiv.div(wij);
       const int x = (int)(wij - (uint32_t)lrow * (uint32_t)p.wpr) * 32 + lane;
       const int row = p.row0 + lrow;
       const int k0 = p.seg.seg_first[sj], nk = p.seg.seg_nlinks[sj];
@@ -1448,7 +1574,7 @@ __global__ void __launch_bounds__(256) emit_single_kernel(EmitParams p, const in
     // descending pixels (FLO = the highest set bit), written back to front;
     // n1 = neg rotated right by 1, so rotr(n1, b) holds pixel b's polarity
     // at bit 31
-    const uint32_t row = (uint32_t)w / (uint32_t)p.wpr;
+    const uint32_t row = p.wdiv.div((uint32_t)w);
     const uint32_t xy = ((uint32_t)w - row * (uint32_t)p.wpr) * 32u | ((uint32_t)(p.row0 + (int)row) << 16);
     const uint32_t n1 = __funnelshift_r(neg, neg, 1);
     uint32_t m = all;
@@ -1772,7 +1898,8 @@ static void launch_chain_mode(const ChainParams& p, cudaStream_t s) {
 
 template <bool kLog, bool kMag, int kB, int kW, int kMinB>
 static void launch_chain_dense_b(const ChainParams& p, size_t sm, cudaStream_t s) {
-  auto* k = chain_dense_kernel<kLog, kMag, kB, kW, kMinB>;
+  auto* k = p.quadf.base ? chain_dense_kernel<kLog, kMag, kB, kW, kMinB, true>
+                         : chain_dense_kernel<kLog, kMag, kB, kW, kMinB, false>;
   set_max_dynamic_smem((const void*)k, 96 * 1024);
   k<<<p.n_blocks, 256, sm, s>>>(p);
 }
@@ -1829,7 +1956,7 @@ void launch_chain(const ChainParams& p, int provider, cudaStream_t s) {
     }
     return;
   }
-  if (provider == kProvDenseGrid && p.kc) {
+  if (provider == kProvDenseGrid && p.kc && p.n_interp + 2 <= kMaxParamK) {
     const size_t sm = (size_t)(p.n_interp + 2) * sizeof(float4) +
                       (size_t)std::max(p.d.n_links * p.n_pairs, 1) * sizeof(uint32_t);
     if (sm <= 96 * 1024) {

@@ -26,6 +26,7 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <exception>
 
 #include "evsim_gpu.h"
 #include "kernels.h"
@@ -109,6 +110,33 @@ void validate_config(const evsim_gpu_config& c) {
     invalid("SimulatorConfig: difference_interp has no log contrast mode");
 }
 
+// The log rule as per-level thresholds for the dense chain:
+// for every reference level r, pos <=> v > hi[r] and neg <=> v < lo[r], with
+// the rule's own fp32 subtraction and comparisons (fsub(L[v], L[r]) is
+// monotone in v, checked here).  Stored biased by kChainBias like the chain's
+// values, with the level's own value: th[4r..4r+3] = (bias + hi, bias + lo,
+// bits of L[r], 0).
+void log_thresholds(const float* L, float c_pos, float c_neg, int32_t* th) {
+  for (int r = 0; r < 256; ++r) {
+    int hi = -1, lo = 256;
+    bool seen_pos = false, seen_nonneg = false;
+    for (int v = 0; v < 256; ++v) {
+      const float d = L[v] - L[r];
+      const bool pos = d > c_pos, neg = d < c_neg;
+      if (pos) seen_pos = true;
+      else if (seen_pos) runtime("log thresholds: rule not monotone");
+      if (!pos) hi = v;
+      if (!neg) seen_nonneg = true;
+      else if (seen_nonneg) runtime("log thresholds: rule not monotone");
+      if (!neg && lo == 256) lo = v;
+    }
+    th[4 * r] = kChainBias + hi;
+    th[4 * r + 1] = kChainBias + lo;
+    std::memcpy(&th[4 * r + 2], &L[r], 4);
+    th[4 * r + 3] = 0;
+  }
+}
+
 void log_lut(float* lut) {
   // L[i] = logf(i / 255 + 1e-3), evaluated once on the host so
   // every consumer (device kernels, CPU oracle) sees the same 256 floats.
@@ -132,6 +160,20 @@ void init_pool(int device) {
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    // grow the pool once up front: the buffers of a handle / a stateless
+    // call are then carved from reserved memory instead of mapping new pages
+    // on the first call at a size (measured ~1 ms at 640x480)
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, (size_t)512 << 20, 0) == cudaSuccess) {
+      cudaFreeAsync(p, 0);
+      cudaStreamSynchronize(0);
+    } else {
+      cudaGetLastError();
+    }
+    cudaSetDevice(cur);
   }
   done[device] = true;
 }
@@ -573,7 +615,18 @@ struct evsim_gpu_sim {
   int launch_cap = 0;
   int band_y0 = 0, band_y1 = 0;  // row band of the events (0, 0 = the whole frame)
 
-  DevBuf frames, quads, mags, lut, ref, consts, place_tab;
+  DevBuf frames, quads, mags, lut, lthr, ref, consts, place_tab;
+  std::vector<float4> h_kc;  // host copy of the chain constants kc (ChainParams::kcp)
+  // dense method: level-0 fp32 lerp quads of every ring slot, the dense
+  // chain's gather source (16 B per pixel: no byte unpack, FFMA lerps);
+  // EVSIM_CHAIN_U8=1 gathers the u8 quads instead (A/B and tests)
+  DevBuf quadf;
+  bool chain_u8 = [] {
+    const char* e = std::getenv("EVSIM_CHAIN_U8");
+    return e && e[0] == '1';
+  }();
+  bool use_quadf() const { return dense_flow() && !chain_u8; }
+  float4* quadf_ptr() { return use_quadf() ? quadf.as<float4>() : nullptr; }
   FlowEngine flow;
   EventEngine ev;
   // sparse (per pair)
@@ -591,6 +644,11 @@ struct evsim_gpu_sim {
   // on s_flow while the chain of sub-batch b runs on `stream` (the chain's
   // per-pixel state orders the chains; the flows are independent)
   cudaStream_t s_flow = nullptr;
+  // dense: the chain's lerp quads of a push's frames are built on s_quad
+  // beside the pyramid and flow (HBM-bound next to compute-bound work); the
+  // chain waits for ev_qdone
+  cudaStream_t s_quad = nullptr;
+  cudaEvent_t ev_qin = nullptr, ev_qdone = nullptr;
   std::vector<cudaEvent_t> pipe_ev;  // [0]: inputs ready; [1 + b]: flow of sub-batch b done
   // streamed call (dense): a chunk's pyramid and flow also run on s_flow,
   // after its upload, so they overlap the previous chunk's chain and emit;
@@ -630,6 +688,9 @@ struct evsim_gpu_sim {
     for (auto& b : h_wl)
       if (b) cudaFreeHost(b);
     if (s_flow) cudaStreamSynchronize(s_flow), cudaStreamDestroy(s_flow);
+    if (s_quad) cudaStreamSynchronize(s_quad), cudaStreamDestroy(s_quad);
+    if (ev_qin) cudaEventDestroy(ev_qin);
+    if (ev_qdone) cudaEventDestroy(ev_qdone);
     for (auto e : pipe_ev) cudaEventDestroy(e);
     if (s_in) cudaStreamSynchronize(s_in), cudaStreamDestroy(s_in);
     if (s_out) cudaStreamSynchronize(s_out), cudaStreamDestroy(s_out);
@@ -749,6 +810,7 @@ struct evsim_gpu_sim {
       kc[4 * k + 2] = oma_f[k];
       kc[4 * k + 3] = alpha_f[k];
     }
+    h_kc.assign(reinterpret_cast<const float4*>(kc), reinterpret_cast<const float4*>(kc) + K);
     consts.ensure(host.size(), stream);
     CK(cudaMemcpyAsync(consts.p, host.data(), host.size(), cudaMemcpyHostToDevice, stream));
     CK(cudaStreamSynchronize(stream));
@@ -786,6 +848,10 @@ struct evsim_gpu_sim {
         std::swap(quads.n, nq.n);
         std::swap(quads.s, nq.s);
       }
+      if (use_quadf()) {  // (prev's lerp quads are rebuilt below)
+        quadf.release();
+        quadf.ensure((size_t)need_R * P * sizeof(float4), stream);
+      }
       if (diff_interp()) {
         DevBuf nm;
         nm.ensure((size_t)need_R * P + 16, stream);
@@ -808,6 +874,11 @@ struct evsim_gpu_sim {
         PyramidParams pp = flow.pyramid_params(src, P, quads.as<uint32_t>(), rhead);
         launch_pyramid(pp, 1, stream);
         CK_LAUNCH("pyramid");
+        if (use_quadf()) {
+          launch_lerp_quads(Ring<const uint8_t>{frames.as<uint8_t>(), P}, Ring<float4>{quadf.as<float4>(), P}, w, h, R,
+                            rhead, 1, stream);
+          CK_LAUNCH("lerp_quads");
+        }
       }
     }
     if (pairs > pair_cap) {
@@ -873,6 +944,7 @@ struct evsim_gpu_sim {
     c.r0 = r0;
     c.frames = Ring<const uint8_t>{frames.as<uint8_t>(), P};
     c.quads = Ring<const uint32_t>{quads.as<uint32_t>(), P};
+    c.quadf = Ring<const float4>{quadf_ptr(), P};
     {
       // gather index of the dense chain: TY_bits * w + TX_bits with TX =
       // 2^23 + x, TY = 2^23 + m_y + y (fp32 bits); it equals y * w + x +
@@ -894,6 +966,7 @@ struct evsim_gpu_sim {
     }
     const int K = N + 2;
     c.kc = consts.as<float4>();
+    for (int k = 0; k < std::min(K, kMaxParamK); ++k) c.kcp[k] = h_kc[k];
     c.alpha = reinterpret_cast<const double*>(c.kc + K);
     c.oma = c.alpha + K;
     c.fwd = reinterpret_cast<const float*>(c.alpha + 2 * K);
@@ -910,6 +983,7 @@ struct evsim_gpu_sim {
     c.c_pos_log = cfg.c_pos_log;
     c.c_neg_log = cfg.c_neg_log;
     c.lut = lut.as<float>();
+    c.lthr = lthr.as<int4>();
     c.ref = ref.as<float>();
     c.masks = ev.masks.as<uint2>();
     c.mcount = ev.mcount.as<uint16_t>();
@@ -943,6 +1017,7 @@ struct evsim_gpu_sim {
     ep.h = h;
     ep.row0 = c.row0;
     ep.wpr = ev.wpr;
+    ep.wdiv = FastDiv::make((uint32_t)ev.wpr);
     ep.n_words = ev.n_words;
     ep.words_per_block = ev.wpb;
     ep.n_blocks = ev.n_blocks;
@@ -1137,6 +1212,29 @@ struct evsim_gpu_sim {
     if (uploaded) CK(cudaStreamWaitEvent(ps, uploaded, 0));
     else upload(pixels, F, base, on_device, stream);
     mark(EVSIM_STAGE_PYRAMID);
+    bool quad_side = false;
+    if (use_quadf()) {
+      const Ring<const uint8_t> fr{frames.as<uint8_t>(), P};
+      const Ring<float4> qr{quadf.as<float4>(), P};
+      if (profiling) {
+        launch_lerp_quads(fr, qr, w, h, R, base, F, ps);  // (stage timing: serialised, counted as pyramid)
+      } else {
+        if (!s_quad) {
+          int lo = 0, hi = 0;
+          CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+          CK(cudaStreamCreateWithPriority(&s_quad, cudaStreamNonBlocking, hi));
+          CK(cudaEventCreateWithFlags(&ev_qin, cudaEventDisableTiming));
+          CK(cudaEventCreateWithFlags(&ev_qdone, cudaEventDisableTiming));
+        }
+        CK(cudaEventRecord(ev_qin, ps));  // the frames are in the ring
+        CK(cudaStreamWaitEvent(s_quad, ev_qin, 0));
+        launch_lerp_quads(fr, qr, w, h, R, base, F, s_quad);
+        CK(cudaEventRecord(ev_qdone, s_quad));
+        quad_side = true;
+      }
+      CK_LAUNCH("lerp_quads");
+      ++launches;
+    }
     if (diff_interp()) {
       // difference magnitudes of the new frames that have a predecessor, and
       // (for the sparse solver) their pyramids
@@ -1225,8 +1323,12 @@ struct evsim_gpu_sim {
         provider = kProvDiffInterp;
       }
       mark(EVSIM_STAGE_CHAIN);
+      if (quad_side) CK(cudaStreamWaitEvent(stream, ev_qdone, 0));
       run_events(c, provider, pts.data(), h_seg, continue_call, sub);
     } else {
+      // (no chain: the handle's stream still orders after the quad build, so
+      // a later ring growth never frees the quads under it)
+      if (quad_side) CK(cudaStreamWaitEvent(stream, ev_qdone, 0));
       if (!continue_call) {
         seg_t.clear();
         seg_off.assign(1, 0);
@@ -1748,6 +1850,10 @@ void make_sim(evsim_gpu_sim* s, const evsim_gpu_config& cfg, int device) {
   log_lut(h_lut);
   s->lut.ensure(sizeof h_lut, s->stream);
   CK(cudaMemcpyAsync(s->lut.p, h_lut, sizeof h_lut, cudaMemcpyHostToDevice, s->stream));
+  int32_t h_th[1024];
+  log_thresholds(h_lut, s->cfg.c_pos_log, s->cfg.c_neg_log, h_th);
+  s->lthr.ensure(sizeof h_th, s->stream);
+  CK(cudaMemcpyAsync(s->lthr.p, h_th, sizeof h_th, cudaMemcpyHostToDevice, s->stream));
   CK(cudaStreamSynchronize(s->stream));
 }
 
@@ -2203,6 +2309,69 @@ int evsim_gpu_accumulate(const evsim_event* ev, int64_t n, int32_t w, int32_t h,
   });
 }
 
+int evsim_gpu_difference_frame(const uint8_t* prev, const uint8_t* curr, int32_t w, int32_t h, int16_t* values) {
+  return guarded([&] {
+    // core.cpp:5-19
+    if (!prev || !curr || !values || w <= 0 || h <= 0) invalid("difference_frame: malformed frames");
+    CK(cudaSetDevice(0));
+    init_pool(0);
+    TmpStream ts;
+    const size_t P = (size_t)w * h;
+    DevBuf f, out;
+    f.ensure(2 * P, ts.s);
+    out.ensure(2 * P, ts.s);
+    CK(cudaMemcpyAsync(f.p, prev, P, cudaMemcpyHostToDevice, ts.s));
+    CK(cudaMemcpyAsync(f.as<uint8_t>() + P, curr, P, cudaMemcpyHostToDevice, ts.s));
+    launch_difference(f.as<uint8_t>(), f.as<uint8_t>() + P, out.as<int16_t>(), (int64_t)P, ts.s);
+    CK_LAUNCH("difference");
+    CK(cudaMemcpyAsync(values, out.p, 2 * P, cudaMemcpyDeviceToHost, ts.s));
+    CK(cudaStreamSynchronize(ts.s));
+  });
+}
+
+int evsim_gpu_threshold_events(const int16_t* values, int32_t w, int32_t h, const evsim_gpu_config* cfg,
+                               int64_t event_time, evsim_event* events, int64_t capacity, int64_t* n_events) {
+  return guarded([&] {
+    // core.cpp:21-46 (config.validate() first, core.cpp:23)
+    if (!cfg || !n_events) invalid("threshold_events: null argument");
+    validate_config(*cfg);
+    if (w < 0 || h < 0 || ((int64_t)w * h > 0 && !values)) invalid("threshold_events: malformed difference frame");
+    const int64_t P = (int64_t)w * h;
+    *n_events = 0;
+    if (P == 0) return;
+    CK(cudaSetDevice(0));
+    init_pool(0);
+    TmpStream ts;
+    const int64_t T = threshold_tiles(P);
+    const int mag = cfg->events_per_crossing == EVSIM_EVENTS_MAGNITUDE ? 1 : 0;
+    DevBuf dv, tiles;
+    dv.ensure((size_t)P * 2, ts.s);
+    tiles.ensure((size_t)T * 8, ts.s);
+    CK(cudaMemcpyAsync(dv.p, values, (size_t)P * 2, cudaMemcpyHostToDevice, ts.s));
+    launch_threshold_count(dv.as<int16_t>(), P, cfg->c_pos, cfg->c_neg, mag, tiles.as<int64_t>(), ts.s);
+    CK_LAUNCH("threshold_count");
+    std::vector<int64_t> off((size_t)T);
+    CK(cudaMemcpyAsync(off.data(), tiles.p, (size_t)T * 8, cudaMemcpyDeviceToHost, ts.s));
+    CK(cudaStreamSynchronize(ts.s));
+    int64_t total = 0;
+    for (auto& o : off) {  // exclusive prefix of the tile totals
+      const int64_t c = o;
+      o = total;
+      total += c;
+    }
+    *n_events = total;
+    if (!events || capacity < total || total == 0) return;
+    DevBuf dout;
+    dout.ensure((size_t)total * sizeof(evsim_event), ts.s);
+    CK(cudaMemcpyAsync(tiles.p, off.data(), (size_t)T * 8, cudaMemcpyHostToDevice, ts.s));
+    launch_threshold_emit(dv.as<int16_t>(), P, w, cfg->c_pos, cfg->c_neg, mag, event_time, tiles.as<int64_t>(),
+                          dout.as<evsim_event>(), ts.s);
+    CK_LAUNCH("threshold_emit");
+    CK(cudaMemcpyAsync(events, dout.p, (size_t)total * sizeof(evsim_event), cudaMemcpyDeviceToHost, ts.s));
+    CK(cudaStreamSynchronize(ts.s));
+  });
+}
+
 void* evsim_gpu_stream(evsim_gpu_sim* sim) { return sim ? (void*)sim->stream : nullptr; }
 
 int evsim_gpu_reset(evsim_gpu_sim* sim) {
@@ -2258,27 +2427,73 @@ namespace {
 
 // Scratch simulator for the free functions: one (prev, curr) pair in ring
 // slots 0 and 1.
+// Stateless entry points (estimate_dense_flow, interpolate_frames, the
+// *_events_with_flow functions) run on a scratch simulator.  Idle scratch
+// simulators are kept per thread (up to 4, keyed by config and frame size)
+// and reused, so a repeated call costs its uploads, kernels and downloads
+// only — not a stream, pinned buffers and device allocations each time.
+struct ScratchCache {
+  struct Entry {
+    evsim_gpu_config cfg;
+    int w, h;
+    evsim_gpu_sim* s;
+  };
+  std::vector<Entry> idle;
+};
+ScratchCache& scratch_cache() {
+  // leaked on purpose: thread-exit destructors may run after the CUDA runtime is gone
+  static thread_local ScratchCache* c = new ScratchCache();
+  return *c;
+}
+void destroy_scratch(evsim_gpu_sim* s) {
+  cudaStream_t st = s->stream;
+  cudaStreamSynchronize(st);
+  delete s;
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+}
+
 struct Scratch {
   std::unique_ptr<evsim_gpu_sim> s;
+  evsim_gpu_config key{};
+  int kw = 0, kh = 0;
   Scratch(const evsim_gpu_config& cfg, int w, int h, const uint8_t* prev, const uint8_t* curr) {
     CK(cudaSetDevice(0));
     init_pool(0);
-    s = std::make_unique<evsim_gpu_sim>();
-    make_sim(s.get(), cfg, 0);
-    s->allocate(w, h);
-    s->ensure_capacity(1);
+    key = cfg;
+    kw = w;
+    kh = h;
+    auto& cache = scratch_cache().idle;
+    for (size_t i = 0; i < cache.size(); ++i) {
+      if (cache[i].w == w && cache[i].h == h && std::memcmp(&cache[i].cfg, &cfg, sizeof cfg) == 0) {
+        s.reset(cache[i].s);
+        cache.erase(cache.begin() + (long)i);
+        break;
+      }
+    }
+    if (!s) {
+      s = std::make_unique<evsim_gpu_sim>();
+      make_sim(s.get(), cfg, 0);
+      s->allocate(w, h);
+      s->ensure_capacity(1);
+    }
     const size_t P = (size_t)w * h;
     CK(cudaMemcpyAsync(s->frames.p, prev, P, cudaMemcpyHostToDevice, s->stream));
     CK(cudaMemcpyAsync(s->frames.as<uint8_t>() + P, curr, P, cudaMemcpyHostToDevice, s->stream));
   }
   ~Scratch() {
-    if (s) {
-      cudaStream_t st = s->stream;
-      cudaStreamSynchronize(st);
-      s.reset();
-      cudaStreamSynchronize(st);
-      cudaStreamDestroy(st);
+    if (!s) return;
+    // a call that failed part-way is not reused (its buffers may be half-written)
+    if (cudaStreamSynchronize(s->stream) == cudaSuccess && std::uncaught_exceptions() == 0) {
+      auto& cache = scratch_cache().idle;
+      if (cache.size() >= 4) {
+        destroy_scratch(cache.front().s);
+        cache.erase(cache.begin());
+      }
+      cache.push_back(ScratchCache::Entry{key, kw, kh, s.release()});
+      return;
     }
+    destroy_scratch(s.release());
   }
   evsim_gpu_sim* operator->() { return s.get(); }
   void pyramids() {

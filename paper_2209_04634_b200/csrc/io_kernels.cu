@@ -143,3 +143,101 @@ void launch_place(const uint32_t* src, const int64_t* off, const int64_t* dst_of
 }
 
 }  // namespace evsim_gpu
+
+namespace evsim_gpu {
+
+// ------------------------------------------------------------ core.hpp free functions
+// difference_frame (core.cpp:5-19): curr - prev per pixel, int16.
+__global__ void difference_kernel(const uint8_t* __restrict__ prev, const uint8_t* __restrict__ curr,
+                                  int16_t* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int16_t)((int)curr[i] - (int)prev[i]);
+}
+
+// threshold_events_into (core.cpp:21-46) over a caller's difference values:
+// a pixel v > c_pos emits count = (magnitude ? v / c_pos : 1) positive
+// events, v < c_neg count = (magnitude ? v / c_neg : 1) negative ones, in
+// scan order.  Tiles of kThrTile pixels per block; kThrPer consecutive pixels
+// per thread.
+constexpr int kThrPer = 8, kThrTile = 256 * kThrPer;
+__device__ __forceinline__ int thr_count(int v, int c_pos, int c_neg, int mag) {
+  if (v > c_pos) return mag ? v / c_pos : 1;
+  if (v < c_neg) return mag ? v / c_neg : 1;
+  return 0;
+}
+
+__global__ void __launch_bounds__(256) threshold_count_kernel(const int16_t* __restrict__ v, int64_t n, int c_pos,
+                                                              int c_neg, int mag, int64_t* __restrict__ tile_total) {
+  __shared__ int64_t s_warp[8];
+  const int64_t i0 = (int64_t)blockIdx.x * kThrTile + (int64_t)threadIdx.x * kThrPer;
+  int64_t c = 0;
+#pragma unroll
+  for (int j = 0; j < kThrPer; ++j)
+    if (i0 + j < n) c += thr_count(v[i0 + j], c_pos, c_neg, mag);
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int k = 0; k < 8; ++k) t += s_warp[k];
+    tile_total[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) threshold_emit_kernel(const int16_t* __restrict__ v, int64_t n, int w,
+                                                             int c_pos, int c_neg, int mag, int64_t t,
+                                                             const int64_t* __restrict__ tile_off,
+                                                             evsim_event* __restrict__ out) {
+  __shared__ int64_t s_warp[8];
+  const int64_t i0 = (int64_t)blockIdx.x * kThrTile + (int64_t)threadIdx.x * kThrPer;
+  int cnt[kThrPer];
+  int64_t c = 0;
+#pragma unroll
+  for (int j = 0; j < kThrPer; ++j) {
+    cnt[j] = i0 + j < n ? thr_count(v[i0 + j], c_pos, c_neg, mag) : 0;
+    c += cnt[j];
+  }
+  // exclusive block scan of the per-thread counts
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t incl = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  int64_t base = tile_off[blockIdx.x];
+  for (int k = 0; k < wid; ++k) base += s_warp[k];
+  int64_t o = base + incl - c;
+#pragma unroll
+  for (int j = 0; j < kThrPer; ++j) {
+    if (!cnt[j]) continue;
+    const int64_t i = i0 + j;
+    const int y = (int)(i / w), x = (int)(i - (int64_t)y * w);
+    const int8_t p = v[i] > c_pos ? 1 : -1;
+    for (int k = 0; k < cnt[j]; ++k) {
+      evsim_event e;
+      e.x = (uint16_t)x;
+      e.y = (uint16_t)y;
+      e.t = t;
+      e.p = p;
+      out[o++] = e;
+    }
+  }
+}
+
+void launch_difference(const uint8_t* prev, const uint8_t* curr, int16_t* out, int64_t n, cudaStream_t s) {
+  if (n > 0) difference_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s>>>(prev, curr, out, n);
+}
+int64_t threshold_tiles(int64_t n) { return (n + kThrTile - 1) / kThrTile; }
+void launch_threshold_count(const int16_t* v, int64_t n, int c_pos, int c_neg, int mag, int64_t* tile_total,
+                            cudaStream_t s) {
+  if (n > 0) threshold_count_kernel<<<(unsigned)threshold_tiles(n), 256, 0, s>>>(v, n, c_pos, c_neg, mag, tile_total);
+}
+void launch_threshold_emit(const int16_t* v, int64_t n, int w, int c_pos, int c_neg, int mag, int64_t t,
+                           const int64_t* tile_off, evsim_event* out, cudaStream_t s) {
+  if (n > 0)
+    threshold_emit_kernel<<<(unsigned)threshold_tiles(n), 256, 0, s>>>(v, n, w, c_pos, c_neg, mag, t, tile_off, out);
+}
+
+}  // namespace evsim_gpu

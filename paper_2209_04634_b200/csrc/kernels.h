@@ -20,6 +20,8 @@ namespace evsim_gpu {
 constexpr int kWarpsPerBlock = 8;  // chain / emit kernels: 256 threads
 constexpr int kMaxLevels = 8;
 constexpr int kMaxBatch = 1024;    // frames per push_frames call
+constexpr int kChainBias = 0x4B000000;  // dense chain values: the fp32 bits of 2^23 + v (an int compare orders them)
+constexpr int kMaxParamK = 64;     // chain frames (N + 2) whose constants travel in the kernel parameters
 
 struct LevelDims {
   int w, h;
@@ -138,6 +140,7 @@ struct ChainParams {
   int R, r0;
   Ring<const uint8_t> frames;
   Ring<const uint32_t> quads;  // u8 quad images (dense provider)
+  Ring<const float4> quadf;    // dense chain: fp32 lerp quads of the same frames (base null: the u8 form)
   float magic_y;               // dense chain: Y truncation magic 2^23 + m_y (exact integer float)
   uint32_t qshift;             // dense chain: (bits(2^23 + m_y) * w + bits(2^23)) mod 2^32, + w*h <= 2^32
   // dense provider, grid form (level-0 patch grid + tables; per-pair pu/pv)
@@ -154,6 +157,11 @@ struct ChainParams {
   const float* oma_f;      // (float)oma
   const float2* nfb;       // (-(float)alpha, (float)(1.0 - alpha))
   const float4* kc;        // (-(float)alpha, (float)(1 - alpha), (float)oma, (float)alpha)
+  // the dense chain's copy of kc in the parameter space (constant bank: the
+  // per-link loads go through the constant cache, not the L1 data pipe);
+  // N + 2 <= kMaxParamK, larger N use the generic chain kernel
+  float4 kcp[kMaxParamK];
+  const int4* lthr;        // log mode: per reference level r (0..255): biased (hi, lo) thresholds, L[r] bits, 0
   // sparse provider (per pair strides)
   uint32_t* claims;        // [pair][N][P] keys (change << 24 | ~j)
   uint32_t* touched;       // [pair][ceil(N/32)][P] bits
@@ -188,8 +196,28 @@ struct OffsetParams {
   int64_t* link_total;     // [g]
 };
 
+// n / d for n < 2^27 by one wide multiply and a shift (d >= 1): s = 27 +
+// ceil(log2 d), m = ceil(2^s / d) < 2^28, and m*d - 2^s < d <= 2^(s-27)
+// makes floor(n*m / 2^s) = floor(n / d) exact (Granlund-Montgomery).
+struct FastDiv {
+  uint32_t m = 1;
+  int s = 0;
+  __host__ __device__ uint32_t div(uint32_t n) const {
+    return (uint32_t)(((unsigned long long)n * m) >> s);
+  }
+  static FastDiv make(uint32_t d) {
+    FastDiv f;
+    int l = 0;
+    while ((1ull << l) < d) ++l;
+    f.s = 27 + l;
+    f.m = (uint32_t)(((1ull << f.s) + d - 1) / d);
+    return f;
+  }
+};
+
 struct EmitParams {
   int w, h, wpr;
+  FastDiv wdiv;            // / wpr (word index -> row)
   int row0;                // first frame row of the word grid
   int64_t n_words;
   int words_per_block;
@@ -274,6 +302,9 @@ void launch_pyramid(const PyramidParams& p, int n_frames, cudaStream_t s);
 void launch_build_quad(const uint8_t* src, uint32_t* dst, int w, int h, cudaStream_t s);
 void launch_dense_lk(const DenseLKParams& p, int n_pairs, cudaStream_t s);
 void launch_densify(const GridGeom& g, float* du, float* dv, cudaStream_t s);
+// the dense chain's fp32 lerp quads of n_frames ring slots from slot0
+void launch_lerp_quads(Ring<const uint8_t> frames, Ring<float4> out, int w, int h, int R, int slot0, int n_frames,
+                       cudaStream_t s);
 void launch_interp_frames(const ChainParams& p, uint8_t* out, cudaStream_t s);
 void launch_segments(const SegParams& p, cudaStream_t s);
 // per-(function, device) MaxDynamicSharedMemorySize, thread-safe; throws
@@ -303,6 +334,13 @@ void launch_unpack_events(const uint32_t* packed, const int64_t* seg_out, int64_
 void launch_luma(const uint8_t* rgb, uint8_t* out, int64_t n, cudaStream_t s);
 void launch_resize(const uint8_t* src, int w, int h, uint8_t* dst, int tw, int th, int n_frames, cudaStream_t s);
 void launch_evs_records(const uint32_t* packed, const int64_t* seg_out, int64_t n, uint8_t* out, cudaStream_t s);
+// core.hpp free functions (core.cpp:5-46): difference_frame and threshold_events
+void launch_difference(const uint8_t* prev, const uint8_t* curr, int16_t* out, int64_t n, cudaStream_t s);
+int64_t threshold_tiles(int64_t n);
+void launch_threshold_count(const int16_t* v, int64_t n, int c_pos, int c_neg, int mag, int64_t* tile_total,
+                            cudaStream_t s);
+void launch_threshold_emit(const int16_t* v, int64_t n, int w, int c_pos, int c_neg, int mag, int64_t t,
+                           const int64_t* tile_off, evsim_event* out, cudaStream_t s);
 void launch_event_counts(const evsim_event* ev, int64_t n, int w, uint32_t* counts, cudaStream_t s);
 void launch_accumulate(const evsim_event* ev, int64_t n, int w, int64_t t0, int64_t t1, uint32_t* bits,
                        uint8_t* classes, int64_t P, cudaStream_t s);

@@ -263,6 +263,37 @@ class PyramidalLucasKanade(SparseFlowEstimator):
         return estimate_sparse_flow(prev, curr, points, self.preset)
 
 
+# --------------------------------------------------------------------------- core.hpp
+
+@dataclasses.dataclass
+class DifferenceFrame:
+    """Signed per-pixel delta (types.hpp:33-46); values int16 (h, w)."""
+    width: int
+    height: int
+    t_start: int
+    t_end: int
+    values: np.ndarray
+
+
+def difference_frame(prev: Frame, curr: Frame) -> DifferenceFrame:
+    """difference_frame (core.cpp:5-19) on the GPU."""
+    if prev.width != curr.width or prev.height != curr.height:
+        raise InvalidArgument(1, f"difference_frame: incompatible input frames ({prev.width}x{prev.height} vs "
+                                 f"{curr.width}x{curr.height})")
+    out = np.zeros((prev.height, prev.width), np.int16)
+    _lib.check(_lib.load().evsim_gpu_difference_frame(_ptr(prev.pixels), _ptr(curr.pixels), prev.width,
+                                                      prev.height, _ptr(out)))
+    return DifferenceFrame(prev.width, prev.height, prev.timestamp, curr.timestamp, out)
+
+
+def threshold_events(diff: DifferenceFrame, config: SimulatorConfig, event_time: int) -> np.ndarray:
+    """threshold_events (core.cpp:21-52) on the GPU: 24-byte event records, scan order."""
+    c = config.to_c()
+    v = np.ascontiguousarray(diff.values, np.int16)
+    return _call_events(_lib.load().evsim_gpu_threshold_events, _ptr(v), diff.width, diff.height, ctypes.byref(c),
+                        int(event_time))
+
+
 # --------------------------------------------------------------------------- pipelines
 
 def _events_from_c(events24: np.ndarray, n: int, w: int, h: int) -> EventStream:
