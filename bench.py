@@ -57,6 +57,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 L2_FLUSH_BYTES = 256 << 20
+CHAIN_KERNEL = {"dense": "chain_dense_kernel", "sparse": "chain_sparse_kernel", "difference_only": "chain_diff_kernel",
+                "difference_interp": "chain_diffinterp_kernel"}
 METRIC = "simulated input frames/sec and events/sec per B200, % of HBM roofline"
 GOLDEN = os.path.join(ROOT, "tests", "golden", "sequences.json")
 
@@ -83,6 +85,8 @@ def parse():
                    help="host event format of e2e (auto: wire when it is smaller than packed records)")
     p.add_argument("--no-parity", action="store_true")
     p.add_argument("--force-band", action="store_true", help=argparse.SUPPRESS)
+    p.add_argument("--no-stack", action="store_true",
+                   help="difference_only streams: one simulator per stream instead of one stacked simulator")
     return p.parse_args()
 
 
@@ -363,20 +367,40 @@ class Arm:
         import torch
 
         from paper_2209_04634_b200 import Simulator, SimulatorConfig
-        from paper_2209_04634_b200.parallel import band_rows, shard_streams
+        from paper_2209_04634_b200.parallel import band_rows, shard_streams, stack_streams
         self.c, self.args, self.ws, self.rank, self.device, self.split = c, args, ws, rank, device, split
         self.n = args.frames or c.n_frames
+        total = args.streams or c.streams
+        # difference_only streams stacked into one simulator (parallel.stack_streams:
+        # exact, every pixel its own chain) — S streams in one launch sequence
+        self.stacked = split == "streams" and c.method == "difference_only" and total > 1 and not args.no_stack
+        if self.stacked:
+            self.streams = list(shard_streams(total, ws, rank))
+            self.band = None
+            data = generate_streams(c, self.n, self.streams)
+            self.frames = [stack_streams([d[0] for d in data])]
+            self.cpu_frames = data[0][0]  # stream 0 alone (the CPU baseline's sample)
+            self.ts = data[0][1]
+            self.H = len(self.streams) * c.height
+            self.sims = [Simulator(SimulatorConfig.from_c(cfg), device=device)]
+            self.P = c.width * self.H
+            self.d_frames = [torch.from_numpy(self.frames[0]).to(f"cuda:{device}")]
+            self.batch = max(1, min(args.batch or self.sims[0].max_batch(c.width, self.H), self.n))
+            self.torch_stream = torch.cuda.ExternalStream(self.sims[0].stream, device=device)
+            self.other_streams = []
+            return
+        self.H = c.height
         if split == "bands":
             self.streams = [0]
             # (--force-band: the band path at N = 1 — one band = the frame — to
             # exercise the placement / merged-output check on one GPU)
             self.band = band_rows(c.height, ws, rank) if (ws > 1 or args.force_band) else None
         else:
-            total = args.streams or c.streams
             self.streams = list(shard_streams(total, ws, rank)) if total > 1 else [rank]
             self.band = None
         data = generate_streams(c, self.n, self.streams)
         self.frames = [d[0] for d in data]
+        self.cpu_frames = self.frames[0]
         self.ts = data[0][1]
         self.sims = []
         for _ in self.streams:
@@ -425,7 +449,7 @@ class Arm:
         from paper_2209_04634_b200.simulator import push_frames_batched_device
         c = self.c
         if len(self.sims) == 1:
-            return [self.sims[0].push_frames_device(self.d_frames[0].data_ptr() + a * self.P, nb, c.width, c.height,
+            return [self.sims[0].push_frames_device(self.d_frames[0].data_ptr() + a * self.P, nb, c.width, self.H,
                                                     self.ts[a:a + nb], on_device=True, sync=sync)]
         return push_frames_batched_device(self.sims, [d.data_ptr() + a * self.P for d in self.d_frames], nb,
                                           c.width, c.height, [self.ts[a:a + nb]] * len(self.sims))
@@ -457,6 +481,30 @@ def push_checksums(arm, a, nb, outs, timeline_counts=None):
     return seg_t, seg_off, push_frame_hashes(int(ev.d_packed), seg_t, seg_off, frame_ts, arm.device, timeline, jbase)
 
 
+def stacked_stream0_checksums(arm, a, nb, ev):
+    """Per-frame (count, checksum) of stream 0 of a stacked push: its events
+    are the rows [0, h) of every segment (parallel.split_stacked)."""
+    from paper_2209_04634_b200.parallel import split_stacked
+    from paper_2209_04634_b200.seqhash import device_int32, frame_hash_packed_np
+    n = int(ev.n_events)
+    S = int(ev.n_segments)
+    seg_t = np.ctypeslib.as_array(ev.seg_t, shape=(S,)).copy() if S else np.zeros(0, np.int64)
+    seg_off = np.ctypeslib.as_array(ev.seg_offset, shape=(S + 1,)).copy() if S else np.zeros(1, np.int64)
+    packed = device_int32(int(ev.d_packed), n, arm.device).cpu().numpy().view(np.uint32) if n else np.zeros(0, np.uint32)
+    rec, st, so = split_stacked(packed, seg_t, seg_off, len(arm.streams), arm.c.height)[0]
+    out = []
+    for k in range(max(a, 1), a + nb):  # frames that close an interval
+        t0, t1 = int(arm.ts[k - 1]), int(arm.ts[k])
+        sel = (st > t0) & (st <= t1)
+        idx = np.nonzero(sel)[0]
+        if len(idx):
+            r = rec[so[idx[0]]:so[idx[-1] + 1]]
+            out.append((len(r), frame_hash_packed_np(r, st[idx], so[idx[0]:idx[-1] + 2] - so[idx[0]], t0)))
+        else:
+            out.append((0, frame_hash_packed_np(np.zeros(0, np.uint32), np.zeros(0), np.zeros(1, np.int64), t0)))
+    return out
+
+
 def parity_pass(arm, g, ws):
     """Untimed pass with the timed pass's batches; per-frame checksums of
     stream 0 compared with the reference's.  Returns (status, events total of
@@ -471,6 +519,9 @@ def parity_pass(arm, g, ws):
     for a, nb in arm.pushes():
         outs = arm.push(a, nb, sync=True)
         ev_total += sum(int(o.n_events) for o in outs)
+        if arm.stacked:
+            frames_out += stacked_stream0_checksums(arm, a, nb, outs[0])
+            continue
         if arm.band is None:
             frames_out += push_checksums(arm, a, nb, outs)[2]
             continue
@@ -579,7 +630,7 @@ def run_ours(args):
     launches = sum(s.kernel_launches for s in arm.sims) - launches0
     # the last timed push, checked against the parity pass (same frames)
     timed_check = "skipped"
-    if frames_out and arm.band is None:
+    if frames_out and arm.band is None and not arm.stacked:
         a, nb = arm.pushes()[-1]
         ev = arm.sims[0].sync()
         part = push_checksums(arm, a, nb, [ev])[2]
@@ -627,8 +678,8 @@ def run_ours(args):
     pairs_prof = prof_steps * (n - 1)
     launches_ev = max(timed_pushes, 1)
     ev_stage_ms = stages["chain"] + stages["scan"] + stages["emit"]
-    E_band = (ev_total / max(len(arm.sims), 1)) / max(n - 1, 1)  # this rank's (band's) events per frame
-    P_band = c.width * (arm.band[1] - arm.band[0]) if arm.band else P
+    E_band = (ev_total / max(len(arm.sims), 1)) / max(n - 1, 1)  # this rank's (band's / stack's) events per pair
+    P_band = c.width * (arm.band[1] - arm.band[0]) if arm.band else arm.P  # rows of stream 0's handle
     b_alg_band = 2 * P_band + 4 * E_band
     bytes_per_launch = b_alg_band * pairs_prof / launches_ev
     ms_per_launch = ev_stage_ms / launches_ev
@@ -637,7 +688,7 @@ def run_ours(args):
     roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4),
                 "traffic": traffic_for(c.name, args.mode, pairs_prof / launches_ev) if ws == 1 else None,
-                "kernel": "event stage = chain_dense_kernel + offsets_kernel + segbase_kernel + emit_kernel "
+                "kernel": f"event stage = {CHAIN_KERNEL[c.method]} + offsets_kernel + segbase_kernel + emit kernel "
                           "(one push_frames call)",
                 "algorithmic_bytes_per_frame": round(b_alg_band), "frames_per_launch": round(pairs_prof / launches_ev, 2),
                 "algorithmic_bytes_per_launch": round(bytes_per_launch), "avg_launch_ms": round(ms_per_launch, 5),
@@ -663,13 +714,13 @@ def run_ours(args):
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         pairs = cpu_pairs_for(c, threads)
-        p, dt, kind, cc, hh = cpu_sample(c, cfg, arm.frames[0], arm.ts, threads, pairs)
+        p, dt, kind, cc, hh = cpu_sample(c, cfg, arm.cpu_frames, arm.ts, threads, pairs)
         cpu = {"value": round(p / dt, 4), "unit": "frames/s", "cores": threads, "kind": kind,
                "sample": f"{c.name} stream 0, frames 0-{p} ({p} intervals), {threads} host threads "
                          f"(evsim_ref_run_sequence, output = one streaming Simulator), {dt:.1f} s",
                "parity": sample_parity(golden_entry(c, args, p + 1), cc, hh)}
         p1 = 2 if c.pixels >= 2_000_000 else 8
-        p, dt, kind, cc, hh = cpu_sample(c, cfg, arm.frames[0], arm.ts, 1, p1)
+        p, dt, kind, cc, hh = cpu_sample(c, cfg, arm.cpu_frames, arm.ts, 1, p1)
         cpu1 = {"value": round(p / dt, 4), "unit": "frames/s", "cores": 1, "kind": kind,
                 "sample": f"{c.name} stream 0, frames 0-{p}, one reference Simulator (single thread), {dt:.1f} s"}
 
@@ -679,7 +730,10 @@ def run_ours(args):
             "metric": METRIC, "value": round(value, 3), "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "u8/f32/f64", "data": "synthetic",
-            "config": {**config_json(c, args, n, split, ws, n_streams), "frames_per_push": arm.batch},
+            "config": {**config_json(c, args, n, split, ws, n_streams), "frames_per_push": arm.batch,
+                       **({"stacked_streams": f"{len(arm.streams)} streams stacked into one {c.width}x{arm.H} "
+                                              "simulator per rank (parallel.stack_streams, exact for difference_only)"}
+                          if arm.stacked else {})},
             "parity": parity, "timed_output_check": timed_check,
             "parity_ref": "tests/golden/sequences.json (compiled reference, per-frame count + checksum)",
             "events_per_s": round(events_per_s, 1), "events_per_frame": round(E_frame, 1),
@@ -713,17 +767,18 @@ def run_e2e(arm, args, ws, n_streams, fmt, steps, max_calls=None):
     from paper_2209_04634_b200.simulator import WireBuffer
     c, n, P = arm.c, arm.n, arm.P
     h_frames = [torch.from_numpy(f).pin_memory() for f in arm.frames]
-    rows = (arm.band[1] - arm.band[0]) if arm.band else c.height
+    H = arm.H
+    rows = (arm.band[1] - arm.band[0]) if arm.band else H
     # a streamed / device call holds <= max_batch frames; a wire call's launches
     # are chunks of <= max_batch pairs, so one call can take the sequence
-    per_call = n if fmt == "wire" else min(n, arm.sims[0].max_batch(c.width, c.height))
+    per_call = n if fmt == "wire" else min(n, arm.sims[0].max_batch(c.width, H))
     calls = [(a, min(per_call, n - a)) for a in range(0, n, per_call)][:max_calls]
     pairs_per_step = sum(nb for _, nb in calls) - 1
     cap = (c.n_interp + 1) * c.width * rows * per_call
     bufs = []
     for s in arm.sims:
         if fmt == "wire":
-            bufs.append(WireBuffer.for_call(s, per_call, c.width, c.height, rows=rows))
+            bufs.append(WireBuffer.for_call(s, per_call, c.width, H, rows=rows))
         elif fmt == "packed":
             bufs.append(torch.empty(cap, dtype=torch.int32).pin_memory())
         else:
@@ -736,14 +791,14 @@ def run_e2e(arm, args, ws, n_streams, fmt, steps, max_calls=None):
         for a, nb in calls:
             ptr = h_frames[i].data_ptr() + a * P
             if fmt == "wire":
-                bufs[i].run(s, ptr, nb, c.width, c.height, arm.ts[a:a + nb], chunk=args.chunk)
+                bufs[i].run(s, ptr, nb, c.width, H, arm.ts[a:a + nb], chunk=args.chunk)
                 d2h += bufs[i].bytes
             elif fmt == "packed":
-                e = s.push_frames_streamed_ptr(ptr, nb, c.width, c.height, arm.ts[a:a + nb], bufs[i].data_ptr(),
+                e = s.push_frames_streamed_ptr(ptr, nb, c.width, H, arm.ts[a:a + nb], bufs[i].data_ptr(),
                                                cap, chunk=args.chunk)
                 d2h += 4 * int(e.n_events) + 16 * (int(e.n_segments) + 1)
             else:
-                e = s.push_frames_device(ptr, nb, c.width, c.height, arm.ts[a:a + nb], on_device=False, sync=True)
+                e = s.push_frames_device(ptr, nb, c.width, H, arm.ts[a:a + nb], on_device=False, sync=True)
                 ev = np.empty(max(int(e.n_events), 1), dtype=[("b", "V24")])
                 s.copy_events(ev.ctypes.data, int(e.n_events), 1)
                 d2h += 24 * int(e.n_events) + 16 * (int(e.n_segments) + 1)

@@ -13,7 +13,9 @@ import threading
 from .abi import CConfig, CEvents, CWire
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libevsim_gpu.so")
+# EVSIM_GPU_LIB=checked loads the bounds-checked build (build.py checked=True)
+LIB_PATH = os.path.join(HERE, "libevsim_gpu_checked.so" if os.environ.get("EVSIM_GPU_LIB") == "checked"
+                        else "libevsim_gpu.so")
 
 _lock = threading.Lock()
 _lib = None
@@ -83,7 +85,7 @@ def load(build_if_missing: bool = True):
             return _lib
         if not os.path.exists(LIB_PATH) and build_if_missing:
             from .build import build
-            build()
+            build(checked=LIB_PATH.endswith("_checked.so"))
         if not os.path.exists(LIB_PATH):
             raise RuntimeError(f"CUDA library missing: {LIB_PATH} (run paper_2209_04634_b200/build.py)")
         lib = ctypes.CDLL(LIB_PATH)

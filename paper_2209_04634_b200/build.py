@@ -15,6 +15,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libevsim_gpu.so")
+# bounds-checked variant (-DEVSIM_CHECKED: device-side checks of the kernels'
+# global writes, evsim_device.cuh EVSIM_CHECK); loaded when EVSIM_GPU_LIB=checked
+OUT_CHECKED = os.path.join(HERE, "libevsim_gpu_checked.so")
 SOURCES = ["evsim_gpu.cu", "flow_kernels.cu", "event_kernels.cu", "io_kernels.cu", "wire_kernels.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
@@ -26,15 +29,15 @@ FLAGS = [
 ]
 
 
-def _stale() -> bool:
-    if not os.path.exists(OUT):
+def _stale(out: str = OUT) -> bool:
+    if not os.path.exists(out):
         return True
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "evsim_gpu.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
     """Compile under an exclusive file lock (torchrun ranks may all call this)
     and publish the library with an atomic rename, so no process ever loads a
     half-written .so."""
@@ -43,20 +46,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with open(os.path.join(HERE, "build", ".lock"), "w") as lk:
         fcntl.flock(lk, fcntl.LOCK_EX)
         try:
-            if not force and not _stale():
-                return OUT
-            return _build(verbose)
+            out = OUT_CHECKED if checked else OUT
+            if not force and not _stale(out):
+                return out
+            return _build(verbose, checked)
         finally:
             fcntl.flock(lk, fcntl.LOCK_UN)
 
 
-def _build(verbose: bool) -> str:
-    objdir = os.path.join(HERE, "build")
+def _build(verbose: bool, checked: bool = False) -> str:
+    objdir = os.path.join(HERE, "build_checked" if checked else "build")
+    out = OUT_CHECKED if checked else OUT
+    flags = FLAGS + (["-DEVSIM_CHECKED"] if checked else [])
     os.makedirs(objdir, exist_ok=True)
 
     def compile_one(src):
         obj = os.path.join(objdir, src.replace(".cu", ".o"))  # (serialised by the build lock)
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *flags, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
@@ -68,14 +74,14 @@ def _build(verbose: bool) -> str:
         for _, log in results:
             sys.stderr.write(log)
     objs = [o for o, _ in results]
-    tmp = f"{OUT}.{os.getpid()}.tmp"
+    tmp = f"{out}.{os.getpid()}.tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
            "-Xcompiler", "-fPIC"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stderr}")
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

@@ -305,7 +305,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) chain_kernel(ChainParams p) {
           for (int l = 0; l < L; ++l)
 #pragma unroll
             for (int q = 0; q < kW; ++q)
-              if (have[q]) p.masks[(size_t)(gbase + l) * p.n_words + wi[q]] = make_uint2(0u, 0u);
+              if (have[q]) {
+                EVSIM_CHECK((size_t)(gbase + l) * p.n_words + wi[q] < p.masks_cap, "chain mask store");
+                p.masks[(size_t)(gbase + l) * p.n_words + wi[q]] = make_uint2(0u, 0u);
+              }
         continue;
       }
       Prov prov[kW];
@@ -351,6 +354,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) chain_kernel(ChainParams p) {
             const unsigned bp = __ballot_sync(kFull, pos);
             const unsigned bn = __ballot_sync(kFull, neg);
             if (!have[q]) continue;
+            EVSIM_CHECK((size_t)g * p.n_words + wi[q] < p.masks_cap, "chain mask store");
             if (lane == 0) p.masks[(size_t)g * p.n_words + wi[q]] = make_uint2(bp, bn);
             if (kMag) {
               const int m = (pos || neg) ? mult : 0;
@@ -379,7 +383,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) chain_kernel(ChainParams p) {
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < G; i += blockDim.x) p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
+  for (int i = threadIdx.x; i < G; i += blockDim.x) {
+    EVSIM_CHECK((size_t)i * p.n_blocks + b < p.counts_cap, "chain count store");
+    p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
+  }
 }
 
 // ------------------------------------------------------------ dense chain kernel
@@ -741,6 +748,7 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
           for (int q = 0; q < kW; ++q) {
             if (!c[q].have) continue;
             const uint2 m = s_stm[warp][q][j];
+            EVSIM_CHECK((size_t)g * p.n_words + c[q].wi < p.masks_cap, "dense chain mask store");
             p.masks[(size_t)g * p.n_words + c[q].wi] = m;
             if (kMag) p.wcount[(size_t)g * p.n_words + c[q].wi] = s_stw[warp][q][j];
             else cnt += __popc(m.x | m.y);  // a pixel crosses one way or not at all
@@ -812,7 +820,106 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < G; i += blockDim.x) p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
+  for (int i = threadIdx.x; i < G; i += blockDim.x) {
+    EVSIM_CHECK((size_t)i * p.n_blocks + b < p.counts_cap, "chain count store");
+    p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
+  }
+}
+
+// ------------------------------------------------------------ difference_only chain
+//
+// chain_kernel specialised for difference_only (N = 0, one link per pair:
+// prev -> curr, simulate.cpp:322-327 -> core.cpp:5-46) in single mode.  A
+// warp owns one 32-pixel word and walks the launch's pairs in order (the log
+// state / the previous value stay in registers); the frame bytes of kP pairs
+// are loaded together before they are chained, so kP loads are in flight per
+// warp — the chain is a pure stream over the frames.  The log rule uses the
+// per-level thresholds (dense_rule_th), the linear one the biased-value
+// difference; masks are staged per warp and stored 32 links at a time, as in
+// the dense chain.
+template <bool kLog, int kP>
+__global__ void __launch_bounds__(256) chain_diff_kernel(ChainParams p) {
+  extern __shared__ uint32_t s_cnt[];  // [n_pairs] event counts of this block
+  __shared__ float s_lut[kLog ? 256 : 1];
+  __shared__ int2 s_th[kLog ? 256 : 1];
+  constexpr int kStage = 32 + kP;
+  __shared__ uint2 s_stm[kWarpsPerBlock][kStage];
+  const int G = p.n_pairs;
+  for (int i = threadIdx.x; i < G; i += blockDim.x) s_cnt[i] = 0;
+  if (kLog) {
+    s_lut[threadIdx.x] = p.lut[threadIdx.x];
+    s_th[threadIdx.x] = make_int2(p.lthr[threadIdx.x].x, p.lthr[threadIdx.x].y);
+  }
+  __syncthreads();
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t th_b = pin((uint32_t)__cvta_generic_to_shared(s_th) - ((uint32_t)kVB << 3));
+  const int64_t wbeg = (int64_t)b * p.words_per_block;
+  const int64_t wend = min(wbeg + p.words_per_block, p.n_words);
+  for (int64_t wi = wbeg + warp; wi < wend; wi += kWarpsPerBlock) {
+    const int row = (int)((uint32_t)wi / (uint32_t)p.wpr);
+    const int x = (int)(wi - (int64_t)row * p.wpr) * 32 + lane;
+    const bool valid = x < p.w;
+    const size_t pix = (size_t)(p.row0 + row) * p.w + (valid ? x : p.w - 1);
+    int before = 0, thh = INT_MAX, thl = INT_MIN, vr = kVB;
+    int sp = p.r0 % p.R;
+    if (kLog) {
+      if (valid) {
+        const float ref = p.ref[pix];
+        int r = 0;  // the level with L[r] == ref (see chain_dense_kernel)
+#pragma unroll
+        for (int st = 128; st >= 1; st >>= 1)
+          if (s_lut[r + st] <= ref) r += st;
+        const int2 t = s_th[r];
+        thh = t.x;
+        thl = t.y;
+        vr = kVB + r;
+      }
+    } else {
+      before = kVB + (int)__ldg(p.frames.at(sp) + pix);
+    }
+    int fbase = 0;
+    for (int i0 = 0; i0 < G; i0 += kP) {
+      int vals[kP];
+#pragma unroll
+      for (int j = 0; j < kP; ++j) {
+        sp = sp + 1 == p.R ? 0 : sp + 1;  // curr of pair i0 + j
+        vals[j] = i0 + j < G ? kVB + (int)__ldg(p.frames.at(sp) + pix) : 0;
+      }
+#pragma unroll
+      for (int j = 0; j < kP; ++j) {
+        if (i0 + j >= G) break;
+        uint2 m;
+        if (kLog) {
+          m = dense_rule_th(th_b, vals[j], thh, thl, vr);
+        } else {
+          const int d = vals[j] - before;  // difference_frame, core.cpp:14-15
+          m = make_uint2(__ballot_sync(kFull, d > p.c_pos && valid), __ballot_sync(kFull, d < p.c_neg && valid));
+          before = vals[j];
+        }
+        if (lane == 0) s_stm[warp][i0 + j - fbase] = m;
+      }
+      const int lend = min(i0 + kP, G);
+      if (lend - fbase >= 32 || lend == G) {  // store the staged links' masks
+        __syncwarp();
+        for (int j = lane; j < lend - fbase; j += 32) {
+          const uint2 m = s_stm[warp][j];
+          EVSIM_CHECK((size_t)(fbase + j) * p.n_words + wi < p.masks_cap, "diff chain mask store");
+          p.masks[(size_t)(fbase + j) * p.n_words + wi] = m;
+          const uint32_t cnt = __popc(m.x | m.y);
+          if (cnt) atomicAdd(&s_cnt[fbase + j], cnt);
+        }
+        __syncwarp();
+        fbase = lend;
+      }
+    }
+    if (kLog && valid) p.ref[pix] = s_lut[vr - kVB];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G; i += blockDim.x) {
+    EVSIM_CHECK((size_t)i * p.n_blocks + b < p.counts_cap, "chain count store");
+    p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
+  }
 }
 
 // ------------------------------------------------------------ lerp quads
@@ -955,9 +1062,11 @@ __global__ void __launch_bounds__(256, 3) chain_sparse_kernel(ChainParams p) {
 #pragma unroll
           for (int q = 0; q < kW; ++q) {
             if (!c[q].have) continue;
+            EVSIM_CHECK((size_t)g * p.n_words + c[q].wi < p.masks_cap, "sparse chain mask store");
             p.masks[(size_t)g * p.n_words + c[q].wi] = lm[q];
             if (kMag) p.wcount[(size_t)g * p.n_words + c[q].wi] = lwc[q];
           }
+          EVSIM_CHECK((size_t)g * p.n_blocks + blk < p.counts_cap, "sparse chain count");
           if (lcnt) atomicAdd(&p.counts[(size_t)g * p.n_blocks + blk], lcnt);
         }
         lcnt = 0;
@@ -1152,6 +1261,7 @@ __global__ void __launch_bounds__(256, 3) chain_diffinterp_kernel(ChainParams p)
 #pragma unroll
           for (int q = 0; q < kW; ++q) {
             if (!c[q].have) continue;
+            EVSIM_CHECK((size_t)g * p.n_words + c[q].wi < p.masks_cap, "sparse chain mask store");
             p.masks[(size_t)g * p.n_words + c[q].wi] = lm[q];
             if (kMag) p.wcount[(size_t)g * p.n_words + c[q].wi] = lwc[q];
           }
@@ -1246,7 +1356,10 @@ __global__ void __launch_bounds__(256, 3) chain_diffinterp_kernel(ChainParams p)
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < G; i += blockDim.x) p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
+  for (int i = threadIdx.x; i < G; i += blockDim.x) {
+    EVSIM_CHECK((size_t)i * p.n_blocks + b < p.counts_cap, "chain count store");
+    p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
+  }
 }
 
 // ------------------------------------------------------------ offsets
@@ -1552,23 +1665,25 @@ __global__ void __launch_bounds__(256) emit_single_kernel(EmitParams p, const in
                                                           int blocks_per_tile, int g0) {
   __shared__ __align__(16) uint32_t s_ev[256 * 32 + 4];
   __shared__ int s_warp[kWarpsPerBlock];
-  const int S = *p.seg.n_segs;
-  if (p.seg_out[1 + 2 * S] > p.capacity) return;  // host grows the buffer and re-emits
   const int g = g0 + blockIdx.y;
   const int b0 = blockIdx.x * blocks_per_tile;
   const int64_t w0 = (int64_t)b0 * p.words_per_block;
   const int64_t w1 = min(w0 + (int64_t)blocks_per_tile * p.words_per_block, p.n_words);
   const int64_t w = w0 + threadIdx.x;
-  uint32_t all = 0, neg = 0;
-  if (w < w1) {
-    const uint2 m = p.masks[(size_t)g * p.n_words + w];
-    all = m.x | m.y;
-    neg = m.y;
-  }
+  // every independent load first (their latencies overlap): the word's masks,
+  // the tile's output offset, and the capacity check's segment count
+  uint2 m = make_uint2(0u, 0u);
+  if (w < w1) m = p.masks[(size_t)g * p.n_words + w];
+  const int64_t tile_off = segbase[g] + p.prefix[(size_t)g * p.n_blocks + b0];
+  const int S = *p.seg.n_segs;
+  const uint32_t all = m.x | m.y, neg = m.y;
   int total;
   const int excl = block_exclusive_scan(__popc(all), s_warp, total);
   if (total == 0) return;  // uniform
-  uint32_t* dst = p.out + segbase[g] + p.prefix[(size_t)g * p.n_blocks + b0];
+  if (p.seg_out[1 + 2 * S] > p.capacity) return;  // host grows the buffer and re-emits
+  uint32_t* dst = p.out + tile_off;
+  EVSIM_CHECK(tile_off >= 0 && tile_off + total <= p.capacity, "emit tile within the event buffer");
+  EVSIM_CHECK(total <= 256 * 32, "emit staging size");
   const int shift = (int)(((uintptr_t)dst >> 2) & 3u);  // dst alignment mod 16 B, in events
   if (all) {
     // descending pixels (FLO = the highest set bit), written back to front;
@@ -1969,6 +2084,14 @@ void launch_chain(const ChainParams& p, int provider, cudaStream_t s) {
       }
       return;
     }
+  }
+  if (provider == kProvNone && !p.magnitude && p.d.n_links == 1 && p.n_interp == 0 && !p.skip_empty &&
+      (size_t)p.n_pairs * sizeof(uint32_t) <= 48 * 1024) {
+    // difference_only: the streaming chain
+    const size_t sm = (size_t)p.n_pairs * sizeof(uint32_t);
+    if (p.log_mode) chain_diff_kernel<true, 16><<<p.n_blocks, 256, sm, s>>>(p);
+    else chain_diff_kernel<false, 16><<<p.n_blocks, 256, sm, s>>>(p);
+    return;
   }
   switch (provider) {
     case kProvDenseGrid: launch_chain_mode<DenseProvider<false>>(p, s); break;

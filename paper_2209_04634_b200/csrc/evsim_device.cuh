@@ -7,8 +7,31 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 
 namespace evsim_gpu {
+
+// Checked build (build.py --checked -> libevsim_gpu_checked.so, -DEVSIM_CHECKED):
+// bounds checks of the kernels' global writes against their buffers' sizes
+// and of the staging indices; a violation prints the site and traps (the
+// context is lost, so the calling test fails loudly).  compute-sanitizer is
+// not available on the GPU pool; tests/test_checked_build.py runs the GPU
+// parity subset on this build instead.  Compiled out otherwise.
+#ifdef EVSIM_CHECKED
+#define EVSIM_CHECK(cond, what)                                                                            \
+  do {                                                                                                     \
+    if (!(cond)) {                                                                                         \
+      printf("EVSIM_CHECKED: %s violated at %s:%d (block %d,%d,%d thread %d)\n", what, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z, (int)threadIdx.x);                         \
+      __trap();                                                                                            \
+    }                                                                                                      \
+  } while (0)
+#else
+#define EVSIM_CHECK(cond, what) \
+  do {                          \
+  } while (0)
+#endif
+
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 

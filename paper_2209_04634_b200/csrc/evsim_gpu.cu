@@ -989,6 +989,8 @@ struct evsim_gpu_sim {
     c.mcount = ev.mcount.as<uint16_t>();
     c.wcount = ev.wcount.as<uint32_t>();
     c.counts = ev.counts.as<uint32_t>();
+    c.masks_cap = (size_t)ev.max_links * (size_t)ev.n_words;
+    c.counts_cap = (size_t)ev.max_links * (size_t)ev.n_blocks;
     c.sched = ev.sched.as<unsigned int>();
     return c;
   }

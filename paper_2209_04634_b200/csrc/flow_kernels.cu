@@ -720,6 +720,7 @@ __global__ void __launch_bounds__(kLKThreads) dense_lk_warp_kernel(DenseLKParams
     }
   }
   if (lane < kPW && valid) {
+    EVSIM_CHECK(pi >= 0 && pi < g.ncx && pj >= 0 && pj < g.ncy, "LK patch-grid store");
     g.pu[(size_t)pj * g.ncx + pi] = u;
     g.pv[(size_t)pj * g.ncx + pi] = v;
   }

@@ -186,6 +186,8 @@ struct ChainParams {
   uint32_t* wcount;        // magnitude: [g][n_words]
   uint32_t* counts;        // [g][n_blocks] events per block
   unsigned int* sched;     // sparse chain: device task counter (zeroed by the launch)
+  size_t masks_cap;        // elements of masks / counts (checked build: EVSIM_CHECK)
+  size_t counts_cap;
 };
 
 struct OffsetParams {

@@ -262,3 +262,50 @@ def close_shared(ptr: int, device: int) -> None:
 
     from . import _lib
     _lib.check(_lib.load().evsim_gpu_ipc_close(device, ctypes.c_void_p(ptr)))
+
+
+# --------------------------------------------------------------------------- stacked streams
+
+def stack_streams(frames: Sequence[np.ndarray]) -> np.ndarray:
+    """S streams of (n, h, w) frames -> (n, S*h, w): frame k of the stack is
+    stream 0's frame k on rows [0, h), stream 1's on [h, 2h), ...
+
+    For difference_only (no flow, every pixel its own chain,
+    simulate.cpp:322-327 -> core.cpp:5-46) one simulator over the stacked frame
+    IS S independent simulators: the per-pixel rule never looks at a
+    neighbour, and within one timestamp the reference orders events by
+    (y, x) (types.hpp:64-69), so each segment of the stacked stream is
+    stream 0's events, then stream 1's, ... — the same structure as row bands.
+    All streams must share their timestamps.  This turns S small streams into
+    one launch sequence (the batched c1 workload)."""
+    arr = np.stack([np.asarray(f, np.uint8) for f in frames], axis=1)  # (n, S, h, w)
+    n, S, h, w = arr.shape
+    return np.ascontiguousarray(arr.reshape(n, S * h, w))
+
+
+def split_stacked(packed: np.ndarray, seg_t: np.ndarray, seg_off: np.ndarray, n_streams: int, height: int) -> list:
+    """The stacked stream's packed records (bits 0-15 x, 16-30 y, 31 negative)
+    and segment table -> per stream (packed records with y - s*height, seg_t,
+    seg_off).  Within a segment the records are ordered by y, so stream s's
+    records are the run with s*height <= y < (s+1)*height."""
+    packed = np.asarray(packed, np.uint32)
+    seg_off = np.asarray(seg_off, np.int64)
+    y = (packed >> np.uint32(16)) & np.uint32(0x7FFF)
+    stream = (y // np.uint32(height)).astype(np.int64)
+    out = []
+    S = len(seg_t)
+    # per segment, the boundaries of each stream's run (searchsorted on the
+    # nondecreasing stream index inside the segment)
+    bounds = np.zeros((S, n_streams + 1), np.int64)
+    for k in range(S):
+        a, b = int(seg_off[k]), int(seg_off[k + 1])
+        bounds[k] = a + np.searchsorted(stream[a:b], np.arange(n_streams + 1), side="left")
+    for s in range(n_streams):
+        idx = np.concatenate([np.arange(bounds[k, s], bounds[k, s + 1]) for k in range(S)]) if S else np.zeros(0, int)
+        rec = packed[idx].copy()
+        rec = (rec & np.uint32(0x8000FFFF)) | (((y[idx] - np.uint32(s * height)) & np.uint32(0x7FFF)) << np.uint32(16))
+        counts = bounds[:, s + 1] - bounds[:, s]
+        keep = counts > 0
+        off = np.concatenate([[0], np.cumsum(counts[keep])]).astype(np.int64)
+        out.append((rec, np.asarray(seg_t, np.int64)[keep], off))
+    return out
