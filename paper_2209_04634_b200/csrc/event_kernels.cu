@@ -876,15 +876,17 @@ __global__ void __launch_bounds__(256) chain_diff_kernel(ChainParams p) {
         vr = kVB + r;
       }
     } else {
-      before = kVB + (int)__ldg(p.frames.at(sp) + pix);
+      before = kVB + (int)__ldg((p.dcurr ? p.dprev : p.frames.at(sp)) + pix);
     }
+    const uint8_t* dc = p.dcurr ? p.dcurr + pix : nullptr;  // direct: pair i's curr at dc + i*P
     int fbase = 0;
     for (int i0 = 0; i0 < G; i0 += kP) {
       int vals[kP];
 #pragma unroll
       for (int j = 0; j < kP; ++j) {
         sp = sp + 1 == p.R ? 0 : sp + 1;  // curr of pair i0 + j
-        vals[j] = i0 + j < G ? kVB + (int)__ldg(p.frames.at(sp) + pix) : 0;
+        const uint8_t* src = dc ? dc + (size_t)(i0 + j) * p.P : p.frames.at(sp) + pix;
+        vals[j] = i0 + j < G ? kVB + (int)__ldg(src) : 0;
       }
 #pragma unroll
       for (int j = 0; j < kP; ++j) {
@@ -920,6 +922,207 @@ __global__ void __launch_bounds__(256) chain_diff_kernel(ChainParams p) {
     EVSIM_CHECK((size_t)i * p.n_blocks + b < p.counts_cap, "chain count store");
     p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
   }
+}
+
+// ---- TMA-staged form -------------------------------------------------------
+// The same chain with the frames staged in shared memory: a block walks its
+// words in chunks of kTW (8 warps x kWPW words); for every pair of the
+// launch one thread bulk-copies the chunk's rows of the pair's curr frame
+// (cp.async.bulk global -> shared, 16-byte aligned range, completion on an
+// mbarrier) into a kNB-deep ring of stage buffers, kNB frames ahead of the
+// warps, which read their bytes with LDS.  One contiguous copy per (chunk,
+// frame) instead of one 32-byte gather per (word, frame): the frames stream
+// from HBM in long runs.  Needs 16-byte aligned frames (P % 16 == 0, aligned
+// base): chain_diff_tma_ok().
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "fence.proxy.async.shared::cta;\n"
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n"
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+constexpr int kDiffWPW = 8;                           // words per warp per chunk
+constexpr int kDiffTW = kWarpsPerBlock * kDiffWPW;   // words per chunk
+constexpr int kDiffNB = 4;                            // frames in flight per block
+
+template <bool kLog>
+__global__ void __launch_bounds__(256) chain_diff_tma_kernel(ChainParams p, int stage_bytes) {
+  extern __shared__ __align__(128) uint8_t s_raw[];  // [kDiffNB][stage_bytes] frames, then [n_pairs] counts
+  __shared__ float s_lut[kLog ? 256 : 1];
+  __shared__ int2 s_th[kLog ? 256 : 1];
+  __shared__ __align__(8) uint64_t s_bar[kDiffNB];
+  __shared__ uint2 s_stm[kWarpsPerBlock][kDiffWPW][32 + 1];
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_raw + (size_t)kDiffNB * stage_bytes);
+  const int G = p.n_pairs;
+  for (int i = threadIdx.x; i < G; i += blockDim.x) s_cnt[i] = 0;
+  if (kLog) {
+    s_lut[threadIdx.x] = p.lut[threadIdx.x];
+    s_th[threadIdx.x] = make_int2(p.lthr[threadIdx.x].x, p.lthr[threadIdx.x].y);
+  }
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(s_bar);
+  const uint32_t buf0 = (uint32_t)__cvta_generic_to_shared(s_raw);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kDiffNB; ++k) mbar_init(bar0 + 8 * k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t th_b = pin((uint32_t)__cvta_generic_to_shared(s_th) - ((uint32_t)kVB << 3));
+  const int64_t wbeg = (int64_t)b * p.words_per_block;
+  const int64_t wend = min(wbeg + p.words_per_block, p.n_words);
+  const int n_chunks = (int)((wend - wbeg + kDiffTW - 1) / kDiffTW);
+  const int64_t total = (int64_t)n_chunks * G;  // (chunk, pair) copies of this block, in order
+  // the byte range [a0, a0 + bytes) of chunk c's rows in a frame (16-aligned)
+  auto range = [&](int c, size_t& a0, uint32_t& bytes) {
+    const int64_t cw0 = wbeg + (int64_t)c * kDiffTW, cw1 = min(cw0 + kDiffTW, wend);
+    const size_t r0 = (size_t)(p.row0 + (int)((uint32_t)cw0 / (uint32_t)p.wpr));
+    const size_t r1 = (size_t)(p.row0 + (int)((uint32_t)(cw1 - 1) / (uint32_t)p.wpr)) + 1;
+    a0 = (r0 * (size_t)p.w) & ~(size_t)15;
+    bytes = (uint32_t)((((r1 * (size_t)p.w) + 15) & ~(size_t)15) - a0);
+  };
+  // producer (thread 0): copy t = (chunk pc, pair pi) into stage t % kDiffNB;
+  // its chunk's range and the pair's ring slot advance incrementally
+  int64_t pt = 0;
+  int pc = 0, pi = 0, pslot = 0;
+  size_t pa0 = 0;
+  uint32_t pbytes = 0;
+  auto issue_next = [&]() {
+    if (pi == 0) {
+      range(pc, pa0, pbytes);
+      pslot = p.r0 + 1;
+      while (pslot >= p.R) pslot -= p.R;
+    }
+    const uint8_t* f = p.dcurr ? p.dcurr + (size_t)pi * p.P : p.frames.at(pslot);
+    const int st = (int)(pt & (kDiffNB - 1));
+    bulk_load(buf0 + (uint32_t)st * (uint32_t)stage_bytes, f + pa0, pbytes, bar0 + 8 * st);
+    ++pt;
+    if (++pi == G) {
+      pi = 0;
+      ++pc;
+    }
+    if (++pslot == p.R) pslot = 0;
+  };
+  if (threadIdx.x == 0)
+    while (pt < total && pt < kDiffNB) issue_next();
+  int64_t t = 0;
+  for (int c = 0; c < n_chunks; ++c) {
+    size_t a0;
+    uint32_t bytes;
+    range(c, a0, bytes);
+    const int64_t cw0 = wbeg + (int64_t)c * kDiffTW;
+    int64_t wq[kDiffWPW];
+    uint32_t off[kDiffWPW];
+    bool have[kDiffWPW], valid[kDiffWPW];
+    int before[kDiffWPW], thh[kDiffWPW], thl[kDiffWPW], vr[kDiffWPW];
+#pragma unroll
+    for (int q = 0; q < kDiffWPW; ++q) {
+      wq[q] = cw0 + q * kWarpsPerBlock + warp;
+      have[q] = wq[q] < wend;
+      const int64_t ww = have[q] ? wq[q] : cw0;
+      const int row = (int)((uint32_t)ww / (uint32_t)p.wpr);
+      const int x = (int)(ww - (int64_t)row * p.wpr) * 32 + lane;
+      valid[q] = have[q] && x < p.w;
+      const size_t pix = (size_t)(p.row0 + row) * p.w + (x < p.w ? x : p.w - 1);
+      off[q] = (uint32_t)(pix - a0);
+      before[q] = 0;
+      thh[q] = INT_MAX;
+      thl[q] = INT_MIN;
+      vr[q] = kVB;
+      if (kLog) {
+        if (valid[q]) {
+          const float ref = p.ref[pix];
+          int r = 0;
+#pragma unroll
+          for (int s2 = 128; s2 >= 1; s2 >>= 1)
+            if (s_lut[r + s2] <= ref) r += s2;
+          const int2 tt = s_th[r];
+          thh[q] = tt.x;
+          thl[q] = tt.y;
+          vr[q] = kVB + r;
+        }
+      } else {
+        before[q] = kVB + (int)__ldg((p.dcurr ? p.dprev : p.frames.at(p.r0 % p.R)) + pix);
+      }
+    }
+    int fbase = 0;
+    for (int i = 0; i < G; ++i, ++t) {
+      const int st = (int)(t & (kDiffNB - 1));
+      mbar_wait(bar0 + 8 * st, (uint32_t)((t / kDiffNB) & 1));
+      const uint8_t* sb = s_raw + (size_t)st * stage_bytes;
+#pragma unroll
+      for (int q = 0; q < kDiffWPW; ++q) {
+        const int val = kVB + (int)sb[off[q]];
+        uint2 m;
+        if (kLog) {
+          m = dense_rule_th(th_b, val, thh[q], thl[q], vr[q]);
+        } else {
+          const int d = val - before[q];  // difference_frame, core.cpp:14-15
+          m = make_uint2(__ballot_sync(kFull, d > p.c_pos && valid[q]), __ballot_sync(kFull, d < p.c_neg && valid[q]));
+          before[q] = val;
+        }
+        if (lane == 0) s_stm[warp][q][i - fbase] = m;
+      }
+      __syncthreads();  // every warp is done with stage st
+      if (threadIdx.x == 0 && pt < total) issue_next();
+      if (i + 1 - fbase == 32 || i + 1 == G) {  // store the staged links' masks
+        const int n = i + 1 - fbase;
+        if (lane < n) {
+#pragma unroll
+          for (int q = 0; q < kDiffWPW; ++q) {
+            if (!have[q]) continue;
+            const uint2 m = s_stm[warp][q][lane];
+            EVSIM_CHECK((size_t)(fbase + lane) * p.n_words + wq[q] < p.masks_cap, "diff chain mask store");
+            p.masks[(size_t)(fbase + lane) * p.n_words + wq[q]] = m;
+            const uint32_t cnt = __popc(m.x | m.y);
+            if (cnt) atomicAdd(&s_cnt[fbase + lane], cnt);
+          }
+        }
+        __syncwarp();
+        fbase = i + 1;
+      }
+    }
+    if (kLog) {
+#pragma unroll
+      for (int q = 0; q < kDiffWPW; ++q)
+        if (valid[q]) p.ref[(size_t)off[q] + a0] = s_lut[vr[q] - kVB];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G; i += blockDim.x) {
+    EVSIM_CHECK((size_t)i * p.n_blocks + b < p.counts_cap, "chain count store");
+    p.counts[(size_t)i * p.n_blocks + b] = s_cnt[i];
+  }
+}
+
+// bytes of one stage buffer: the rows kDiffTW words can span, 16-aligned on both ends
+static int diff_stage_bytes(const ChainParams& p) {
+  const int rows = (kDiffTW + p.wpr - 1) / p.wpr + 1;
+  return (int)((((size_t)rows * p.w + 32) + 127) & ~(size_t)127);
+}
+
+static bool chain_diff_tma_ok(const ChainParams& p) {
+  const uintptr_t base = p.dcurr ? (uintptr_t)p.dcurr : (uintptr_t)p.frames.base;
+  const size_t stride = p.dcurr ? p.P : p.frames.stride;
+  if ((base & 15) || (stride & 15) || (p.dprev && ((uintptr_t)p.dprev & 15))) return false;
+  const size_t sm = (size_t)kDiffNB * diff_stage_bytes(p) + (size_t)p.n_pairs * 4;
+  return sm <= 160 * 1024;
 }
 
 // ------------------------------------------------------------ lerp quads
@@ -1662,59 +1865,71 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
 // the < 16-byte head and tail go out as plain stores.  The tile starts at
 // segbase[g] + the chain's per-(link, block) exclusive prefix.
 __global__ void __launch_bounds__(256) emit_single_kernel(EmitParams p, const int64_t* __restrict__ segbase,
-                                                          int blocks_per_tile, int g0) {
+                                                          int blocks_per_tile, int g0, int g1, int links_per_block) {
   __shared__ __align__(16) uint32_t s_ev[256 * 32 + 4];
   __shared__ int s_warp[kWarpsPerBlock];
-  const int g = g0 + blockIdx.y;
+  const int ga = g0 + (int)blockIdx.y * links_per_block, gb = min(ga + links_per_block, g1);
   const int b0 = blockIdx.x * blocks_per_tile;
   const int64_t w0 = (int64_t)b0 * p.words_per_block;
   const int64_t w1 = min(w0 + (int64_t)blocks_per_tile * p.words_per_block, p.n_words);
   const int64_t w = w0 + threadIdx.x;
-  // every independent load first (their latencies overlap): the word's masks,
-  // the tile's output offset, and the capacity check's segment count
-  uint2 m = make_uint2(0u, 0u);
-  if (w < w1) m = p.masks[(size_t)g * p.n_words + w];
-  const int64_t tile_off = segbase[g] + p.prefix[(size_t)g * p.n_blocks + b0];
+  const bool in = w < w1;
+  // a block emits one tile of words for links [ga, gb): the tile geometry,
+  // the capacity check and the word's (x, y) once; each link's masks and
+  // output offset are loaded one link ahead
   const int S = *p.seg.n_segs;
-  const uint32_t all = m.x | m.y, neg = m.y;
-  int total;
-  const int excl = block_exclusive_scan(__popc(all), s_warp, total);
-  if (total == 0) return;  // uniform
+  const uint32_t row = p.wdiv.div((uint32_t)(in ? w : w0));
+  const uint32_t xy = ((uint32_t)(in ? w : w0) - row * (uint32_t)p.wpr) * 32u | ((uint32_t)(p.row0 + (int)row) << 16);
+  uint2 m_next = in ? p.masks[(size_t)ga * p.n_words + w] : make_uint2(0u, 0u);
+  int64_t off_next = segbase[ga] + p.prefix[(size_t)ga * p.n_blocks + b0];
   if (p.seg_out[1 + 2 * S] > p.capacity) return;  // host grows the buffer and re-emits
-  uint32_t* dst = p.out + tile_off;
-  EVSIM_CHECK(tile_off >= 0 && tile_off + total <= p.capacity, "emit tile within the event buffer");
-  EVSIM_CHECK(total <= 256 * 32, "emit staging size");
-  const int shift = (int)(((uintptr_t)dst >> 2) & 3u);  // dst alignment mod 16 B, in events
-  if (all) {
-    // descending pixels (FLO = the highest set bit), written back to front;
-    // n1 = neg rotated right by 1, so rotr(n1, b) holds pixel b's polarity
-    // at bit 31
-    const uint32_t row = p.wdiv.div((uint32_t)w);
-    const uint32_t xy = ((uint32_t)w - row * (uint32_t)p.wpr) * 32u | ((uint32_t)(p.row0 + (int)row) << 16);
-    const uint32_t n1 = __funnelshift_r(neg, neg, 1);
-    uint32_t m = all;
-    uint32_t* o = s_ev + shift + excl + __popc(all) - 1;
-    do {
-      uint32_t b;
-      asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(m));  // FLO: the highest set bit
-      m ^= 1u << b;
-      *o-- = (xy + b) | (__funnelshift_r(n1, n1, b) & 0x80000000u);
-    } while (m);
-  }
-  __syncthreads();
-  const int head = min(total, (4 - shift) & 3);
-  const int nbody = (total - head) & ~3;
-  if ((int)threadIdx.x < head) dst[threadIdx.x] = s_ev[shift + threadIdx.x];
-  const int t0 = head + nbody;
-  if ((int)threadIdx.x >= 32 && (int)threadIdx.x - 32 < total - t0)
-    dst[t0 + threadIdx.x - 32] = s_ev[shift + t0 + threadIdx.x - 32];
-  if (threadIdx.x == 0 && nbody > 0) {
-    const uint32_t src = (uint32_t)__cvta_generic_to_shared(s_ev + shift + head);
-    asm volatile("fence.proxy.async.shared::cta;\n"
-                 "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
-                 "cp.async.bulk.commit_group;\n"
-                 "cp.async.bulk.wait_group.read 0;\n" ::"l"(dst + head), "r"(src), "r"(nbody * 4)
-                 : "memory");
+  for (int g = ga; g < gb; ++g) {
+    const uint2 m = m_next;
+    const int64_t tile_off = off_next;
+    if (g + 1 < gb) {
+      m_next = in ? p.masks[(size_t)(g + 1) * p.n_words + w] : make_uint2(0u, 0u);
+      off_next = segbase[g + 1] + p.prefix[(size_t)(g + 1) * p.n_blocks + b0];
+    }
+    const uint32_t all = m.x | m.y, neg = m.y;
+    int total;
+    // (the scan's barriers also order the previous link's staged reads, which
+    // thread 0 finished waiting for, before this link's writes)
+    const int excl = block_exclusive_scan(__popc(all), s_warp, total);
+    if (total == 0) continue;  // uniform
+    uint32_t* dst = p.out + tile_off;
+    EVSIM_CHECK(tile_off >= 0 && tile_off + total <= p.capacity, "emit tile within the event buffer");
+    EVSIM_CHECK(total <= 256 * 32, "emit staging size");
+    const int shift = (int)(((uintptr_t)dst >> 2) & 3u);  // dst alignment mod 16 B, in events
+    if (all) {
+      // descending pixels (FLO = the highest set bit), written back to front;
+      // n1 = neg rotated right by 1, so rotr(n1, b) holds pixel b's polarity
+      // at bit 31
+      const uint32_t n1 = __funnelshift_r(neg, neg, 1);
+      uint32_t mm = all;
+      uint32_t* o = s_ev + shift + excl + __popc(all) - 1;
+      do {
+        uint32_t bit;
+        asm("bfind.u32 %0, %1;" : "=r"(bit) : "r"(mm));  // FLO: the highest set bit
+        mm ^= 1u << bit;
+        *o-- = (xy + bit) | (__funnelshift_r(n1, n1, bit) & 0x80000000u);
+      } while (mm);
+    }
+    __syncthreads();
+    const int head = min(total, (4 - shift) & 3);
+    const int nbody = (total - head) & ~3;
+    if ((int)threadIdx.x < head) dst[threadIdx.x] = s_ev[shift + threadIdx.x];
+    const int t0 = head + nbody;
+    if ((int)threadIdx.x >= 32 && (int)threadIdx.x - 32 < total - t0)
+      dst[t0 + threadIdx.x - 32] = s_ev[shift + t0 + threadIdx.x - 32];
+    if (threadIdx.x == 0 && nbody > 0) {
+      const uint32_t src = (uint32_t)__cvta_generic_to_shared(s_ev + shift + head);
+      asm volatile("fence.proxy.async.shared::cta;\n"
+                   "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                   "cp.async.bulk.commit_group;\n"
+                   "cp.async.bulk.wait_group.read 0;\n" ::"l"(dst + head), "r"(src), "r"(nbody * 4)
+                   : "memory");
+    }
+    __syncthreads();  // head / tail lanes and the bulk copy are done with s_ev
   }
 }
 
@@ -2089,6 +2304,18 @@ void launch_chain(const ChainParams& p, int provider, cudaStream_t s) {
       (size_t)p.n_pairs * sizeof(uint32_t) <= 48 * 1024) {
     // difference_only: the streaming chain
     const size_t sm = (size_t)p.n_pairs * sizeof(uint32_t);
+    static const bool no_tma = [] {
+      const char* e = std::getenv("EVSIM_DIFF_NO_TMA");
+      return e && e[0] == '1';
+    }();
+    if (!no_tma && chain_diff_tma_ok(p)) {
+      const int sb = diff_stage_bytes(p);
+      const size_t smt = (size_t)kDiffNB * sb + sm;
+      auto* k = p.log_mode ? chain_diff_tma_kernel<true> : chain_diff_tma_kernel<false>;
+      set_max_dynamic_smem((const void*)k, 160 * 1024);
+      k<<<p.n_blocks, 256, smt, s>>>(p, sb);
+      return;
+    }
     if (p.log_mode) chain_diff_kernel<true, 16><<<p.n_blocks, 256, sm, s>>>(p);
     else chain_diff_kernel<false, 16><<<p.n_blocks, 256, sm, s>>>(p);
     return;
@@ -2127,7 +2354,13 @@ bool launch_emit_single(const EmitParams& p, int64_t* segbase, int g0, int g1, c
   segbase_kernel<<<1, 1024, 0, s>>>(p, segbase);
   const int bpt = std::max(1, 256 / p.words_per_block);
   const int tiles = (p.n_blocks + bpt - 1) / bpt;
-  emit_single_kernel<<<dim3((unsigned)tiles, (unsigned)(g1 - g0)), 256, 0, s>>>(p, segbase, bpt, g0);
+  // links per block: enough blocks to fill the GPU a few times over, each
+  // amortising its setup over up to 8 links
+  const int n_links = g1 - g0;
+  int lpb = 1;
+  while (lpb < 8 && (int64_t)tiles * ((n_links + 2 * lpb - 1) / (2 * lpb)) >= 148 * 16) lpb *= 2;
+  const int ys = (n_links + lpb - 1) / lpb;
+  emit_single_kernel<<<dim3((unsigned)tiles, (unsigned)ys), 256, 0, s>>>(p, segbase, bpt, g0, g1, lpb);
   return true;
 }
 

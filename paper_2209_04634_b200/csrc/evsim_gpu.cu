@@ -1211,8 +1211,12 @@ struct evsim_gpu_sim {
     cudaStream_t ps = xc ? s_flow : stream;  // upload wait + pyramid
     begin_group();
     mark(EVSIM_STAGE_UPLOAD);
+    // difference_only from device memory: the chain reads the caller's frames
+    // in place and only the last one is kept in the ring (the next push's prev)
+    const bool direct = on_device && !uploaded && !profiling && cfg.method == EVSIM_METHOD_DIFFERENCE_ONLY &&
+                        !magnitude() && n_interp_eff() == 0;
     if (uploaded) CK(cudaStreamWaitEvent(ps, uploaded, 0));
-    else upload(pixels, F, base, on_device, stream);
+    else if (!direct) upload(pixels, F, base, on_device, stream);
     mark(EVSIM_STAGE_PYRAMID);
     bool quad_side = false;
     if (use_quadf()) {
@@ -1263,7 +1267,8 @@ struct evsim_gpu_sim {
     if (!has_prev && log_mode()) {
       // warm-up frame: ref := L(frame0)
       if (xc) CK(cudaStreamWaitEvent(stream, uploaded, 0));
-      launch_init_ref(frames.as<uint8_t>() + (size_t)base * P, lut.as<float>(), ref.as<float>(), (int64_t)P, stream);
+      launch_init_ref(direct ? pixels : frames.as<uint8_t>() + (size_t)base * P, lut.as<float>(), ref.as<float>(),
+                      (int64_t)P, stream);
       CK_LAUNCH("init_ref");
       ++launches;
     }
@@ -1278,6 +1283,10 @@ struct evsim_gpu_sim {
     }
     if (n_pairs > 0) {
       ChainParams c = chain_params(r0, n_pairs);
+      if (direct) {
+        c.dprev = has_prev ? frames.as<uint8_t>() + (size_t)rhead * P : pixels;
+        c.dcurr = has_prev ? pixels : pixels + P;
+      }
       int provider = kProvNone;
       std::vector<int> sub;
       if (dense_flow()) {
@@ -1338,6 +1347,9 @@ struct evsim_gpu_sim {
       }
       pending = false;
     }
+    if (direct)  // the last frame into its ring slot (the next push's prev)
+      CK(cudaMemcpyAsync(frames.as<uint8_t>() + (size_t)((base + F - 1) % R) * P, pixels + (size_t)(F - 1) * P, P,
+                         cudaMemcpyDeviceToDevice, stream));
     end_group();
     rhead = (base + F - 1) % R;
     prev_t = ts[F - 1];

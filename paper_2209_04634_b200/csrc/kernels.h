@@ -141,6 +141,10 @@ struct ChainParams {
   Ring<const uint8_t> frames;
   Ring<const uint32_t> quads;  // u8 quad images (dense provider)
   Ring<const float4> quadf;    // dense chain: fp32 lerp quads of the same frames (base null: the u8 form)
+  // difference_only device pushes read the caller's frames in place:
+  // pair i = (i ? dcurr + (i-1)*P : dprev, dcurr + i*P); null = the ring
+  const uint8_t* dcurr;
+  const uint8_t* dprev;
   float magic_y;               // dense chain: Y truncation magic 2^23 + m_y (exact integer float)
   uint32_t qshift;             // dense chain: (bits(2^23 + m_y) * w + bits(2^23)) mod 2^32, + w*h <= 2^32
   // dense provider, grid form (level-0 patch grid + tables; per-pair pu/pv)
