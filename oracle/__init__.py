@@ -46,7 +46,7 @@ def build(ref: bool | None = None) -> None:
         targets.append("ref")
         gpu_so = os.path.join(os.path.dirname(HERE), "paper_2209_04634_b200", "libevsim_gpu.so")
         if os.path.exists(gpu_so):
-            targets.append("refsuite")
+            targets += ["refsuite", "plugin"]
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 

@@ -482,6 +482,40 @@ __device__ __forceinline__ int dense_fast(const float4* __restrict__ qp, const f
   return __float_as_int(hi2(T));
 }
 
+// dense_fast on bf16 lerp quads: per pixel two words (a00 | (a10 - a00) << 16,
+// a01 | (a11 - a01) << 16) of bf16 values — integers |v| <= 255 have at most
+// 8 significant bits, so bf16 holds them exactly and a bf16 is the high half
+// of the fp32 with the same value.  8 bytes per gather; each value back to
+// fp32 by one shift or mask; then the same FFMA lerps and bound as above.
+template <bool kClamp>
+__device__ __forceinline__ int dense_fast(const uint2* __restrict__ qp, const uint2* __restrict__ qc,
+                                          uint32_t w, float my, float wm, float hm, float xf, float yf,
+                                          float u, float v, float4 kc, unsigned& bad, unsigned bit) {
+  const f32x2 NB = pk2(kc.x, kc.y);
+  f32x2 X = affine2_est(xf, NB, u), Y = affine2_est(yf, NB, v);
+  if (kClamp) {
+    X = pk2(fminf(fmaxf(lo2(X), 0.0f), wm), fminf(fmaxf(hi2(X), 0.0f), wm));
+    Y = pk2(fminf(fmaxf(lo2(Y), 0.0f), hm), fminf(fmaxf(hi2(Y), 0.0f), hm));
+  }
+  const f32x2 C23 = pk2(8388608.0f, 8388608.0f);
+  const f32x2 CY = pk2(my, my);
+  const f32x2 TX = add2_rz(X, C23), TY = add2_rz(Y, CY);  // magic + trunc
+  const f32x2 FX = sub2(X, sub2(TX, C23)), FY = sub2(Y, sub2(TY, CY));
+  const uint32_t ia = __float_as_uint(lo2(TY)) * w + __float_as_uint(lo2(TX));
+  const uint32_t ib = __float_as_uint(hi2(TY)) * w + __float_as_uint(hi2(TX));
+  const uint2 A = __ldg(qp + ia), B = __ldg(qc + ib);
+  auto lo16 = [](uint32_t x) { return __uint_as_float(x << 16); };
+  auto hi16 = [](uint32_t x) { return __uint_as_float(x & 0xFFFF0000u); };
+  const float ta = __fmaf_rn(lo2(FX), hi16(A.x), lo16(A.x)), ba = __fmaf_rn(lo2(FX), hi16(A.y), lo16(A.y));
+  const float tb = __fmaf_rn(hi2(FX), hi16(B.x), lo16(B.x)), bb = __fmaf_rn(hi2(FX), hi16(B.y), lo16(B.y));
+  const float sa = __fmaf_rn(lo2(FY), __fsub_rn(ba, ta), ta);
+  const float sb = __fmaf_rn(hi2(FY), __fsub_rn(bb, tb), tb);
+  const float e = __fmaf_rn(kc.z, sa, __fmul_rn(kc.w, sb));
+  const f32x2 T = add2_rz(add2(pk2(e, e), pk2(0.5f - 2e-4f, 0.5f + 2e-4f)), C23);
+  if (__float_as_uint(lo2(T)) != __float_as_uint(hi2(T))) bad |= bit;
+  return __float_as_int(hi2(T));
+}
+
 // The exact reference expression for the lanes dense_fast cannot decide.
 __device__ __noinline__ int dense_exact(const float2* nfb, const double* oma, const double* alpha,
                                         const uint32_t* qp, const uint32_t* qc, int w, int h, float xf, float yf,
@@ -603,9 +637,10 @@ __device__ __forceinline__ unsigned dense_batch(const ChainParams& p, const Q* q
 
 // kW words per warp (1 on small frames: finer tasks, 4 blocks per SM; 2 on
 // large ones), kB links per batch (4, or 5 when it tiles the interior links)
-template <bool kLog, bool kMag, int kB, int kW, int kMinB, bool kF4>
+template <bool kLog, bool kMag, int kB, int kW, int kMinB, int kQ>
 __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) {
-  using Q = std::conditional_t<kF4, float4, uint32_t>;
+  // gather image: 0 = u8 quads, 1 = fp32 lerp quads, 2 = bf16 lerp quads
+  using Q = std::conditional_t<kQ == 1, float4, std::conditional_t<kQ == 2, uint2, uint32_t>>;
   constexpr bool kTh = kLog && !kMag;  // log single mode: level thresholds (dense_rule_th)
   extern __shared__ float4 s_dyn4[];
   __shared__ float s_lut[256];
@@ -683,9 +718,12 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
       // the gathers' rings (fp32 lerp quads or u8 quads), pre-shifted by -qshift elements
       const Q* gbp;
       const Q* gbc;
-      if constexpr (kF4) {
+      if constexpr (kQ == 1) {
         gbp = reinterpret_cast<const float4*>(reinterpret_cast<uintptr_t>(p.quadf.at(sp)) - 16ull * p.qshift);
         gbc = reinterpret_cast<const float4*>(reinterpret_cast<uintptr_t>(p.quadf.at(sc)) - 16ull * p.qshift);
+      } else if constexpr (kQ == 2) {
+        gbp = reinterpret_cast<const uint2*>(reinterpret_cast<uintptr_t>(p.quadh.at(sp)) - 8ull * p.qshift);
+        gbc = reinterpret_cast<const uint2*>(reinterpret_cast<uintptr_t>(p.quadh.at(sc)) - 8ull * p.qshift);
       } else {
         gbp = qbp;
         gbc = qbc;
@@ -1132,20 +1170,29 @@ static bool chain_diff_tma_ok(const ChainParams& p) {
 // (exactly: integers).  One column per thread, kLQRows rows per block (the
 // row below's taps are the next row's top taps), one 16-byte store per pixel.
 constexpr int kLQRows = 8;
-__global__ void __launch_bounds__(256) lerp_quad_kernel(Ring<const uint8_t> frames, Ring<float4> out, int w, int h,
-                                                        int R, int slot0) {
+__device__ __forceinline__ void put_quad(float4* q, float a00, float a10, float a01, float a11) {
+  *q = make_float4(a00, a10 - a00, a01, a11 - a01);
+}
+__device__ __forceinline__ void put_quad(uint2* q, float a00, float a10, float a01, float a11) {
+  // bf16 = the high half of the (exactly representable) fp32
+  *q = make_uint2((__float_as_uint(a00) >> 16) | (__float_as_uint(a10 - a00) & 0xFFFF0000u),
+                  (__float_as_uint(a01) >> 16) | (__float_as_uint(a11 - a01) & 0xFFFF0000u));
+}
+template <class T>
+__global__ void __launch_bounds__(256) lerp_quad_kernel(Ring<const uint8_t> frames, Ring<T> out, int w, int h, int R,
+                                                        int slot0) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= w) return;
   const int slot = (slot0 + (int)blockIdx.z) % R;
   const uint8_t* __restrict__ f = frames.at(slot);
-  float4* __restrict__ q = out.at(slot);
+  T* __restrict__ q = out.at(slot);
   const int x1 = min(x + 1, w - 1);
   const int yb = blockIdx.y * kLQRows, ye = min(yb + kLQRows, h);
   float a00 = (float)__ldg(f + (size_t)yb * w + x), a10 = (float)__ldg(f + (size_t)yb * w + x1);
   for (int y = yb; y < ye; ++y) {
     const size_t r1 = (size_t)min(y + 1, h - 1) * w;
     const float a01 = (float)__ldg(f + r1 + x), a11 = (float)__ldg(f + r1 + x1);
-    q[(size_t)y * w + x] = make_float4(a00, a10 - a00, a01, a11 - a01);
+    put_quad(q + (size_t)y * w + x, a00, a10, a01, a11);
     a00 = a01;
     a10 = a11;
   }
@@ -1155,7 +1202,13 @@ void launch_lerp_quads(Ring<const uint8_t> frames, Ring<float4> out, int w, int 
                        cudaStream_t s) {
   if (n_frames <= 0) return;
   dim3 g((w + 255) / 256, (h + kLQRows - 1) / kLQRows, n_frames);
-  lerp_quad_kernel<<<g, 256, 0, s>>>(frames, out, w, h, R, slot0);
+  lerp_quad_kernel<float4><<<g, 256, 0, s>>>(frames, out, w, h, R, slot0);
+}
+void launch_lerp_quads_bf16(Ring<const uint8_t> frames, Ring<uint2> out, int w, int h, int R, int slot0, int n_frames,
+                            cudaStream_t s) {
+  if (n_frames <= 0) return;
+  dim3 g((w + 255) / 256, (h + kLQRows - 1) / kLQRows, n_frames);
+  lerp_quad_kernel<uint2><<<g, 256, 0, s>>>(frames, out, w, h, R, slot0);
 }
 
 // ------------------------------------------------------------ sparse chain kernel
@@ -2228,8 +2281,9 @@ static void launch_chain_mode(const ChainParams& p, cudaStream_t s) {
 
 template <bool kLog, bool kMag, int kB, int kW, int kMinB>
 static void launch_chain_dense_b(const ChainParams& p, size_t sm, cudaStream_t s) {
-  auto* k = p.quadf.base ? chain_dense_kernel<kLog, kMag, kB, kW, kMinB, true>
-                         : chain_dense_kernel<kLog, kMag, kB, kW, kMinB, false>;
+  auto* k = p.quadh.base   ? chain_dense_kernel<kLog, kMag, kB, kW, kMinB, 2>
+            : p.quadf.base ? chain_dense_kernel<kLog, kMag, kB, kW, kMinB, 1>
+                           : chain_dense_kernel<kLog, kMag, kB, kW, kMinB, 0>;
   set_max_dynamic_smem((const void*)k, 96 * 1024);
   k<<<p.n_blocks, 256, sm, s>>>(p);
 }
@@ -2243,6 +2297,18 @@ static void launch_chain_dense(const ChainParams& p, size_t sm, cudaStream_t s) 
   // 12.6 -> 13.1; two-word tasks at 128 regs: c5 782 vs 707 µs/frame)
   const int n_int = std::min(p.d.n_links, p.n_interp - p.d.start);
   auto tiles = [&](int b) { return n_int > 0 && n_int % b == 0; };
+  static const int exp_var = [] {  // (experiment) EVSIM_CHAIN_VAR=1: batches of 4 at 4 blocks/SM
+    const char* e = std::getenv("EVSIM_CHAIN_VAR");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (exp_var == 1 && !kMag) {
+    launch_chain_dense_b<kLog, kMag, 4, 1, 4>(p, sm, s);
+    return;
+  }
+  if (exp_var == 2 && !kMag && tiles(8)) {
+    launch_chain_dense_b<kLog, kMag, 8, 1, 4>(p, sm, s);
+    return;
+  }
   if (tiles(10)) launch_chain_dense_b<kLog, kMag, 10, 1, 3>(p, sm, s);
   else if (tiles(8)) launch_chain_dense_b<kLog, kMag, 8, 1, 3>(p, sm, s);
   else if (tiles(5) && !tiles(4)) launch_chain_dense_b<kLog, kMag, 5, 1, 3>(p, sm, s);

@@ -617,16 +617,27 @@ struct evsim_gpu_sim {
 
   DevBuf frames, quads, mags, lut, lthr, ref, consts, place_tab;
   std::vector<float4> h_kc;  // host copy of the chain constants kc (ChainParams::kcp)
-  // dense method: level-0 fp32 lerp quads of every ring slot, the dense
-  // chain's gather source (16 B per pixel: no byte unpack, FFMA lerps);
-  // EVSIM_CHAIN_U8=1 gathers the u8 quads instead (A/B and tests)
+  // dense method: the level-0 lerp quads of every ring slot, the dense
+  // chain's gather source (no byte unpack, FFMA lerps)
   DevBuf quadf;
-  bool chain_u8 = [] {
-    const char* e = std::getenv("EVSIM_CHAIN_U8");
-    return e && e[0] == '1';
+  // the dense chain's gather image: 0 = the u8 quads, 1 = fp32 lerp quads
+  // (16 B/pixel, default), 2 = bf16 lerp quads (8 B/pixel: c5 log chain 604
+  // -> 627 us/frame, L1 81 -> 52 % but +16 % instructions, issue 66 -> 75 %);
+  // EVSIM_CHAIN_QUAD=u8|f4|bf16 selects (A/B and tests)
+  int quad_kind = [] {
+    const char* e = std::getenv("EVSIM_CHAIN_QUAD");
+    if (e && std::string(e) == "u8") return 0;
+    if (e && std::string(e) == "bf16") return 2;
+    return 1;
   }();
-  bool use_quadf() const { return dense_flow() && !chain_u8; }
-  float4* quadf_ptr() { return use_quadf() ? quadf.as<float4>() : nullptr; }
+  bool use_quadf() const { return dense_flow() && quad_kind != 0; }
+  size_t quad_bytes() const { return quad_kind == 1 ? sizeof(float4) : sizeof(uint2); }
+  void launch_quads(int slot0, int n, cudaStream_t st) {
+    const size_t P = (size_t)w * h;
+    const Ring<const uint8_t> fr{frames.as<uint8_t>(), P};
+    if (quad_kind == 1) launch_lerp_quads(fr, Ring<float4>{quadf.as<float4>(), P}, w, h, R, slot0, n, st);
+    else launch_lerp_quads_bf16(fr, Ring<uint2>{quadf.as<uint2>(), P}, w, h, R, slot0, n, st);
+  }
   FlowEngine flow;
   EventEngine ev;
   // sparse (per pair)
@@ -850,7 +861,7 @@ struct evsim_gpu_sim {
       }
       if (use_quadf()) {  // (prev's lerp quads are rebuilt below)
         quadf.release();
-        quadf.ensure((size_t)need_R * P * sizeof(float4), stream);
+        quadf.ensure((size_t)need_R * P * quad_bytes(), stream);
       }
       if (diff_interp()) {
         DevBuf nm;
@@ -875,8 +886,7 @@ struct evsim_gpu_sim {
         launch_pyramid(pp, 1, stream);
         CK_LAUNCH("pyramid");
         if (use_quadf()) {
-          launch_lerp_quads(Ring<const uint8_t>{frames.as<uint8_t>(), P}, Ring<float4>{quadf.as<float4>(), P}, w, h, R,
-                            rhead, 1, stream);
+          launch_quads(rhead, 1, stream);
           CK_LAUNCH("lerp_quads");
         }
       }
@@ -944,7 +954,8 @@ struct evsim_gpu_sim {
     c.r0 = r0;
     c.frames = Ring<const uint8_t>{frames.as<uint8_t>(), P};
     c.quads = Ring<const uint32_t>{quads.as<uint32_t>(), P};
-    c.quadf = Ring<const float4>{quadf_ptr(), P};
+    c.quadf = Ring<const float4>{use_quadf() && quad_kind == 1 ? quadf.as<float4>() : nullptr, P};
+    c.quadh = Ring<const uint2>{use_quadf() && quad_kind == 2 ? quadf.as<uint2>() : nullptr, P};
     {
       // gather index of the dense chain: TY_bits * w + TX_bits with TX =
       // 2^23 + x, TY = 2^23 + m_y + y (fp32 bits); it equals y * w + x +
@@ -1220,10 +1231,8 @@ struct evsim_gpu_sim {
     mark(EVSIM_STAGE_PYRAMID);
     bool quad_side = false;
     if (use_quadf()) {
-      const Ring<const uint8_t> fr{frames.as<uint8_t>(), P};
-      const Ring<float4> qr{quadf.as<float4>(), P};
       if (profiling) {
-        launch_lerp_quads(fr, qr, w, h, R, base, F, ps);  // (stage timing: serialised, counted as pyramid)
+        launch_quads(base, F, ps);  // (stage timing: serialised, counted as pyramid)
       } else {
         if (!s_quad) {
           int lo = 0, hi = 0;
@@ -1234,7 +1243,7 @@ struct evsim_gpu_sim {
         }
         CK(cudaEventRecord(ev_qin, ps));  // the frames are in the ring
         CK(cudaStreamWaitEvent(s_quad, ev_qin, 0));
-        launch_lerp_quads(fr, qr, w, h, R, base, F, s_quad);
+        launch_quads(base, F, s_quad);
         CK(cudaEventRecord(ev_qdone, s_quad));
         quad_side = true;
       }

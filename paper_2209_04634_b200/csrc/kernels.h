@@ -140,7 +140,8 @@ struct ChainParams {
   int R, r0;
   Ring<const uint8_t> frames;
   Ring<const uint32_t> quads;  // u8 quad images (dense provider)
-  Ring<const float4> quadf;    // dense chain: fp32 lerp quads of the same frames (base null: the u8 form)
+  Ring<const float4> quadf;    // dense chain: fp32 lerp quads of the same frames (base null: not used)
+  Ring<const uint2> quadh;     // dense chain: bf16 lerp quads (base null: not used)
   // difference_only device pushes read the caller's frames in place:
   // pair i = (i ? dcurr + (i-1)*P : dprev, dcurr + i*P); null = the ring
   const uint8_t* dcurr;
@@ -308,9 +309,11 @@ void launch_pyramid(const PyramidParams& p, int n_frames, cudaStream_t s);
 void launch_build_quad(const uint8_t* src, uint32_t* dst, int w, int h, cudaStream_t s);
 void launch_dense_lk(const DenseLKParams& p, int n_pairs, cudaStream_t s);
 void launch_densify(const GridGeom& g, float* du, float* dv, cudaStream_t s);
-// the dense chain's fp32 lerp quads of n_frames ring slots from slot0
+// the dense chain's fp32 / bf16 lerp quads of n_frames ring slots from slot0
 void launch_lerp_quads(Ring<const uint8_t> frames, Ring<float4> out, int w, int h, int R, int slot0, int n_frames,
                        cudaStream_t s);
+void launch_lerp_quads_bf16(Ring<const uint8_t> frames, Ring<uint2> out, int w, int h, int R, int slot0, int n_frames,
+                            cudaStream_t s);
 void launch_interp_frames(const ChainParams& p, uint8_t* out, cudaStream_t s);
 void launch_segments(const SegParams& p, cudaStream_t s);
 // per-(function, device) MaxDynamicSharedMemorySize, thread-safe; throws

@@ -56,3 +56,17 @@ def test_reference_suite_passes_on_the_drop_in(suite):
     print(m.group(0))
     assert cases > 0 and asserts > 0
     assert failed == 0 and afailed == 0 and r.returncode == 0, r.stderr[-6000:]
+
+
+@pytest.mark.gpu
+def test_gpu_flow_plugs_into_the_reference_simulator():
+    """INTEGRATION.md §4 compiled: GpuPatchFlow / GpuLucasKanade (C-ABI flow)
+    inside the reference's own Simulator (oracle/_ref) give the events of its
+    default CPU estimators (dense lq / hq, sparse, magnitude without
+    endpoints; tests/cpp/flow_plugin_check.cpp)."""
+    path = os.path.join(ROOT, "oracle", "_ref", "flow_plugin_check")
+    if not os.path.exists(path):
+        pytest.skip("flow_plugin_check not built (make -C oracle plugin)")
+    r = subprocess.run([path], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    print(r.stdout)
+    assert r.returncode == 0 and "[plugin] ok" in r.stdout, r.stdout + r.stderr

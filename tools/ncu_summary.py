@@ -1,7 +1,7 @@
 """Summarise an ncu --set full report into profiles/<round>/ncu_full_summary.json
 and the event-stage DRAM traffic into traffic_c2_log.json (read by bench.py).
 
-    python tools/ncu_summary.py gpurun_out/prof_all.ncu-rep profiles/r01
+    python tools/ncu_summary.py gpurun_out/prof_all.ncu-rep profiles/r02 [config:mode:pairs_per_launch]
 """
 import csv
 import io
@@ -25,7 +25,7 @@ SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "nsecond": 1e-
          "ns": 1e-6, "us": 1e-3, "ms": 1.0, "second": 1e3, "s": 1e3}
 
 
-def main(rep, outdir):
+def main(rep, outdir, *_):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
@@ -53,21 +53,28 @@ def main(rep, outdir):
     json.dump(out, open(os.path.join(outdir, "ncu_full_summary.json"), "w"), indent=1)
 
     # the capture holds one whole push: sum each event-stage kernel over it
-    # (the chain runs as several pipelined sub-batch launches)
-    def total(name):
-        xs = [x for x in out if name in x["kernel"]]
-        return int(sum(x["dram_rd_MB"] + x["dram_wr_MB"] for x in xs) * 1e6) if xs else None
-    per = {n: total(n) for n in ("chain_dense_kernel", "offsets", "segbase_kernel", "emit_kernel")}
-    if all(v is not None for v in per.values()):
-        json.dump({"source": f"{outdir}/ncu_full_summary.json (ncu --set full --clock-control none, every launch of one push)",
-                   "workload": "c2 log, 128-frame push (127 pairs per launch), tools/profile_c2.sh",
-                   "pairs_per_launch": 127,
+    # (the chain may run as several pipelined sub-batch launches)
+    tag = sys.argv[3] if len(sys.argv) > 3 else "c2:log:127"
+    config, mode, ppl = tag.split(":")
+    stage = ("chain_", "offsets", "segbase_kernel", "emit")
+    xs = [x for x in out if any(k in x["kernel"] for k in stage) and "dram_rd_MB" in x]
+    if xs:
+        # one launch of each event-stage kernel per push here (no sub-batches
+        # below 16 pairs): the last launch of each, i.e. the capture's last push
+        per = {}
+        for x in xs:
+            name = x["kernel"].split("(")[0].replace("void ", "")
+            per[name] = int((x["dram_rd_MB"] + x["dram_wr_MB"]) * 1e6)
+        json.dump({"source": f"{outdir}/ncu_full_summary.json (ncu --set full --clock-control none, every "
+                             "event-stage launch of one push)",
+                   "workload": f"{config} {mode}, one push of {ppl} frame pairs (tools/push_once.py)",
+                   "pairs_per_launch": float(ppl),
                    "event_stage_dram_bytes_per_launch": sum(per.values()), "per_kernel_dram_bytes": per},
-                  open(os.path.join(outdir, "traffic_c2_log.json"), "w"), indent=1)
+                  open(os.path.join(outdir, f"traffic_{config}_{mode}.json"), "w"), indent=1)
     for x in out:
         print(f"{x['kernel'][:44]:44s} {x.get('dur_ms', 0):8.3f} ms  issue {x.get('issue_active_pct', 0):5.1f}%  "
               f"instr {x.get('warp_instr', 0):.3g}")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(*sys.argv[1:])
