@@ -2297,15 +2297,11 @@ static void launch_chain_dense(const ChainParams& p, size_t sm, cudaStream_t s) 
   // 12.6 -> 13.1; two-word tasks at 128 regs: c5 782 vs 707 µs/frame)
   const int n_int = std::min(p.d.n_links, p.n_interp - p.d.start);
   auto tiles = [&](int b) { return n_int > 0 && n_int % b == 0; };
-  static const int exp_var = [] {  // (experiment) EVSIM_CHAIN_VAR=1: batches of 4 at 4 blocks/SM
-    const char* e = std::getenv("EVSIM_CHAIN_VAR");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (exp_var == 1 && !kMag) {
-    launch_chain_dense_b<kLog, kMag, 4, 1, 4>(p, sm, s);
-    return;
-  }
-  if (exp_var == 2 && !kMag && tiles(8)) {
+  // log single mode, batches of 8: 4 blocks/SM at 64 registers (the level
+  // thresholds need fewer registers than the fp32 rule; c5 log chain 604 ->
+  // 581 us/frame; the same cap on batches of 4 / 5 / 10 or on linear mode
+  // measured equal or slower: c2 log 10.5 -> 11.8 us/frame at batches of 10)
+  if (kLog && !kMag && tiles(8)) {
     launch_chain_dense_b<kLog, kMag, 8, 1, 4>(p, sm, s);
     return;
   }
