@@ -702,12 +702,13 @@ def run_ours(args):
         fmt = args.e2e_format
         if fmt == "auto":
             fmt = "wire" if wire_is_smaller(c, E_frame) else "packed"
-        e2e = run_e2e(arm, args, ws, n_streams, fmt, args.steps)
+        e2e = run_e2e(arm, args, ws, n_streams, fmt, args.steps, events_per_frame=E_frame)
         # the other host formats, one step each (bounded: the 24-byte records
         # of c5 are 1.6-3.8 GB per frame)
         for other in ("packed", "wire", "event24"):
             if other != fmt and not args.no_e2e_extra:
-                r = run_e2e(arm, args, ws, n_streams, other, 1, max_calls=1 if other == "event24" else None)
+                r = run_e2e(arm, args, ws, n_streams, other, 1, max_calls=1 if other == "event24" else None,
+                            events_per_frame=E_frame)
                 e2e_other[other] = {k: r[k] for k in ("value", "unit", "d2h_bytes_per_step")}
 
     cpu = cpu1 = None
@@ -751,7 +752,7 @@ def run_ours(args):
     return 0
 
 
-def run_e2e(arm, args, ws, n_streams, fmt, steps, max_calls=None):
+def run_e2e(arm, args, ws, n_streams, fmt, steps, max_calls=None, events_per_frame=0.0):
     """Steps through the public C-ABI with pinned host frames in and the
     events on the host (one host thread per handle), host wall clock:
       wire    evsim_gpu_push_frames_wire: planes + polarity bits (lossless,
@@ -772,9 +773,20 @@ def run_e2e(arm, args, ws, n_streams, fmt, steps, max_calls=None):
     # a streamed / device call holds <= max_batch frames; a wire call's launches
     # are chunks of <= max_batch pairs, so one call can take the sequence
     per_call = n if fmt == "wire" else min(n, arm.sims[0].max_batch(c.width, H))
+    # many resident handles (c4: 32 streams): every handle's call buffers
+    # (device chunks, host planes / records) scale with its frames per call;
+    # keep calls at the device pushes' batch and size the packed host records
+    # from the events the device pass produced instead of the every-link-pixel
+    # bound
+    multi = len(arm.sims) > 1
+    if multi:
+        per_call = min(per_call, arm.batch)
+    chunk = args.chunk or (arm.batch if multi else 0)
     calls = [(a, min(per_call, n - a)) for a in range(0, n, per_call)][:max_calls]
     pairs_per_step = sum(nb for _, nb in calls) - 1
     cap = (c.n_interp + 1) * c.width * rows * per_call
+    if multi and events_per_frame:
+        cap = min(cap, int(3 * events_per_frame * per_call) + (1 << 20))
     bufs = []
     for s in arm.sims:
         if fmt == "wire":
@@ -791,11 +803,11 @@ def run_e2e(arm, args, ws, n_streams, fmt, steps, max_calls=None):
         for a, nb in calls:
             ptr = h_frames[i].data_ptr() + a * P
             if fmt == "wire":
-                bufs[i].run(s, ptr, nb, c.width, H, arm.ts[a:a + nb], chunk=args.chunk)
+                bufs[i].run(s, ptr, nb, c.width, H, arm.ts[a:a + nb], chunk=chunk)
                 d2h += bufs[i].bytes
             elif fmt == "packed":
                 e = s.push_frames_streamed_ptr(ptr, nb, c.width, H, arm.ts[a:a + nb], bufs[i].data_ptr(),
-                                               cap, chunk=args.chunk)
+                                               cap, chunk=chunk)
                 d2h += 4 * int(e.n_events) + 16 * (int(e.n_segments) + 1)
             else:
                 e = s.push_frames_device(ptr, nb, c.width, H, arm.ts[a:a + nb], on_device=False, sync=True)
