@@ -482,47 +482,6 @@ __device__ __forceinline__ int dense_fast(const float4* __restrict__ qp, const f
   return __float_as_int(hi2(T));
 }
 
-// dense_fast on the fp32 lerp quads, reusing the previous link's gathers: a
-// warp whose taps did not move since the previous link of the pair (every
-// lane's gather index unchanged — with a smooth flow the taps move every
-// 1/|fwd'u| links, ~2 on c5) skips that side's 16-byte gather and keeps the
-// values in registers (warp-uniform branch, so no L1 traffic at all).  The
-// values are the same bits, so the result is identical to dense_fast.
-template <bool kClamp>
-__device__ __forceinline__ int dense_fast_skip(const float4* __restrict__ qp, const float4* __restrict__ qc,
-                                               uint32_t w, float my, float wm, float hm, float xf, float yf,
-                                               float u, float v, float4 kc, unsigned& bad, unsigned bit,
-                                               uint32_t& ia_prev, uint32_t& ib_prev, float4& A, float4& B) {
-  const f32x2 NB = pk2(kc.x, kc.y);
-  f32x2 X = affine2_est(xf, NB, u), Y = affine2_est(yf, NB, v);
-  if (kClamp) {
-    X = pk2(fminf(fmaxf(lo2(X), 0.0f), wm), fminf(fmaxf(hi2(X), 0.0f), wm));
-    Y = pk2(fminf(fmaxf(lo2(Y), 0.0f), hm), fminf(fmaxf(hi2(Y), 0.0f), hm));
-  }
-  const f32x2 C23 = pk2(8388608.0f, 8388608.0f);
-  const f32x2 CY = pk2(my, my);
-  const f32x2 TX = add2_rz(X, C23), TY = add2_rz(Y, CY);  // magic + trunc
-  const f32x2 FX = sub2(X, sub2(TX, C23)), FY = sub2(Y, sub2(TY, CY));
-  const uint32_t ia = __float_as_uint(lo2(TY)) * w + __float_as_uint(lo2(TX));
-  const uint32_t ib = __float_as_uint(hi2(TY)) * w + __float_as_uint(hi2(TX));
-  if (!__all_sync(kFull, ia == ia_prev)) {
-    A = __ldg(qp + ia);
-    ia_prev = ia;
-  }
-  if (!__all_sync(kFull, ib == ib_prev)) {
-    B = __ldg(qc + ib);
-    ib_prev = ib;
-  }
-  const float ta = __fmaf_rn(lo2(FX), A.y, A.x), ba = __fmaf_rn(lo2(FX), A.w, A.z);
-  const float tb = __fmaf_rn(hi2(FX), B.y, B.x), bb = __fmaf_rn(hi2(FX), B.w, B.z);
-  const float sa = __fmaf_rn(lo2(FY), __fsub_rn(ba, ta), ta);
-  const float sb = __fmaf_rn(hi2(FY), __fsub_rn(bb, tb), tb);
-  const float e = __fmaf_rn(kc.z, sa, __fmul_rn(kc.w, sb));
-  const f32x2 T = add2_rz(add2(pk2(e, e), pk2(0.5f - 2e-4f, 0.5f + 2e-4f)), C23);
-  if (__float_as_uint(lo2(T)) != __float_as_uint(hi2(T))) bad |= bit;
-  return __float_as_int(hi2(T));
-}
-
 // dense_fast on bf16 lerp quads: per pixel two words (a00 | (a10 - a00) << 16,
 // a01 | (a11 - a01) << 16) of bf16 values — integers |v| <= 255 have at most
 // 8 significant bits, so bf16 holds them exactly and a bf16 is the high half
@@ -660,28 +619,18 @@ __device__ __forceinline__ uint2 dense_rule_th(uint32_t th_b, int val, int& thh,
   return make_uint2(bp, bn);
 }
 
-struct GatherCache {  // the skipping gathers' state of one word (dense_fast_skip)
-  uint32_t ia, ib;
-  float4 A, B;
-};
-
-template <int kW, int kNB, bool kClamp, int kBM, class Q, bool kSkip = false>
+template <int kW, int kNB, bool kClamp, int kBM, class Q>
 __device__ __forceinline__ unsigned dense_batch(const ChainParams& p, const Q* qp, const Q* qc,
                                                 uint32_t w, float my, float wm, float hm, const DenseWord* c,
-                                                int k0, int (&vals)[kW][kBM], GatherCache* gc = nullptr) {
+                                                int k0, int (&vals)[kW][kBM]) {
   unsigned bad = 0;
 #pragma unroll
   for (int j = 0; j < kNB; ++j) {
     const float4 kc = p.kcp[k0 + j];
 #pragma unroll
-    for (int q = 0; q < kW; ++q) {
-      if constexpr (kSkip)
-        vals[q][j] = dense_fast_skip<kClamp>(qp, qc, w, my, wm, hm, c[q].xf, c[q].yf, c[q].u, c[q].v, kc, bad,
-                                             1u << (q * kBM + j), gc[q].ia, gc[q].ib, gc[q].A, gc[q].B);
-      else
-        vals[q][j] = dense_fast<kClamp>(qp, qc, w, my, wm, hm, c[q].xf, c[q].yf, c[q].u, c[q].v, kc, bad,
-                                        1u << (q * kBM + j));
-    }
+    for (int q = 0; q < kW; ++q)
+      vals[q][j] = dense_fast<kClamp>(qp, qc, w, my, wm, hm, c[q].xf, c[q].yf, c[q].u, c[q].v, kc, bad,
+                                      1u << (q * kBM + j));
   }
   return bad;
 }
@@ -690,10 +639,8 @@ __device__ __forceinline__ unsigned dense_batch(const ChainParams& p, const Q* q
 // large ones), kB links per batch (4, or 5 when it tiles the interior links)
 template <bool kLog, bool kMag, int kB, int kW, int kMinB, int kQ>
 __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) {
-  // gather image: 0 = u8 quads, 1 = fp32 lerp quads, 2 = bf16 lerp quads,
-  // 3 = fp32 lerp quads with the previous link's gathers reused (dense_fast_skip)
-  constexpr bool kSkip = kQ == 3;
-  using Q = std::conditional_t<kQ == 1 || kQ == 3, float4, std::conditional_t<kQ == 2, uint2, uint32_t>>;
+  // gather image: 0 = u8 quads, 1 = fp32 lerp quads, 2 = bf16 lerp quads
+  using Q = std::conditional_t<kQ == 1, float4, std::conditional_t<kQ == 2, uint2, uint32_t>>;
   constexpr bool kTh = kLog && !kMag;  // log single mode: level thresholds (dense_rule_th)
   extern __shared__ float4 s_dyn4[];
   __shared__ float s_lut[256];
@@ -771,7 +718,7 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
       // the gathers' rings (fp32 lerp quads or u8 quads), pre-shifted by -qshift elements
       const Q* gbp;
       const Q* gbc;
-      if constexpr (kQ == 1 || kQ == 3) {
+      if constexpr (kQ == 1) {
         gbp = reinterpret_cast<const float4*>(reinterpret_cast<uintptr_t>(p.quadf.at(sp)) - 16ull * p.qshift);
         gbc = reinterpret_cast<const float4*>(reinterpret_cast<uintptr_t>(p.quadf.at(sc)) - 16ull * p.qshift);
       } else if constexpr (kQ == 2) {
@@ -784,9 +731,6 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
       PairCtx pc{};
       pc.pu = p.g0.pu + (size_t)i * p.g0.pair_stride;
       pc.pv = p.g0.pv + (size_t)i * p.g0.pair_stride;
-      GatherCache gcache[kW];  // (kSkip) nothing gathered yet for this pair's frames
-#pragma unroll
-      for (int q = 0; q < kW; ++q) gcache[q].ia = gcache[q].ib = 0xFFFFFFFFu;
       bool safe = true;
 #pragma unroll
       for (int q = 0; q < kW; ++q) {
@@ -859,18 +803,14 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_kernel(ChainParams p) 
         int vals[kW][kB];
         unsigned bad;
         if (nb == kB) {
-          bad = safe ? dense_batch<kW, kB, false, kB, Q, kSkip>(p, gbp, gbc, w, my, wm, hm, c, kfirst + l0, vals,
-                                                               gcache)
-                     : dense_batch<kW, kB, true, kB, Q, kSkip>(p, gbp, gbc, w, my, wm, hm, c, kfirst + l0, vals,
-                                                              gcache);
+          bad = safe ? dense_batch<kW, kB, false>(p, gbp, gbc, w, my, wm, hm, c, kfirst + l0, vals)
+                     : dense_batch<kW, kB, true>(p, gbp, gbc, w, my, wm, hm, c, kfirst + l0, vals);
         } else {
           bad = 0;
           for (int j = 0; j < nb; ++j) {
             int v1[kW][kB];
-            bad |= (safe ? dense_batch<kW, 1, false, kB, Q, kSkip>(p, gbp, gbc, w, my, wm, hm, c, kfirst + l0 + j,
-                                                                  v1, gcache)
-                         : dense_batch<kW, 1, true, kB, Q, kSkip>(p, gbp, gbc, w, my, wm, hm, c, kfirst + l0 + j,
-                                                                 v1, gcache))
+            bad |= (safe ? dense_batch<kW, 1, false>(p, gbp, gbc, w, my, wm, hm, c, kfirst + l0 + j, v1)
+                         : dense_batch<kW, 1, true>(p, gbp, gbc, w, my, wm, hm, c, kfirst + l0 + j, v1))
                    << j;
 #pragma unroll
             for (int q = 0; q < kW; ++q)
@@ -2341,11 +2281,9 @@ static void launch_chain_mode(const ChainParams& p, cudaStream_t s) {
 
 template <bool kLog, bool kMag, int kB, int kW, int kMinB>
 static void launch_chain_dense_b(const ChainParams& p, size_t sm, cudaStream_t s) {
-  const bool skip = p.gather_skip != 0;
-  auto* k = p.quadh.base            ? chain_dense_kernel<kLog, kMag, kB, kW, kMinB, 2>
-            : p.quadf.base && skip ? chain_dense_kernel<kLog, kMag, kB, kW, kMinB, 3>
-            : p.quadf.base         ? chain_dense_kernel<kLog, kMag, kB, kW, kMinB, 1>
-                                   : chain_dense_kernel<kLog, kMag, kB, kW, kMinB, 0>;
+  auto* k = p.quadh.base   ? chain_dense_kernel<kLog, kMag, kB, kW, kMinB, 2>
+            : p.quadf.base ? chain_dense_kernel<kLog, kMag, kB, kW, kMinB, 1>
+                           : chain_dense_kernel<kLog, kMag, kB, kW, kMinB, 0>;
   set_max_dynamic_smem((const void*)k, 96 * 1024);
   k<<<p.n_blocks, 256, sm, s>>>(p);
 }
@@ -2363,7 +2301,7 @@ static void launch_chain_dense(const ChainParams& p, size_t sm, cudaStream_t s) 
   // thresholds need fewer registers than the fp32 rule; c5 log chain 604 ->
   // 581 us/frame; the same cap on batches of 4 / 5 / 10 or on linear mode
   // measured equal or slower: c2 log 10.5 -> 11.8 us/frame at batches of 10)
-  if (kLog && !kMag && tiles(8) && !p.gather_skip) {
+  if (kLog && !kMag && tiles(8)) {
     launch_chain_dense_b<kLog, kMag, 8, 1, 4>(p, sm, s);
     return;
   }

@@ -631,12 +631,6 @@ struct evsim_gpu_sim {
     return 1;
   }();
   bool use_quadf() const { return dense_flow() && quad_kind != 0; }
-  // EVSIM_CHAIN_SKIP=1: the dense chain reuses the previous link's gathers
-  // when a warp's taps did not move (dense_fast_skip)
-  int gather_skip = [] {
-    const char* e = std::getenv("EVSIM_CHAIN_SKIP");
-    return e && e[0] == '1' ? 1 : 0;
-  }();
   size_t quad_bytes() const { return quad_kind == 1 ? sizeof(float4) : sizeof(uint2); }
   void launch_quads(int slot0, int n, cudaStream_t st) {
     const size_t P = (size_t)w * h;
@@ -962,7 +956,6 @@ struct evsim_gpu_sim {
     c.quads = Ring<const uint32_t>{quads.as<uint32_t>(), P};
     c.quadf = Ring<const float4>{use_quadf() && quad_kind == 1 ? quadf.as<float4>() : nullptr, P};
     c.quadh = Ring<const uint2>{use_quadf() && quad_kind == 2 ? quadf.as<uint2>() : nullptr, P};
-    c.gather_skip = gather_skip;
     {
       // gather index of the dense chain: TY_bits * w + TX_bits with TX =
       // 2^23 + x, TY = 2^23 + m_y + y (fp32 bits); it equals y * w + x +

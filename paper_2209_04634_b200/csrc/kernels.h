@@ -142,7 +142,6 @@ struct ChainParams {
   Ring<const uint32_t> quads;  // u8 quad images (dense provider)
   Ring<const float4> quadf;    // dense chain: fp32 lerp quads of the same frames (base null: not used)
   Ring<const uint2> quadh;     // dense chain: bf16 lerp quads (base null: not used)
-  int gather_skip;             // dense chain, fp32 quads: reuse the previous link's gathers (dense_fast_skip)
   // difference_only device pushes read the caller's frames in place:
   // pair i = (i ? dcurr + (i-1)*P : dprev, dcurr + i*P); null = the ring
   const uint8_t* dcurr;

@@ -1,6 +1,5 @@
 """GPU: the dense chain's three gather images (EVSIM_CHAIN_QUAD = u8 quads,
-fp32 lerp quads, bf16 lerp quads; EVSIM_CHAIN_SKIP = the fp32 form reusing
-the previous link's gathers) give the same bit-exact
+fp32 lerp quads, bf16 lerp quads) give the same bit-exact
 events as the oracle — pipelined pushes of a c2-like sequence (sub-batches,
 flow / chain overlap), both contrast modes, magnitude and no-endpoint chains.
 The setting is read when a simulator is created."""
@@ -16,11 +15,10 @@ from paper_2209_04634_b200.abi import EventsPerCrossing, Method, make_config
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("kind", ["u8", "f4", "bf16", "f4-skip"])
+@pytest.mark.parametrize("kind", ["u8", "f4", "bf16"])
 @pytest.mark.parametrize("mode,mag,incl", [(1, 0, 1), (0, 0, 1), (1, 1, 1), (0, 0, 0)])
 def test_quad_kinds_match_oracle(oracle, kind, mode, mag, incl, monkeypatch):
-    monkeypatch.setenv("EVSIM_CHAIN_QUAD", kind.split("-")[0])
-    monkeypatch.setenv("EVSIM_CHAIN_SKIP", "1" if kind.endswith("skip") else "0")
+    monkeypatch.setenv("EVSIM_CHAIN_QUAD", kind)
     frames, ts = scenes.generate("c2", n_frames=34, width=131, height=77)
     cfg = make_config(Method.dense, n_interp=10, contrast_mode=mode, c_pos_log=0.1, c_neg_log=-0.1,
                       events_per_crossing=int(EventsPerCrossing.magnitude) if mag else 0, include_endpoints=incl)
