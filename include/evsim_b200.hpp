@@ -8,6 +8,7 @@
 // evsim_b200;`).  Header-only; link with -levsim_gpu.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -428,20 +429,26 @@ class Simulator {
     h_.reset(h);
   }
   // Alternate flow backends (simulate.hpp:68-77): the flow comes from the
-  // estimators, interpolation + events run on the GPU (linear mode).
+  // estimators; the stream's state (prev frame, log reference state) and
+  // everything else stay on the GPU (evsim_gpu_push_frame_with_flow /
+  // _with_tracks), so both contrast modes work through the seam.
   Simulator(SimulatorConfig config, std::shared_ptr<const DenseFlowEstimator> dense_flow,
-            std::shared_ptr<const SparseFlowEstimator> sparse_flow)
-      : config_(config), dense_(std::move(dense_flow)), sparse_(std::move(sparse_flow)) {
+            std::shared_ptr<const SparseFlowEstimator> sparse_flow, int device = 0)
+      : config_(config), dense_(std::move(dense_flow)), sparse_(std::move(sparse_flow)), custom_(true) {
     config_.validate();
     if (!dense_ || !sparse_) throw std::invalid_argument("Simulator: flow estimators must not be null");
     if (config_.method == Method::difference_interp)
       throw std::invalid_argument("Simulator: custom flow estimators are not supported for difference_interp");
+    const evsim_gpu_config c = config_.to_c();
+    evsim_gpu_sim* h = nullptr;
+    detail::check(evsim_gpu_create(&c, device, &h));
+    h_.reset(h);
   }
 
   EventStream push_frame(const Frame& frame) {
     if (frame.width <= 0 || frame.height <= 0 || frame.pixels.size() != frame.pixel_count())
       throw std::invalid_argument("push_frame: malformed frame");
-    if (!h_) return push_custom(frame);
+    if (custom_) return push_custom(frame);
     evsim_gpu_events ev{};
     detail::check(evsim_gpu_push_frame(h_.get(), frame.pixels.data(), frame.width, frame.height, frame.timestamp, 0,
                                        &ev));
@@ -453,7 +460,7 @@ class Simulator {
   EventStream push_frames(const std::vector<Frame>& frames) {
     EventStream all{frames.empty() ? 0 : frames[0].width, frames.empty() ? 0 : frames[0].height, {}};
     if (frames.empty()) return all;
-    if (!h_) {
+    if (custom_) {
       for (const auto& f : frames) all.append(push_frame(f));
       return all;
     }
@@ -481,24 +488,22 @@ class Simulator {
   // write_events_binary / write_events_text (io.hpp:30-36) of the last push's
   // events, formatted on the device (library handle only).
   void write_events_binary(const std::string& path) {
-    if (!h_) throw std::invalid_argument("write_events_binary: not available with custom flow estimators");
     detail::check(evsim_gpu_write_events_binary(h_.get(), path.c_str()));
   }
   void write_events_text(const std::string& path) {
-    if (!h_) throw std::invalid_argument("write_events_text: not available with custom flow estimators");
     detail::check(evsim_gpu_write_events_text(h_.get(), path.c_str()));
   }
 
   // Row band (evsim_gpu_set_row_band): emit only rows [y0, y1); stream start only.
   void set_row_band(int y0, int y1) {
-    if (!h_) throw std::invalid_argument("set_row_band: not available with custom flow estimators");
+    if (custom_) throw std::invalid_argument("set_row_band: not available with custom flow estimators");
     detail::check(evsim_gpu_set_row_band(h_.get(), y0, y1));
   }
 
   const SimulatorConfig& config() const { return config_; }
   void reset() {
     prev_.reset();
-    if (h_) detail::check(evsim_gpu_reset(h_.get()));
+    detail::check(evsim_gpu_reset(h_.get()));
   }
 
  private:
@@ -515,39 +520,56 @@ class Simulator {
   }
 
   EventStream push_custom(const Frame& frame) {
-    EventStream out{frame.width, frame.height, {}};
     if (prev_) {
       if (frame.width != prev_->width || frame.height != prev_->height)
         throw std::invalid_argument("push_frame: frame dimensions changed mid-stream");
       if (frame.timestamp <= prev_->timestamp)
         throw std::invalid_argument("push_frame: timestamps must be strictly increasing");
-      SimulatorConfig c = config_;
-      if (config_.method == Method::dense && config_.n_interp > 0) {
-        out = dense_events_with_flow(*prev_, frame, dense_->estimate(*prev_, frame), c);
-      } else if (config_.method == Method::sparse && config_.n_interp > 0) {
-        std::vector<PixelPoint> pts;
-        const int sel = c.effective_selection_threshold();
+    }
+    evsim_gpu_events ev{};
+    if (config_.method == Method::sparse && config_.n_interp > 0) {
+      // the points the reference selects (simulate.cpp:150-157, scan order)
+      // and the estimator's tracks for them
+      std::vector<int32_t> pts;
+      SparseFlow fl;
+      if (prev_) {
+        std::vector<PixelPoint> sel;
+        const int t = config_.effective_selection_threshold();
+        const bool logm = config_.contrast_mode == ContrastMode::log;
+        float lut[256];
+        if (logm) evsim_gpu_log_lut(lut);  // log mode: |L[curr] - L[prev]| > sel_log
+        const float tl = config_.sel_log > 0.0f ? config_.sel_log : config_.c_pos_log;
         for (int y = 0; y < frame.height; ++y)
           for (int x = 0; x < frame.width; ++x) {
-            const int d = static_cast<int>(frame.at(x, y)) - static_cast<int>(prev_->at(x, y));
-            if ((d < 0 ? -d : d) > sel) pts.push_back({x, y});
+            const int a = prev_->at(x, y), c = frame.at(x, y);
+            const bool take = logm ? std::fabs(lut[c] - lut[a]) > tl : (c - a < 0 ? a - c : c - a) > t;
+            if (take) sel.push_back({x, y});
           }
-        SparseFlow fl;
-        if (!pts.empty()) fl = sparse_->estimate(*prev_, frame, pts);
-        out = sparse_events_with_flow(*prev_, frame, fl, c);
-      } else {
-        c.n_interp = 0;
-        out = dense_events_with_flow(*prev_, frame, FlowField(frame.width, frame.height), c);
+        if (!sel.empty()) fl = sparse_->estimate(*prev_, frame, sel);
+        pts.reserve(sel.size() * 2);
+        for (const auto& p : sel) pts.push_back(p.x), pts.push_back(p.y);
       }
+      detail::check(evsim_gpu_push_frame_with_tracks(
+          h_.get(), frame.pixels.data(), frame.width, frame.height, frame.timestamp, pts.data(),
+          static_cast<int64_t>(pts.size() / 2), reinterpret_cast<const float*>(fl.displacements.data()),
+          fl.status.data(), &ev));
+    } else {
+      FlowField fl;
+      const bool flow = prev_ && config_.method == Method::dense && config_.n_interp > 0;
+      if (flow) fl = dense_->estimate(*prev_, frame);
+      detail::check(evsim_gpu_push_frame_with_flow(h_.get(), frame.pixels.data(), frame.width, frame.height,
+                                                   frame.timestamp, flow ? fl.du.data() : nullptr,
+                                                   flow ? fl.dv.data() : nullptr, &ev));
     }
     prev_ = std::make_unique<Frame>(frame);
-    return out;
+    return collect(ev);
   }
 
   SimulatorConfig config_;
   std::unique_ptr<evsim_gpu_sim, Deleter> h_;
   std::shared_ptr<const DenseFlowEstimator> dense_;
   std::shared_ptr<const SparseFlowEstimator> sparse_;
+  bool custom_ = false;
   std::unique_ptr<Frame> prev_;
 };
 

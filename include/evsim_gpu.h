@@ -293,6 +293,33 @@ EVSIM_GPU_API int evsim_gpu_ingest_frames(const uint8_t* src, int32_t channels, 
  * writing"). */
 EVSIM_GPU_API int evsim_gpu_write_events_binary(evsim_gpu_sim* sim, const char* path);
 EVSIM_GPU_API int evsim_gpu_write_events_text(evsim_gpu_sim* sim, const char* path);
+/* Simulator::push_frame with the flow from a caller's estimator
+ * (Simulator(config, dense_flow, sparse_flow), include/evsim/simulate.hpp:68-77):
+ * the handle keeps the stream's state — prev frame, the log reference state
+ * (so log mode works through the plug-in seam) — and takes only the flow from
+ * the caller.
+ *   _with_flow   dense method: du, dv = the DenseFlowEstimator's FlowField for
+ *                (prev, this frame), W*H floats each (ignored on the warm-up
+ *                frame and when n_interp == 0);
+ *   _with_tracks sparse method: the SparseFlowEstimator's result for the
+ *                points the reference selects (|curr - prev| > selection
+ *                threshold, scan order, simulate.cpp:150-157): n_points
+ *                (x, y) pairs, 2*n_points displacements, n_points status.
+ * difference_only handles accept either call (no flow).  A handle fed this
+ * way takes only these pushes until evsim_gpu_reset.  Errors as
+ * evsim_gpu_push_frame. */
+EVSIM_GPU_API int evsim_gpu_push_frame_with_flow(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t width,
+                                                 int32_t height, int64_t t_us, const float* du, const float* dv,
+                                                 evsim_gpu_events* out);
+EVSIM_GPU_API int evsim_gpu_push_frame_with_tracks(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t width,
+                                                   int32_t height, int64_t t_us, const int32_t* points_xy,
+                                                   int64_t n_points, const float* disp, const uint8_t* status,
+                                                   evsim_gpu_events* out);
+/* The log-intensity table of the log contrast mode:
+ * lut[i] = logf(i / 255 + 1e-3), the exact fp32 values the kernels use — for
+ * callers that restate the sparse selection |L[curr] - L[prev]| > sel_log on
+ * the host (the flow plug-in seam, evsim_gpu_push_frame_with_tracks). */
+EVSIM_GPU_API void evsim_gpu_log_lut(float* lut256);
 /* difference_frame (include/evsim/core.hpp:8, src/core.cpp:5-19): values[i]
  * = curr[i] - prev[i] as int16 over w*h pixels (the caller checks that the
  * two frames have one size; the reference's message is "difference_frame:

@@ -52,6 +52,10 @@ _SIGS = {
                        ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]),
     "evsim_gpu_accumulate": (ctypes.c_int, [_vp, _i64, _i32, _i32, _i64, _i64, _vp]),
     "evsim_gpu_difference_frame": (ctypes.c_int, [_vp, _vp, _i32, _i32, _vp]),
+    "evsim_gpu_log_lut": (None, [_vp]),
+    "evsim_gpu_push_frame_with_flow": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i64, _vp, _vp, ctypes.POINTER(CEvents)]),
+    "evsim_gpu_push_frame_with_tracks": (
+        ctypes.c_int, [_vp, _vp, _i32, _i32, _i64, _vp, _i64, _vp, _vp, ctypes.POINTER(CEvents)]),
     "evsim_gpu_threshold_events": (
         ctypes.c_int, [_vp, _i32, _i32, ctypes.POINTER(CConfig), _i64, _vp, _i64, ctypes.POINTER(_i64)]),
     "evsim_gpu_set_row_band": (ctypes.c_int, [_vp, _i32, _i32]),

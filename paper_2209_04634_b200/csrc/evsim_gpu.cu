@@ -1159,7 +1159,9 @@ struct evsim_gpu_sim {
   // ---- push ----------------------------------------------------------------
   // Simulator::push_frame (src/simulate.cpp:306-347) applied to F frames in
   // order; the whole batch is validated first and rejected atomically.
-  void validate_batch(const uint8_t* pixels, int F, int fw, int fh, const int64_t* ts, bool wire = false) const {
+  void validate_batch(const uint8_t* pixels, int F, int fw, int fh, const int64_t* ts, bool wire = false,
+                      bool custom_push = false) const {
+    if (custom && has_prev && !custom_push) invalid(kCustomMsg);
     if (F < 1) invalid("push_frames: n_frames must be >= 1");
     if (fw <= 0 || fh <= 0 || !pixels || !ts) invalid("push_frame: malformed frame");
     if (has_prev) {
@@ -1211,6 +1213,90 @@ struct evsim_gpu_sim {
     enqueue(pixels, F, ts, on_device, nullptr, h_seg_out, false);
   }
 
+  // ---- push with caller-supplied flow ---------------------------------------
+  // Simulator::push_frame with the flow from a caller's DenseFlowEstimator /
+  // SparseFlowEstimator (include/evsim/simulate.hpp:68-77): the handle keeps
+  // the stream's state (prev frame, log reference state) exactly as for its
+  // own flow; only the flow comes from the caller — the dense field of
+  // (prev, frame), or the tracks of the points the reference selects
+  // (simulate.cpp:150-157, scan order).  A handle fed this way takes only
+  // such pushes until reset() (its frames get no pyramids).
+  bool custom = false;
+  static constexpr const char* kCustomMsg =
+      "push_frame: this simulator is fed caller-supplied flow (push_frame_with_flow); reset() first";
+  DevBuf field;
+  void push_custom(const uint8_t* pixels, int fw, int fh, int64_t t, const float* du, const float* dv,
+                   const int32_t* pts, int64_t n_pts, const float* disp, const uint8_t* st) {
+    validate_batch(pixels, 1, fw, fh, &t, false, true);
+    if (diff_interp()) invalid("Simulator: custom flow estimators are not supported for difference_interp");
+    const size_t P = (size_t)fw * fh;
+    std::vector<uint32_t> idx;
+    if (has_prev && sparse_flow()) {
+      if (n_pts < 0 || (n_pts > 0 && (!pts || !disp || !st))) invalid("push_frame_with_tracks: malformed tracks");
+      if ((uint64_t)n_pts > P) invalid("push_frame_with_tracks: more points than pixels");
+      idx.resize((size_t)std::max<int64_t>(n_pts, 1));
+      for (int64_t i = 0; i < n_pts; ++i) {
+        const int x = pts[2 * i], y = pts[2 * i + 1];
+        if (x < 0 || x >= fw || y < 0 || y >= fh) invalid("simulate_sparse: point outside frame bounds");
+        idx[i] = (uint32_t)y * (uint32_t)fw + (uint32_t)x;
+        if (i && idx[i] <= idx[i - 1]) invalid("push_frame_with_tracks: points must be in scan order");
+      }
+    }
+    if (has_prev && dense_flow() && (!du || !dv)) invalid("push_frame_with_flow: null flow field");
+    prepare(1, fw, fh);
+    custom = true;
+    const int base = next_slot();
+    upload(pixels, 1, base, false, stream);
+    if (dense_flow()) {  // the u8 quads the field-form interpolation samples
+      launch_build_quad(frames.as<uint8_t>() + (size_t)base * P, quads.as<uint32_t>() + (size_t)base * P, w, h, stream);
+      CK_LAUNCH("build_quad");
+      ++launches;
+    }
+    if (!has_prev) {  // warm-up frame
+      if (log_mode()) {
+        launch_init_ref(frames.as<uint8_t>() + (size_t)base * P, lut.as<float>(), ref.as<float>(), (int64_t)P, stream);
+        CK_LAUNCH("init_ref");
+        ++launches;
+      }
+      seg_t.clear();
+      seg_off.assign(1, 0);
+      n_events = 0;
+      pending = false;
+    } else {
+      ChainParams c = chain_params(rhead, 1);
+      c.quadf = Ring<const float4>{nullptr, P};
+      c.quadh = Ring<const uint2>{nullptr, P};
+      int provider = kProvNone;
+      if (dense_flow()) {
+        field.ensure(P * 8, stream);
+        CK(cudaMemcpyAsync(field.p, du, P * 4, cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(field.as<float>() + P, dv, P * 4, cudaMemcpyHostToDevice, stream));
+        c.du = field.as<float>();
+        c.dv = field.as<float>() + P;
+        provider = kProvDenseField;
+      } else if (sparse_flow()) {
+        const int np = (int)n_pts;
+        if (np > 0) {
+          CK(cudaMemcpyAsync(points.p, idx.data(), (size_t)np * 4, cudaMemcpyHostToDevice, stream));
+          CK(cudaMemcpyAsync(this->disp.p, disp, (size_t)np * 8, cudaMemcpyHostToDevice, stream));
+          CK(cudaMemcpyAsync(this->status.p, st, (size_t)np, cudaMemcpyHostToDevice, stream));
+        }
+        CK(cudaMemcpyAsync(n_points.p, &np, sizeof np, cudaMemcpyHostToDevice, stream));
+        splat_stage(rhead, 1, c);
+        launches += 2;
+        provider = kProvSparse;
+      }
+      const int64_t ts2[2] = {prev_t, t};
+      run_events(c, provider, ts2, h_seg_out);
+      CK(cudaStreamSynchronize(stream));  // (the host staging above must outlive its copies)
+    }
+    rhead = base;
+    prev_t = t;
+    has_prev = true;
+    n_seen += 1;
+  }
+
+
   // Everything of one push after validation: upload (unless `uploaded` says
   // the frames are already in the ring), pyramid, flow, chain, emit.
   void enqueue(const uint8_t* pixels, int F, const int64_t* ts, bool on_device, cudaEvent_t uploaded, int64_t* h_seg,
@@ -1241,15 +1327,19 @@ struct evsim_gpu_sim {
           CK(cudaEventCreateWithFlags(&ev_qin, cudaEventDisableTiming));
           CK(cudaEventCreateWithFlags(&ev_qdone, cudaEventDisableTiming));
         }
-        CK(cudaEventRecord(ev_qin, ps));  // the frames are in the ring
-        CK(cudaStreamWaitEvent(s_quad, ev_qin, 0));
-        launch_quads(base, F, s_quad);
-        CK(cudaEventRecord(ev_qdone, s_quad));
-        quad_side = true;
+        quad_side = true;  // launched after the pyramid (below)
       }
-      CK_LAUNCH("lerp_quads");
       ++launches;
     }
+    // the lerp quads on s_quad, after the pyramid (beside the LK solve;
+    // starting them beside the pyramid measured the same on c2 / c5)
+    auto side_quads = [&]() {
+      CK(cudaEventRecord(ev_qin, ps));
+      CK(cudaStreamWaitEvent(s_quad, ev_qin, 0));
+      launch_quads(base, F, s_quad);
+      CK(cudaEventRecord(ev_qdone, s_quad));
+      CK_LAUNCH("lerp_quads");
+    };
     if (diff_interp()) {
       // difference magnitudes of the new frames that have a predecessor, and
       // (for the sparse solver) their pyramids
@@ -1273,6 +1363,7 @@ struct evsim_gpu_sim {
       CK_LAUNCH("pyramid");
       launches += flow.levels;
     }
+    if (quad_side) side_quads();
     if (!has_prev && log_mode()) {
       // warm-up frame: ref := L(frame0)
       if (xc) CK(cudaStreamWaitEvent(stream, uploaded, 0));
@@ -2395,6 +2486,37 @@ int evsim_gpu_threshold_events(const int16_t* values, int32_t w, int32_t h, cons
   });
 }
 
+void evsim_gpu_log_lut(float* lut256) {
+  if (lut256) log_lut(lut256);
+}
+
+int evsim_gpu_push_frame_with_flow(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t width, int32_t height,
+                                   int64_t t_us, const float* du, const float* dv, evsim_gpu_events* out) {
+  return guarded([&] {
+    if (!sim) invalid("evsim_gpu_push_frame_with_flow: null simulator");
+    CK(cudaSetDevice(sim->device));
+    if (sim->cfg.method == EVSIM_METHOD_SPARSE && sim->n_interp_eff() > 0)
+      invalid("push_frame_with_flow: a sparse simulator takes tracks (evsim_gpu_push_frame_with_tracks)");
+    sim->push_custom(pixels, width, height, t_us, du, dv, nullptr, 0, nullptr, nullptr);
+    sim->finish();
+    sim->fill_out(out);
+  });
+}
+
+int evsim_gpu_push_frame_with_tracks(evsim_gpu_sim* sim, const uint8_t* pixels, int32_t width, int32_t height,
+                                     int64_t t_us, const int32_t* points_xy, int64_t n_points, const float* disp,
+                                     const uint8_t* status, evsim_gpu_events* out) {
+  return guarded([&] {
+    if (!sim) invalid("evsim_gpu_push_frame_with_tracks: null simulator");
+    CK(cudaSetDevice(sim->device));
+    if (sim->cfg.method == EVSIM_METHOD_DENSE && sim->n_interp_eff() > 0)
+      invalid("push_frame_with_tracks: a dense simulator takes a flow field (evsim_gpu_push_frame_with_flow)");
+    sim->push_custom(pixels, width, height, t_us, nullptr, nullptr, points_xy, n_points, disp, status);
+    sim->finish();
+    sim->fill_out(out);
+  });
+}
+
 void* evsim_gpu_stream(evsim_gpu_sim* sim) { return sim ? (void*)sim->stream : nullptr; }
 
 int evsim_gpu_reset(evsim_gpu_sim* sim) {
@@ -2404,6 +2526,7 @@ int evsim_gpu_reset(evsim_gpu_sim* sim) {
     sim->finish();
     // Simulator::reset  include/evsim/simulate.hpp:83-86
     sim->has_prev = false;
+    sim->custom = false;
     sim->n_seen = 0;
     sim->n_events = 0;
     sim->seg_t.clear();

@@ -341,9 +341,18 @@ def dense_events_with_flow(prev: Frame, curr: Frame, flow: FlowField, config: Si
 
 def select_points(prev: Frame, curr: Frame, config: SimulatorConfig) -> np.ndarray:
     """Host restatement of simulate.cpp:149-159 (scan-order selection) — used
-    only when a custom SparseFlowEstimator must receive the point list."""
-    d = np.abs(curr.pixels.astype(np.int32) - prev.pixels.astype(np.int32))
-    ys, xs = np.nonzero(d > config.effective_selection_threshold())
+    only when a custom SparseFlowEstimator must receive the point list.  Log
+    mode: |L[curr] - L[prev]| > sel_log in fp32 with the library's own table
+    (evsim_gpu_log_lut), exactly as the device selection."""
+    if config.contrast_mode == ContrastMode.log:
+        lut = np.zeros(256, np.float32)
+        _lib.load().evsim_gpu_log_lut(_ptr(lut))
+        sel = np.float32(config.sel_log if config.sel_log > 0 else config.c_pos_log)
+        d = np.abs(lut[curr.pixels] - lut[prev.pixels])  # float32 IEEE subtraction
+        ys, xs = np.nonzero(d > sel)
+    else:
+        d = np.abs(curr.pixels.astype(np.int32) - prev.pixels.astype(np.int32))
+        ys, xs = np.nonzero(d > config.effective_selection_threshold())
     return np.stack([xs, ys], axis=1).astype(np.int32)
 
 
@@ -414,8 +423,8 @@ class Simulator:
 
     ``Simulator(config)`` runs the whole push on the device.  Passing custom
     ``dense_flow`` / ``sparse_flow`` estimators (the reference's plug-in seam,
-    simulate.hpp:68-77) routes the flow through them and the interpolation +
-    event chain through the GPU free functions (linear mode).
+    simulate.hpp:68-77) routes the flow through them; the stream's state and
+    everything else stay on the device (both contrast modes).
     """
 
     def __init__(self, config: SimulatorConfig, dense_flow: Optional[DenseFlowEstimator] = None,
@@ -614,6 +623,11 @@ class Simulator:
         return int(self._lib.evsim_gpu_kernel_launches(self._h))
 
     def _push_custom(self, frame: Frame, pixels: np.ndarray) -> EventStream:
+        """push_frame with the flow from the caller's estimators: the flow on
+        the host (the estimator), the stream's state — prev frame, log
+        reference state — and everything else on the device
+        (evsim_gpu_push_frame_with_flow / _with_tracks), so log mode works
+        through the seam too."""
         prev = self._prev
         f = Frame(frame.width, frame.height, int(frame.timestamp), pixels)
         if prev is not None:
@@ -621,19 +635,34 @@ class Simulator:
                 raise InvalidArgument(1, "push_frame: frame dimensions changed mid-stream")
             if frame.timestamp <= prev.timestamp:
                 raise InvalidArgument(1, "push_frame: timestamps must be strictly increasing")
-        out = EventStream(frame.width, frame.height)
-        if prev is not None:
-            m = self._config.method
-            if m == Method.dense:
-                out = simulate_dense(prev, f, self._config, self._dense or PyramidalPatchFlow(self._config.preset()))
-            elif m == Method.sparse:
-                out = simulate_sparse(prev, f, self._config,
-                                      self._sparse or PyramidalLucasKanade(self._config.preset()))
-            else:
-                out = dense_events_with_flow(prev, f, FlowField.zeros(f.width, f.height),
-                                             dataclasses.replace(self._config, n_interp=0))
+        cfg = self._config
+        m, n = Method(cfg.method), cfg.n_interp
+        ev = CEvents()
+        w, h, t = frame.width, frame.height, int(frame.timestamp)
+        if m == Method.sparse and n > 0:
+            pts = np.zeros((0, 2), np.int32)
+            disp = np.zeros((0, 2), np.float32)
+            st = np.zeros(0, np.uint8)
+            if prev is not None:
+                pts = select_points(prev, f, cfg)
+                if len(pts):
+                    fl = (self._sparse or PyramidalLucasKanade(cfg.preset())).estimate(prev, f, pts)
+                    disp = np.ascontiguousarray(fl.displacements, np.float32).reshape(-1, 2)
+                    st = np.ascontiguousarray(fl.status, np.uint8)
+            pts = np.ascontiguousarray(pts, np.int32)
+            _lib.check(self._lib.evsim_gpu_push_frame_with_tracks(
+                self._h, _ptr(pixels), w, h, t, _ptr(pts), len(pts), _ptr(disp), _ptr(st), ctypes.byref(ev)))
+        else:
+            du = dv = None
+            if prev is not None and m == Method.dense and n > 0:
+                fl = (self._dense or PyramidalPatchFlow(cfg.preset())).estimate(prev, f)
+                du = np.ascontiguousarray(fl.du, np.float32)
+                dv = np.ascontiguousarray(fl.dv, np.float32)
+            _lib.check(self._lib.evsim_gpu_push_frame_with_flow(
+                self._h, _ptr(pixels), w, h, t, None if du is None else _ptr(du), None if dv is None else _ptr(dv),
+                ctypes.byref(ev)))
         self._prev = f
-        return out
+        return self._collect(ev)
 
     def reset(self) -> None:
         """Simulator::reset (simulate.hpp:83-86)."""

@@ -24,7 +24,7 @@ def declared_functions():
 def test_header_declares_entry_points():
     names = declared_functions()
     assert "evsim_gpu_push_frame" in names and "evsim_gpu_dense_flow" in names
-    assert len(names) == 38
+    assert len(names) == 41
 
 
 def test_library_loads_and_exports_every_declared_symbol():
