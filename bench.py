@@ -693,7 +693,9 @@ def run_ours(args):
                 "algorithmic_bytes_per_frame": round(b_alg_band), "frames_per_launch": round(pairs_prof / launches_ev, 2),
                 "algorithmic_bytes_per_launch": round(bytes_per_launch), "avg_launch_ms": round(ms_per_launch, 5),
                 "peak_source": peak_src, "end_to_end_frac": round(e2e_frac, 5),
-                "stage_us_per_frame": {k: round(1e3 * v / pairs_prof, 3) for k, v in stages.items()}}
+                "stage_us_per_frame": {k: round(1e3 * v / pairs_prof, 3) for k, v in stages.items()},
+                "issue_roofline": issue_roofline(c.name, args.mode, args.preset, pairs_prof / launches_ev,
+                                                 stages["chain"] / launches_ev) if ws == 1 else None}
 
     # ---- e2e through the C-ABI with host buffers ---------------------------------
     e2e = None
@@ -861,6 +863,31 @@ def flow_rate(c, args, stages, pairs):
     if s is None or ms <= 0 or c.method != "dense":
         return None
     return round(s * pairs / (ms / 1e3) / 1e9, 2)
+
+
+def issue_roofline(config: str, mode: str, preset: str, pairs_per_launch: float, chain_ms_per_launch: float):
+    """The chain kernel against the SM issue peak: warp-instructions per launch
+    from the committed ncu capture of the same workload (lq preset, the same
+    pairs per launch) over the chain's average launch time in this run;
+    peak = 148 SMs x 4 schedulers x the SM clock (profiles/r02/peaks.json)."""
+    if preset != "lq" or chain_ms_per_launch <= 0:
+        return None
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r02", f"traffic_{config}_{mode}.json")))
+        pk = json.load(open(os.path.join(ROOT, "profiles", "r02", "peaks.json")))
+    except Exception:
+        return None
+    if abs(pairs_per_launch - t.get("pairs_per_launch", -1)) >= 0.5:
+        return None
+    instr = sum(v for k, v in t.get("per_kernel_warp_instr", {}).items() if k.startswith("chain_"))
+    if not instr:
+        return None
+    instr = int(instr * pairs_per_launch / t["pairs_per_launch"])  # per pair x this run's pairs per launch
+    achieved = instr / (chain_ms_per_launch / 1e3) / 1e9
+    peak = float(pk["issue_peak_G_per_s_theoretical"])
+    return {"bound": "issue", "kernel": "chain kernel", "warp_instr_per_launch": instr,
+            "achieved": round(achieved, 1), "peak": peak, "unit": "G warp-instr/s", "frac": round(achieved / peak, 4),
+            "source": f"profiles/r02/traffic_{config}_{mode}.json (ncu instruction count) + this run's chain time"}
 
 
 def traffic_for(config: str, mode: str, pairs_per_launch: float):

@@ -61,15 +61,17 @@ def main(rep, outdir, *_):
     if xs:
         # one launch of each event-stage kernel per push here (no sub-batches
         # below 16 pairs): the last launch of each, i.e. the capture's last push
-        per = {}
+        per, instr = {}, {}
         for x in xs:
             name = x["kernel"].split("(")[0].replace("void ", "")
             per[name] = int((x["dram_rd_MB"] + x["dram_wr_MB"]) * 1e6)
+            instr[name] = int(x.get("warp_instr", 0))
         json.dump({"source": f"{outdir}/ncu_full_summary.json (ncu --set full --clock-control none, every "
                              "event-stage launch of one push)",
                    "workload": f"{config} {mode}, one push of {ppl} frame pairs (tools/push_once.py)",
                    "pairs_per_launch": float(ppl),
-                   "event_stage_dram_bytes_per_launch": sum(per.values()), "per_kernel_dram_bytes": per},
+                   "event_stage_dram_bytes_per_launch": sum(per.values()), "per_kernel_dram_bytes": per,
+                   "per_kernel_warp_instr": instr},
                   open(os.path.join(outdir, f"traffic_{config}_{mode}.json"), "w"), indent=1)
     for x in out:
         print(f"{x['kernel'][:44]:44s} {x.get('dur_ms', 0):8.3f} ms  issue {x.get('issue_active_pct', 0):5.1f}%  "
