@@ -998,9 +998,10 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
 constexpr int kDiffWPW = 8;                           // words per warp per chunk
 constexpr int kDiffTW = kWarpsPerBlock * kDiffWPW;   // words per chunk
 constexpr int kDiffNB = 4;                            // frames in flight per block
+constexpr int kDiffMinB = 4;                          // blocks per SM (64 registers)
 
 template <bool kLog>
-__global__ void __launch_bounds__(256) chain_diff_tma_kernel(ChainParams p, int stage_bytes) {
+__global__ void __launch_bounds__(256, kDiffMinB) chain_diff_tma_kernel(ChainParams p, int stage_bytes) {
   extern __shared__ __align__(128) uint8_t s_raw[];  // [kDiffNB][stage_bytes] frames, then [n_pairs] counts
   __shared__ float s_lut[kLog ? 256 : 1];
   __shared__ int2 s_th[kLog ? 256 : 1];
@@ -1065,15 +1066,15 @@ __global__ void __launch_bounds__(256) chain_diff_tma_kernel(ChainParams p, int 
     uint32_t bytes;
     range(c, a0, bytes);
     const int64_t cw0 = wbeg + (int64_t)c * kDiffTW;
-    int64_t wq[kDiffWPW];
+    uint32_t wq[kDiffWPW];  // (n_words < 2^32)
     uint32_t off[kDiffWPW];
     bool have[kDiffWPW], valid[kDiffWPW];
     int before[kDiffWPW], thh[kDiffWPW], thl[kDiffWPW], vr[kDiffWPW];
 #pragma unroll
     for (int q = 0; q < kDiffWPW; ++q) {
-      wq[q] = cw0 + q * kWarpsPerBlock + warp;
-      have[q] = wq[q] < wend;
-      const int64_t ww = have[q] ? wq[q] : cw0;
+      wq[q] = (uint32_t)(cw0 + q * kWarpsPerBlock + warp);
+      have[q] = (int64_t)wq[q] < wend;
+      const int64_t ww = have[q] ? (int64_t)wq[q] : cw0;
       const int row = (int)((uint32_t)ww / (uint32_t)p.wpr);
       const int x = (int)(ww - (int64_t)row * p.wpr) * 32 + lane;
       valid[q] = have[q] && x < p.w;

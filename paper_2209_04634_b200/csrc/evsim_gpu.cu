@@ -509,6 +509,13 @@ struct EventEngine {
     const int64_t target = 148 * 8;
     int64_t per = (n_words + target - 1) / target;
     per = std::max<int64_t>(kWarpsPerBlock, (per + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock);
+    // a power of two (down): whole chain blocks tile the emit's 256-word
+    // tiles without idle threads (stacked c1 x64: 160 -> 128-word blocks)
+    {
+      int64_t p2 = kWarpsPerBlock;
+      while (p2 * 2 <= per) p2 *= 2;
+      per = p2;
+    }
     words_per_warp = 2;
     if (fine) {
       // one-word warp tasks; 8-word blocks up to 8192 blocks, beyond that
