@@ -1012,7 +1012,8 @@ __global__ void __launch_bounds__(256, kDiffMinB) chain_diff_tma_kernel(ChainPar
   for (int i = threadIdx.x; i < G; i += blockDim.x) s_cnt[i] = 0;
   if (kLog) {
     s_lut[threadIdx.x] = p.lut[threadIdx.x];
-    s_th[threadIdx.x] = make_int2(p.lthr[threadIdx.x].x, p.lthr[threadIdx.x].y);
+    // (hi, lo) of level threadIdx.x, unbiased: this chain compares raw bytes
+    s_th[threadIdx.x] = make_int2(p.lthr[threadIdx.x].x - kVB, p.lthr[threadIdx.x].y - kVB);
   }
   const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(s_bar);
   const uint32_t buf0 = (uint32_t)__cvta_generic_to_shared(s_raw);
@@ -1023,7 +1024,10 @@ __global__ void __launch_bounds__(256, kDiffMinB) chain_diff_tma_kernel(ChainPar
   __syncthreads();
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t th_b = pin((uint32_t)__cvta_generic_to_shared(s_th) - ((uint32_t)kVB << 3));
+  const uint32_t th_b = pin((uint32_t)__cvta_generic_to_shared(s_th));
+  // lane 0 stages link (i - fbase)'s masks of word q at st_b + (i - fbase) * 8 + q * kStRow
+  constexpr uint32_t kStRow = sizeof(s_stm[0][0]);
+  const uint32_t st_b = pin((uint32_t)__cvta_generic_to_shared(&s_stm[warp][0][0]));
   const int64_t wbeg = (int64_t)b * p.words_per_block;
   const int64_t wend = min(wbeg + p.words_per_block, p.n_words);
   const int n_chunks = (int)((wend - wbeg + kDiffTW - 1) / kDiffTW);
@@ -1083,7 +1087,7 @@ __global__ void __launch_bounds__(256, kDiffMinB) chain_diff_tma_kernel(ChainPar
       before[q] = 0;
       thh[q] = INT_MAX;
       thl[q] = INT_MIN;
-      vr[q] = kVB;
+      vr[q] = 0;
       if (kLog) {
         if (valid[q]) {
           const float ref = p.ref[pix];
@@ -1094,10 +1098,10 @@ __global__ void __launch_bounds__(256, kDiffMinB) chain_diff_tma_kernel(ChainPar
           const int2 tt = s_th[r];
           thh[q] = tt.x;
           thl[q] = tt.y;
-          vr[q] = kVB + r;
+          vr[q] = r;
         }
       } else {
-        before[q] = kVB + (int)__ldg((p.dcurr ? p.dprev : p.frames.at(p.r0 % p.R)) + pix);
+        before[q] = (int)__ldg((p.dcurr ? p.dprev : p.frames.at(p.r0 % p.R)) + pix);
       }
     }
     int fbase = 0;
@@ -1105,18 +1109,24 @@ __global__ void __launch_bounds__(256, kDiffMinB) chain_diff_tma_kernel(ChainPar
       const int st = (int)(t & (kDiffNB - 1));
       mbar_wait(bar0 + 8 * st, (uint32_t)((t / kDiffNB) & 1));
       const uint8_t* sb = s_raw + (size_t)st * stage_bytes;
+      // the pair's bytes of this warp's words first (8 loads in flight), then
+      // the rule; the staging address is one add per pair
+      int val[kDiffWPW];
+#pragma unroll
+      for (int q = 0; q < kDiffWPW; ++q) val[q] = (int)sb[off[q]];
+      const uint32_t sta = pin(st_b + (uint32_t)(i - fbase) * 8u);
 #pragma unroll
       for (int q = 0; q < kDiffWPW; ++q) {
-        const int val = kVB + (int)sb[off[q]];
         uint2 m;
         if (kLog) {
-          m = dense_rule_th(th_b, val, thh[q], thl[q], vr[q]);
+          m = dense_rule_th(th_b, val[q], thh[q], thl[q], vr[q]);
         } else {
-          const int d = val - before[q];  // difference_frame, core.cpp:14-15
+          const int d = val[q] - before[q];  // difference_frame, core.cpp:14-15
           m = make_uint2(__ballot_sync(kFull, d > p.c_pos && valid[q]), __ballot_sync(kFull, d < p.c_neg && valid[q]));
-          before[q] = val;
+          before[q] = val[q];
         }
-        if (lane == 0) s_stm[warp][q][i - fbase] = m;
+        if (lane == 0)
+          asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(sta + (uint32_t)q * kStRow), "r"(m.x), "r"(m.y) : "memory");
       }
       __syncthreads();  // every warp is done with stage st
       if (threadIdx.x == 0 && pt < total) issue_next();
@@ -1140,7 +1150,7 @@ __global__ void __launch_bounds__(256, kDiffMinB) chain_diff_tma_kernel(ChainPar
     if (kLog) {
 #pragma unroll
       for (int q = 0; q < kDiffWPW; ++q)
-        if (valid[q]) p.ref[(size_t)off[q] + a0] = s_lut[vr[q] - kVB];
+        if (valid[q]) p.ref[(size_t)off[q] + a0] = s_lut[vr[q]];
     }
   }
   __syncthreads();
@@ -1165,6 +1175,371 @@ static bool chain_diff_tma_ok(const ChainParams& p) {
 }
 
 // ------------------------------------------------------------ lerp quads
+// ------------------------------------------------------------ tile-staged dense chain
+//
+// chain_dense_kernel with the gather images staged in shared memory.  The
+// global 16-byte gathers of the fp32 lerp quads bound that kernel by the L1
+// data pipe (every quarter-warp request touches two or more lines).  Here a
+// block owns a 2-D tile of kTileW words x kTileH rows (warp r = tile row r,
+// its kTileW words one after another); for every pair of the launch the block
+// reduces the exact bounds of its pixels' sample positions (prev is read
+// along x - fwd*u between x and x - u, curr between x and x + u; rounding is
+// monotone, so RN(x -/+ u) bound every link's position), bulk-copies that
+// region of both frames' (a00, a10 - a00) rows into shared memory
+// (cp.async.bulk global -> shared, one copy per row, completion on an
+// mbarrier) and the samples become two conflict-free 8-byte LDS each (the
+// bottom pair of a pixel is the top pair of the row below; the row pitch is a
+// multiple of 128 bytes).  Same arithmetic on the same values as
+// dense_fast(float4): bit-identical decisions.  A (tile, pair) whose region
+// does not fit the staging rows falls back to the u8-quad gathers.  One
+// count block = one tile row (words_per_block = kTileW), so the per-(link,
+// block) counts are stored by the owning warp, no block-level accumulation.
+constexpr int kTileW = 4;                    // words per tile row = words_per_block
+constexpr int kTileH = kWarpsPerBlock;       // tile rows = warps
+constexpr int kTilePitch = 144;              // float2 per staged row (128 px + flow extent <= 16)
+constexpr uint32_t kTilePB = kTilePitch * 8; // bytes per staged row (9 x 128)
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// mbar_wait with a suspend-time hint: the waiting warps sleep in the barrier
+// unit instead of spinning on the issue slots the other resident blocks need
+__device__ __forceinline__ void mbar_wait_hint(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITH_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITH_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load_tx(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+template <bool kClamp>
+__device__ __forceinline__ int dense_fast_tile(const uint8_t* __restrict__ s_reg, uint32_t ba, uint32_t bb, float my,
+                                               float wm, float hm, float xf, float yf, float u, float v, float4 kc,
+                                               unsigned& bad, unsigned bit) {
+  const f32x2 NB = pk2(kc.x, kc.y);
+  f32x2 X = affine2_est(xf, NB, u), Y = affine2_est(yf, NB, v);
+  if (kClamp) {
+    X = pk2(fminf(fmaxf(lo2(X), 0.0f), wm), fminf(fmaxf(hi2(X), 0.0f), wm));
+    Y = pk2(fminf(fmaxf(lo2(Y), 0.0f), hm), fminf(fmaxf(hi2(Y), 0.0f), hm));
+  }
+  const f32x2 C23 = pk2(8388608.0f, 8388608.0f);
+  const f32x2 CY = pk2(my, my);
+  const f32x2 TX = add2_rz(X, C23), TY = add2_rz(Y, CY);  // magic + trunc
+  const f32x2 FX = sub2(X, sub2(TX, C23)), FY = sub2(Y, sub2(TY, CY));
+  // byte offsets into the staged regions (ba / bb fold the magic bits and the region origins)
+  const uint32_t oa = __float_as_uint(lo2(TY)) * kTilePB + (__float_as_uint(lo2(TX)) * 8u + ba);
+  const uint32_t ob = __float_as_uint(hi2(TY)) * kTilePB + (__float_as_uint(hi2(TX)) * 8u + bb);
+  const float2 At = *reinterpret_cast<const float2*>(s_reg + oa);
+  const float2 Ab = *reinterpret_cast<const float2*>(s_reg + oa + kTilePB);
+  const float2 Bt = *reinterpret_cast<const float2*>(s_reg + ob);
+  const float2 Bb = *reinterpret_cast<const float2*>(s_reg + ob + kTilePB);
+  const float ta = __fmaf_rn(lo2(FX), At.y, At.x), ba2 = __fmaf_rn(lo2(FX), Ab.y, Ab.x);
+  const float tb = __fmaf_rn(hi2(FX), Bt.y, Bt.x), bb2 = __fmaf_rn(hi2(FX), Bb.y, Bb.x);
+  const float sa = __fmaf_rn(lo2(FY), __fsub_rn(ba2, ta), ta);
+  const float sb = __fmaf_rn(hi2(FY), __fsub_rn(bb2, tb), tb);
+  const float e = __fmaf_rn(kc.z, sa, __fmul_rn(kc.w, sb));
+  const f32x2 T = add2_rz(add2(pk2(e, e), pk2(0.5f - 2e-4f, 0.5f + 2e-4f)), C23);
+  if (__float_as_uint(lo2(T)) != __float_as_uint(hi2(T))) bad |= bit;
+  return __float_as_int(hi2(T));
+}
+
+template <int kNB, bool kClamp, int kBM>
+__device__ __forceinline__ unsigned dense_batch_tile(const ChainParams& p, const uint8_t* s_reg, uint32_t ba,
+                                                     uint32_t bb, float my, float wm, float hm, const DenseWord& c,
+                                                     int k0, int (&vals)[1][kBM]) {
+  unsigned bad = 0;
+#pragma unroll
+  for (int j = 0; j < kNB; ++j)
+    vals[0][j] = dense_fast_tile<kClamp>(s_reg, ba, bb, my, wm, hm, c.xf, c.yf, c.u, c.v, p.kcp[k0 + j], bad, 1u << j);
+  return bad;
+}
+
+template <bool kLog, int kB, int kMinB>
+__global__ void __launch_bounds__(256, kMinB) chain_dense_tile_kernel(ChainParams p) {
+  extern __shared__ __align__(128) uint8_t s_reg[];  // tile_cap_rows staged rows of kTilePB bytes
+  __shared__ float s_lut[256];
+  __shared__ int2 s_th[kLog ? 256 : 1];
+  constexpr int kStage = 32 + kB;
+  __shared__ uint2 s_stm[kWarpsPerBlock][kStage];
+  __shared__ uint32_t s_wcnt[kWarpsPerBlock][kMaxParamK];  // the pair's events per link of this warp's row
+  __shared__ int s_bnd[2][8];  // per pair parity: min (px, py, cx, cy), max (px, py, cx, cy)
+  __shared__ __align__(8) uint64_t s_bar;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int L = p.d.n_links, N = p.n_interp;
+  if (kLog) {
+    s_lut[threadIdx.x] = p.lut[threadIdx.x];
+    s_th[threadIdx.x] = make_int2(p.lthr[threadIdx.x].x, p.lthr[threadIdx.x].y);
+  }
+  for (int i = threadIdx.x; i < kWarpsPerBlock * kMaxParamK; i += blockDim.x) (&s_wcnt[0][0])[i] = 0;
+  if (threadIdx.x < 16) (&s_bnd[0][0])[threadIdx.x] = (threadIdx.x & 4) ? INT_MIN : INT_MAX;
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+  const uint32_t reg0 = (uint32_t)__cvta_generic_to_shared(s_reg);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t w = (uint32_t)p.w;
+  const float wm = (float)(p.w - 1), hm = (float)(p.h - 1);
+  const float my = p.magic_y;
+  const uint32_t lut_b = pin((uint32_t)__cvta_generic_to_shared(s_lut) - ((uint32_t)kVB << 2));
+  const uint32_t th_b = pin((uint32_t)__cvta_generic_to_shared(s_th) - ((uint32_t)kVB << 3));
+  const int kfirst = p.d.start + 1;
+  const int n_int = min(L, N - p.d.start);
+  // the tile: words [tx*kTileW, +kTileW) of word-grid rows [ty*kTileH, +kTileH)
+  const int tiles_x = p.wpr / kTileW;
+  const int ty = (int)blockIdx.x / tiles_x, tx = (int)blockIdx.x - ty * tiles_x;
+  const int grid_h = (int)(p.n_words / p.wpr);
+  const int trow = ty * kTileH + warp;
+  const bool have = trow < grid_h;  // (the last tile row may hang over the grid)
+  const int y = p.row0 + min(trow, grid_h - 1);
+  const float yf = (float)y;
+  const uint32_t wi0 = (uint32_t)min(trow, grid_h - 1) * (uint32_t)p.wpr + (uint32_t)(tx * kTileW);
+  const uint32_t cb = (uint32_t)min(trow, grid_h - 1) * (uint32_t)tiles_x + (uint32_t)tx;
+  // per-word state across the pairs (indexed in a rolled loop: local memory,
+  // touched once per (word, pair))
+  int st_hi[kTileW], st_lo[kTileW], st_vr[kTileW];
+  float st_u[kTileW], st_v[kTileW];
+#pragma unroll
+  for (int q = 0; q < kTileW; ++q) {
+    st_hi[q] = INT_MAX;
+    st_lo[q] = INT_MIN;
+    st_vr[q] = kVB;
+    st_u[q] = st_v[q] = 0.0f;
+    if (kLog) {
+      const int x = (tx * kTileW + q) * 32 + lane;
+      if (have && x < p.w) {
+        const float ref = p.ref[(uint32_t)y * w + (uint32_t)x];
+        int r = 0;
+#pragma unroll
+        for (int st = 128; st >= 1; st >>= 1)
+          if (s_lut[r + st] <= ref) r += st;
+        const int2 t = s_th[r];
+        st_hi[q] = t.x;
+        st_lo[q] = t.y;
+        st_vr[q] = kVB + r;
+      }
+    }
+  }
+  int sp = p.r0 % p.R;
+  uint32_t fills = 0;
+  for (int i = 0; i < p.n_pairs; ++i) {
+    const int sc = sp + 1 == p.R ? 0 : sp + 1;
+    const uint32_t* qp = p.quads.at(sp);
+    const uint32_t* qc = p.quads.at(sc);
+    const uint32_t* qbp = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(qp) - 4ull * p.qshift);
+    const uint32_t* qbc = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(qc) - 4ull * p.qshift);
+    PairCtx pc{};
+    pc.pu = p.g0.pu + (size_t)i * p.g0.pair_stride;
+    pc.pv = p.g0.pv + (size_t)i * p.g0.pair_stride;
+    // ---- the pair's flow at this row's pixels and the tile's sample bounds
+    if (have) {
+      int lo0 = INT_MAX, lo1 = INT_MAX, lo2b = INT_MAX, lo3 = INT_MAX;
+      int hi0 = INT_MIN, hi1 = INT_MIN, hi2b = INT_MIN, hi3 = INT_MIN;
+#pragma unroll
+      for (int q = 0; q < kTileW; ++q) {
+        const int x = min((tx * kTileW + q) * 32 + lane, p.w - 1);
+        PixelCtx pxc;
+        pxc.x = x;
+        pxc.y = y;
+        DenseProvider<false> prov;
+        prov.init(p, pc, pxc);
+        st_u[q] = prov.u;
+        st_v[q] = prov.v;
+        const float xf = (float)x;
+        const float xa = fminf(fmaxf(fsub(xf, prov.u), 0.0f), wm), xb = fminf(fmaxf(fadd(xf, prov.u), 0.0f), wm);
+        const float ya = fminf(fmaxf(fsub(yf, prov.v), 0.0f), hm), yb = fminf(fmaxf(fadd(yf, prov.v), 0.0f), hm);
+        lo0 = min(lo0, __float2int_rz(fminf(xf, xa)));
+        hi0 = max(hi0, __float2int_rz(fmaxf(xf, xa)));
+        lo1 = min(lo1, __float2int_rz(fminf(yf, ya)));
+        hi1 = max(hi1, __float2int_rz(fmaxf(yf, ya)));
+        lo2b = min(lo2b, __float2int_rz(fminf(xf, xb)));
+        hi2b = max(hi2b, __float2int_rz(fmaxf(xf, xb)));
+        lo3 = min(lo3, __float2int_rz(fminf(yf, yb)));
+        hi3 = max(hi3, __float2int_rz(fmaxf(yf, yb)));
+      }
+      lo0 = __reduce_min_sync(kFull, lo0);
+      lo1 = __reduce_min_sync(kFull, lo1);
+      lo2b = __reduce_min_sync(kFull, lo2b);
+      lo3 = __reduce_min_sync(kFull, lo3);
+      hi0 = __reduce_max_sync(kFull, hi0);
+      hi1 = __reduce_max_sync(kFull, hi1);
+      hi2b = __reduce_max_sync(kFull, hi2b);
+      hi3 = __reduce_max_sync(kFull, hi3);
+      if (lane == 0) {
+        int* bn = s_bnd[i & 1];
+        atomicMin(bn + 0, lo0);
+        atomicMin(bn + 1, lo1);
+        atomicMin(bn + 2, lo2b);
+        atomicMin(bn + 3, lo3);
+        atomicMax(bn + 4, hi0);
+        atomicMax(bn + 5, hi1);
+        atomicMax(bn + 6, hi2b);
+        atomicMax(bn + 7, hi3);
+      }
+    }
+    __syncthreads();  // bounds complete; every warp is done with the previous pair's staged rows
+    const int* bn = s_bnd[i & 1];
+    const int xloA = bn[0] & ~1, ncA = (bn[4] - xloA + 2) & ~1;  // even origin and count: 16-byte copies
+    const int yloA = bn[1], nrA = bn[5] - yloA + 2;              // + the row below (bottom pairs)
+    const int xloB = bn[2] & ~1, ncB = (bn[6] - xloB + 2) & ~1;
+    const int yloB = bn[3], nrB = bn[7] - yloB + 2;
+    const bool fits = ncA <= kTilePitch && ncB <= kTilePitch && nrA + nrB <= p.tile_cap_rows;
+    if (threadIdx.x == 0) {  // (before this thread's mbarrier arrive / the barrier below)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s_bnd[(i + 1) & 1][k] = (k & 4) ? INT_MIN : INT_MAX;
+    }
+    if (fits) {
+      if (warp == 0) {
+        if (lane == 0) mbar_expect_tx(bar, (uint32_t)(nrA * ncA + nrB * ncB) * 8u);
+        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const float2* gA = p.quadt.at(sp);
+        const float2* gB = p.quadt.at(sc);
+        for (int r = lane; r < nrA + nrB; r += 32) {
+          const bool isA = r < nrA;
+          const int ys = min((isA ? yloA + r : yloB + r - nrA), p.h - 1);  // replicate the last row
+          const float2* src = (isA ? gA : gB) + (size_t)ys * w + (isA ? xloA : xloB);
+          bulk_load_tx(reg0 + (uint32_t)r * kTilePB, src, (uint32_t)(isA ? ncA : ncB) * 8u, bar);
+        }
+      }
+      mbar_wait_hint(bar, fills & 1u);
+      ++fills;
+    } else {
+      __syncthreads();  // (orders the s_bnd reset before the next pair's bounds)
+    }
+    const uint32_t BY = __float_as_uint(my);
+    const uint32_t biasA = 0u - ((BY + (uint32_t)yloA) * kTilePB + (0x4B000000u + (uint32_t)xloA) * 8u);
+    const uint32_t biasB =
+        (uint32_t)nrA * kTilePB - ((BY + (uint32_t)yloB) * kTilePB + (0x4B000000u + (uint32_t)xloB) * 8u);
+    // ---- the links of this row's words
+    if (have) {
+      const int gbase = i * L;
+#pragma unroll 1
+      for (int q = 0; q < kTileW; ++q) {
+        DenseWord c;
+        c.have = true;
+        c.wi = wi0 + (uint32_t)q;
+        const int x = (tx * kTileW + q) * 32 + lane;
+        c.valid = x < p.w;
+        c.x = x < p.w ? x : p.w - 1;
+        c.y = y;
+        c.pix = (uint32_t)y * w + (uint32_t)c.x;
+        c.xf = (float)c.x;
+        c.yf = yf;
+        c.u = st_u[q];
+        c.v = st_v[q];
+        int thh = st_hi[q], thl = st_lo[q], vr = st_vr[q];
+        float ref = 0.0f;
+        int before = 0;
+        // every sample x + s*u, |s| <= 1, stays in [0, w-1]: no clamp needed
+        const bool safe = __all_sync(
+            kFull, fabsf(c.u) <= fminf(c.xf, wm - c.xf) && fabsf(c.v) <= fminf(c.yf, hm - c.yf));
+        if (!kLog)
+          before = kVB + (p.d.start == 0 ? (int)p.frames.at(sp)[c.pix]
+                                         : dense_exact(p.nfb, p.oma, p.alpha, qp, qc, p.w, p.h, c.xf, c.yf, c.u, c.v, 1));
+        int fbase = 0;
+        auto step = [&](int l, int val) {
+          uint2 m;
+          if constexpr (kLog) m = dense_rule_th(th_b, val, thh, thl, vr);
+          else m = dense_rule<false>(p, lut_b, c, val, ref, before);
+          if (lane == 0) s_stm[warp][l - fbase] = m;
+        };
+        auto flush = [&](int lend, bool force) {
+          const int n = lend - fbase;
+          if (n < 32 && !force) return;
+          __syncwarp();
+          for (int j = lane; j < n; j += 32) {
+            const int g = gbase + fbase + j;
+            const uint2 m = s_stm[warp][j];
+            EVSIM_CHECK((size_t)g * p.n_words + c.wi < p.masks_cap, "tile chain mask store");
+            p.masks[(size_t)g * p.n_words + c.wi] = m;
+            s_wcnt[warp][fbase + j] += __popc(m.x | m.y);  // a pixel crosses one way or not at all
+          }
+          __syncwarp();
+          fbase = lend;
+        };
+        for (int l0 = 0; l0 < n_int; l0 += kB) {
+          const int nb = min(kB, n_int - l0);
+          int vals[1][kB];
+          unsigned bad;
+          if (nb == kB) {
+            if (fits)
+              bad = safe ? dense_batch_tile<kB, false>(p, s_reg, biasA, biasB, my, wm, hm, c, kfirst + l0, vals)
+                         : dense_batch_tile<kB, true>(p, s_reg, biasA, biasB, my, wm, hm, c, kfirst + l0, vals);
+            else
+              bad = safe ? dense_batch<1, kB, false>(p, qbp, qbc, w, my, wm, hm, &c, kfirst + l0, vals)
+                         : dense_batch<1, kB, true>(p, qbp, qbc, w, my, wm, hm, &c, kfirst + l0, vals);
+          } else {
+            bad = 0;
+            for (int j = 0; j < nb; ++j) {
+              int v1[1][kB];
+              unsigned b1;
+              if (fits)
+                b1 = safe ? dense_batch_tile<1, false>(p, s_reg, biasA, biasB, my, wm, hm, c, kfirst + l0 + j, v1)
+                          : dense_batch_tile<1, true>(p, s_reg, biasA, biasB, my, wm, hm, c, kfirst + l0 + j, v1);
+              else
+                b1 = safe ? dense_batch<1, 1, false>(p, qbp, qbc, w, my, wm, hm, &c, kfirst + l0 + j, v1)
+                          : dense_batch<1, 1, true>(p, qbp, qbc, w, my, wm, hm, &c, kfirst + l0 + j, v1);
+              bad |= b1 << j;
+#pragma unroll
+              for (int jj = 0; jj < kB; ++jj)
+                if (jj == j) vals[0][jj] = v1[0][0];
+            }
+          }
+          if (__any_sync(kFull, bad != 0u)) {
+#pragma unroll
+            for (int j = 0; j < kB; ++j)
+              if ((bad >> j) & 1u)
+                vals[0][j] = kVB + dense_exact(p.nfb, p.oma, p.alpha, qp, qc, p.w, p.h, c.xf, c.yf, c.u, c.v,
+                                               kfirst + l0 + j);
+          }
+          if (nb == kB) {  // (straight-line: the rule's loads stay predicated)
+#pragma unroll
+            for (int j = 0; j < kB; ++j) step(l0 + j, vals[0][j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < kB; ++j) {
+              if (j >= nb) break;
+              step(l0 + j, vals[0][j]);
+            }
+          }
+          flush(l0 + nb, false);
+        }
+        if (n_int < L) step(L - 1, kVB + (int)p.frames.at(sc)[c.pix]);  // the link into curr (include_endpoints)
+        flush(L, true);
+        st_hi[q] = thh;
+        st_lo[q] = thl;
+        st_vr[q] = vr;
+      }
+      // the row segment is one count block: its events per link of this pair
+      for (int l = lane; l < L; l += 32) {
+        EVSIM_CHECK((size_t)(gbase + l) * p.n_blocks + cb < p.counts_cap, "tile chain count store");
+        p.counts[(size_t)(gbase + l) * p.n_blocks + cb] = s_wcnt[warp][l];
+        s_wcnt[warp][l] = 0;
+      }
+      __syncwarp();
+    }
+    sp = sc;
+  }
+  if (kLog && have) {
+#pragma unroll
+    for (int q = 0; q < kTileW; ++q) {
+      const int x = (tx * kTileW + q) * 32 + lane;
+      if (x < p.w) p.ref[(uint32_t)y * w + (uint32_t)x] = s_lut[st_vr[q] - kVB];
+    }
+  }
+}
+
 // The dense chain's gather image of a frame: per pixel (a00, a10 - a00, a01,
 // a11 - a01) in fp32 — the four taps sample_u8 reads at (x0, y0)
 // (simulate.cpp:10-26, replicate clamp) with the row differences formed
@@ -1178,6 +1553,11 @@ __device__ __forceinline__ void put_quad(uint2* q, float a00, float a10, float a
   // bf16 = the high half of the (exactly representable) fp32
   *q = make_uint2((__float_as_uint(a00) >> 16) | (__float_as_uint(a10 - a00) & 0xFFFF0000u),
                   (__float_as_uint(a01) >> 16) | (__float_as_uint(a11 - a01) & 0xFFFF0000u));
+}
+// tile-staged chain (chain_dense_tile_kernel): the top pair only — a pixel's
+// bottom pair is the top pair of the row below (replicate-clamped)
+__device__ __forceinline__ void put_quad(float2* q, float a00, float a10, float, float) {
+  *q = make_float2(a00, a10 - a00);
 }
 template <class T>
 __global__ void __launch_bounds__(256) lerp_quad_kernel(Ring<const uint8_t> frames, Ring<T> out, int w, int h, int R,
@@ -1210,6 +1590,13 @@ void launch_lerp_quads_bf16(Ring<const uint8_t> frames, Ring<uint2> out, int w, 
   if (n_frames <= 0) return;
   dim3 g((w + 255) / 256, (h + kLQRows - 1) / kLQRows, n_frames);
   lerp_quad_kernel<uint2><<<g, 256, 0, s>>>(frames, out, w, h, R, slot0);
+}
+
+void launch_lerp_quads_f2(Ring<const uint8_t> frames, Ring<float2> out, int w, int h, int R, int slot0, int n_frames,
+                          cudaStream_t s) {
+  if (n_frames <= 0) return;
+  dim3 g((w + 255) / 256, (h + kLQRows - 1) / kLQRows, n_frames);
+  lerp_quad_kernel<float2><<<g, 256, 0, s>>>(frames, out, w, h, R, slot0);
 }
 
 // ------------------------------------------------------------ sparse chain kernel
@@ -2289,6 +2676,32 @@ static void launch_chain_dense_b(const ChainParams& p, size_t sm, cudaStream_t s
   k<<<p.n_blocks, 256, sm, s>>>(p);
 }
 
+// the tile-staged form (log / linear single mode, tile geometry): shared
+// memory = the staging rows only (counts go out per tile row)
+template <bool kLog, int kB>
+static void launch_chain_dense_tile_b(const ChainParams& p, cudaStream_t s) {
+  const size_t sm = (size_t)p.tile_cap_rows * kTilePB;
+  const int tiles = (p.wpr / kTileW) * (int)((p.n_words / p.wpr + kTileH - 1) / kTileH);
+  if (p.tile_min_blocks >= 4) {
+    auto* k = chain_dense_tile_kernel<kLog, kB, 4>;
+    set_max_dynamic_smem((const void*)k, (int)sm);
+    k<<<tiles, 256, sm, s>>>(p);
+  } else {
+    auto* k = chain_dense_tile_kernel<kLog, kB, 3>;
+    set_max_dynamic_smem((const void*)k, (int)sm);
+    k<<<tiles, 256, sm, s>>>(p);
+  }
+}
+template <bool kLog>
+static void launch_chain_dense_tile(const ChainParams& p, cudaStream_t s) {
+  const int n_int = std::min(p.d.n_links, p.n_interp - p.d.start);
+  auto tiles = [&](int b) { return n_int > 0 && n_int % b == 0; };
+  if (tiles(8)) launch_chain_dense_tile_b<kLog, 8>(p, s);
+  else if (tiles(10)) launch_chain_dense_tile_b<kLog, 10>(p, s);
+  else if (tiles(5) && !tiles(4)) launch_chain_dense_tile_b<kLog, 5>(p, s);
+  else launch_chain_dense_tile_b<kLog, 4>(p, s);
+}
+
 template <bool kLog, bool kMag>
 static void launch_chain_dense(const ChainParams& p, size_t sm, cudaStream_t s) {
   // the longest batch that tiles the interior links (more gathers in flight
@@ -2347,6 +2760,12 @@ void launch_chain(const ChainParams& p, int provider, cudaStream_t s) {
       if (p.magnitude) launch_chain_sparse<false, true>(p, sm, s);
       else launch_chain_sparse<false, false>(p, sm, s);
     }
+    return;
+  }
+  if (provider == kProvDenseGrid && p.kc && p.n_interp + 2 <= kMaxParamK && p.quadt.base && !p.magnitude &&
+      p.words_per_block == kTileW && p.wpr % kTileW == 0) {
+    if (p.log_mode) launch_chain_dense_tile<true>(p, s);
+    else launch_chain_dense_tile<false>(p, s);
     return;
   }
   if (provider == kProvDenseGrid && p.kc && p.n_interp + 2 <= kMaxParamK) {

@@ -500,11 +500,22 @@ struct EventEngine {
   // fine = true (dense): one word per warp, 8 words per block on frames up
   // to 1080p — finer tasks balance the few waves of a small frame (measured:
   // c2 chain 16.4 -> 15.0 us/frame; 1080p c4 124 -> 112)
-  void geometry(int w_, int h_, bool fine = false) {
+  // tile = true (the tile-staged dense chain, csrc/event_kernels.cu): one
+  // count block per tile row of kTileWords words
+  static constexpr int kTileWords = 4, kTileRows = 8;
+  void geometry(int w_, int h_, bool fine = false, bool tile = false) {
     w = w_;
     h = h_;
     wpr = (w + 31) / 32;
     n_words = (int64_t)h * wpr;
+    if (tile) {
+      words_per_warp = 1;
+      wpb = kTileWords;
+      n_blocks = (int)(n_words / wpb);
+      max_links = 0;
+      capacity = 0;
+      return;
+    }
     // ~8 resident blocks of 256 threads on each of the 148 SMs
     const int64_t target = 148 * 8;
     int64_t per = (n_words + target - 1) / target;
@@ -631,18 +642,42 @@ struct evsim_gpu_sim {
   // (16 B/pixel, default), 2 = bf16 lerp quads (8 B/pixel: c5 log chain 604
   // -> 627 us/frame, L1 81 -> 52 % but +16 % instructions, issue 66 -> 75 %);
   // EVSIM_CHAIN_QUAD=u8|f4|bf16 selects (A/B and tests)
-  int quad_kind = [] {
+  // 3 = the top pairs (a00, a10 - a00) (8 B/pixel) staged per (tile, pair) in
+  // shared memory by chain_dense_tile_kernel (single mode, even width,
+  // 128-pixel tile columns).  Measured equal to the fp32 quads on c5 / c4
+  // (the chain is issue-bound either way and the 4-word
+  // count blocks cost the offsets scan 24 us/frame), so it is opt-in:
+  // EVSIM_CHAIN_QUAD=tile selects it wherever the geometry allows
+  int quad_req = [] {
     const char* e = std::getenv("EVSIM_CHAIN_QUAD");
     if (e && std::string(e) == "u8") return 0;
+    if (e && std::string(e) == "f4") return 1;
     if (e && std::string(e) == "bf16") return 2;
-    return 1;
+    if (e && std::string(e) == "tile") return 3;
+    return -1;
   }();
+  int quad_kind = 1;
+  // staging rows / resident blocks per SM of the tile kernel (EVSIM_TILE_BLOCKS=3|4)
+  int tile_min_blocks = [] {
+    const char* e = std::getenv("EVSIM_TILE_BLOCKS");
+    return e && e[0] == '4' ? 4 : 3;
+  }();
+  bool tile_possible() const {
+    return dense_flow() && !magnitude() && n_interp_eff() + 2 <= kMaxParamK && w % 2 == 0 &&
+           ((w + 31) / 32) % EventEngine::kTileWords == 0;
+  }
+  void choose_quad_kind(int grid_h) {
+    quad_kind = quad_req < 0 ? 1 : quad_req;
+    if (quad_req == 3 && !tile_possible()) quad_kind = 1;
+    (void)grid_h;
+  }
   bool use_quadf() const { return dense_flow() && quad_kind != 0; }
   size_t quad_bytes() const { return quad_kind == 1 ? sizeof(float4) : sizeof(uint2); }
   void launch_quads(int slot0, int n, cudaStream_t st) {
     const size_t P = (size_t)w * h;
     const Ring<const uint8_t> fr{frames.as<uint8_t>(), P};
     if (quad_kind == 1) launch_lerp_quads(fr, Ring<float4>{quadf.as<float4>(), P}, w, h, R, slot0, n, st);
+    else if (quad_kind == 3) launch_lerp_quads_f2(fr, Ring<float2>{quadf.as<float2>(), P}, w, h, R, slot0, n, st);
     else launch_lerp_quads_bf16(fr, Ring<uint2>{quadf.as<uint2>(), P}, w, h, R, slot0, n, st);
   }
   FlowEngine flow;
@@ -800,7 +835,8 @@ struct evsim_gpu_sim {
       if (band && dense_flow()) flow.plan_band(band_y0, band_y1);
     }
     if (log_mode()) ref.ensure((size_t)w * h * sizeof(float), stream);
-    ev.geometry(w, band ? band_y1 - band_y0 : h, dense_flow());
+    choose_quad_kind(band ? band_y1 - band_y0 : h);
+    ev.geometry(w, band ? band_y1 - band_y0 : h, dense_flow(), dense_flow() && quad_kind == 3);
     // interpolation constants, interpolate_frames simulate.cpp:97-100
     const int N = n_interp_eff();
     const int K = N + 2;
@@ -963,6 +999,11 @@ struct evsim_gpu_sim {
     c.quads = Ring<const uint32_t>{quads.as<uint32_t>(), P};
     c.quadf = Ring<const float4>{use_quadf() && quad_kind == 1 ? quadf.as<float4>() : nullptr, P};
     c.quadh = Ring<const uint2>{use_quadf() && quad_kind == 2 ? quadf.as<uint2>() : nullptr, P};
+    c.quadt = Ring<const float2>{use_quadf() && quad_kind == 3 ? quadf.as<float2>() : nullptr, P};
+    // staging rows: what 3 (4) resident blocks per SM leave of the 227 KB
+    // after the kernel's static shared memory (~8 KB) and the per-block reserve
+    c.tile_min_blocks = tile_min_blocks;
+    c.tile_cap_rows = tile_min_blocks >= 4 ? 42 : 58;
     {
       // gather index of the dense chain: TY_bits * w + TX_bits with TX =
       // 2^23 + x, TY = 2^23 + m_y + y (fp32 bits); it equals y * w + x +

@@ -142,6 +142,13 @@ struct ChainParams {
   Ring<const uint32_t> quads;  // u8 quad images (dense provider)
   Ring<const float4> quadf;    // dense chain: fp32 lerp quads of the same frames (base null: not used)
   Ring<const uint2> quadh;     // dense chain: bf16 lerp quads (base null: not used)
+  // tile-staged dense chain (chain_dense_tile_kernel): per pixel the top pair
+  // (a00, a10 - a00) in fp32, staged per (tile, pair) in shared memory; base
+  // null: not used.  tile_cap_rows = staging rows per block, tile_min_blocks =
+  // resident blocks per SM the launch asks for (3 or 4)
+  Ring<const float2> quadt;
+  int tile_cap_rows;
+  int tile_min_blocks;
   // difference_only device pushes read the caller's frames in place:
   // pair i = (i ? dcurr + (i-1)*P : dprev, dcurr + i*P); null = the ring
   const uint8_t* dcurr;
@@ -312,6 +319,8 @@ void launch_densify(const GridGeom& g, float* du, float* dv, cudaStream_t s);
 // the dense chain's fp32 / bf16 lerp quads of n_frames ring slots from slot0
 void launch_lerp_quads(Ring<const uint8_t> frames, Ring<float4> out, int w, int h, int R, int slot0, int n_frames,
                        cudaStream_t s);
+void launch_lerp_quads_f2(Ring<const uint8_t> frames, Ring<float2> out, int w, int h, int R, int slot0, int n_frames,
+                          cudaStream_t s);
 void launch_lerp_quads_bf16(Ring<const uint8_t> frames, Ring<uint2> out, int w, int h, int R, int slot0, int n_frames,
                             cudaStream_t s);
 void launch_interp_frames(const ChainParams& p, uint8_t* out, cudaStream_t s);
