@@ -2308,7 +2308,8 @@ __global__ void __launch_bounds__(256) emit_kernel(EmitParams p, const int64_t* 
 __global__ void __launch_bounds__(256) emit_single_kernel(EmitParams p, const int64_t* __restrict__ segbase,
                                                           int blocks_per_tile, int g0, int g1, int links_per_block) {
   __shared__ __align__(16) uint32_t s_ev[256 * 32 + 4];
-  __shared__ int s_warp[kWarpsPerBlock];
+  __shared__ int s_tot[2][kWarpsPerBlock];  // the warps' event totals, double-buffered by link parity
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ga = g0 + (int)blockIdx.y * links_per_block, gb = min(ga + links_per_block, g1);
   const int b0 = blockIdx.x * blocks_per_tile;
   const int64_t w0 = (int64_t)b0 * p.words_per_block;
@@ -2332,11 +2333,26 @@ __global__ void __launch_bounds__(256) emit_single_kernel(EmitParams p, const in
       off_next = segbase[g + 1] + p.prefix[(size_t)(g + 1) * p.n_blocks + b0];
     }
     const uint32_t all = m.x | m.y, neg = m.y;
-    int total;
-    // (the scan's barriers also order the previous link's staged reads, which
-    // thread 0 finished waiting for, before this link's writes)
-    const int excl = block_exclusive_scan(__popc(all), s_warp, total);
+    // block scan of the words' event counts with ONE barrier: a warp scan,
+    // the 8 warp totals through shared memory (double-buffered by link
+    // parity, so the next link's totals need no second barrier), and two
+    // REDUX sums for the tile's total and the warps before this one.  The
+    // barrier also orders the previous link's staged reads (head / tail
+    // lanes, and the bulk copy thread 0 waited for) before this link's writes.
+    const int nev = __popc(all);
+    int incl = nev;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int* tot = s_tot[(g - ga) & 1];
+    if (lane == 31) tot[warp] = incl;
+    __syncthreads();
+    const int wt = lane < kWarpsPerBlock ? tot[lane] : 0;
+    const int total = __reduce_add_sync(kFull, wt);
     if (total == 0) continue;  // uniform
+    const int excl = __reduce_add_sync(kFull, lane < warp ? wt : 0) + incl - nev;
     uint32_t* dst = p.out + tile_off;
     EVSIM_CHECK(tile_off >= 0 && tile_off + total <= p.capacity, "emit tile within the event buffer");
     EVSIM_CHECK(total <= 256 * 32, "emit staging size");
@@ -2370,7 +2386,7 @@ __global__ void __launch_bounds__(256) emit_single_kernel(EmitParams p, const in
                    "cp.async.bulk.wait_group.read 0;\n" ::"l"(dst + head), "r"(src), "r"(nbody * 4)
                    : "memory");
     }
-    __syncthreads();  // head / tail lanes and the bulk copy are done with s_ev
+    // (no barrier here: the next link's scan barrier comes before its staging writes)
   }
 }
 

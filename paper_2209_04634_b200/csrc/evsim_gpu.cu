@@ -527,6 +527,10 @@ struct EventEngine {
       while (p2 * 2 <= per) p2 *= 2;
       per = p2;
     }
+    if (const char* e = std::getenv("EVSIM_WPB")) {  // A/B of the non-dense block size
+      const int v = std::atoi(e);
+      if (v >= kWarpsPerBlock && !fine) per = v;
+    }
     words_per_warp = 2;
     if (fine) {
       // one-word warp tasks; 8-word blocks up to 8192 blocks, beyond that
