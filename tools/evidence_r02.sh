@@ -43,6 +43,13 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cha
   --no-parity > gpurun_out/ev_full_c1x64.log 2>&1
 python tools/ncu_summary.py /tmp/ev_full_c1x64.ncu-rep gpurun_out/ev_full_c1x64 c1x64:log:63 > gpurun_out/ev_full_c1x64.txt 2>&1
 python tools/ncu_source_hot.py /tmp/ev_full_c1x64.ncu-rep chain_diff 25 > gpurun_out/ev_hot_c1x64.txt 2>&1
+# the opt-in tile-staged chain on the same push
+EVSIM_CHAIN_QUAD=tile EVSIM_TILE_BLOCKS=4 timeout 600 ncu --set full --clock-control none --import-source on \
+  -k regex:"chain_dense_tile" --launch-skip 1 -c 1 -f -o /tmp/ev_tile_c5 python tools/push_once.py c5 log 7 1 \
+  > gpurun_out/ev_tile_c5.log 2>&1
+python tools/ncu_kernel_metrics.py /tmp/ev_tile_c5.ncu-rep > gpurun_out/ev_tile_c5.txt 2>&1
+python tools/ncu_kernel_metrics.py /tmp/ev_full_c1x64.ncu-rep chain_diff > gpurun_out/ev_c1x64_diff_chain.txt 2>&1
+python tools/ncu_kernel_metrics.py /tmp/ev_full_c5.ncu-rep > gpurun_out/ev_full_c5_metrics.txt 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"chain_dense" --launch-skip 1 -c 1 \
   -f -o gpurun_out/ev_chain_c5 python tools/push_once.py c5 log 7 1 > gpurun_out/ev_chain_c5.log 2>&1
 fi
