@@ -1224,7 +1224,7 @@ __device__ __forceinline__ void bulk_load_tx(uint32_t dst, const void* src, uint
 template <bool kClamp>
 __device__ __forceinline__ int dense_fast_tile(const uint8_t* __restrict__ s_reg, uint32_t ba, uint32_t bb, float my,
                                                float wm, float hm, float xf, float yf, float u, float v, float4 kc,
-                                               unsigned& bad, unsigned bit) {
+                                               unsigned& bad, unsigned bit, uint32_t lim_a, uint32_t lim_b) {
   const f32x2 NB = pk2(kc.x, kc.y);
   f32x2 X = affine2_est(xf, NB, u), Y = affine2_est(yf, NB, v);
   if (kClamp) {
@@ -1238,6 +1238,11 @@ __device__ __forceinline__ int dense_fast_tile(const uint8_t* __restrict__ s_reg
   // byte offsets into the staged regions (ba / bb fold the magic bits and the region origins)
   const uint32_t oa = __float_as_uint(lo2(TY)) * kTilePB + (__float_as_uint(lo2(TX)) * 8u + ba);
   const uint32_t ob = __float_as_uint(hi2(TY)) * kTilePB + (__float_as_uint(hi2(TX)) * 8u + bb);
+  // (checked build: both taps' rows inside the frame's staged rows; lim_a =
+  // end of prev's rows = start of curr's, lim_b = end of curr's)
+  EVSIM_CHECK(oa + kTilePB + 8u <= lim_a, "tile chain: prev sample inside its staged region");
+  EVSIM_CHECK(ob >= lim_a && ob + kTilePB + 8u <= lim_b, "tile chain: curr sample inside its staged region");
+  (void)lim_a, (void)lim_b;
   const float2 At = *reinterpret_cast<const float2*>(s_reg + oa);
   const float2 Ab = *reinterpret_cast<const float2*>(s_reg + oa + kTilePB);
   const float2 Bt = *reinterpret_cast<const float2*>(s_reg + ob);
@@ -1255,11 +1260,12 @@ __device__ __forceinline__ int dense_fast_tile(const uint8_t* __restrict__ s_reg
 template <int kNB, bool kClamp, int kBM>
 __device__ __forceinline__ unsigned dense_batch_tile(const ChainParams& p, const uint8_t* s_reg, uint32_t ba,
                                                      uint32_t bb, float my, float wm, float hm, const DenseWord& c,
-                                                     int k0, int (&vals)[1][kBM]) {
+                                                     int k0, int (&vals)[1][kBM], uint32_t lim_a, uint32_t lim_b) {
   unsigned bad = 0;
 #pragma unroll
   for (int j = 0; j < kNB; ++j)
-    vals[0][j] = dense_fast_tile<kClamp>(s_reg, ba, bb, my, wm, hm, c.xf, c.yf, c.u, c.v, p.kcp[k0 + j], bad, 1u << j);
+    vals[0][j] = dense_fast_tile<kClamp>(s_reg, ba, bb, my, wm, hm, c.xf, c.yf, c.u, c.v, p.kcp[k0 + j], bad, 1u << j,
+                                        lim_a, lim_b);
   return bad;
 }
 
@@ -1421,6 +1427,7 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_tile_kernel(ChainParam
     const uint32_t biasA = 0u - ((BY + (uint32_t)yloA) * kTilePB + (0x4B000000u + (uint32_t)xloA) * 8u);
     const uint32_t biasB =
         (uint32_t)nrA * kTilePB - ((BY + (uint32_t)yloB) * kTilePB + (0x4B000000u + (uint32_t)xloB) * 8u);
+    const uint32_t lim_a = (uint32_t)nrA * kTilePB, lim_b = (uint32_t)(nrA + nrB) * kTilePB;
     // ---- the links of this row's words
     if (have) {
       const int gbase = i * L;
@@ -1474,8 +1481,8 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_tile_kernel(ChainParam
           unsigned bad;
           if (nb == kB) {
             if (fits)
-              bad = safe ? dense_batch_tile<kB, false>(p, s_reg, biasA, biasB, my, wm, hm, c, kfirst + l0, vals)
-                         : dense_batch_tile<kB, true>(p, s_reg, biasA, biasB, my, wm, hm, c, kfirst + l0, vals);
+              bad = safe ? dense_batch_tile<kB, false>(p, s_reg, biasA, biasB, my, wm, hm, c, kfirst + l0, vals, lim_a, lim_b)
+                         : dense_batch_tile<kB, true>(p, s_reg, biasA, biasB, my, wm, hm, c, kfirst + l0, vals, lim_a, lim_b);
             else
               bad = safe ? dense_batch<1, kB, false>(p, qbp, qbc, w, my, wm, hm, &c, kfirst + l0, vals)
                          : dense_batch<1, kB, true>(p, qbp, qbc, w, my, wm, hm, &c, kfirst + l0, vals);
@@ -1485,8 +1492,8 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_tile_kernel(ChainParam
               int v1[1][kB];
               unsigned b1;
               if (fits)
-                b1 = safe ? dense_batch_tile<1, false>(p, s_reg, biasA, biasB, my, wm, hm, c, kfirst + l0 + j, v1)
-                          : dense_batch_tile<1, true>(p, s_reg, biasA, biasB, my, wm, hm, c, kfirst + l0 + j, v1);
+                b1 = safe ? dense_batch_tile<1, false>(p, s_reg, biasA, biasB, my, wm, hm, c, kfirst + l0 + j, v1, lim_a, lim_b)
+                          : dense_batch_tile<1, true>(p, s_reg, biasA, biasB, my, wm, hm, c, kfirst + l0 + j, v1, lim_a, lim_b);
               else
                 b1 = safe ? dense_batch<1, 1, false>(p, qbp, qbc, w, my, wm, hm, &c, kfirst + l0 + j, v1)
                           : dense_batch<1, 1, true>(p, qbp, qbc, w, my, wm, hm, &c, kfirst + l0 + j, v1);
