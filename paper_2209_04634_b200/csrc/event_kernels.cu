@@ -406,6 +406,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) chain_kernel(ChainParams p) {
 // (ChainParams::magic_y); the gather index TY_bits * w + TX_bits then equals
 // y * w + x + qshift without wrapping, and qp / qc come pre-shifted by
 // -qshift elements, so the index costs one IMAD.
+// The blend weights are two of the position constants: kc = (-(float)alpha,
+// (float)(1 - alpha), (float)oma, (float)alpha) holds oma_f = kc.y and
+// alpha_f = -kc.x bit for bit (host: evsim_gpu.cu allocate()), so a link
+// needs one 8-byte constant load, not two.
 template <bool kClamp>
 __device__ __forceinline__ int dense_fast(const uint32_t* __restrict__ qp, const uint32_t* __restrict__ qc,
                                           uint32_t w, float my, float wm, float hm, float xf, float yf,
@@ -438,7 +442,7 @@ __device__ __forceinline__ int dense_fast(const uint32_t* __restrict__ qp, const
   // s = RN64(RN64(oma*fp) + RN64(alpha*fc)); e below satisfies |e - s| < 6.2e-5
   // (see DenseProvider::interp), RN(e + c) adds < 1.6e-5.  If
   // floor(e + 0.5 -/+ 2e-4) agree, that floor is lround(s) = floor(s + 0.5).
-  const float e = __fmaf_rn(kc.z, lo2(S), __fmul_rn(kc.w, hi2(S)));
+  const float e = __fmaf_rn(kc.y, lo2(S), __fmul_rn(-kc.x, hi2(S)));  // (oma_f = kc.y, alpha_f = -kc.x)
   const f32x2 T = add2_rz(add2(pk2(e, e), pk2(0.5f - 2e-4f, 0.5f + 2e-4f)), C23);
   if (__float_as_uint(lo2(T)) != __float_as_uint(hi2(T))) bad |= bit;
   return __float_as_int(hi2(T));  // kVB + value (the bias folds into the LUT address / cancels in differences)
@@ -476,7 +480,7 @@ __device__ __forceinline__ int dense_fast(const float4* __restrict__ qp, const f
   const float tb = __fmaf_rn(hi2(FX), B.y, B.x), bb = __fmaf_rn(hi2(FX), B.w, B.z);
   const float sa = __fmaf_rn(lo2(FY), __fsub_rn(ba, ta), ta);
   const float sb = __fmaf_rn(hi2(FY), __fsub_rn(bb, tb), tb);
-  const float e = __fmaf_rn(kc.z, sa, __fmul_rn(kc.w, sb));
+  const float e = __fmaf_rn(kc.y, sa, __fmul_rn(-kc.x, sb));  // (oma_f = kc.y, alpha_f = -kc.x)
   const f32x2 T = add2_rz(add2(pk2(e, e), pk2(0.5f - 2e-4f, 0.5f + 2e-4f)), C23);
   if (__float_as_uint(lo2(T)) != __float_as_uint(hi2(T))) bad |= bit;
   return __float_as_int(hi2(T));
@@ -510,7 +514,7 @@ __device__ __forceinline__ int dense_fast(const uint2* __restrict__ qp, const ui
   const float tb = __fmaf_rn(hi2(FX), hi16(B.x), lo16(B.x)), bb = __fmaf_rn(hi2(FX), hi16(B.y), lo16(B.y));
   const float sa = __fmaf_rn(lo2(FY), __fsub_rn(ba, ta), ta);
   const float sb = __fmaf_rn(hi2(FY), __fsub_rn(bb, tb), tb);
-  const float e = __fmaf_rn(kc.z, sa, __fmul_rn(kc.w, sb));
+  const float e = __fmaf_rn(kc.y, sa, __fmul_rn(-kc.x, sb));  // (oma_f = kc.y, alpha_f = -kc.x)
   const f32x2 T = add2_rz(add2(pk2(e, e), pk2(0.5f - 2e-4f, 0.5f + 2e-4f)), C23);
   if (__float_as_uint(lo2(T)) != __float_as_uint(hi2(T))) bad |= bit;
   return __float_as_int(hi2(T));
@@ -1251,7 +1255,7 @@ __device__ __forceinline__ int dense_fast_tile(const uint8_t* __restrict__ s_reg
   const float tb = __fmaf_rn(hi2(FX), Bt.y, Bt.x), bb2 = __fmaf_rn(hi2(FX), Bb.y, Bb.x);
   const float sa = __fmaf_rn(lo2(FY), __fsub_rn(ba2, ta), ta);
   const float sb = __fmaf_rn(hi2(FY), __fsub_rn(bb2, tb), tb);
-  const float e = __fmaf_rn(kc.z, sa, __fmul_rn(kc.w, sb));
+  const float e = __fmaf_rn(kc.y, sa, __fmul_rn(-kc.x, sb));  // (oma_f = kc.y, alpha_f = -kc.x)
   const f32x2 T = add2_rz(add2(pk2(e, e), pk2(0.5f - 2e-4f, 0.5f + 2e-4f)), C23);
   if (__float_as_uint(lo2(T)) != __float_as_uint(hi2(T))) bad |= bit;
   return __float_as_int(hi2(T));
