@@ -138,10 +138,11 @@ def config_json(c, args, n_frames, split, ws, n_streams):
 
 def golden_entry(c, args, n_frames, stream=0):
     """The committed reference checksums of this sequence, if pinned."""
-    if args.preset != "lq" or stream != 0:
+    if stream != 0:
         return None
     try:
-        g = json.load(open(GOLDEN)).get(f"{c.name}:{args.mode}")
+        key = f"{c.name}:{args.mode}" + ("" if args.preset == "lq" else f":{args.preset}")
+        g = json.load(open(GOLDEN)).get(key)
     except Exception:
         return None
     if not g or g["n_frames"] < n_frames:

@@ -14,7 +14,8 @@ Here the same sequences run through
 * frame-by-frame pushes for the smaller configs.
 
 Full sizes: c1 346x260 x64, c2 640x480 x128, c3 1280x720 x256, c4 stream 0
-1920x1080 x120, c5 3840x2160 x60; both contrast modes.
+1920x1080 x120, c5 3840x2160 x60; both contrast modes; c2 also with the
+high-quality flow preset (keys "c2:<mode>:hq").
 """
 from __future__ import annotations
 
@@ -40,18 +41,26 @@ def _frames(name):
     return _frames_cache[name]
 
 
-def _cfg(name, mode):
+def _split(key):
+    """(config, mode, preset) of a key "c2:log" / "c2:log:hq"."""
+    return (tuple(key.split(":")) + ("lq",))[:3]
+
+
+def _cfg(name, mode, preset="lq"):
     from paper_2209_04634_b200.abi import Method, make_config
     c = scenes.CONFIGS[name]
     cp, cn = scenes.LINEAR_THRESHOLDS[c.method]
     return make_config(Method[c.method], n_interp=c.n_interp, c_pos=cp, c_neg=cn,
-                       contrast_mode=1 if mode == "log" else 0, c_pos_log=c.contrast, c_neg_log=-c.contrast)
+                       contrast_mode=1 if mode == "log" else 0, c_pos_log=c.contrast, c_neg_log=-c.contrast,
+                       flow_preset=1 if preset == "hq" else 0)
 
 
 def test_golden_sequences_cover_every_config():
     """The committed checksums pin c1-c5 (c4: stream 0) in both modes, for the
     frames scenes.generate makes (the generator's output hash is recorded)."""
-    assert sorted(SEQS) == sorted(f"{c}:{m}" for c in ("c1", "c2", "c3", "c4", "c5") for m in ("log", "linear"))
+    want = [f"{c}:{m}" for c in ("c1", "c2", "c3", "c4", "c5") for m in ("log", "linear")]
+    want += ["c2:log:hq", "c2:linear:hq"]  # the high-quality flow preset (types.hpp:93)
+    assert sorted(SEQS) == sorted(want)
     for k, g in SEQS.items():
         assert len(g["counts"]) == g["n_frames"] == scenes.CONFIGS[g["config"]].n_frames, k
         assert g["counts"][0] == 0  # the warm-up frame emits nothing
@@ -77,14 +86,14 @@ def _check(key, got):
                     f"{counts[bad[0]]} events vs {g['counts'][bad[0] + 1]}"
 
 
-def _device_pass(name, mode, batch=0):
+def _device_pass(name, mode, batch=0, preset="lq"):
     import torch
 
     from paper_2209_04634_b200 import Simulator, SimulatorConfig
     from paper_2209_04634_b200.seqhash import push_frame_hashes
     frames, ts = _frames(name)
     c = scenes.CONFIGS[name]
-    sim = Simulator(SimulatorConfig.from_c(_cfg(name, mode)))
+    sim = Simulator(SimulatorConfig.from_c(_cfg(name, mode, preset)))
     d = torch.from_numpy(frames).cuda()
     P = c.width * c.height
     mb = sim.max_batch(c.width, c.height)
@@ -105,29 +114,30 @@ def _device_pass(name, mode, batch=0):
 @pytest.mark.gpu
 @pytest.mark.parametrize("key", KEYS)
 def test_sequence_pipelined_push_matches_reference(key):
-    name, mode = key.split(":")
-    _check(key, _device_pass(name, mode))
+    name, mode, preset = _split(key)
+    _check(key, _device_pass(name, mode, preset=preset))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("key", ["c2:log", "c2:linear", "c3:log", "c1:log"])
+@pytest.mark.parametrize("key", ["c2:log", "c2:linear", "c3:log", "c1:log", "c2:log:hq"])
 def test_sequence_small_batches_match_reference(key):
     """Batches of 5 frames: a push boundary inside the sequence every 5
     frames (the state carried across pushes: ring, pyramids, log state)."""
-    name, mode = key.split(":")
-    _check(key, _device_pass(name, mode, batch=5))
+    name, mode, preset = _split(key)
+    _check(key, _device_pass(name, mode, batch=5, preset=preset))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("key", ["c1:log", "c1:linear", "c2:log", "c2:linear", "c3:log", "c3:linear"])
+@pytest.mark.parametrize("key", ["c1:log", "c1:linear", "c2:log", "c2:linear", "c3:log", "c3:linear",
+                                 "c2:linear:hq"])
 def test_sequence_streamed_call_matches_reference(key):
     """Host frames in, host events out (evsim_gpu_push_frames_streamed)."""
     from paper_2209_04634_b200 import Simulator, SimulatorConfig
     from paper_2209_04634_b200.seqhash import frame_hash_packed_np
-    name, mode = key.split(":")
+    name, mode, preset = _split(key)
     frames, ts = _frames(name)
     c = scenes.CONFIGS[name]
-    sim = Simulator(SimulatorConfig.from_c(_cfg(name, mode)))
+    sim = Simulator(SimulatorConfig.from_c(_cfg(name, mode, preset)))
     mb = sim.max_batch(c.width, c.height)
     got = []
     for a0 in range(0, len(frames), mb):  # calls of at most max_batch frames, chunks of 24 inside
