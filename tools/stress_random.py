@@ -4,6 +4,7 @@ thresholds / batch cuts / timestamp gaps against the C oracle, optionally with
 library switches (e.g. EVSIM_CHAIN_QUAD=tile on tile-compatible widths).
 
     python tools/stress_random.py 2000 [tile]      # prints mismatching seeds, exits 1 on any
+    EVSIM_STRESS_BASE=910000 python tools/stress_random.py 2000   # other seeds
 """
 import os
 import sys
@@ -44,8 +45,9 @@ def main():
     oracle = Oracle()
     bad = []
     total_ev = 0
+    base = int(os.environ.get("EVSIM_STRESS_BASE", "770000"))  # a new base = seeds no earlier campaign used
     for seed in range(n_seeds):
-        rng = np.random.default_rng(770000 + seed + (10 ** 6 if tile else 0))
+        rng = np.random.default_rng(base + seed + (10 ** 6 if tile else 0))
         if tile:
             os.environ["EVSIM_TILE_BLOCKS"] = str(int(rng.choice([3, 4])))
             w = int(rng.choice([128, 250, 256, 384, 512, 640]))
