@@ -448,13 +448,16 @@ __device__ __forceinline__ int dense_fast(const uint32_t* __restrict__ qp, const
   return __float_as_int(hi2(T));  // kVB + value (the bias folds into the LUT address / cancels in differences)
 }
 
-// dense_fast on the fp32 lerp quads (a00, a10 - a00, a01, a11 - a01) of the
-// frames: one 16-byte gather per sample, no byte unpack, and each sample's
-// three lerps as FFMA — an estimate, like e.  The positions X, Y and their
-// splits are the reference's exactly (as above).  Bound (u = 2^-17, half an
-// ulp in [128, 256)): the reference's fp32 sample (simulate.cpp:10-26) is
-// within 5u of the exact bilinear value (2u per row lerp, + the rounded
-// difference, product and sum), this one within 3u, so |fp - fp_ref| <= 8u
+// dense_fast on the fp32 lerp quads (a00, dx = a10 - a00, dy = a01 - a00,
+// dxy = (a11 - a01) - (a10 - a00)) of the frames: one 16-byte gather per
+// sample, no byte unpack, and each sample as three FFMA — top = a00 + fx*dx,
+// (bottom - top) = dy + fx*dxy (exactly the difference of the two row lerps,
+// |.| <= 255, one rounding), s = top + fy*(bottom - top) — an estimate, like
+// e.  The positions X, Y and their splits are the reference's exactly (as
+// above).  Bound (u = 2^-17, half an ulp in [128, 256)): the reference's fp32
+// sample (simulate.cpp:10-26) is within 5u of the exact bilinear value (2u
+// per row lerp, + the rounded difference, product and sum), this one within
+// 3u (u for top, u for the difference, fy <= 1, u for s), so |fp - fp_ref| <= 8u
 // = 6.1e-5, the same for fc; with the fp32 weights (|oma_f - oma| <= 2^-25,
 // oma + alpha = 1) and e's two fp32 roundings, |e - s| <= 255 * 2^-24 + 8u
 // + 2u < 9.2e-5, and RN(e + 0.5 -/+ 2e-4) adds < 1.6e-5: inside the 2e-4
@@ -475,11 +478,12 @@ __device__ __forceinline__ int dense_fast(const float4* __restrict__ qp, const f
   const f32x2 FX = sub2(X, sub2(TX, C23)), FY = sub2(Y, sub2(TY, CY));
   const uint32_t ia = __float_as_uint(lo2(TY)) * w + __float_as_uint(lo2(TX));
   const uint32_t ib = __float_as_uint(hi2(TY)) * w + __float_as_uint(hi2(TX));
+  // quad = (a00, dx, dy, dxy): top = a00 + fx*dx, bottom - top = dy + fx*dxy
   const float4 A = __ldg(qp + ia), B = __ldg(qc + ib);
-  const float ta = __fmaf_rn(lo2(FX), A.y, A.x), ba = __fmaf_rn(lo2(FX), A.w, A.z);
-  const float tb = __fmaf_rn(hi2(FX), B.y, B.x), bb = __fmaf_rn(hi2(FX), B.w, B.z);
-  const float sa = __fmaf_rn(lo2(FY), __fsub_rn(ba, ta), ta);
-  const float sb = __fmaf_rn(hi2(FY), __fsub_rn(bb, tb), tb);
+  const float ta = __fmaf_rn(lo2(FX), A.y, A.x), da = __fmaf_rn(lo2(FX), A.w, A.z);
+  const float tb = __fmaf_rn(hi2(FX), B.y, B.x), db = __fmaf_rn(hi2(FX), B.w, B.z);
+  const float sa = __fmaf_rn(lo2(FY), da, ta);
+  const float sb = __fmaf_rn(hi2(FY), db, tb);
   const float e = __fmaf_rn(kc.y, sa, __fmul_rn(-kc.x, sb));  // (oma_f = kc.y, alpha_f = -kc.x)
   const f32x2 T = add2_rz(add2(pk2(e, e), pk2(0.5f - 2e-4f, 0.5f + 2e-4f)), C23);
   if (__float_as_uint(lo2(T)) != __float_as_uint(hi2(T))) bad |= bit;
@@ -1551,14 +1555,14 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_tile_kernel(ChainParam
   }
 }
 
-// The dense chain's gather image of a frame: per pixel (a00, a10 - a00, a01,
-// a11 - a01) in fp32 — the four taps sample_u8 reads at (x0, y0)
+// The dense chain's gather image of a frame: per pixel (a00, a10 - a00,
+// a01 - a00, (a11 - a01) - (a10 - a00)) in fp32 — the four taps sample_u8 reads at (x0, y0)
 // (simulate.cpp:10-26, replicate clamp) with the row differences formed
 // (exactly: integers).  One column per thread, kLQRows rows per block (the
 // row below's taps are the next row's top taps), one 16-byte store per pixel.
 constexpr int kLQRows = 8;
 __device__ __forceinline__ void put_quad(float4* q, float a00, float a10, float a01, float a11) {
-  *q = make_float4(a00, a10 - a00, a01, a11 - a01);
+  *q = make_float4(a00, a10 - a00, a01 - a00, (a11 - a01) - (a10 - a00));  // exact: small integers
 }
 __device__ __forceinline__ void put_quad(uint2* q, float a00, float a10, float a01, float a11) {
   // bf16 = the high half of the (exactly representable) fp32
