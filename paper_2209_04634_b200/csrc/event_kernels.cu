@@ -448,8 +448,9 @@ __device__ __forceinline__ int dense_fast(const uint32_t* __restrict__ qp, const
   return __float_as_int(hi2(T));  // kVB + value (the bias folds into the LUT address / cancels in differences)
 }
 
-// dense_fast on the fp32 lerp quads (a00, dx = a10 - a00, dy = a01 - a00,
-// dxy = (a11 - a01) - (a10 - a00)) of the frames: one 16-byte gather per
+// dense_fast on the fp32 lerp quads of the frames — with dx = a10 - a00,
+// dy = a01 - a00, dxy = (a11 - a01) - (a10 - a00), stored relative to the
+// tap column (see below) — one 16-byte gather per
 // sample, no byte unpack, and each sample as three FFMA — top = a00 + fx*dx,
 // (bottom - top) = dy + fx*dxy (exactly the difference of the two row lerps,
 // |.| <= 255, one rounding), s = top + fy*(bottom - top) — an estimate, like
@@ -475,13 +476,17 @@ __device__ __forceinline__ int dense_fast(const float4* __restrict__ qp, const f
   const f32x2 C23 = pk2(8388608.0f, 8388608.0f);
   const f32x2 CY = pk2(my, my);
   const f32x2 TX = add2_rz(X, C23), TY = add2_rz(Y, CY);  // magic + trunc
-  const f32x2 FX = sub2(X, sub2(TX, C23)), FY = sub2(Y, sub2(TY, CY));
+  const f32x2 FY = sub2(Y, sub2(TY, CY));
   const uint32_t ia = __float_as_uint(lo2(TY)) * w + __float_as_uint(lo2(TX));
   const uint32_t ib = __float_as_uint(hi2(TY)) * w + __float_as_uint(hi2(TX));
-  // quad = (a00, dx, dy, dxy): top = a00 + fx*dx, bottom - top = dy + fx*dxy
+  // quad of tap column x0 = (a00 - x0*dx, dx, dy - x0*dxy, dxy), exact integers
+  // below 2^24 (kLerpQuadMaxW): the fma forms X*dx + (a00 - x0*dx) exactly
+  // before its one rounding, and X - x0 is the x fraction exactly, so
+  // top = RN(a00 + fx*dx) and bottom - top = RN(dy + fx*dxy) bit for bit —
+  // without ever forming fx
   const float4 A = __ldg(qp + ia), B = __ldg(qc + ib);
-  const float ta = __fmaf_rn(lo2(FX), A.y, A.x), da = __fmaf_rn(lo2(FX), A.w, A.z);
-  const float tb = __fmaf_rn(hi2(FX), B.y, B.x), db = __fmaf_rn(hi2(FX), B.w, B.z);
+  const float ta = __fmaf_rn(lo2(X), A.y, A.x), da = __fmaf_rn(lo2(X), A.w, A.z);
+  const float tb = __fmaf_rn(hi2(X), B.y, B.x), db = __fmaf_rn(hi2(X), B.w, B.z);
   const float sa = __fmaf_rn(lo2(FY), da, ta);
   const float sb = __fmaf_rn(hi2(FY), db, tb);
   const float e = __fmaf_rn(kc.y, sa, __fmul_rn(-kc.x, sb));  // (oma_f = kc.y, alpha_f = -kc.x)
@@ -1555,23 +1560,25 @@ __global__ void __launch_bounds__(256, kMinB) chain_dense_tile_kernel(ChainParam
   }
 }
 
-// The dense chain's gather image of a frame: per pixel (a00, a10 - a00,
-// a01 - a00, (a11 - a01) - (a10 - a00)) in fp32 — the four taps sample_u8 reads at (x0, y0)
+// The dense chain's gather image of a frame: per pixel (a00 - x*dx, dx =
+// a10 - a00, dy - x*dxy, dxy = (a11 - a01) - (a10 - a00)), dy = a01 - a00, in fp32 — the four taps sample_u8 reads at (x0, y0)
 // (simulate.cpp:10-26, replicate clamp) with the row differences formed
 // (exactly: integers).  One column per thread, kLQRows rows per block (the
 // row below's taps are the next row's top taps), one 16-byte store per pixel.
 constexpr int kLQRows = 8;
-__device__ __forceinline__ void put_quad(float4* q, float a00, float a10, float a01, float a11) {
-  *q = make_float4(a00, a10 - a00, a01 - a00, (a11 - a01) - (a10 - a00));  // exact: small integers
+__device__ __forceinline__ void put_quad(float4* q, int x, float a00, float a10, float a01, float a11) {
+  // (a00 - x*dx, dx, dy - x*dxy, dxy): integers, |.| <= 255 + 510 * (w - 1) < 2^24 (kLerpQuadMaxW)
+  const int dx = (int)a10 - (int)a00, dy = (int)a01 - (int)a00, dxy = ((int)a11 - (int)a01) - dx;
+  *q = make_float4((float)((int)a00 - x * dx), (float)dx, (float)(dy - x * dxy), (float)dxy);
 }
-__device__ __forceinline__ void put_quad(uint2* q, float a00, float a10, float a01, float a11) {
+__device__ __forceinline__ void put_quad(uint2* q, int, float a00, float a10, float a01, float a11) {
   // bf16 = the high half of the (exactly representable) fp32
   *q = make_uint2((__float_as_uint(a00) >> 16) | (__float_as_uint(a10 - a00) & 0xFFFF0000u),
                   (__float_as_uint(a01) >> 16) | (__float_as_uint(a11 - a01) & 0xFFFF0000u));
 }
 // tile-staged chain (chain_dense_tile_kernel): the top pair only — a pixel's
 // bottom pair is the top pair of the row below (replicate-clamped)
-__device__ __forceinline__ void put_quad(float2* q, float a00, float a10, float, float) {
+__device__ __forceinline__ void put_quad(float2* q, int, float a00, float a10, float, float) {
   *q = make_float2(a00, a10 - a00);
 }
 template <class T>
@@ -1588,7 +1595,7 @@ __global__ void __launch_bounds__(256) lerp_quad_kernel(Ring<const uint8_t> fram
   for (int y = yb; y < ye; ++y) {
     const size_t r1 = (size_t)min(y + 1, h - 1) * w;
     const float a01 = (float)__ldg(f + r1 + x), a11 = (float)__ldg(f + r1 + x1);
-    put_quad(q + (size_t)y * w + x, a00, a10, a01, a11);
+    put_quad(q + (size_t)y * w + x, x, a00, a10, a01, a11);
     a00 = a01;
     a10 = a11;
   }

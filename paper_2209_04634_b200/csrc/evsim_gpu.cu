@@ -673,6 +673,7 @@ struct evsim_gpu_sim {
   void choose_quad_kind(int grid_h) {
     quad_kind = quad_req < 0 ? 1 : quad_req;
     if (quad_req == 3 && !tile_possible()) quad_kind = 1;
+    if (quad_kind == 1 && w > kLerpQuadMaxW) quad_kind = 2;  // fp32 quads' tap-relative constants stay exact up to there
     (void)grid_h;
   }
   bool use_quadf() const { return dense_flow() && quad_kind != 0; }

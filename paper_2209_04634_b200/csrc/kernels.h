@@ -317,6 +317,9 @@ void launch_build_quad(const uint8_t* src, uint32_t* dst, int w, int h, cudaStre
 void launch_dense_lk(const DenseLKParams& p, int n_pairs, cudaStream_t s);
 void launch_densify(const GridGeom& g, float* du, float* dv, cudaStream_t s);
 // the dense chain's fp32 / bf16 lerp quads of n_frames ring slots from slot0
+// widest frame whose fp32 lerp quads (tap-relative constants a00 - x*dx, dy -
+// x*dxy) are exact integers below 2^24: 255 + 510 * (w - 1) < 2^24
+constexpr int kLerpQuadMaxW = 32768;
 void launch_lerp_quads(Ring<const uint8_t> frames, Ring<float4> out, int w, int h, int R, int slot0, int n_frames,
                        cudaStream_t s);
 void launch_lerp_quads_f2(Ring<const uint8_t> frames, Ring<float2> out, int w, int h, int R, int slot0, int n_frames,
