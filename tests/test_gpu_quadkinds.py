@@ -26,3 +26,22 @@ def test_quad_kinds_match_oracle(oracle, kind, mode, mag, incl, monkeypatch):
     sim = Simulator(SimulatorConfig.from_c(cfg))
     got = concat([sim.push_frames(frames[a:b], ts[a:b]).events for a, b in ((0, 1), (1, 34))])
     assert_same_events(got, exp, what=f"{kind} mode={mode} mag={mag} incl={incl}")
+
+
+@pytest.mark.parametrize("width", [32768, 32770])
+def test_fp32_quads_at_their_width_bound(oracle, width):
+    """The fp32 quads hold tap-relative constants (a00 - x*dx, dy - x*dxy) that
+    are exact integers below 2^24 up to 32768 columns (kernels.h
+    kLerpQuadMaxW); wider frames take the bf16 quads.  Strong contrast in the
+    last columns (|dx| = 255, |dxy| = 510) with motion there, on both sides
+    of the bound."""
+    rng = np.random.default_rng(width)
+    h, n = 24, 4
+    base = rng.integers(0, 2, size=(h, width + 8)).astype(np.uint8) * 255  # checker-like extremes
+    frames = np.stack([np.ascontiguousarray(base[:, k:k + width]) for k in range(n)])
+    ts = np.arange(n, dtype=np.int64) * 33333
+    cfg = make_config(Method.dense, n_interp=4, contrast_mode=0, c_pos=2, c_neg=-2)
+    exp = concat(run_oracle_stream(oracle, cfg, frames, ts))
+    sim = Simulator(SimulatorConfig.from_c(cfg))
+    got = concat([sim.push_frames(frames[a:b], ts[a:b]).events for a, b in ((0, 1), (1, n))])
+    assert_same_events(got, exp, what=f"width {width}")
